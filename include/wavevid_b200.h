@@ -1,0 +1,143 @@
+/*
+ * wavevid_b200.h — C ABI of the B200 decode hot path for the wavelet
+ * 360-degree video codec of arXiv 2208.10859 (reference package `wavevid`,
+ * citations relative to /root/reference).
+ *
+ * The reference is pure Python; its decode seam is the Python method
+ * DecodeSession._decode (pkg/src/wavevid/decoding.py:260-307), reached from
+ * decode_viewport / decode_foveated / decode_full (decoding.py:309-331).
+ * Each entry point below replaces one stage of that method:
+ *
+ *   wv_select            LevelMaskSet.from_pixel_mask      wavelets.py:272-306
+ *                        foveation_masks                   decoding.py:124-152
+ *                        upscale_mask                      fileio.py:430-436
+ *                        inclusion_grid + block ids        wavelets.py:337-348,
+ *                                                          decoding.py:265-268
+ *                        footprint cascade                 wavelets.py:380-392
+ *                        bytes_loaded / records_processed  decoding.py:271-285
+ *   wv_dequant_temporal  dequantize_records                decoding.py:37-50
+ *                        temporal_inverse_sparse           decoding.py:53-90
+ *                        inclusion masking                 wavelets.py:372-378
+ *   wv_synthesize        synthesize_2d_region synthesis    wavelets.py:396-443
+ *                        + u8 conversion                   decoding.py:301
+ *   wv_decode_frame      DecodeSession._decode (all of the above)
+ *   wv_render_perspective render_perspective               projection.py:111-172
+ *
+ * Conventions: plain pointers and sizes only.  Every pointer named d_* or
+ * documented as "device" is CUDA device memory owned by the caller; the
+ * library allocates nothing and keeps no global mutable state.  `stream` is
+ * a cudaStream_t passed as void*.  Calls are asynchronous on that stream and
+ * return a WV_* status for argument/launch errors; data-dependent errors
+ * (corrupt stream, coverage) are reported through device-side result words
+ * the caller reads after synchronising.
+ */
+#ifndef WAVEVID_B200_H
+#define WAVEVID_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WV_ABI_VERSION 1
+#define WV_MAX_LEVELS 12
+
+enum wv_status {
+  WV_OK = 0,
+  WV_ERR_ARG = 1,          /* invalid geometry / argument */
+  WV_ERR_CUDA = 2,         /* a CUDA runtime call or launch failed */
+  WV_ERR_UNSUPPORTED = 3   /* geometry outside what the kernels handle */
+};
+
+enum wv_mode { WV_MODE_FULL = 0, WV_MODE_VIEWPORT = 1, WV_MODE_FOVEATED = 2 };
+
+/* wv_frame_args.flags */
+enum wv_flags {
+  WV_FLAG_ACCOUNT_ONLY = 1   /* wv_select only: update the set's cache accounting
+                                (DecodeSession.advance prefetch, decoding.py:335-354);
+                                no work lists, no footprint, dirty maps untouched */
+};
+
+/* device error word bits (wv_frame_result.error) */
+enum wv_device_error {
+  WV_DERR_OFFSET = 1,      /* record offset >= block_size^2 -> CorruptStreamError */
+  WV_DERR_TABLE = 2        /* BlockEnd span outside payload / misaligned */
+};
+
+/* Decode geometry = the .wvv header fields the kernels need
+ * (fileio.py:38-61). */
+typedef struct wv_geometry {
+  int32_t width, height, channels, levels;
+  int32_t inter_size, block_size, float_mode;
+  int32_t mask_w, mask_h;
+} wv_geometry;
+
+/* Device-side per-call result (caller allocates, library overwrites). */
+typedef struct wv_frame_result {
+  unsigned long long new_bytes;   /* span bytes of blocks newly added to the set's cache entry */
+  unsigned long long set_bytes;   /* cache entry total after this call (decoding.py:231) */
+  unsigned long long records;     /* records_processed (decoding.py:284) */
+  uint32_t n_missing;             /* blocks newly added to the entry */
+  uint32_t n_selected;            /* blocks selected by the level masks */
+  uint32_t error;                 /* WV_DERR_* bits */
+  uint32_t n_tiles;               /* level-1 synthesis tiles computed */
+} wv_frame_result;
+
+typedef struct wv_frame_args {
+  int32_t mode;                   /* wv_mode */
+  int32_t t;                      /* display time inside the set, 0 <= t < inter_size */
+  int32_t flags;                  /* wv_flags */
+  int32_t reserved;
+  const uint8_t* d_mask;          /* (mask_h, mask_w) bytes 0/1; unused for FULL */
+  int32_t fovea[WV_MAX_LEVELS][4];/* FOVEATED: detail level k at [k-1]: r0, r1, c0, c1
+                                     pixel window, half-open (decoding.py:147-150) */
+  const void* d_payload;          /* set payload: BlockEnd table (n*NB u64) + packed records, 16-B aligned */
+  uint64_t payload_bytes;
+  const float* d_extrema;         /* (n, C, 4) float32 (fileio.py:123) */
+  uint32_t* d_set_loaded;         /* NB-bit block bitmap of the set's cache entry */
+  unsigned long long* d_set_bytes;/* the entry's cumulative bytes */
+  uint8_t* d_canvas;              /* (H, W, C) u8 output; must persist across calls of one workspace */
+  uint32_t* d_footprint;          /* (H, ceil(W/32)) bit rows output, bit i of word w = column 32w+i */
+  wv_frame_result* d_result;
+} wv_frame_args;
+
+/* One perspective view (projection.py:111-172). */
+typedef struct wv_view_args {
+  const uint8_t* d_canvas;        /* (canvas_h, W, C) u8 */
+  const uint32_t* d_footprint;    /* bit rows of the same canvas */
+  int32_t row0, rows;             /* equirect region = canvas rows [row0, row0+rows) (a stereo eye) */
+  int32_t width, channels;
+  double rot[9];                  /* world-from-camera rotation, row major (projection.py:39-52) */
+  double tan_h, tan_v;            /* tan(fov_h/2), tan(fov_v/2) */
+  int32_t out_w, out_h;
+  uint8_t* d_out;                 /* (out_h, out_w, C) u8 */
+  uint32_t* d_uncovered;          /* device counter: output pixels with a tap outside the footprint */
+} wv_view_args;
+
+int wv_abi_version(void);
+const char* wv_status_string(int status);
+
+/* Bytes of device workspace one decode stream needs for this geometry. */
+int wv_workspace_bytes(const wv_geometry* g, uint64_t* bytes);
+/* Zero the workspace (coefficient plane, dirty maps). Call once after allocation. */
+int wv_workspace_reset(const wv_geometry* g, void* d_workspace, void* stream);
+
+int wv_select(const wv_geometry* g, const wv_frame_args* a, void* d_workspace, void* stream);
+int wv_dequant_temporal(const wv_geometry* g, const wv_frame_args* a, void* d_workspace, void* stream);
+int wv_synthesize(const wv_geometry* g, const wv_frame_args* a, void* d_workspace, void* stream);
+int wv_decode_frame(const wv_geometry* g, const wv_frame_args* a, void* d_workspace, void* stream);
+
+int wv_render_perspective(const wv_view_args* views, int n_views, void* stream);
+
+/* Views into the workspace for parity tests (no launches). */
+int wv_plane_view(const wv_geometry* g, void* d_workspace, float** d_plane);
+int wv_level_mask_view(const wv_geometry* g, void* d_workspace, int level,
+                       uint32_t** d_bits, int32_t* words_per_row);
+int wv_block_list_view(const wv_geometry* g, void* d_workspace,
+                       uint32_t** d_list, uint32_t** d_count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WAVEVID_B200_H */

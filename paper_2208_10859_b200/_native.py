@@ -1,0 +1,96 @@
+"""ctypes binding of the C ABI in include/wavevid_b200.h.
+
+The decode path has no CPU fallback: if the library is missing or a call
+fails, this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_wvb200.so")
+
+WV_OK, WV_ERR_ARG, WV_ERR_CUDA, WV_ERR_UNSUPPORTED = 0, 1, 2, 3
+WV_MODE_FULL, WV_MODE_VIEWPORT, WV_MODE_FOVEATED = 0, 1, 2
+WV_FLAG_ACCOUNT_ONLY = 1
+WV_DERR_OFFSET, WV_DERR_TABLE = 1, 2
+WV_MAX_LEVELS = 12
+
+EXPORTS = ["wv_abi_version", "wv_status_string", "wv_workspace_bytes", "wv_workspace_reset",
+           "wv_select", "wv_dequant_temporal", "wv_synthesize", "wv_decode_frame",
+           "wv_render_perspective", "wv_plane_view", "wv_level_mask_view",
+           "wv_block_list_view"]
+
+
+class Geometry(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("width", "height", "channels", "levels", "inter_size",
+                                         "block_size", "float_mode", "mask_w", "mask_h")]
+
+
+class FrameResult(C.Structure):
+    _fields_ = [("new_bytes", C.c_uint64), ("set_bytes", C.c_uint64), ("records", C.c_uint64),
+                ("n_missing", C.c_uint32), ("n_selected", C.c_uint32), ("error", C.c_uint32),
+                ("n_tiles", C.c_uint32)]
+
+
+class FrameArgs(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("t", C.c_int32), ("flags", C.c_int32),
+                ("reserved", C.c_int32), ("d_mask", C.c_void_p),
+                ("fovea", (C.c_int32 * 4) * WV_MAX_LEVELS),
+                ("d_payload", C.c_void_p), ("payload_bytes", C.c_uint64),
+                ("d_extrema", C.c_void_p), ("d_set_loaded", C.c_void_p),
+                ("d_set_bytes", C.c_void_p), ("d_canvas", C.c_void_p),
+                ("d_footprint", C.c_void_p), ("d_result", C.c_void_p)]
+
+
+class ViewArgs(C.Structure):
+    _fields_ = [("d_canvas", C.c_void_p), ("d_footprint", C.c_void_p), ("row0", C.c_int32),
+                ("rows", C.c_int32), ("width", C.c_int32), ("channels", C.c_int32),
+                ("rot", C.c_double * 9), ("tan_h", C.c_double), ("tan_v", C.c_double),
+                ("out_w", C.c_int32), ("out_h", C.c_int32), ("d_out", C.c_void_p),
+                ("d_uncovered", C.c_void_p)]
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the decode library (raises if it is absent: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeError(
+            f"B200 decode library not built: {path} (run python -m paper_2208_10859_b200.build)")
+    lib = C.CDLL(path)
+    G, A, V = C.POINTER(Geometry), C.POINTER(FrameArgs), C.POINTER(ViewArgs)
+    lib.wv_abi_version.restype = C.c_int
+    lib.wv_status_string.restype = C.c_char_p
+    lib.wv_status_string.argtypes = [C.c_int]
+    lib.wv_workspace_bytes.argtypes = [G, C.POINTER(C.c_uint64)]
+    lib.wv_workspace_reset.argtypes = [G, C.c_void_p, C.c_void_p]
+    for fn in ("wv_select", "wv_dequant_temporal", "wv_synthesize", "wv_decode_frame"):
+        getattr(lib, fn).argtypes = [G, A, C.c_void_p, C.c_void_p]
+    lib.wv_render_perspective.argtypes = [V, C.c_int, C.c_void_p]
+    lib.wv_plane_view.argtypes = [G, C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.wv_level_mask_view.argtypes = [G, C.c_void_p, C.c_int, C.POINTER(C.c_void_p),
+                                       C.POINTER(C.c_int32)]
+    lib.wv_block_list_view.argtypes = [G, C.c_void_p, C.POINTER(C.c_void_p),
+                                       C.POINTER(C.c_void_p)]
+    for fn in EXPORTS[2:]:
+        getattr(lib, fn).restype = C.c_int
+    if lib.wv_abi_version() != 1:
+        raise NativeError("decode library ABI mismatch")
+    _lib = lib
+    return lib
+
+
+def check(status: int, what: str) -> None:
+    if status != WV_OK:
+        msg = load().wv_status_string(status).decode()
+        raise NativeError(f"{what} failed: {msg} (status {status})")

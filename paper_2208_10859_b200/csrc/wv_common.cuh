@@ -1,0 +1,113 @@
+// Shared device/host definitions for the B200 decode path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/wavevid_b200.h"
+
+namespace wv {
+
+// synthesis tile: TY x TX coefficients per subband -> (2TY) x (2TX) outputs
+constexpr int TY = 32;
+constexpr int TX = 32;
+constexpr int HALO = 2;               // lifting support per side
+// TMA box: the innermost box coordinate must be 16-byte aligned (unaligned or
+// negative-unaligned starts raise an illegal-instruction fault on B200), so
+// the box starts at ax-4 (ax is a multiple of 32) and spans 40 floats.
+constexpr int XPAD = 4;
+constexpr int BOX_W = TX + 2 * XPAD;
+constexpr int BOX_H = TY + 2 * HALO;
+constexpr int OUT_H = 2 * TY;
+constexpr int OUT_W = 2 * TX;
+constexpr uint32_t ZERO_FLAG = 0x80000000u;  // work-list entry: zero-fill only
+constexpr int DIL = 4;                // WaveletKind.CDF97.half_width (wavelets.py:30-32)
+
+__host__ __device__ inline int wpr(int cols) { return (cols + 31) >> 5; }
+__host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// Offsets of every workspace region (bytes from the workspace base).
+struct Layout {
+  int L, C, H, W, NB, nbx, bs, n;
+  int mh, mw;
+  int wpr_[WV_MAX_LEVELS + 1];           // words per bit row at level j
+  uint64_t mrows;                        // mask rows at full width (mh x wpr0)
+  uint64_t stack[WV_MAX_LEVELS + 1];     // level j (1..L): (L+1) masks
+  uint64_t stack_stride[WV_MAX_LEVELS + 1];
+  uint64_t fp[WV_MAX_LEVELS + 1];        // footprint intermediates, level 1..L-1
+  uint64_t sel, prev_sel;                // NB-bit bitmaps
+  uint64_t blist;                        // NB u32 entries
+  int nty[WV_MAX_LEVELS + 1], ntx[WV_MAX_LEVELS + 1];  // tile grid of synthesis level k
+  uint64_t need[WV_MAX_LEVELS + 1];      // u8 per tile
+  uint64_t prev_need;                    // level 1, u8 per tile
+  uint64_t tlist[WV_MAX_LEVELS + 1];     // u32 per tile
+  uint64_t counters;                     // u32[64]
+  uint64_t plane;                        // C x H x W f32
+  uint64_t ybuf[WV_MAX_LEVELS + 1];      // level k (1..L-1): C x (H>>k) x pitch[k] f32
+  int ypitch[WV_MAX_LEVELS + 1];
+  uint64_t total;
+};
+
+// counter slots
+enum { CNT_BLOCKS = 0, CNT_TILES = 1 /* + level */ };
+
+inline int build_layout(const wv_geometry* g, Layout* o) {
+  if (!g || !o) return WV_ERR_ARG;
+  const int L = g->levels, W = g->width, H = g->height, C = g->channels;
+  const int bs = g->block_size, n = g->inter_size;
+  if (L < 1 || L > WV_MAX_LEVELS - 1 || C < 1 || C > 4 || bs < 1 || bs > 64 || n < 1 ||
+      n > 256 || W < 2 || H < 2 || (W % (1 << L)) || (H % (1 << L)) || (W % bs) || (H % bs) ||
+      g->mask_w < 1 || g->mask_h < 1 || (bs & (bs - 1)) || (n & (n - 1)))
+    return WV_ERR_ARG;
+  if ((W % 4) != 0) return WV_ERR_UNSUPPORTED;  // TMA row strides need 16-B multiples
+  o->L = L; o->C = C; o->H = H; o->W = W; o->bs = bs; o->n = n;
+  o->nbx = W / bs; o->NB = (W / bs) * (H / bs);
+  o->mh = g->mask_h; o->mw = g->mask_w;
+  uint64_t off = 0;
+  auto take = [&](uint64_t bytes) { uint64_t r = off; off += (bytes + 255) & ~uint64_t(255); return r; };
+  for (int j = 0; j <= L; ++j) o->wpr_[j] = wpr(W >> j);
+  o->mrows = take(uint64_t(g->mask_h) * o->wpr_[0] * 4);
+  for (int j = 1; j <= L; ++j) {
+    uint64_t one = uint64_t(H >> j) * o->wpr_[j] * 4;
+    one = (one + 255) & ~uint64_t(255);
+    o->stack_stride[j] = one;
+    o->stack[j] = take(one * (L + 1));
+  }
+  for (int j = 1; j < L; ++j) o->fp[j] = take(uint64_t(H >> j) * o->wpr_[j] * 4);
+  o->sel = take(uint64_t(wpr(o->NB)) * 4);
+  o->prev_sel = take(uint64_t(wpr(o->NB)) * 4);
+  o->blist = take(uint64_t(o->NB) * 4);
+  for (int k = 1; k <= L; ++k) {
+    o->nty[k] = cdiv(H >> k, TY);
+    o->ntx[k] = cdiv(W >> k, TX);
+    uint64_t nt = uint64_t(o->nty[k]) * o->ntx[k];
+    o->need[k] = take(nt);
+    o->tlist[k] = take(nt * 4 * (k == 1 ? 2 : 1));
+  }
+  o->prev_need = take(uint64_t(o->nty[1]) * o->ntx[1]);
+  o->counters = take(64 * 4);
+  o->plane = take(uint64_t(C) * H * W * 4);
+  for (int k = 1; k < L; ++k) {
+    int cols = W >> k;
+    o->ypitch[k] = (cols + 3) & ~3;
+    o->ybuf[k] = take(uint64_t(C) * (H >> k) * o->ypitch[k] * 4);
+  }
+  o->total = off;
+  return WV_OK;
+}
+
+#define WV_CUDA(x)                                   \
+  do {                                               \
+    cudaError_t e_ = (x);                            \
+    if (e_ != cudaSuccess) return WV_ERR_CUDA;       \
+  } while (0)
+
+// ---- kernel launchers (defined in the .cu files) ----
+int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
+                  cudaStream_t s);
+int launch_temporal(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
+                    cudaStream_t s);
+int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
+                     cudaStream_t s);
+int launch_perspective(const wv_view_args* v, int n, cudaStream_t s);
+
+}  // namespace wv

@@ -1,0 +1,408 @@
+// K3 — per-level inverse 2-D CDF 9/7 synthesis, TMA-fed, column+row lifting
+// fused in shared memory; the finest level fuses the u8 colour conversion
+// and request masking (K4 colour step).
+//
+// Reference: synthesize_2d_region (wavelets.py:355-444) -> synthesize_1d
+// (wavelets.py:68-91) per level, columns (y) first then rows (x), and
+// decoding.py:301 for clip(rint(x*255)).  Inside the requested area the
+// reference's windowed result equals a full-frame synthesis of the masked
+// pyramid (verified by tests/test_oracle_golden.py), so each 32x32 coefficient
+// tile is computed independently from a 2-coefficient halo: outputs equal the
+// full-frame values bit for bit.  Boundary symmetric extension is applied at
+// every lifting step at the true level borders only (index clamp, as numpy's
+// _shift_left/_shift_right do).
+//
+// Per (tile, channel) item: one elected thread issues four TMA box loads
+// (LL, HL, LH, HH; 40x36 f32 each, far-edge out-of-range zero-filled) completing on an
+// mbarrier.  The column pass streams each box column through registers with
+// the L-half (LL/LH) and H-half (HL/HH) lines packed as float2 and lifted with
+// Blackwell's paired FP32 ops (__fadd2_rn/__fmul2_rn, RN, no FMA); results land
+// row-pair-interleaved so the row pass again lifts two output rows per
+// thread as one float2 stream.  The output tile is staged in shared memory and
+// written with coalesced stores.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "wv_common.cuh"
+
+namespace wv {
+namespace {
+
+constexpr int BOX_FLOATS = BOX_W * BOX_H;
+constexpr int BOX_SLOT = ((BOX_FLOATS * 4 + 127) / 128) * 128;  // bytes
+constexpr int CB_PITCH = BOX_W + 1;   // float2 units, odd -> conflict-free row pass
+constexpr int OB_PITCH = OUT_W + 1;   // float2 units (row pairs), odd
+constexpr int NTHREADS = 128;
+static_assert(TY * OB_PITCH * 8 <= 4 * BOX_SLOT, "output tile must fit in the box region");
+
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+// x - k*(y1 + y2), written as x + (-k)*(y1+y2): identical rounding.  The
+// final add is issued as two scalar FADDs: ptxas contracts a paired
+// mul.rn.f32x2 feeding add.rn.f32x2 into FFMA2 (observed with CUDA 12.9),
+// which would change the rounding; scalar adds keep the product rounded.
+__device__ __forceinline__ float2 lstep(float2 x, float2 nk, float2 y1, float2 y2) {
+  const float2 t = __fmul2_rn(nk, __fadd2_rn(y1, y2));
+  return make_float2(__fadd_rn(x.x, t.x), __fadd_rn(x.y, t.y));
+}
+
+// Inverse CDF 9/7 lifting of one line (two packed lines) over global
+// coefficient indices [g0, g1) of a level of length N; emits pairs p in
+// [a, b) as (s3[p], d3[p]).  Left/right symmetric extension applies only when
+// g0 == 0 / g1 == N (wavelets.py:82-91, :94-101).
+template <class Load, class Emit>
+__device__ __forceinline__ void lift_line(int g0, int g1, int N, int a, int b, Load load,
+                                          Emit emit) {
+  const float2 KS = f2(__uint_as_float(0x3f9d7658u));    // K
+  const float2 IK = f2(__uint_as_float(0x3f5019c3u));    // 1/K
+  const float2 ND = f2(-__uint_as_float(0x3ee31355u));   // -delta
+  const float2 NG = f2(-__uint_as_float(0x3f620676u));   // -gamma
+  const float2 NB = f2(-__uint_as_float(0xbd5901aeu));   // -beta
+  const float2 NA = f2(-__uint_as_float(0xbfcb0673u));   // -alpha
+  float2 sr, dr;
+  // j = g0 (at the left border d1[-1] = d1[0]; elsewhere the value is a halo)
+  load(g0, sr, dr);
+  float2 d1m = __fmul2_rn(dr, IK);
+  float2 s2m = lstep(__fmul2_rn(sr, KS), ND, d1m, d1m);
+  float2 d2mm = d1m, s3mm = s2m;
+  if (g1 - g0 >= 2) {
+    // j = g0 + 1 (at the left border d2[-1] = d2[0])
+    load(g0 + 1, sr, dr);
+    float2 d1 = __fmul2_rn(dr, IK);
+    float2 s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);
+    float2 d2 = lstep(d1m, NG, s2m, s2);
+    s3mm = lstep(s2m, NB, d2, d2);
+    d2mm = d2;
+    d1m = d1;
+    s2m = s2;
+#pragma unroll 4
+    for (int j = g0 + 2; j < g1; ++j) {
+      load(j, sr, dr);
+      d1 = __fmul2_rn(dr, IK);
+      s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);   // s2[j]
+      d2 = lstep(d1m, NG, s2m, s2);                   // d2[j-1]
+      float2 s3 = lstep(s2m, NB, d2mm, d2);           // s3[j-1]
+      float2 d3 = lstep(d2mm, NA, s3mm, s3);          // d3[j-2]
+      const int p = j - 2;
+      if (p >= a && p < b) emit(p, s3mm, d3);
+      d2mm = d2;
+      s3mm = s3;
+      d1m = d1;
+      s2m = s2;
+    }
+  }
+  if (g1 == N) {
+    float2 d2 = lstep(d1m, NG, s2m, s2m);                     // d2[N-1]
+    float2 s3 = lstep(s2m, NB, N == 1 ? d2 : d2mm, d2);       // s3[N-1]
+    if (N >= 2 && N - 2 >= a && N - 2 < b) emit(N - 2, s3mm, lstep(d2mm, NA, s3mm, s3));
+    if (N - 1 >= a && N - 1 < b) emit(N - 1, s3, lstep(d2, NA, s3, s3));
+  }
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct LevelArgs {
+  int k, bh, bw, C, ntx;
+  const uint32_t* list;
+  const uint32_t* count;
+  float* out;          // non-final: Y_{k-1} planar
+  int out_pitch;       // floats
+  uint8_t* canvas;     // final: (H, W, C) u8
+  const uint32_t* R;   // final: requested rows
+  int mh, wpr0;
+  int use_tma;         // subband widths are 16-byte multiples
+  const float* ll_ptr; int ll_pitch, ll_rows;   // LDG fallback sources
+  const float* plane; int plane_w, plane_h;
+};
+
+template <bool FINAL>
+__global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUtensorMap tm_ll,
+                                                    const __grid_constant__ CUtensorMap tm_det,
+                                                    LevelArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  float* box = reinterpret_cast<float*>(smem);                      // 4 slots
+  float2* colL = reinterpret_cast<float2*>(smem + 4 * BOX_SLOT);    // [TY][CB_PITCH]
+  float2* colH = colL + TY * CB_PITCH;
+  float2* outb = reinterpret_cast<float2*>(smem);                   // aliases boxes
+  uint8_t* outu8 = smem + 4 * BOX_SLOT + 2 * TY * CB_PITCH * 8;     // FINAL: [OUT_H][OUT_W*C]
+  __shared__ uint64_t bar;
+  const float* bLL = box;
+  const float* bHL = box + BOX_SLOT / 4;
+  const float* bLH = box + 2 * BOX_SLOT / 4;
+  const float* bHH = box + 3 * BOX_SLOT / 4;
+
+  const int tid = threadIdx.x;
+  if (tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  const int C = a.C;
+  const uint32_t ntile = *a.count;
+  const uint32_t nitems = FINAL ? ntile : ntile * C;
+  const int H = 2 * a.bh, W = 2 * a.bw;
+
+  for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const uint32_t entry = a.list[FINAL ? item : item / C];
+    const uint32_t tile = entry & ~ZERO_FLAG;
+    const int ty = tile / a.ntx, tx = tile % a.ntx;
+    const int ay = ty * TY, ax = tx * TX;
+    const int by = min(ay + TY, a.bh), bx = min(ax + TX, a.bw);
+    const int ny = 2 * (by - ay), nx = 2 * (bx - ax);
+    if (FINAL && (entry & ZERO_FLAG)) {
+      // tile left the request: clear what the previous frame wrote there
+      const int rowbytes = nx * C;
+      for (int r = 0; r < ny; ++r) {
+        uint8_t* dst = a.canvas + ((uint64_t)(2 * ay + r) * W + 2 * ax) * C;
+        for (int i = tid; i < rowbytes; i += NTHREADS) dst[i] = 0;
+      }
+      continue;
+    }
+    // box origin: TMA faults on negative box coordinates (observed on B200,
+    // driver 580), so tiles at the top/left border start their box at 0
+    const int oy = max(ay - HALO, 0), ox = max(ax - XPAD, 0);
+    const int c_first = FINAL ? 0 : (int)(item % C);
+    const int c_last = FINAL ? C : c_first + 1;
+    for (int c = c_first; c < c_last; ++c) {
+      if (a.use_tma) {
+        if (tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&bar, 4u * BOX_FLOATS * 4u);
+          tma_load_3d(box, &tm_ll, ox, oy, c, &bar);
+          tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar);
+          tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar);
+          tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar);
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+      } else {
+        // tiny levels whose subband width is not a multiple of 4 floats
+        for (int i = tid; i < 4 * BOX_FLOATS; i += NTHREADS) {
+          const int q = i / BOX_FLOATS, e = i % BOX_FLOATS;
+          const int yy = oy + e / BOX_W, xx = ox + e % BOX_W;
+          float v = 0.0f;
+          if (yy < a.bh && xx < a.bw) {
+            const bool ll = q == 0;
+            const float* src = ll ? a.ll_ptr : a.plane;
+            const int pitch = ll ? a.ll_pitch : a.plane_w;
+            const int rows = ll ? a.ll_rows : a.plane_h;
+            const int gy = yy + ((q >= 2) ? a.bh : 0), gx = xx + ((q & 1) ? a.bw : 0);
+            v = src[((uint64_t)c * rows + gy) * pitch + gx];
+          }
+          box[q * (BOX_SLOT / 4) + e] = v;
+        }
+        __syncthreads();
+      }
+
+      // column pass: one thread per box column, L and H halves packed
+      if (tid < BOX_W) {
+        const int lc = tid;
+        const int cg = ox + lc;
+        if (cg >= max(ax - HALO, 0) && cg < min(bx + HALO, a.bw)) {
+          const int g0 = oy, g1 = min(by + HALO, a.bh);
+          const int rbase = oy;
+          lift_line(
+              g0, g1, a.bh, ay, by,
+              [&](int j, float2& s, float2& d) {
+                const int o = (j - rbase) * BOX_W + lc;
+                s = make_float2(bLL[o], bHL[o]);
+                d = make_float2(bLH[o], bHH[o]);
+              },
+              [&](int p, float2 s3, float2 d3) {
+                const int q = p - ay;
+                colL[q * CB_PITCH + lc] = make_float2(s3.x, d3.x);
+                colH[q * CB_PITCH + lc] = make_float2(s3.y, d3.y);
+              });
+        }
+      }
+      __syncthreads();
+      // row pass: one thread per output row pair
+      if (tid < by - ay) {
+        const int i = tid;
+        const int g0 = max(ax - HALO, 0), g1 = min(bx + HALO, a.bw);
+        const int cbase = ox;
+        lift_line(
+            g0, g1, a.bw, ax, bx,
+            [&](int j, float2& s, float2& d) {
+              s = colL[i * CB_PITCH + (j - cbase)];
+              d = colH[i * CB_PITCH + (j - cbase)];
+            },
+            [&](int p, float2 s3, float2 d3) {
+              const int q = p - ax;
+              outb[i * OB_PITCH + 2 * q] = s3;
+              outb[i * OB_PITCH + 2 * q + 1] = d3;
+            });
+      }
+      __syncthreads();
+      if (!FINAL) {
+        float* base = a.out + ((uint64_t)c * H + 2 * ay) * a.out_pitch + 2 * ax;
+        const int half = nx >> 1;   // float2 columns per row
+        for (int idx = tid; idx < (ny >> 1) * half; idx += NTHREADS) {
+          const int i = idx / half, x2 = idx % half;
+          float2 u = outb[i * OB_PITCH + 2 * x2];
+          float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
+          float* r0 = base + (uint64_t)(2 * i) * a.out_pitch + 2 * x2;
+          *reinterpret_cast<float2*>(r0) = make_float2(u.x, v.x);
+          *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
+        }
+      } else {
+        for (int idx = tid; idx < (ny >> 1) * nx; idx += NTHREADS) {
+          const int i = idx / nx, x = idx % nx;
+          const float2 u = outb[i * OB_PITCH + x];
+          const int gx = 2 * ax + x;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int gy = 2 * ay + 2 * i + h;
+            const uint32_t rw =
+                a.R[(uint64_t)((long long)gy * a.mh / H) * a.wpr0 + (gx >> 5)];
+            float v = h ? u.y : u.x;
+            float q = rintf(__fmul_rn(v, 255.0f));
+            q = fminf(fmaxf(q, 0.0f), 255.0f);
+            uint8_t o = ((rw >> (gx & 31)) & 1u) ? (uint8_t)q : (uint8_t)0;
+            outu8[(2 * i + h) * (OUT_W * C) + x * C + c] = o;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (FINAL) {
+      const int rowbytes = nx * C;
+      if (((W * C) & 3) == 0 && ((2 * ax * C) & 3) == 0 && (rowbytes & 3) == 0) {
+        const int rw = rowbytes >> 2;
+        for (int idx = tid; idx < ny * rw; idx += NTHREADS) {
+          const int r = idx / rw, w = idx % rw;
+          uint32_t* dst = reinterpret_cast<uint32_t*>(a.canvas +
+                                                      ((uint64_t)(2 * ay + r) * W + 2 * ax) * C);
+          dst[w] = reinterpret_cast<const uint32_t*>(outu8 + r * (OUT_W * C))[w];
+        }
+      } else {
+        for (int idx = tid; idx < ny * rowbytes; idx += NTHREADS) {
+          const int r = idx / rowbytes, w = idx % rowbytes;
+          a.canvas[((uint64_t)(2 * ay + r) * W + 2 * ax) * C + w] = outu8[r * (OUT_W * C) + w];
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+}
+
+int make_map(CUtensorMap* m, const float* base, int cols, int rows, int pitch, int chans) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = get_encoder();  // immutable after init
+  if (!enc) return WV_ERR_CUDA;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)chans};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch * 4, (cuuint64_t)pitch * 4 * rows};
+  cuuint32_t box[3] = {BOX_W, BOX_H, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? WV_OK : WV_ERR_CUDA;
+}
+
+}  // namespace
+
+int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
+                     cudaStream_t s) {
+  (void)g;
+  const int L = lo.L, C = lo.C;
+  float* plane = (float*)(ws + lo.plane);
+  const uint32_t* counters = (const uint32_t*)(ws + lo.counters);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem_mid = 4 * BOX_SLOT + 2 * TY * CB_PITCH * 8;
+  const size_t smem_fin = smem_mid + (size_t)OUT_H * OUT_W * 4;
+  WV_CUDA(cudaFuncSetAttribute(k_level<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem_mid));
+  WV_CUDA(cudaFuncSetAttribute(k_level<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem_fin));
+  int occ_mid = 1, occ_fin = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_mid, k_level<false>, NTHREADS, smem_mid);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fin, k_level<true>, NTHREADS, smem_fin);
+  CUtensorMap tm_plane;
+  if (make_map(&tm_plane, plane, lo.W, lo.H, lo.W, C) != WV_OK) return WV_ERR_CUDA;
+  for (int k = L; k >= 1; --k) {
+    CUtensorMap tm_ll = tm_plane;
+    if (k < L) {
+      if (make_map(&tm_ll, (const float*)(ws + lo.ybuf[k]), lo.W >> k, lo.H >> k, lo.ypitch[k],
+                   C) != WV_OK)
+        return WV_ERR_CUDA;
+    }
+    LevelArgs la{};
+    la.k = k; la.bh = lo.H >> k; la.bw = lo.W >> k; la.C = C; la.ntx = lo.ntx[k];
+    la.use_tma = (la.bw % 4) == 0;
+    la.ll_ptr = k < L ? (const float*)(ws + lo.ybuf[k]) : plane;
+    la.ll_pitch = k < L ? lo.ypitch[k] : lo.W;
+    la.ll_rows = k < L ? (lo.H >> k) : lo.H;
+    la.plane = plane; la.plane_w = lo.W; la.plane_h = lo.H;
+    la.list = (const uint32_t*)(ws + lo.tlist[k]);
+    la.count = counters + CNT_TILES + k;
+    const int ntiles = lo.nty[k] * lo.ntx[k];
+    if (k > 1) {
+      la.out = (float*)(ws + lo.ybuf[k - 1]);
+      la.out_pitch = lo.ypitch[k - 1];
+      int grid = max(1, min(ntiles * C, sms * occ_mid));
+      k_level<false><<<grid, NTHREADS, smem_mid, s>>>(tm_ll, tm_plane, la);
+    } else {
+      la.canvas = a->d_canvas;
+      la.R = (const uint32_t*)(ws + lo.mrows);
+      la.mh = lo.mh;
+      la.wpr0 = lo.wpr_[0];
+      int grid = max(1, min(ntiles, sms * occ_fin));
+      k_level<true><<<grid, NTHREADS, smem_fin, s>>>(tm_ll, tm_plane, la);
+    }
+    WV_CUDA(cudaGetLastError());
+    if (getenv("WV_DEBUG_SYNC")) {
+      cudaError_t e = cudaStreamSynchronize(s);
+      fprintf(stderr, "[wv] level %d (%s): %s\n", k, k > 1 ? "mid" : "final", cudaGetErrorString(e));
+      if (e != cudaSuccess) return WV_ERR_CUDA;
+    }
+  }
+  return WV_OK;
+}
+
+}  // namespace wv

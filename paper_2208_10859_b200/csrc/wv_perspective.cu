@@ -1,0 +1,102 @@
+// K4 — equirectangular -> perspective writeout with footprint coverage check.
+//
+// Reference: render_perspective (projection.py:111-172).  Per output pixel:
+// camera ray through the pixel centre, normalised, rotated to world
+// (float64), lon/lat via atan2/asin, fractional source position, bilinear
+// blend of the u8 canvas in float32 with the reference's operation order,
+// rint, clamp.  Any tap outside the decoded footprint counts as uncovered
+// (the caller raises CoverageError).  Float64 geometry follows the reference
+// (libm vs CUDA ulp differences can move a value by at most 1 LSB: the
+// parity bar for this stage is +-1 LSB).
+#include "wv_common.cuh"
+
+namespace wv {
+namespace {
+
+constexpr double kRad2Deg = 57.29577951308232;  // numpy.degrees factor 180/pi
+
+constexpr int kMaxViews = 4;
+struct Views {
+  wv_view_args v[kMaxViews];
+};
+
+__global__ void k_perspective(const __grid_constant__ Views views) {
+  const wv_view_args& v = views.v[blockIdx.z];
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const bool live = x < v.out_w && y < v.out_h;
+  bool uncovered = false;
+  if (live) {
+    const double u = __dsub_rn(__dmul_rn(__ddiv_rn(__dadd_rn((double)x, 0.5), (double)v.out_w), 2.0), 1.0);
+    const double w = __dsub_rn(1.0, __dmul_rn(__ddiv_rn(__dadd_rn((double)y, 0.5), (double)v.out_h), 2.0));
+    double rx = __dmul_rn(u, v.tan_h), ry = __dmul_rn(w, v.tan_v), rz = 1.0;
+    const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)), __dmul_rn(rz, rz)));
+    rx = __ddiv_rn(rx, nrm);
+    ry = __ddiv_rn(ry, nrm);
+    rz = __ddiv_rn(rz, nrm);
+    const double* R = v.rot;
+    const double wx = __dadd_rn(__dadd_rn(__dmul_rn(rx, R[0]), __dmul_rn(ry, R[1])), __dmul_rn(rz, R[2]));
+    const double wy = __dadd_rn(__dadd_rn(__dmul_rn(rx, R[3]), __dmul_rn(ry, R[4])), __dmul_rn(rz, R[5]));
+    const double wz = __dadd_rn(__dadd_rn(__dmul_rn(rx, R[6]), __dmul_rn(ry, R[7])), __dmul_rn(rz, R[8]));
+    const double lon = __dmul_rn(atan2(wx, wz), kRad2Deg);
+    const double lat = __dmul_rn(asin(fmin(fmax(wy, -1.0), 1.0)), kRad2Deg);
+    const int m = v.rows, n = v.width;
+    const double fx = __dsub_rn(__dmul_rn(__ddiv_rn(__dadd_rn(lon, 180.0), 360.0), (double)n), 0.5);
+    const double fy = __dsub_rn(__dmul_rn(__ddiv_rn(__dsub_rn(90.0, lat), 180.0), (double)m), 0.5);
+    const double flx = floor(fx), fly = floor(fy);
+    const long long x0 = (long long)flx, y0 = (long long)fly;
+    const float ax = (float)__dsub_rn(fx, flx);
+    const float ay = (float)__dsub_rn(fy, fly);
+    long long xa = x0 % n; if (xa < 0) xa += n;
+    long long xb = (x0 + 1) % n; if (xb < 0) xb += n;
+    const int ya = (int)min(max(y0, 0ll), (long long)(m - 1));
+    const int yb = (int)min(max(y0 + 1, 0ll), (long long)(m - 1));
+    const int wpr0 = (n + 31) >> 5;
+    const uint32_t* F = v.d_footprint + (uint64_t)v.row0 * wpr0;
+    auto fp = [&](int yy, long long xx) {
+      return (F[(uint64_t)yy * wpr0 + (xx >> 5)] >> (xx & 31)) & 1u;
+    };
+    uncovered = !(fp(ya, xa) & fp(ya, xb) & fp(yb, xa) & fp(yb, xb));
+    const int C = v.channels;
+    const uint8_t* img = v.d_canvas + (uint64_t)v.row0 * n * C;
+    const float one_x = __fsub_rn(1.0f, ax), one_y = __fsub_rn(1.0f, ay);
+    uint8_t* out = v.d_out + ((uint64_t)y * v.out_w + x) * C;
+    for (int c = 0; c < C; ++c) {
+      const float p00 = img[((uint64_t)ya * n + xa) * C + c];
+      const float p01 = img[((uint64_t)ya * n + xb) * C + c];
+      const float p10 = img[((uint64_t)yb * n + xa) * C + c];
+      const float p11 = img[((uint64_t)yb * n + xb) * C + c];
+      const float top = __fadd_rn(__fmul_rn(p00, one_x), __fmul_rn(p01, ax));
+      const float bot = __fadd_rn(__fmul_rn(p10, one_x), __fmul_rn(p11, ax));
+      float o = rintf(__fadd_rn(__fmul_rn(top, one_y), __fmul_rn(bot, ay)));
+      o = fminf(fmaxf(o, 0.0f), 255.0f);
+      out[c] = (uint8_t)o;
+    }
+  }
+  const unsigned cnt = __popc(__ballot_sync(0xFFFFFFFFu, uncovered));
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(v.d_uncovered, cnt);
+}
+
+}  // namespace
+
+int launch_perspective(const wv_view_args* views, int n, cudaStream_t s) {
+  if (n < 1 || n > kMaxViews) return WV_ERR_ARG;
+  Views pv{};
+  int mw = 0, mh = 0;
+  for (int i = 0; i < n; ++i) {
+    const wv_view_args& v = views[i];
+    if (!v.d_canvas || !v.d_footprint || !v.d_out || !v.d_uncovered || v.out_w < 1 ||
+        v.out_h < 1 || v.channels < 1 || v.width < 1 || v.rows < 1)
+      return WV_ERR_ARG;
+    pv.v[i] = v;
+    mw = max(mw, v.out_w);
+    mh = max(mh, v.out_h);
+  }
+  dim3 block(32, 8);
+  dim3 grid(cdiv(mw, 32), cdiv(mh, 8), n);
+  k_perspective<<<grid, block, 0, s>>>(pv);
+  WV_CUDA(cudaGetLastError());
+  return WV_OK;
+}
+
+}  // namespace wv

@@ -1,0 +1,496 @@
+"""DecodeSession on the B200: the drop-in for wavevid.decoding.DecodeSession.
+
+Public behaviour follows pkg/src/wavevid/decoding.py:184-354 (same methods,
+arguments, return types, errors, stats and two-set cache bookkeeping); the
+work inside ``_decode`` (decoding.py:260-307) is three C-ABI calls into the
+sm_100a kernels (include/wavevid_b200.h):
+
+  K1 wv_select            level masks, foveation windows, block work list,
+                          synthesis tile lists, footprint, byte/record stats
+  K2 wv_dequant_temporal  dequantise + inverse temporal Haar + inclusion
+  K3 wv_synthesize        per-level inverse CDF 9/7 + u8 conversion
+
+The compressed set payload (BlockEnd table + packed records) is read from
+the file once per set into pinned memory and copied to HBM; the kernels
+address records through the table in place.  One session = one CUDA stream.
+There is no CPU fallback: without the extension or a GPU, construction
+raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+import time
+from collections import OrderedDict, deque
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .fileio import VideoReader
+from .projection import CameraPose, CoverageError, launch_views, unpack_footprint, view_args
+
+
+class DecodeError(ValueError):
+    pass
+
+
+class CorruptStreamError(DecodeError):
+    pass
+
+
+@dataclass
+class FoveationSchedule:
+    """Per-level retained viewport fraction, coarsest first, plus the gaze
+    point in viewport coordinates (decoding.py:93-121)."""
+
+    fractions: tuple
+    gaze_u: float = 0.5
+    gaze_v: float = 0.5
+
+    def __post_init__(self):
+        f = tuple(float(x) for x in self.fractions)
+        if not f or f[0] != 1.0:
+            raise DecodeError("coarsest fraction must be 1.0")
+        if any(b > a for a, b in zip(f, f[1:])):
+            raise DecodeError("fractions must be non-increasing toward finer levels")
+        if not (0.0 <= self.gaze_u <= 1.0 and 0.0 <= self.gaze_v <= 1.0):
+            raise DecodeError("gaze must lie inside the viewport")
+        self.fractions = f
+
+    @classmethod
+    def default(cls, levels: int, gaze_u: float = 0.5, gaze_v: float = 0.5):
+        if levels == 6:
+            fr = (1.0, 0.65, 0.40, 0.22, 0.10, 0.04, 0.02)
+        elif levels == 1:
+            fr = (1.0, 0.02)
+        else:
+            fr = (1.0,) + tuple(np.geomspace(0.65, 0.02, levels))
+        return cls(fr, gaze_u, gaze_v)
+
+
+@dataclass
+class DecodeStats:
+    bytes_loaded: int = 0
+    records_processed: int = 0
+    load_ms: float = 0.0
+    temporal_ms: float = 0.0
+    synthesis_ms: float = 0.0
+
+    @property
+    def decode_ms(self) -> float:
+        return self.load_ms + self.temporal_ms + self.synthesis_ms
+
+
+@dataclass
+class SessionStats:
+    bytes_loaded: int = 0
+    records_processed: int = 0
+    frames_decoded: int = 0
+    total_ms: float = 0.0
+
+
+def mask_bbox(mask: np.ndarray, width: int, height: int):
+    """Bounding box (y0, y1, x0, x1) of the upscaled pixel mask, computed
+    from the low-resolution mask through the nearest-neighbour index maps
+    (fileio.py:430-436) without materialising the full-resolution mask."""
+    m = np.asarray(mask, bool)
+    mh, mw = m.shape
+    rows = m.any(axis=1)[np.arange(height, dtype=np.int64) * mh // height]
+    cols = m.any(axis=0)[np.arange(width, dtype=np.int64) * mw // width]
+    ry, cx = np.flatnonzero(rows), np.flatnonzero(cols)
+    if ry.size == 0 or cx.size == 0:
+        return None
+    return int(ry[0]), int(ry[-1]) + 1, int(cx[0]), int(cx[-1]) + 1
+
+
+def fovea_rects(bbox, height: int, width: int, schedule: FoveationSchedule, levels: int):
+    """Per detail level (finest first) the gaze window (r0, r1, c0, c1) in
+    pixels, float64 arithmetic as decoding.py:133-151."""
+    y0, y1, x0, x1 = bbox
+    gw, gh = x1 - x0, y1 - y0
+    cx = x0 + schedule.gaze_u * gw
+    cy = y0 + schedule.gaze_v * gh
+    fr = list(schedule.fractions[1:])
+    while len(fr) < levels:
+        fr.append(fr[-1] if fr else 1.0)
+    out = []
+    for k in range(1, levels + 1):
+        f = fr[levels - k]
+        hw, hh = f * gw / 2.0, f * gh / 2.0
+        out.append((max(0, int(cy - hh)), min(height, int(math.ceil(cy + hh))),
+                    max(0, int(cx - hw)), min(width, int(math.ceil(cx + hw)))))
+    return out
+
+
+class _Entry:
+    """Reference cache entry (decoding.py:168-173): which blocks of a set
+    have been accounted and their cumulative span bytes, kept on device."""
+
+    def __init__(self, set_index: int, nb: int, device):
+        self.set_index = set_index
+        self.loaded = torch.zeros(max(1, (nb + 31) // 32), dtype=torch.int32, device=device)
+        self.nbytes = torch.zeros(1, dtype=torch.int64, device=device)
+        self.bytes_loaded = 0
+
+
+class _Pending:
+    __slots__ = ("slot", "set_index", "entry", "existed", "may_evict", "event", "ev",
+                 "account_only", "stats")
+
+    def __init__(self):
+        self.stats = None
+
+
+class DeviceFrame:
+    """Device-resident decode result.  ``canvas`` (H, W, C) u8 and
+    ``footprint_bits`` (H, ceil(W/32)) int32 are the session's buffers and
+    stay valid until the next decode call on the session."""
+
+    def __init__(self, session, pending: _Pending, canvas, footprint_bits):
+        self._session = session
+        self._pending = pending
+        self.canvas = canvas
+        self.footprint_bits = footprint_bits
+
+    def stats(self) -> DecodeStats:
+        self._session._settle_until(self._pending)
+        return self._pending.stats
+
+
+_RESULT_BYTES = C.sizeof(N.FrameResult)
+_RING = 64
+
+
+class DecodeSession:
+    """Single-owner decode session on one GPU stream with one-slot prefetch."""
+
+    def __init__(self, path, device=None, max_resident_sets: int = 4):
+        if not torch.cuda.is_available():
+            raise RuntimeError("the B200 decode path needs a CUDA device (no CPU fallback)")
+        self._lib = N.load()
+        self.reader = VideoReader(path)
+        h = self.reader.header
+        self.header = h
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self._geom = N.Geometry(h.width, h.height, h.channels, h.levels, h.inter_size,
+                                h.block_size, int(h.float_mode), h.mask_w, h.mask_h)
+        nbytes = C.c_uint64()
+        N.check(self._lib.wv_workspace_bytes(C.byref(self._geom), C.byref(nbytes)),
+                "wv_workspace_bytes")
+        self.stream = torch.cuda.Stream(self.device)
+        self._copy_stream = torch.cuda.Stream(self.device)
+        self._io_lock = threading.Lock()
+        wpr0 = (h.width + 31) // 32
+        with torch.cuda.stream(self.stream):
+            self._ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
+            N.check(self._lib.wv_workspace_reset(C.byref(self._geom), C.c_void_p(self._ws.data_ptr()),
+                                                 C.c_void_p(self.stream.cuda_stream)),
+                    "wv_workspace_reset")
+            self._canvas = torch.zeros((h.height, h.width, h.channels), dtype=torch.uint8,
+                                       device=self.device)
+            self._footprint = torch.zeros((h.height, wpr0), dtype=torch.int32, device=self.device)
+            self._mask_dev = torch.zeros((_RING, h.mask_h * h.mask_w), dtype=torch.uint8,
+                                         device=self.device)
+            self._results = torch.zeros((_RING, _RESULT_BYTES), dtype=torch.uint8,
+                                        device=self.device)
+            self._uncovered = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._mask_host = torch.zeros((_RING, h.mask_h * h.mask_w), dtype=torch.uint8).pin_memory()
+        self._results_host = torch.zeros((_RING, _RESULT_BYTES), dtype=torch.uint8).pin_memory()
+        self._slot = 0
+        self._cache: dict[int, _Entry] = {}
+        self._resident: OrderedDict = OrderedDict()
+        self._max_resident = max(2, max_resident_sets)
+        self._pending: deque = deque()
+        self._stats = SessionStats()
+        self._prefetch_thread: threading.Thread | None = None
+        self._prefetch_job = None
+        self.time_stages = True
+
+    # -- lifecycle ------------------------------------------------------------
+
+    def close(self):
+        self.join_prefetch()
+        if self._pending:
+            self._settle_until(None)
+        self.reader.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def stats(self) -> SessionStats:
+        self._settle_until(None)
+        return self._stats
+
+    # -- set payloads -----------------------------------------------------------
+
+    def _read_payload(self, set_index: int) -> torch.Tensor:
+        n = self.reader.payload_length(set_index)
+        host = torch.empty(n, dtype=torch.uint8).pin_memory()
+        with self._io_lock:
+            self.reader.read_set_payload(set_index, memoryview(host.numpy()))
+        return host
+
+    def _make_resident(self, set_index: int, host: torch.Tensor | None = None):
+        if set_index in self._resident:
+            self._resident.move_to_end(set_index)
+            return self._resident[set_index]
+        if host is None:
+            host = self._read_payload(set_index)
+        meta = self.reader.set_meta[set_index]
+        with torch.cuda.stream(self.stream):
+            dev = torch.empty(host.numel(), dtype=torch.uint8, device=self.device)
+            dev.copy_(host, non_blocking=True)
+            ext = torch.from_numpy(np.ascontiguousarray(meta.extrema, np.float32)).to(
+                self.device, non_blocking=False)
+        self._resident[set_index] = (dev, ext, host)
+        while len(self._resident) > self._max_resident:
+            self._resident.popitem(last=False)
+        return self._resident[set_index]
+
+    # -- reference cache bookkeeping -------------------------------------------
+
+    def _store(self, entry: _Entry):
+        """decoding.py:236-241."""
+        self._cache[entry.set_index] = entry
+        if len(self._cache) > 2:
+            oldest = min(self._cache)
+            if oldest != entry.set_index:
+                del self._cache[oldest]
+
+    def _entry_for(self, set_index: int) -> tuple[_Entry, bool, bool]:
+        if any(p.may_evict for p in self._pending):
+            self._settle_until(None)
+        entry = self._cache.get(set_index)
+        if entry is None:
+            entry = _Entry(set_index, self.header.num_blocks, self.device)
+            self._store(entry)
+            return entry, False, False
+        return entry, True, len(self._cache) > 2
+
+    # -- decode core ------------------------------------------------------------
+
+    def _frame_set(self, frame: int) -> tuple[int, int]:
+        if not 0 <= frame < self.header.frame_count:
+            raise DecodeError(f"frame {frame} out of range [0, {self.header.frame_count})")
+        return frame // self.header.inter_size, frame % self.header.inter_size
+
+    def _check_mask(self, mask: np.ndarray) -> np.ndarray:
+        h = self.header
+        m = np.asarray(mask)
+        if m.shape != (h.mask_h, h.mask_w):
+            raise DecodeError(f"mask dims {m.shape} != header ({h.mask_h}, {h.mask_w})")
+        return m.astype(bool)
+
+    def _mode_args(self, mode: str, mask, schedule, slot: int):
+        h = self.header
+        args = N.FrameArgs()
+        if mode == "full":
+            args.mode = N.WV_MODE_FULL
+            return args
+        m = self._check_mask(mask)
+        self._mask_host[slot].numpy()[:] = m.reshape(-1)
+        self._mask_dev[slot].copy_(self._mask_host[slot], non_blocking=True)
+        args.d_mask = self._mask_dev[slot].data_ptr()
+        args.mode = N.WV_MODE_VIEWPORT
+        if mode == "foveated":
+            bbox = mask_bbox(m, h.width, h.height)
+            if bbox is not None:   # empty viewport: plain masks (decoding.py:131-132)
+                args.mode = N.WV_MODE_FOVEATED
+                for k, rect in enumerate(fovea_rects(bbox, h.height, h.width, schedule, h.levels)):
+                    for q in range(4):
+                        args.fovea[k][q] = rect[q]
+        return args
+
+    def _launch(self, frame: int, mode: str, mask=None, schedule=None,
+                account_only: bool = False, time_stages: bool = False) -> _Pending:
+        self.join_prefetch()
+        si, t = self._frame_set(frame)
+        if mode != "full":
+            self._check_mask(mask)
+        s = self.stream
+        p = _Pending()
+        if len(self._pending) >= _RING:
+            self._settle_until(self._pending[0])
+        slot = self._slot
+        self._slot = (self._slot + 1) % _RING
+        with torch.cuda.stream(s):
+            ev0 = torch.cuda.Event(enable_timing=True) if time_stages else None
+            if ev0 is not None:
+                ev0.record(s)
+            dev, ext, _ = self._make_resident(si)
+            args = self._mode_args(mode, mask, schedule, slot)
+            entry, existed, may_evict = self._entry_for(si)
+            args.t = t
+            args.flags = N.WV_FLAG_ACCOUNT_ONLY if account_only else 0
+            args.d_payload = dev.data_ptr()
+            args.payload_bytes = dev.numel()
+            args.d_extrema = ext.data_ptr()
+            args.d_set_loaded = entry.loaded.data_ptr()
+            args.d_set_bytes = entry.nbytes.data_ptr()
+            args.d_canvas = self._canvas.data_ptr()
+            args.d_footprint = self._footprint.data_ptr()
+            args.d_result = self._results[slot].data_ptr()
+            g, ws, cs = C.byref(self._geom), C.c_void_p(self._ws.data_ptr()), C.c_void_p(s.cuda_stream)
+            evs = None
+            if account_only:
+                N.check(self._lib.wv_select(g, C.byref(args), ws, cs), "wv_select")
+            elif time_stages:
+                evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                N.check(self._lib.wv_select(g, C.byref(args), ws, cs), "wv_select")
+                evs[0].record(s)
+                N.check(self._lib.wv_dequant_temporal(g, C.byref(args), ws, cs),
+                        "wv_dequant_temporal")
+                evs[1].record(s)
+                N.check(self._lib.wv_synthesize(g, C.byref(args), ws, cs), "wv_synthesize")
+                evs[2].record(s)
+            else:
+                N.check(self._lib.wv_decode_frame(g, C.byref(args), ws, cs), "wv_decode_frame")
+            self._results_host[slot].copy_(self._results[slot], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(s)
+        p.slot, p.set_index, p.entry, p.existed, p.may_evict = slot, si, entry, existed, may_evict
+        p.event, p.ev, p.account_only = done, (ev0, evs), account_only
+        self._pending.append(p)
+        return p
+
+    def _settle_until(self, target: _Pending | None):
+        """Apply results of launched decodes in order (stats, corrupt-stream
+        errors, cache store/eviction of existing entries)."""
+        while self._pending:
+            p = self._pending.popleft()
+            p.event.synchronize()
+            r = N.FrameResult.from_buffer_copy(bytes(self._results_host[p.slot].numpy()))
+            entry = p.entry
+            if p.existed and r.n_missing and self._cache.get(p.set_index) is entry:
+                self._store(entry)
+            entry.bytes_loaded = int(r.set_bytes)
+            st = DecodeStats(bytes_loaded=int(r.new_bytes if r.new_bytes else r.set_bytes),
+                             records_processed=int(r.records))
+            ev0, evs = p.ev
+            if evs is not None:
+                st.load_ms = ev0.elapsed_time(evs[0])
+                st.temporal_ms = evs[0].elapsed_time(evs[1])
+                st.synthesis_ms = evs[1].elapsed_time(evs[2])
+            p.stats = st
+            if not p.account_only:
+                self._stats.bytes_loaded += st.bytes_loaded
+                self._stats.records_processed += st.records_processed
+                self._stats.frames_decoded += 1
+                self._stats.total_ms += st.decode_ms
+            if r.error:
+                raise CorruptStreamError(
+                    "record offset outside block" if r.error & N.WV_DERR_OFFSET
+                    else "BlockEnd table inconsistent with payload")
+            if p is target:
+                return
+
+    def _decode(self, frame: int, mode: str, mask=None, schedule=None):
+        p = self._launch(frame, mode, mask, schedule, time_stages=self.time_stages)
+        self._settle_until(p)
+        h = self.header
+        pixels = self._canvas.cpu().numpy()
+        footprint = unpack_footprint(self._footprint.cpu().numpy(), h.width)
+        return pixels, footprint, p.stats
+
+    # -- public API (decoding.py:309-354) ----------------------------------------
+
+    def decode_viewport(self, frame: int, mask: np.ndarray):
+        """Full-quality decode of the masked region: (pixels, footprint, stats)."""
+        return self._decode(frame, "viewport", mask)
+
+    def decode_foveated(self, frame: int, mask: np.ndarray,
+                        schedule: FoveationSchedule | None = None):
+        schedule = schedule or FoveationSchedule.default(self.header.levels)
+        return self._decode(frame, "foveated", mask, schedule)
+
+    def decode_full(self, frame: int):
+        return self._decode(frame, "full")
+
+    # device-resident variants for throughput (no host sync, no D2H)
+    def decode_viewport_device(self, frame: int, mask: np.ndarray) -> DeviceFrame:
+        return DeviceFrame(self, self._launch(frame, "viewport", mask), self._canvas,
+                           self._footprint)
+
+    def decode_foveated_device(self, frame: int, mask: np.ndarray,
+                               schedule: FoveationSchedule | None = None) -> DeviceFrame:
+        schedule = schedule or FoveationSchedule.default(self.header.levels)
+        return DeviceFrame(self, self._launch(frame, "foveated", mask, schedule), self._canvas,
+                           self._footprint)
+
+    def decode_full_device(self, frame: int) -> DeviceFrame:
+        return DeviceFrame(self, self._launch(frame, "full"), self._canvas, self._footprint)
+
+    def render_views(self, pose: CameraPose, out_dims, out: torch.Tensor | None = None,
+                     check: bool = True) -> torch.Tensor:
+        """Perspective writeout (K4) of the current canvas: one view, or one
+        per eye for top-bottom stereo.  Returns
+        (views, out_h, out_w, C) u8 on the device."""
+        h = self.header
+        out_w, out_h = out_dims
+        eyes = [(0, h.height)] if not h.stereo else [(0, h.height // 2),
+                                                     (h.height // 2, h.height // 2)]
+        if out is None:
+            out = torch.empty((len(eyes), out_h, out_w, h.channels), dtype=torch.uint8,
+                              device=self.device)
+        with torch.cuda.stream(self.stream):
+            self._uncovered.zero_()
+            views = [view_args(self._canvas, self._footprint, r0, rows, h.width, h.channels,
+                               pose, out[i], self._uncovered) for i, (r0, rows) in enumerate(eyes)]
+            launch_views(views, self.stream)
+        if check:
+            self.stream.synchronize()
+            missing = int(self._uncovered.item())
+            if missing:
+                raise CoverageError(f"{missing} output pixels sample outside the footprint")
+        return out
+
+    def plane(self) -> torch.Tensor:
+        """K2 output (C, H, W) float32 of the last decode (parity tests)."""
+        ptr = C.c_void_p()
+        N.check(self._lib.wv_plane_view(C.byref(self._geom), C.c_void_p(self._ws.data_ptr()),
+                                        C.byref(ptr)), "wv_plane_view")
+        h = self.header
+        off = ptr.value - self._ws.data_ptr()
+        n = h.channels * h.height * h.width
+        return self._ws[off: off + 4 * n].view(torch.float32).view(h.channels, h.height, h.width)
+
+    # -- prefetch (decoding.py:335-354) -------------------------------------------
+
+    def advance(self, current_frame: int, next_mask: np.ndarray) -> None:
+        """Read the next inter-frame set in the background; its payload goes
+        to HBM and its blocks for ``next_mask`` are accounted in the cache."""
+        set_index = current_frame // self.header.inter_size + 1
+        if set_index >= self.header.num_sets:
+            return
+        mask = self._check_mask(next_mask)
+        self.join_prefetch()
+        job = {"set": set_index, "mask": mask, "host": None}
+
+        def work():
+            if set_index not in self._resident:
+                job["host"] = self._read_payload(set_index)
+
+        self._prefetch_job = job
+        self._prefetch_thread = threading.Thread(target=work, daemon=True)
+        self._prefetch_thread.start()
+
+    def join_prefetch(self):
+        if self._prefetch_thread is not None:
+            self._prefetch_thread.join()
+            self._prefetch_thread = None
+        job, self._prefetch_job = self._prefetch_job, None
+        if job is not None:
+            si = job["set"]
+            self._make_resident(si, job["host"])
+            # the set's first frame is always a real frame (pad < inter_size)
+            p = self._launch(si * self.header.inter_size, "viewport", job["mask"],
+                             account_only=True)
+            self._settle_until(p)
