@@ -1,0 +1,498 @@
+#!/usr/bin/env python
+"""Headline benchmark: 8192x8192 stereo 360-degree viewport decode on B200.
+
+Workload (BASELINE.json configs[2]): a synthetic
+8192x8192x3 top-bottom stereo clip (make_synthetic_clip restated for HxW),
+encoded with the reference encoder's algorithm (package torch encoder,
+alpha 0.1, beta 0.005, n 4, 32-px blocks, 6 levels, 256x256 mask grid,
+120 fps header).  One step = one display frame: stereo viewport mask of the
+circle-trajectory pose (90x90 FOV) -> K1 select -> K2 dequant+temporal ->
+K3 6-level synthesis into the u8 canvas -> K4 per-eye perspective
+writeout to 2000x2000.  Inputs are resident in HBM; L2 is flushed (256 MiB
+write) before every timed step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N>1 runs under torchrun: sets are sharded round-robin over ranks (weak
+scaling), and every step gathers each rank's two eye images to rank 0 over
+NCCL (the display GPU), the path's only exchange.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("decoded frames/s (Mpixel/s) for 8K×8K stereo 360° viewport decode "
+          "at 1/2/4/8 B200")
+OUT_W = OUT_H = 2000
+FPS = 120.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--size", type=int, default=8192, help="frame width = height")
+    ap.add_argument("--sets", type=int, default=0, help="inter-frame sets (default max(2, N))")
+    ap.add_argument("--mode", choices=["viewport", "foveated", "full"], default="viewport")
+    ap.add_argument("--cache-dir", default="/tmp/wvb200_bench")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="a few decodes for ncu; prints nothing")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ inputs
+
+def input_path(args, n_sets: int) -> str:
+    return os.path.join(args.cache_dir, f"c3_{args.size}_s{n_sets}_v1.wvv")
+
+
+def make_input(path: str, size: int, n_sets: int, device) -> None:
+    """Encode the synthetic stereo clip once (not timed)."""
+    import torch
+    from paper_2208_10859_b200.encoding import EncodeParams, MappingKind, encode_video
+    from paper_2208_10859_b200.fileio import write_video
+    from paper_2208_10859_b200.synthetic import make_synthetic_clip_torch
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    frames = 4 * n_sets
+    params = EncodeParams(alpha=0.1, inter_threshold=0.005, inter_size=4, block_size=32,
+                          mapping=MappingKind.EQUIRECTANGULAR, stereo=True, fps=FPS,
+                          mask_w=256, mask_h=256)
+    sets = []
+    video = None
+    for si in range(n_sets):
+        clip = make_synthetic_clip_torch(4, size, size, 3, seed=7, device=device,
+                                         first_frame=4 * si, total_frames=frames)
+        v = encode_video(clip, params, device=device, keep_arrays=False)
+        sets.extend(v.sets)
+        video = v
+        del clip
+        if torch.cuda.is_available():
+            torch.cuda.empty_cache()
+    video.sets = sets
+    video.frame_count = frames
+    video.pad_frames = 0
+    tmp = path + f".tmp{os.getpid()}"
+    write_video(video, tmp)
+    os.replace(tmp, path)
+
+
+def poses_and_masks(header, frames):
+    from paper_2208_10859_b200.projection import CameraPose, stereo_mask
+    from paper_2208_10859_b200.synthetic import circle_trajectory
+    traj = circle_trajectory()
+    out = {}
+    for f in frames:
+        _, yaw, pitch, roll, gu, gv = traj.sample_at(f * 1000.0 / header.fps)
+        pose = CameraPose(yaw=float(yaw), pitch=float(pitch), roll=float(roll), fov_h=90, fov_v=90)
+        mask = (stereo_mask(pose, (header.mask_w, header.mask_h)) if header.stereo else None)
+        out[f] = (pose, mask, (float(gu), float(gv)))
+    return out
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+        else:
+            self.lines = []
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ ours
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_k3_final_r01.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
+    except (OSError, ValueError):
+        return None, None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2208_10859_b200 as wv
+    from paper_2208_10859_b200 import build
+    from paper_2208_10859_b200.decoding import FoveationSchedule
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
+    n_sets = args.sets or max(2, world)
+    path = input_path(args, n_sets)
+    if rank == 0 and not os.path.exists(path):
+        make_input(path, args.size, n_sets, dev)
+    if world > 1:
+        dist.barrier()
+
+    sess = wv.DecodeSession(path, device=dev, max_resident_sets=n_sets + 1)
+    sess.time_stages = False
+    h = sess.header
+    my_sets = [s for s in range(h.num_sets) if s % world == rank] or [rank % h.num_sets]
+    frames = [s * h.inter_size + t for s in my_sets for t in range(h.inter_size)
+              if s * h.inter_size + t < h.frame_count]
+    pm = poses_and_masks(h, frames)
+    views = 2 if h.stereo else 1
+    out = torch.empty((views, OUT_H, OUT_W, h.channels), dtype=torch.uint8, device=dev)
+    gather_buf = ([torch.empty_like(out) for _ in range(world)] if (world > 1 and rank == 0)
+                  else None)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = sess.stream
+
+    def step(i):
+        f = frames[i % len(frames)]
+        pose, mask, gaze = pm[f]
+        if args.mode == "full":
+            sess.decode_full_device(f)
+        elif args.mode == "foveated":
+            sess.decode_foveated_device(f, mask, FoveationSchedule.default(h.levels, *gaze))
+        else:
+            sess.decode_viewport_device(f, mask)
+        if args.mode != "full":
+            sess.render_views(pose, (OUT_W, OUT_H), out=out, check=False)
+
+    def gather():
+        if world > 1:
+            with torch.cuda.stream(stream):
+                dist.gather(out, gather_buf if rank == 0 else None, dst=0)
+
+    # make every set resident and warm up
+    for s in my_sets:
+        sess._make_resident(s)
+    for i in range(args.warmup):
+        step(i)
+        gather()
+    stream.synchronize()
+    sess._settle_until(None)
+    if args.profile_only:
+        return
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            ev[i][0].record(stream)
+            step(args.warmup + i)
+            gather()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    sess._settle_until(None)
+    unc = int(sess._uncovered.item())
+
+    # per-kernel timing pass (events on the launching stream), L2 flushed
+    sess.kernel_timing = True
+    sess.kernel_events = []
+    frames_out = []
+    R = max(5, min(20, args.steps))
+    for i in range(R):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        f = frames[i % len(frames)]
+        pose, mask, gaze = pm[f]
+        if args.mode == "full":
+            frames_out.append(sess.decode_full_device(f))
+        elif args.mode == "foveated":
+            frames_out.append(sess.decode_foveated_device(f, mask, FoveationSchedule.default(h.levels, *gaze)))
+        else:
+            frames_out.append(sess.decode_viewport_device(f, mask))
+        if args.mode != "full":
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sess.render_views(pose, (OUT_W, OUT_H), out=out, check=False)
+            e1.record(stream)
+            sess.kernel_events[-1].extend([e0, e1])
+    torch.cuda.synchronize()
+    sess.kernel_timing = False
+    ks = sess.kernel_events
+    mean = lambda xs: sum(xs) / len(xs)
+    k1 = mean([e[0].elapsed_time(e[1]) for e in ks])
+    k2 = mean([e[1].elapsed_time(e[2]) for e in ks])
+    k3m = mean([e[2].elapsed_time(e[3]) for e in ks])
+    k3f = mean([e[3].elapsed_time(e[4]) for e in ks])
+    k4 = mean([e[5].elapsed_time(e[6]) for e in ks]) if args.mode != "full" else 0.0
+    tiles = mean([fo.result().n_tiles for fo in frames_out])
+    sel_blocks = mean([fo.result().n_selected for fo in frames_out])
+    C = h.channels
+    # K3 finest level, per launch: read 4 subband tiles (32x32 f32 each per
+    # channel) and write a 64x64 u8 tile per channel (SURVEY §8d K3+K4 terms)
+    alg = tiles * (4 * 32 * 32 * 4 * C + 64 * 64 * C)
+    peak, peak_kind = peaks()
+    achieved = alg / (k3f * 1e-3) / 1e9
+    traffic, _ = ncu_traffic()
+
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pinned = {s: sess.pinned_payload(s) for s in my_sets}
+        host_out = torch.empty(out.shape, dtype=torch.uint8).pin_memory()
+        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        bi = bo = 0
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            f = frames[i % len(frames)]
+            s = f // h.inter_size
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            eev[i][0].record(stream)
+            sess.upload_set(s, pinned[s])
+            step(i)
+            gather()
+            with torch.cuda.stream(stream):
+                host_out.copy_(out, non_blocking=True)
+            eev[i][1].record(stream)
+            bi += pinned[s].numel() + h.mask_w * h.mask_h
+            bo += host_out.numel()
+        torch.cuda.synchronize()
+        e2e_ms = sum(a.elapsed_time(b) for a, b in eev)
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * args.steps / (float(te.item()) / 1000.0), "unit": "frames/s",
+               "h2d_bytes_per_step": bi // args.steps, "d2h_bytes_per_step": bo // args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(path, frames[0], pm[frames[0]], args.mode)
+
+    if rank == 0:
+        fps = world * args.steps / (max_ms / 1000.0)
+        out_px = views * OUT_W * OUT_H if args.mode != "full" else h.width * h.height
+        line = {
+            "metric": METRIC,
+            "value": round(fps, 2),
+            "unit": "frames/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(max_ms / args.steps, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (make_synthetic_clip HxW, encoded by the package encoder = reference algorithm)",
+            "config": {
+                "workload": (f"C3 {h.width}x{h.height} stereo 360 {args.mode} decode + per-eye "
+                             f"{OUT_W}x{OUT_H} perspective writeout, 90x90 FOV, circle trajectory"
+                             if args.mode != "full" else f"{h.width}x{h.height} full-frame decode"),
+                "levels": h.levels, "inter_size": h.inter_size, "block_size": h.block_size,
+                "mask": f"{h.mask_w}x{h.mask_h}", "alpha": 0.1, "inter_threshold": 0.005,
+                "sets": h.num_sets, "frames": h.frame_count, "sets_per_rank": len(my_sets),
+                "l2": "flushed before every timed step (256 MiB write, outside the events)",
+                "parallelism": f"sets round-robin over {world} GPU(s), eye images gathered to rank 0",
+            },
+            "mpix_per_s": round(fps * out_px / 1e6, 1),
+            "roofline": {"bound": "hbm", "kernel": "k_level<FINAL> (K3 finest level + u8 writeout)",
+                         "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "algorithmic_bytes_per_launch": int(alg),
+                         "launch_ms": round(k3f, 4)},
+            "stage_ms": {"k1_select": round(k1, 4), "k2_dequant_temporal": round(k2, 4),
+                         "k3_levels_L_to_2": round(k3m, 4), "k3_level1_final": round(k3f, 4),
+                         "k4_perspective": round(k4, 4)},
+            "selected_blocks": sel_blocks, "level1_tiles": tiles,
+            "uncovered_pixels": unc,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            # per frame: K1 2L+4 (mask rows, L cascades, L footprint, blocks,
+            # tiles, finalize) + K2 1 + K3 L + K4 1 (not in full mode)
+            "gpu_launches": args.steps * (3 * h.levels + 5 + (1 if args.mode != "full" else 0)),
+        }
+        print(json.dumps(line), flush=True)
+    sess.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------- CPU (oracle) legs
+
+def _oracle_frame(path, frame, pose_t, mask, mode):
+    """One display frame through the CPU oracle (decode + per-eye render)."""
+    from oracle import wavevid_oracle as wo
+    sess = wo.OracleSession(path)
+    h = sess.header
+    t0 = time.perf_counter()
+    kind = {"viewport": "viewport", "foveated": "foveated", "full": "full"}[mode]
+    pix, fp, _ = sess.decode(frame, kind, None if mode == "full" else mask)
+    if mode != "full":
+        yaw, pitch, roll = pose_t
+        rot = wo.pose_rotation(yaw, pitch, roll)
+        half = h.height // 2 if h.stereo else h.height
+        for e in range(2 if h.stereo else 1):
+            wo.perspective(pix[e * half:(e + 1) * half], fp[e * half:(e + 1) * half], rot,
+                           90.0, 90.0, OUT_W, OUT_H)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_sample(path, frame, pm_entry, mode):
+    pose, mask, _ = pm_entry
+    el = _oracle_frame(path, frame, (pose.yaw, pose.pitch, pose.roll), mask, mode)
+    return {"value": round(1.0 / el, 4), "unit": "frames/s", "cores": 1, "kind": "port",
+            "sample": (f"1 display frame ({mode} decode of frame {frame} + "
+                       f"{'2 eye' if mode != 'full' else 'no'} {OUT_W}x{OUT_H} renders), "
+                       f"numpy oracle, single process, {el:.1f} s")}
+
+
+def _worker(a):
+    path, frame, pose_t, mask, mode = a
+    return _oracle_frame(path, frame, pose_t, mask, mode)
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU algorithm (oracle port; the
+    reference package is Python and cannot be compiled) on the host cores,
+    frames decoded in parallel worker processes."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    import numpy as np
+    n_sets = args.sets or max(2, world)
+    path = input_path(args, n_sets)
+    if not os.path.exists(path):
+        import torch
+        make_input(path, args.size, n_sets,
+                   torch.device("cuda", 0) if torch.cuda.is_available() else "cpu")
+    from paper_2208_10859_b200.fileio import read_header
+    h, _ = read_header(path)
+    frames = list(range(h.frame_count))
+    pm = poses_and_masks(h, frames)
+    cores = len(os.sched_getaffinity(0))
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 16 << 30
+    per = 7 << 30 if args.size >= 8192 else max(1 << 28, (args.size * args.size * 100))
+    procs = max(1, min(cores, int(avail // per), args.steps))
+    jobs = [(path, f, (pm[f][0].yaw, pm[f][0].pitch, pm[f][0].roll), pm[f][1], args.mode)
+            for f in frames]
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs) as pool:
+        wj = [jobs[i % len(jobs)] for i in range(max(1, min(args.warmup, procs)))]
+        pool.map(_worker, wj)
+        tj = [jobs[i % len(jobs)] for i in range(args.steps)]
+        t0 = time.perf_counter()
+        pool.map(_worker, tj, chunksize=1)
+        wall = time.perf_counter() - t0
+    fps = args.steps / wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(fps, 4), "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(wall * 1000.0 / args.steps, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"C3 {h.width}x{h.height} stereo 360 {args.mode} decode + per-eye "
+                               f"{OUT_W}x{OUT_H} perspective writeout (CPU oracle port)",
+                   "frames": h.frame_count},
+        "cpu_baseline": {"value": round(fps, 4), "unit": "frames/s", "cores": procs,
+                         "kind": "port",
+                         "sample": f"{args.steps} display frames over {procs} worker processes "
+                                   f"(numpy oracle of the reference decode + render)"},
+        "e2e": {"value": round(fps, 4), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

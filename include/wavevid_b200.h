@@ -127,6 +127,10 @@ int wv_select(const wv_geometry* g, const wv_frame_args* a, void* d_workspace, v
 int wv_dequant_temporal(const wv_geometry* g, const wv_frame_args* a, void* d_workspace, void* stream);
 int wv_synthesize(const wv_geometry* g, const wv_frame_args* a, void* d_workspace, void* stream);
 int wv_decode_frame(const wv_geometry* g, const wv_frame_args* a, void* d_workspace, void* stream);
+/* One synthesis level k (1 = finest, writes the u8 canvas) of wv_synthesize;
+ * levels must run L..1 after wv_select/wv_dequant_temporal (timing, profiling). */
+int wv_synthesize_level(const wv_geometry* g, const wv_frame_args* a, void* d_workspace,
+                        int level, void* stream);
 
 int wv_render_perspective(const wv_view_args* views, int n_views, void* stream);
 

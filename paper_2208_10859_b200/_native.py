@@ -19,6 +19,7 @@ WV_MAX_LEVELS = 12
 
 EXPORTS = ["wv_abi_version", "wv_status_string", "wv_workspace_bytes", "wv_workspace_reset",
            "wv_select", "wv_dequant_temporal", "wv_synthesize", "wv_decode_frame",
+           "wv_synthesize_level",
            "wv_render_perspective", "wv_plane_view", "wv_level_mask_view",
            "wv_block_list_view"]
 
@@ -76,6 +77,7 @@ def load(path: str = LIB_PATH):
     lib.wv_workspace_reset.argtypes = [G, C.c_void_p, C.c_void_p]
     for fn in ("wv_select", "wv_dequant_temporal", "wv_synthesize", "wv_decode_frame"):
         getattr(lib, fn).argtypes = [G, A, C.c_void_p, C.c_void_p]
+    lib.wv_synthesize_level.argtypes = [G, A, C.c_void_p, C.c_int, C.c_void_p]
     lib.wv_render_perspective.argtypes = [V, C.c_int, C.c_void_p]
     lib.wv_plane_view.argtypes = [G, C.c_void_p, C.POINTER(C.c_void_p)]
     lib.wv_level_mask_view.argtypes = [G, C.c_void_p, C.c_int, C.POINTER(C.c_void_p),

@@ -91,6 +91,15 @@ int wv_decode_frame(const wv_geometry* g, const wv_frame_args* a, void* ws, void
   return launch_synthesis(lo, g, a, (uint8_t*)ws, s);
 }
 
+int wv_synthesize_level(const wv_geometry* g, const wv_frame_args* a, void* ws, int level,
+                        void* stream) {
+  Layout lo;
+  int st = check(g, a, &lo);
+  if (st != WV_OK) return st;
+  if (!ws || level < 1 || level > lo.L) return WV_ERR_ARG;
+  return launch_synthesis(lo, g, a, (uint8_t*)ws, (cudaStream_t)stream, level);
+}
+
 int wv_render_perspective(const wv_view_args* views, int n_views, void* stream) {
   if (!views) return WV_ERR_ARG;
   return launch_perspective(views, n_views, (cudaStream_t)stream);

@@ -107,7 +107,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
 int launch_temporal(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
                     cudaStream_t s);
 int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
-                     cudaStream_t s);
+                     cudaStream_t s, int only_level = 0);
 int launch_perspective(const wv_view_args* v, int n, cudaStream_t s);
 
 }  // namespace wv

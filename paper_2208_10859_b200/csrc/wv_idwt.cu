@@ -346,7 +346,7 @@ int make_map(CUtensorMap* m, const float* base, int cols, int rows, int pitch, i
 }  // namespace
 
 int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
-                     cudaStream_t s) {
+                     cudaStream_t s, int only_level) {
   (void)g;
   const int L = lo.L, C = lo.C;
   float* plane = (float*)(ws + lo.plane);
@@ -366,6 +366,7 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
   CUtensorMap tm_plane;
   if (make_map(&tm_plane, plane, lo.W, lo.H, lo.W, C) != WV_OK) return WV_ERR_CUDA;
   for (int k = L; k >= 1; --k) {
+    if (only_level && k != only_level) continue;
     CUtensorMap tm_ll = tm_plane;
     if (k < L) {
       if (make_map(&tm_ll, (const float*)(ws + lo.ybuf[k]), lo.W >> k, lo.H >> k, lo.ypitch[k],

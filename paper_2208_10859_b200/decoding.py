@@ -138,10 +138,11 @@ class _Entry:
 
 class _Pending:
     __slots__ = ("slot", "set_index", "entry", "existed", "may_evict", "event", "ev",
-                 "account_only", "stats")
+                 "account_only", "stats", "raw")
 
     def __init__(self):
         self.stats = None
+        self.raw = None
 
 
 class DeviceFrame:
@@ -158,6 +159,11 @@ class DeviceFrame:
     def stats(self) -> DecodeStats:
         self._session._settle_until(self._pending)
         return self._pending.stats
+
+    def result(self) -> N.FrameResult:
+        """Raw device result (tile/block counts) after settling."""
+        self._session._settle_until(self._pending)
+        return self._pending.raw
 
 
 _RESULT_BYTES = C.sizeof(N.FrameResult)
@@ -209,6 +215,8 @@ class DecodeSession:
         self._prefetch_thread: threading.Thread | None = None
         self._prefetch_job = None
         self.time_stages = True
+        self.kernel_timing = False
+        self.kernel_events: list = []
 
     # -- lifecycle ------------------------------------------------------------
 
@@ -238,6 +246,17 @@ class DecodeSession:
             self.reader.read_set_payload(set_index, memoryview(host.numpy()))
         return host
 
+    def pinned_payload(self, set_index: int) -> torch.Tensor:
+        """The set's payload (BlockEnd table + records) read into pinned host
+        memory, for callers that stream sets themselves (upload_set)."""
+        return self._read_payload(set_index)
+
+    def upload_set(self, set_index: int, host: torch.Tensor) -> None:
+        """Copy a set payload from (pinned) host memory to HBM on the session
+        stream, replacing any resident copy (end-to-end host-buffer path)."""
+        self._resident.pop(set_index, None)
+        self._make_resident(set_index, host)
+
     def _make_resident(self, set_index: int, host: torch.Tensor | None = None):
         if set_index in self._resident:
             self._resident.move_to_end(set_index)
@@ -245,12 +264,13 @@ class DecodeSession:
         if host is None:
             host = self._read_payload(set_index)
         meta = self.reader.set_meta[set_index]
+        ext_host = torch.from_numpy(np.ascontiguousarray(meta.extrema, np.float32)).pin_memory()
         with torch.cuda.stream(self.stream):
             dev = torch.empty(host.numel(), dtype=torch.uint8, device=self.device)
             dev.copy_(host, non_blocking=True)
-            ext = torch.from_numpy(np.ascontiguousarray(meta.extrema, np.float32)).to(
-                self.device, non_blocking=False)
-        self._resident[set_index] = (dev, ext, host)
+            ext = torch.empty(ext_host.shape, dtype=torch.float32, device=self.device)
+            ext.copy_(ext_host, non_blocking=True)
+        self._resident[set_index] = (dev, ext, (host, ext_host))
         while len(self._resident) > self._max_resident:
             self._resident.popitem(last=False)
         return self._resident[set_index]
@@ -342,6 +362,23 @@ class DecodeSession:
             evs = None
             if account_only:
                 N.check(self._lib.wv_select(g, C.byref(args), ws, cs), "wv_select")
+            elif self.kernel_timing:
+                # per-kernel CUDA events on this stream: K1, K2, K3 levels L..2, K3 level 1
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+                e[0].record(s)
+                N.check(self._lib.wv_select(g, C.byref(args), ws, cs), "wv_select")
+                e[1].record(s)
+                N.check(self._lib.wv_dequant_temporal(g, C.byref(args), ws, cs),
+                        "wv_dequant_temporal")
+                e[2].record(s)
+                for k in range(self.header.levels, 1, -1):
+                    N.check(self._lib.wv_synthesize_level(g, C.byref(args), ws, k, cs),
+                            "wv_synthesize_level")
+                e[3].record(s)
+                N.check(self._lib.wv_synthesize_level(g, C.byref(args), ws, 1, cs),
+                        "wv_synthesize_level")
+                e[4].record(s)
+                self.kernel_events.append(e)
             elif time_stages:
                 evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 N.check(self._lib.wv_select(g, C.byref(args), ws, cs), "wv_select")
@@ -380,6 +417,7 @@ class DecodeSession:
                 st.temporal_ms = evs[0].elapsed_time(evs[1])
                 st.synthesis_ms = evs[1].elapsed_time(evs[2])
             p.stats = st
+            p.raw = r
             if not p.account_only:
                 self._stats.bytes_loaded += st.bytes_loaded
                 self._stats.records_processed += st.records_processed
