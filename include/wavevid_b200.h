@@ -97,17 +97,18 @@ typedef struct wv_frame_args {
   const float* d_extrema;         /* (n, C, 4) float32 (fileio.py:123) */
   uint32_t* d_set_loaded;         /* NB-bit block bitmap of the set's cache entry */
   unsigned long long* d_set_bytes;/* the entry's cumulative bytes */
-  uint8_t* d_canvas;              /* (H, W, C) u8 output; must persist across calls of one workspace */
+  uint8_t* d_canvas;              /* planar (C, H, W) u8 output; must persist across calls of one workspace */
   uint32_t* d_footprint;          /* (H, ceil(W/32)) bit rows output, bit i of word w = column 32w+i */
   wv_frame_result* d_result;
 } wv_frame_args;
 
 /* One perspective view (projection.py:111-172). */
 typedef struct wv_view_args {
-  const uint8_t* d_canvas;        /* (canvas_h, W, C) u8 */
+  const uint8_t* d_canvas;        /* planar (C, canvas_h, W) u8 */
   const uint32_t* d_footprint;    /* bit rows of the same canvas */
   int32_t row0, rows;             /* equirect region = canvas rows [row0, row0+rows) (a stereo eye) */
   int32_t width, channels;
+  int32_t canvas_h, reserved;
   double rot[9];                  /* world-from-camera rotation, row major (projection.py:39-52) */
   double tan_h, tan_v;            /* tan(fov_h/2), tan(fov_v/2) */
   int32_t out_w, out_h;

@@ -48,6 +48,7 @@ class FrameArgs(C.Structure):
 class ViewArgs(C.Structure):
     _fields_ = [("d_canvas", C.c_void_p), ("d_footprint", C.c_void_p), ("row0", C.c_int32),
                 ("rows", C.c_int32), ("width", C.c_int32), ("channels", C.c_int32),
+                ("canvas_h", C.c_int32), ("reserved", C.c_int32),
                 ("rot", C.c_double * 9), ("tan_h", C.c_double), ("tan_v", C.c_double),
                 ("out_w", C.c_int32), ("out_h", C.c_int32), ("d_out", C.c_void_p),
                 ("d_uncovered", C.c_void_p)]

@@ -31,6 +31,7 @@ struct Layout {
   int mh, mw;
   int wpr_[WV_MAX_LEVELS + 1];           // words per bit row at level j
   uint64_t mrows;                        // mask rows at full width (mh x wpr0)
+  uint64_t rowmap;                       // u32[H]: pixel row -> mask row (fileio.py:434)
   uint64_t stack[WV_MAX_LEVELS + 1];     // level j (1..L): (L+1) masks
   uint64_t stack_stride[WV_MAX_LEVELS + 1];
   uint64_t fp[WV_MAX_LEVELS + 1];        // footprint intermediates, level 1..L-1
@@ -66,6 +67,7 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
   auto take = [&](uint64_t bytes) { uint64_t r = off; off += (bytes + 255) & ~uint64_t(255); return r; };
   for (int j = 0; j <= L; ++j) o->wpr_[j] = wpr(W >> j);
   o->mrows = take(uint64_t(g->mask_h) * o->wpr_[0] * 4);
+  o->rowmap = take(uint64_t(H) * 4);
   for (int j = 1; j <= L; ++j) {
     uint64_t one = uint64_t(H >> j) * o->wpr_[j] * 4;
     one = (one + 255) & ~uint64_t(255);
@@ -80,7 +82,8 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
     o->nty[k] = cdiv(H >> k, TY);
     o->ntx[k] = cdiv(W >> k, TX);
     uint64_t nt = uint64_t(o->nty[k]) * o->ntx[k];
-    o->need[k] = take(nt);
+    // level 1: need bits (rows of tiles); other levels unused
+    o->need[k] = take(k == 1 ? uint64_t(o->nty[1]) * wpr(o->ntx[1]) * 4 : 4);
     o->tlist[k] = take(nt * 4 * (k == 1 ? 2 : 1));
   }
   o->prev_need = take(uint64_t(o->nty[1]) * o->ntx[1]);

@@ -142,16 +142,21 @@ struct LevelArgs {
   int k, bh, bw, C, ntx;
   const uint32_t* list;
   const uint32_t* count;
-  float* out;          // non-final: Y_{k-1} planar
+  float* out;          // non-final: Y_{k-1} planar C x 2bh x out_pitch
   int out_pitch;       // floats
-  uint8_t* canvas;     // final: (H, W, C) u8
-  const uint32_t* R;   // final: requested rows
-  int mh, wpr0;
+  uint8_t* canvas;     // final: planar C x H x W u8
+  const uint32_t* R;   // final: requested-mask rows (mh x wpr0)
+  const uint32_t* rowmap;  // final: pixel row -> mask row
+  int wpr0;
   int use_tma;         // subband widths are 16-byte multiples
   const float* ll_ptr; int ll_pitch, ll_rows;   // LDG fallback sources
   const float* plane; int plane_w, plane_h;
 };
 
+// Items are (tile, channel).  Column pass: 2 segments x BOX_W columns (each
+// segment lifts 16 output row pairs from its own 2-row halo); row pass: 2
+// segments x TY row pairs.  Store pass: coalesced f32 (mid levels) or packed
+// u8 with the request mask applied (finest level).
 template <bool FINAL>
 __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUtensorMap tm_ll,
                                                     const __grid_constant__ CUtensorMap tm_det,
@@ -161,106 +166,103 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   float2* colL = reinterpret_cast<float2*>(smem + 4 * BOX_SLOT);    // [TY][CB_PITCH]
   float2* colH = colL + TY * CB_PITCH;
   float2* outb = reinterpret_cast<float2*>(smem);                   // aliases boxes
-  uint8_t* outu8 = smem + 4 * BOX_SLOT + 2 * TY * CB_PITCH * 8;     // FINAL: [OUT_H][OUT_W*C]
   __shared__ uint64_t bar;
   const float* bLL = box;
   const float* bHL = box + BOX_SLOT / 4;
   const float* bLH = box + 2 * BOX_SLOT / 4;
   const float* bHH = box + 3 * BOX_SLOT / 4;
+  constexpr int SEG = TY / 2;   // == TX / 2
 
   const int tid = threadIdx.x;
   if (tid == 0) mbar_init(&bar, 1);
   __syncthreads();
   uint32_t phase = 0;
   const int C = a.C;
-  const uint32_t ntile = *a.count;
-  const uint32_t nitems = FINAL ? ntile : ntile * C;
+  const uint32_t nitems = *a.count * (uint32_t)C;
   const int H = 2 * a.bh, W = 2 * a.bw;
 
   for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const uint32_t entry = a.list[FINAL ? item : item / C];
+    const uint32_t entry = a.list[item / C];
+    const int c = (int)(item % C);
     const uint32_t tile = entry & ~ZERO_FLAG;
     const int ty = tile / a.ntx, tx = tile % a.ntx;
     const int ay = ty * TY, ax = tx * TX;
     const int by = min(ay + TY, a.bh), bx = min(ax + TX, a.bw);
     const int ny = 2 * (by - ay), nx = 2 * (bx - ax);
     if (FINAL && (entry & ZERO_FLAG)) {
-      // tile left the request: clear what the previous frame wrote there
-      const int rowbytes = nx * C;
-      for (int r = 0; r < ny; ++r) {
-        uint8_t* dst = a.canvas + ((uint64_t)(2 * ay + r) * W + 2 * ax) * C;
-        for (int i = tid; i < rowbytes; i += NTHREADS) dst[i] = 0;
+      // tile left the request: clear what an earlier frame wrote there
+      const int qw = nx >> 2;
+      for (int idx = tid; idx < ny * qw; idx += NTHREADS) {
+        const int r = idx / qw, q = idx % qw;
+        *reinterpret_cast<uint32_t*>(a.canvas + ((uint64_t)c * H + 2 * ay + r) * W + 2 * ax +
+                                     4 * q) = 0u;
       }
       continue;
     }
-    // box origin: TMA faults on negative box coordinates (observed on B200,
-    // driver 580), so tiles at the top/left border start their box at 0
+    // box origin: TMA faults on unaligned/negative innermost coordinates
+    // (observed on B200, driver 580), so x starts at ax-4 clamped to 0
     const int oy = max(ay - HALO, 0), ox = max(ax - XPAD, 0);
-    const int c_first = FINAL ? 0 : (int)(item % C);
-    const int c_last = FINAL ? C : c_first + 1;
-    for (int c = c_first; c < c_last; ++c) {
-      if (a.use_tma) {
-        if (tid == 0) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_expect_tx(&bar, 4u * BOX_FLOATS * 4u);
-          tma_load_3d(box, &tm_ll, ox, oy, c, &bar);
-          tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar);
-          tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar);
-          tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar);
-        }
-        mbar_wait(&bar, phase);
-        phase ^= 1u;
-      } else {
-        // tiny levels whose subband width is not a multiple of 4 floats
-        for (int i = tid; i < 4 * BOX_FLOATS; i += NTHREADS) {
-          const int q = i / BOX_FLOATS, e = i % BOX_FLOATS;
-          const int yy = oy + e / BOX_W, xx = ox + e % BOX_W;
-          float v = 0.0f;
-          if (yy < a.bh && xx < a.bw) {
-            const bool ll = q == 0;
-            const float* src = ll ? a.ll_ptr : a.plane;
-            const int pitch = ll ? a.ll_pitch : a.plane_w;
-            const int rows = ll ? a.ll_rows : a.plane_h;
-            const int gy = yy + ((q >= 2) ? a.bh : 0), gx = xx + ((q & 1) ? a.bw : 0);
-            v = src[((uint64_t)c * rows + gy) * pitch + gx];
-          }
-          box[q * (BOX_SLOT / 4) + e] = v;
-        }
-        __syncthreads();
+    if (a.use_tma) {
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar, 4u * BOX_FLOATS * 4u);
+        tma_load_3d(box, &tm_ll, ox, oy, c, &bar);
+        tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar);
+        tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar);
+        tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar);
       }
-
-      // column pass: one thread per box column, L and H halves packed
-      if (tid < BOX_W) {
-        const int lc = tid;
-        const int cg = ox + lc;
-        if (cg >= max(ax - HALO, 0) && cg < min(bx + HALO, a.bw)) {
-          const int g0 = oy, g1 = min(by + HALO, a.bh);
-          const int rbase = oy;
-          lift_line(
-              g0, g1, a.bh, ay, by,
-              [&](int j, float2& s, float2& d) {
-                const int o = (j - rbase) * BOX_W + lc;
-                s = make_float2(bLL[o], bHL[o]);
-                d = make_float2(bLH[o], bHH[o]);
-              },
-              [&](int p, float2 s3, float2 d3) {
-                const int q = p - ay;
-                colL[q * CB_PITCH + lc] = make_float2(s3.x, d3.x);
-                colH[q * CB_PITCH + lc] = make_float2(s3.y, d3.y);
-              });
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+    } else {
+      // tiny levels whose subband width is not a multiple of 4 floats
+      for (int i = tid; i < 4 * BOX_FLOATS; i += NTHREADS) {
+        const int q = i / BOX_FLOATS, e = i % BOX_FLOATS;
+        const int yy = oy + e / BOX_W, xx = ox + e % BOX_W;
+        float v = 0.0f;
+        if (yy < a.bh && xx < a.bw) {
+          const bool ll = q == 0;
+          const float* src = ll ? a.ll_ptr : a.plane;
+          const int pitch = ll ? a.ll_pitch : a.plane_w;
+          const int rows = ll ? a.ll_rows : a.plane_h;
+          const int gy = yy + ((q >= 2) ? a.bh : 0), gx = xx + ((q & 1) ? a.bw : 0);
+          v = src[((uint64_t)c * rows + gy) * pitch + gx];
         }
+        box[q * (BOX_SLOT / 4) + e] = v;
       }
       __syncthreads();
-      // row pass: one thread per output row pair
-      if (tid < by - ay) {
-        const int i = tid;
-        const int g0 = max(ax - HALO, 0), g1 = min(bx + HALO, a.bw);
-        const int cbase = ox;
+    }
+
+    // column pass: (segment, box column) per thread, L and H halves packed
+    if (tid < 2 * BOX_W) {
+      const int lc = tid % BOX_W, sg = tid / BOX_W;
+      const int cg = ox + lc;
+      const int pa = ay + sg * SEG, pb = sg ? by : min(ay + SEG, by);
+      if (pa < pb && cg >= max(ax - HALO, 0) && cg < min(bx + HALO, a.bw)) {
         lift_line(
-            g0, g1, a.bw, ax, bx,
+            max(pa - HALO, 0), min(pb + HALO, a.bh), a.bh, pa, pb,
             [&](int j, float2& s, float2& d) {
-              s = colL[i * CB_PITCH + (j - cbase)];
-              d = colH[i * CB_PITCH + (j - cbase)];
+              const int o = (j - oy) * BOX_W + lc;
+              s = make_float2(bLL[o], bHL[o]);
+              d = make_float2(bLH[o], bHH[o]);
+            },
+            [&](int p, float2 s3, float2 d3) {
+              const int q = p - ay;
+              colL[q * CB_PITCH + lc] = make_float2(s3.x, d3.x);
+              colH[q * CB_PITCH + lc] = make_float2(s3.y, d3.y);
+            });
+      }
+    }
+    __syncthreads();
+    // row pass: (segment, output row pair) per thread, two rows packed
+    if (tid < 2 * TY) {
+      const int i = tid % TY, sg = tid / TY;
+      const int pa = ax + sg * SEG, pb = sg ? bx : min(ax + SEG, bx);
+      if (i < by - ay && pa < pb) {
+        lift_line(
+            max(pa - HALO, 0), min(pb + HALO, a.bw), a.bw, pa, pb,
+            [&](int j, float2& s, float2& d) {
+              s = colL[i * CB_PITCH + (j - ox)];
+              d = colH[i * CB_PITCH + (j - ox)];
             },
             [&](int p, float2 s3, float2 d3) {
               const int q = p - ax;
@@ -268,56 +270,44 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
               outb[i * OB_PITCH + 2 * q + 1] = d3;
             });
       }
-      __syncthreads();
-      if (!FINAL) {
-        float* base = a.out + ((uint64_t)c * H + 2 * ay) * a.out_pitch + 2 * ax;
-        const int half = nx >> 1;   // float2 columns per row
-        for (int idx = tid; idx < (ny >> 1) * half; idx += NTHREADS) {
-          const int i = idx / half, x2 = idx % half;
-          float2 u = outb[i * OB_PITCH + 2 * x2];
-          float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
-          float* r0 = base + (uint64_t)(2 * i) * a.out_pitch + 2 * x2;
-          *reinterpret_cast<float2*>(r0) = make_float2(u.x, v.x);
-          *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
-        }
-      } else {
-        for (int idx = tid; idx < (ny >> 1) * nx; idx += NTHREADS) {
-          const int i = idx / nx, x = idx % nx;
-          const float2 u = outb[i * OB_PITCH + x];
-          const int gx = 2 * ax + x;
+    }
+    __syncthreads();
+    if (!FINAL) {
+      float* base = a.out + ((uint64_t)c * H + 2 * ay) * a.out_pitch + 2 * ax;
+      const int half = nx >> 1;   // float2 columns per row
+      for (int idx = tid; idx < (ny >> 1) * half; idx += NTHREADS) {
+        const int i = idx / half, x2 = idx % half;
+        const float2 u = outb[i * OB_PITCH + 2 * x2];
+        const float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
+        float* r0 = base + (uint64_t)(2 * i) * a.out_pitch + 2 * x2;
+        *reinterpret_cast<float2*>(r0) = make_float2(u.x, v.x);
+        *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
+      }
+    } else {
+      // clip(rint(x*255)) (decoding.py:301), zero outside the request
+      const int qw = nx >> 2;     // 4-pixel groups per row
+      for (int idx = tid; idx < (ny >> 1) * qw; idx += NTHREADS) {
+        const int i = idx / qw, q = idx % qw;
+        const int gx = 2 * ax + 4 * q;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int gy = 2 * ay + 2 * i + h;
-            const uint32_t rw =
-                a.R[(uint64_t)((long long)gy * a.mh / H) * a.wpr0 + (gx >> 5)];
-            float v = h ? u.y : u.x;
-            float q = rintf(__fmul_rn(v, 255.0f));
-            q = fminf(fmaxf(q, 0.0f), 255.0f);
-            uint8_t o = ((rw >> (gx & 31)) & 1u) ? (uint8_t)q : (uint8_t)0;
-            outu8[(2 * i + h) * (OUT_W * C) + x * C + c] = o;
+        for (int h = 0; h < 2; ++h) {
+          const int gy = 2 * ay + 2 * i + h;
+          const uint32_t rbits =
+              (a.R[(uint64_t)a.rowmap[gy] * a.wpr0 + (gx >> 5)] >> (gx & 31)) & 0xFu;
+          uint32_t word = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 u = outb[i * OB_PITCH + 4 * q + e];
+            float v = rintf(__fmul_rn(h ? u.y : u.x, 255.0f));
+            v = fminf(fmaxf(v, 0.0f), 255.0f);
+            const uint32_t b = ((rbits >> e) & 1u) ? (uint32_t)v : 0u;
+            word |= b << (8 * e);
           }
+          *reinterpret_cast<uint32_t*>(a.canvas + ((uint64_t)c * H + gy) * W + gx) = word;
         }
       }
-      __syncthreads();
     }
-    if (FINAL) {
-      const int rowbytes = nx * C;
-      if (((W * C) & 3) == 0 && ((2 * ax * C) & 3) == 0 && (rowbytes & 3) == 0) {
-        const int rw = rowbytes >> 2;
-        for (int idx = tid; idx < ny * rw; idx += NTHREADS) {
-          const int r = idx / rw, w = idx % rw;
-          uint32_t* dst = reinterpret_cast<uint32_t*>(a.canvas +
-                                                      ((uint64_t)(2 * ay + r) * W + 2 * ax) * C);
-          dst[w] = reinterpret_cast<const uint32_t*>(outu8 + r * (OUT_W * C))[w];
-        }
-      } else {
-        for (int idx = tid; idx < ny * rowbytes; idx += NTHREADS) {
-          const int r = idx / rowbytes, w = idx % rowbytes;
-          a.canvas[((uint64_t)(2 * ay + r) * W + 2 * ax) * C + w] = outu8[r * (OUT_W * C) + w];
-        }
-      }
-      __syncthreads();
-    }
+    __syncthreads();
   }
 }
 
@@ -355,7 +345,7 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem_mid = 4 * BOX_SLOT + 2 * TY * CB_PITCH * 8;
-  const size_t smem_fin = smem_mid + (size_t)OUT_H * OUT_W * 4;
+  const size_t smem_fin = smem_mid;
   WV_CUDA(cudaFuncSetAttribute(k_level<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem_mid));
   WV_CUDA(cudaFuncSetAttribute(k_level<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -391,9 +381,9 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
     } else {
       la.canvas = a->d_canvas;
       la.R = (const uint32_t*)(ws + lo.mrows);
-      la.mh = lo.mh;
+      la.rowmap = (const uint32_t*)(ws + lo.rowmap);
       la.wpr0 = lo.wpr_[0];
-      int grid = max(1, min(ntiles, sms * occ_fin));
+      int grid = max(1, min(ntiles * C, sms * occ_fin));
       k_level<true><<<grid, NTHREADS, smem_fin, s>>>(tm_ll, tm_plane, la);
     }
     WV_CUDA(cudaGetLastError());

@@ -44,28 +44,30 @@ __global__ void k_perspective(const __grid_constant__ Views views) {
     const double fx = __dsub_rn(__dmul_rn(__ddiv_rn(__dadd_rn(lon, 180.0), 360.0), (double)n), 0.5);
     const double fy = __dsub_rn(__dmul_rn(__ddiv_rn(__dsub_rn(90.0, lat), 180.0), (double)m), 0.5);
     const double flx = floor(fx), fly = floor(fy);
-    const long long x0 = (long long)flx, y0 = (long long)fly;
+    const int x0 = (int)flx, y0 = (int)fly;
     const float ax = (float)__dsub_rn(fx, flx);
     const float ay = (float)__dsub_rn(fy, fly);
-    long long xa = x0 % n; if (xa < 0) xa += n;
-    long long xb = (x0 + 1) % n; if (xb < 0) xb += n;
-    const int ya = (int)min(max(y0, 0ll), (long long)(m - 1));
-    const int yb = (int)min(max(y0 + 1, 0ll), (long long)(m - 1));
+    // fx lies in [-0.5, n - 0.5]: x0 in [-1, n-1]; wrap without division
+    const int xa = x0 < 0 ? x0 + n : (x0 >= n ? x0 - n : x0);
+    const int xb = x0 + 1 >= n ? x0 + 1 - n : (x0 + 1 < 0 ? x0 + 1 + n : x0 + 1);
+    const int ya = min(max(y0, 0), m - 1);
+    const int yb = min(max(y0 + 1, 0), m - 1);
     const int wpr0 = (n + 31) >> 5;
     const uint32_t* F = v.d_footprint + (uint64_t)v.row0 * wpr0;
-    auto fp = [&](int yy, long long xx) {
+    auto fp = [&](int yy, int xx) {
       return (F[(uint64_t)yy * wpr0 + (xx >> 5)] >> (xx & 31)) & 1u;
     };
     uncovered = !(fp(ya, xa) & fp(ya, xb) & fp(yb, xa) & fp(yb, xb));
     const int C = v.channels;
-    const uint8_t* img = v.d_canvas + (uint64_t)v.row0 * n * C;
+    const uint64_t plane = (uint64_t)v.canvas_h * n;
+    const uint8_t* img = v.d_canvas + (uint64_t)v.row0 * n;
     const float one_x = __fsub_rn(1.0f, ax), one_y = __fsub_rn(1.0f, ay);
     uint8_t* out = v.d_out + ((uint64_t)y * v.out_w + x) * C;
+    const uint64_t o00 = (uint64_t)ya * n + xa, o01 = (uint64_t)ya * n + xb;
+    const uint64_t o10 = (uint64_t)yb * n + xa, o11 = (uint64_t)yb * n + xb;
     for (int c = 0; c < C; ++c) {
-      const float p00 = img[((uint64_t)ya * n + xa) * C + c];
-      const float p01 = img[((uint64_t)ya * n + xb) * C + c];
-      const float p10 = img[((uint64_t)yb * n + xa) * C + c];
-      const float p11 = img[((uint64_t)yb * n + xb) * C + c];
+      const uint8_t* pc = img + c * plane;
+      const float p00 = pc[o00], p01 = pc[o01], p10 = pc[o10], p11 = pc[o11];
       const float top = __fadd_rn(__fmul_rn(p00, one_x), __fmul_rn(p01, ax));
       const float bot = __fadd_rn(__fmul_rn(p10, one_x), __fmul_rn(p11, ax));
       float o = rintf(__fadd_rn(__fmul_rn(top, one_y), __fmul_rn(bot, ay)));
@@ -86,7 +88,8 @@ int launch_perspective(const wv_view_args* views, int n, cudaStream_t s) {
   for (int i = 0; i < n; ++i) {
     const wv_view_args& v = views[i];
     if (!v.d_canvas || !v.d_footprint || !v.d_out || !v.d_uncovered || v.out_w < 1 ||
-        v.out_h < 1 || v.channels < 1 || v.width < 1 || v.rows < 1)
+        v.out_h < 1 || v.channels < 1 || v.width < 1 || v.rows < 1 ||
+        v.canvas_h < v.row0 + v.rows)
       return WV_ERR_ARG;
     pv.v[i] = v;
     mw = max(mw, v.out_w);

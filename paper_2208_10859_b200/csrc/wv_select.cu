@@ -69,22 +69,31 @@ __device__ __forceinline__ uint32_t shrink(uint32_t p, uint32_t c, uint32_t n) {
 }
 
 // ---------------------------------------------------------------- mask rows
-__global__ void k_mask_rows(const uint8_t* __restrict__ mask, uint32_t* __restrict__ R, int mh,
-                            int mw, int W, int wpr0, int full) {
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+// Distinct pixel-mask rows R[my] (nearest column map, fileio.py:435) and the
+// row map rowmap[y] = (y*mh)/H (fileio.py:434).
+__global__ void k_mask_rows(const uint8_t* __restrict__ mask, uint32_t* __restrict__ R,
+                            uint32_t* __restrict__ rowmap, int mh, int mw, int W, int H, int wpr0,
+                            int full) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < H) rowmap[idx] = (uint32_t)(((uint64_t)idx * mh) / H);
   if (idx >= mh * wpr0) return;
-  int my = idx / wpr0, w = idx % wpr0;
+  const int my = idx / wpr0, w = idx % wpr0;
   uint32_t bits = 0;
   for (int i = 0; i < 32; ++i) {
-    int x = 32 * w + i;
+    const int x = 32 * w + i;
     if (x >= W) break;
-    int mx = (int)(((long long)x * mw) / W);
-    if (full || mask[(long long)my * mw + mx]) bits |= 1u << i;
+    const int mx = (int)(((uint64_t)x * mw) / W);
+    if (full || mask[(uint64_t)my * mw + mx]) bits |= 1u << i;
   }
   R[idx] = bits;
 }
 
 // ------------------------------------------------------------- cascade step
+// C_j = dilate4(downmap2(C_{j-1})) on a 32-row x 8-word output tile: the
+// pooled words of the tile plus a 4-row / 1-word apron are staged in shared
+// memory once, then each thread ORs its 9x3 neighbourhood.
+constexpr int CT_R = 32, CT_W = 8;
+
 struct CascadeArgs {
   int j, L, H;
   int rows, cols, wpr;        // output level j
@@ -92,7 +101,7 @@ struct CascadeArgs {
   const uint32_t* src;        // j > 1: stack[j-1]
   uint64_t src_stride;        // words per batch mask
   const uint32_t* R;          // j == 1: pixel rows
-  int mh;
+  const uint32_t* rowmap;
   uint32_t* dst;
   uint64_t dst_stride;
   int nbatch;
@@ -102,9 +111,9 @@ struct CascadeArgs {
 };
 
 __device__ __forceinline__ uint32_t cas_src(const CascadeArgs& a, int b, int rr, int ww) {
-  if (ww < 0 || ww >= a.pwpr || rr < 0 || rr >= a.prow_n) return 0u;
+  if (ww >= a.pwpr || rr >= a.prow_n) return 0u;
   if (a.j == 1) {
-    uint32_t v = a.R[(long long)((long long)rr * a.mh / a.H) * a.pwpr + ww];
+    uint32_t v = a.R[(uint64_t)a.rowmap[rr] * a.pwpr + ww];
     if (b > 0) {
       const int* r = a.rect[b];
       if (rr < r[0] || rr >= r[1]) return 0u;
@@ -115,36 +124,52 @@ __device__ __forceinline__ uint32_t cas_src(const CascadeArgs& a, int b, int rr,
   return a.src[(uint64_t)b * a.src_stride + (uint64_t)rr * a.pwpr + ww];
 }
 
-// downmapped word at output level (row r, word w)
+// downmapped word at output level (row r, word w), both in range
 __device__ __forceinline__ uint32_t cas_down(const CascadeArgs& a, int b, int r, int w) {
-  if (w < 0 || w >= a.wpr) return 0u;
-  uint32_t lo = cas_src(a, b, 2 * r, 2 * w) | cas_src(a, b, 2 * r + 1, 2 * w);
-  uint32_t hi = cas_src(a, b, 2 * r, 2 * w + 1) | cas_src(a, b, 2 * r + 1, 2 * w + 1);
+  const uint32_t lo = cas_src(a, b, 2 * r, 2 * w) | cas_src(a, b, 2 * r + 1, 2 * w);
+  const uint32_t hi = cas_src(a, b, 2 * r, 2 * w + 1) | cas_src(a, b, 2 * r + 1, 2 * w + 1);
   return pool_pairs((uint64_t)lo | ((uint64_t)hi << 32));
 }
 
-__device__ uint32_t cas_word(const CascadeArgs& a, int b, int r, int w) {
-  uint32_t p = 0, c = 0, n = 0;
-  int r0 = max(r - DIL, 0), r1 = min(r + DIL, a.rows - 1);
-  for (int rr = r0; rr <= r1; ++rr) {
-    p |= cas_down(a, b, rr, w - 1);
-    c |= cas_down(a, b, rr, w);
-    n |= cas_down(a, b, rr, w + 1);
+__global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
+  __shared__ uint32_t dm[2][CT_R + 2 * DIL][CT_W + 2];
+  const int b = a.batch[blockIdx.y];
+  const bool both = a.fov && b == a.j;
+  const int r0 = blockIdx.z * CT_R, w0 = blockIdx.x * CT_W;
+  for (int e = threadIdx.x; e < (CT_R + 2 * DIL) * (CT_W + 2); e += blockDim.x) {
+    const int lr = e / (CT_W + 2), lw = e % (CT_W + 2);
+    const int r = r0 - DIL + lr, w = w0 - 1 + lw;
+    uint32_t v0 = 0, v1 = 0;
+    if (r >= 0 && r < a.rows && w >= 0 && w < a.wpr) {
+      v0 = cas_down(a, b, r, w);
+      if (both) v1 = cas_down(a, 0, r, w);
+    }
+    dm[0][lr][lw] = v0;
+    dm[1][lr][lw] = v1;
   }
-  return spread(p, c, n) & last_word_mask(a.cols, w);
-}
-
-__global__ void k_cascade(CascadeArgs a) {
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= a.rows * a.wpr) return;
-  int b = a.batch[blockIdx.y];
-  int r = idx / a.wpr, w = idx % a.wpr;
-  uint32_t v = cas_word(a, b, r, w);
-  if (a.fov && b == a.j) v &= cas_word(a, 0, r, w);
-  a.dst[(uint64_t)b * a.dst_stride + idx] = v;
+  __syncthreads();
+  const int tr = threadIdx.x / CT_W, tw = threadIdx.x % CT_W;
+  const int r = r0 + tr, w = w0 + tw;
+  if (r >= a.rows || w >= a.wpr) return;
+  uint32_t p = 0, c = 0, n = 0, p1 = 0, c1 = 0, n1 = 0;
+#pragma unroll
+  for (int k = 0; k <= 2 * DIL; ++k) {
+    p |= dm[0][tr + k][tw];
+    c |= dm[0][tr + k][tw + 1];
+    n |= dm[0][tr + k][tw + 2];
+    p1 |= dm[1][tr + k][tw];
+    c1 |= dm[1][tr + k][tw + 1];
+    n1 |= dm[1][tr + k][tw + 2];
+  }
+  uint32_t v = spread(p, c, n);
+  if (both) v &= spread(p1, c1, n1);
+  a.dst[(uint64_t)b * a.dst_stride + (uint64_t)r * a.wpr + w] = v & last_word_mask(a.cols, w);
 }
 
 // ----------------------------------------------------------- footprint step
+// V_{j-1} = shrink4(upsample2(V_j & D_j)) (outside the grid counts as set);
+// the finest step also ANDs the request.  Upsampling duplicates rows, so the
+// 9-row AND is taken over the 5 distinct source rows before bit doubling.
 struct FootArgs {
   int j, L, H;
   int rows, cols, wpr;        // output level j-1
@@ -153,35 +178,52 @@ struct FootArgs {
   const uint32_t* D;          // detail mask level j
   uint32_t* out;              // level j-1
   const uint32_t* R;          // j == 1: requested rows
-  int mh;
+  const uint32_t* rowmap;
 };
 
-__device__ __forceinline__ uint32_t fp_up(const FootArgs& a, int r, int w) {
-  // upsampled (V_j & D_j) word at level j-1, outside the grid = all set
-  if (r < 0 || r >= a.rows || w < 0 || w >= a.wpr) return 0xFFFFFFFFu;
-  int sr = r >> 1, sw = w >> 1;
-  uint32_t s = a.D[(uint64_t)sr * a.swpr + sw];
-  if (a.V) s &= a.V[(uint64_t)sr * a.swpr + sw];
-  uint32_t v = double_bits(s >> (16 * (w & 1)));
-  return v | ~last_word_mask(a.cols, w);
-}
+constexpr int FP_SR = CT_R / 2 + DIL + 1;  // source rows staged per tile (21)
+constexpr int FP_SW = CT_W / 2 + 2;        // source words staged per tile (6)
 
-__global__ void k_footprint(FootArgs a) {
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= a.rows * a.wpr) return;
-  int r = idx / a.wpr, w = idx % a.wpr;
-  uint32_t p = ~0u, c = ~0u, n = ~0u;
-  for (int rr = r - DIL; rr <= r + DIL; ++rr) {
-    p &= fp_up(a, rr, w - 1);
-    c &= fp_up(a, rr, w);
-    n &= fp_up(a, rr, w + 1);
+__global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
+  __shared__ uint32_t sv[FP_SR][FP_SW];
+  const int r0 = blockIdx.z * CT_R, w0 = blockIdx.x * CT_W;
+  const int sr0 = (r0 - DIL) >> 1, sw0 = (w0 >> 1) - 1;
+  for (int e = threadIdx.x; e < FP_SR * FP_SW; e += blockDim.x) {
+    const int lr = e / FP_SW, lw = e % FP_SW;
+    const int sr = sr0 + lr, sw = sw0 + lw;
+    uint32_t v = 0xFFFFFFFFu;
+    if (sr >= 0 && sr < a.srows && sw >= 0 && sw < a.swpr) {
+      v = a.D[(uint64_t)sr * a.swpr + sw];
+      if (a.V) v &= a.V[(uint64_t)sr * a.swpr + sw];
+    }
+    sv[lr][lw] = v;
   }
-  uint32_t v = shrink(p, c, n) & last_word_mask(a.cols, w);
-  if (a.j == 1) v &= a.R[(uint64_t)((long long)r * a.mh / a.H) * a.wpr + w];
-  a.out[idx] = v;
+  __syncthreads();
+  const int tr = threadIdx.x / CT_W, tw = threadIdx.x % CT_W;
+  const int r = r0 + tr, w = w0 + tw;
+  if (r >= a.rows || w >= a.wpr) return;
+  const int s_lo = ((r - DIL) >> 1) - sr0, s_hi = ((r + DIL) >> 1) - sr0;
+  uint32_t nb[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int ww = w - 1 + q;
+    if (ww < 0 || ww >= a.wpr) {
+      nb[q] = 0xFFFFFFFFu;
+      continue;
+    }
+    uint32_t v = 0xFFFFFFFFu;
+    for (int k = s_lo; k <= s_hi; ++k) v &= sv[k][(ww >> 1) - sw0];
+    nb[q] = double_bits(v >> (16 * (ww & 1))) | ~last_word_mask(a.cols, ww);
+  }
+  uint32_t v = shrink(nb[0], nb[1], nb[2]) & last_word_mask(a.cols, w);
+  if (a.j == 1) v &= a.R[(uint64_t)a.rowmap[r] * a.wpr + w];
+  a.out[(uint64_t)r * a.wpr + w] = v;
 }
 
 // -------------------------------------------------------------- block select
+// One warp per 32x32 coefficient block (lane = block row); 8 blocks per CTA
+// aggregate their list appends and statistics before touching global
+// counters.
 struct BlockArgs {
   int L, H, W, bs, nbx, NB, n, rs;
   const uint32_t* D[WV_MAX_LEVELS + 1];
@@ -208,7 +250,7 @@ __device__ __forceinline__ bool row_any(const uint32_t* row, int c0, int c1) {
 __device__ bool incl_row_any(const BlockArgs& a, int y, int x0, int x1) {
   if (y < (a.H >> a.L) && x0 < (a.W >> a.L)) return true;
   for (int k = 1; k <= a.L; ++k) {
-    int bh = a.H >> k, bw = a.W >> k;
+    const int bh = a.H >> k, bw = a.W >> k;
     if (y < bh) {
       if (row_any(a.D[k] + (uint64_t)y * a.dwpr[k], max(x0, bw) - bw, min(x1, 2 * bw) - bw))
         return true;
@@ -221,150 +263,171 @@ __device__ bool incl_row_any(const BlockArgs& a, int y, int x0, int x1) {
   return false;
 }
 
-__global__ void k_blocks(BlockArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int b0 = wid * 32;
-  if (b0 >= a.NB) return;
-  uint32_t selmask = 0;
-  for (int i = 0; i < 32 && b0 + i < a.NB; ++i) {
-    int b = b0 + i;
-    int by = b / a.nbx, bx = b % a.nbx;
-    int x0 = bx * a.bs, x1 = x0 + a.bs;
+constexpr int BLK_WARPS = 8;
+
+__global__ void __launch_bounds__(32 * BLK_WARPS) k_blocks(BlockArgs a) {
+  __shared__ uint32_t s_sel[BLK_WARPS], s_emit[BLK_WARPS], s_base, s_miss;
+  __shared__ unsigned long long s_recs, s_newb;
+  __shared__ uint32_t s_err;
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const int b = blockIdx.x * BLK_WARPS + wi;
+  if (threadIdx.x == 0) { s_recs = 0; s_newb = 0; s_err = 0; s_miss = 0; }
+  bool sel = false;
+  if (b < a.NB) {
+    const int by = b / a.nbx, bx = b % a.nbx;
+    const int x0 = bx * a.bs, x1 = x0 + a.bs;
     bool any = false;
     for (int r = lane; r < a.bs; r += 32) any |= incl_row_any(a, by * a.bs + r, x0, x1);
-    if (__any_sync(0xFFFFFFFFu, any)) selmask |= 1u << i;
+    sel = __any_sync(0xFFFFFFFFu, any);
   }
-  const int b = b0 + lane;
-  const bool valid = b < a.NB;
-  const bool sel = valid && ((selmask >> lane) & 1u);
-  const uint32_t word = b0 >> 5;
-  const uint32_t prevw = a.prev_sel[word];
-  const uint32_t loadw = a.loaded[word];
-  const bool prev = valid && ((prevw >> lane) & 1u);
-  const bool was = (loadw >> lane) & 1u;
   unsigned long long bytes = 0, recs = 0;
   uint32_t err = 0;
   if (sel) {
-    for (int t = 0; t < a.n; ++t) {
-      uint64_t i = (uint64_t)t * a.NB + b;
-      unsigned long long e = a.ends[i];
-      unsigned long long s = i ? a.ends[i - 1] : 0ull;
-      if (e < s || e > a.rec_bytes || (e - s) % a.rs || (e - s) / a.rs > (unsigned long long)a.bs * a.bs)
+    for (int t = lane; t < a.n; t += 32) {
+      const uint64_t i = (uint64_t)t * a.NB + b;
+      const unsigned long long e = a.ends[i];
+      const unsigned long long s = i ? a.ends[i - 1] : 0ull;
+      if (e < s || e > a.rec_bytes || (e - s) % a.rs ||
+          (e - s) / a.rs > (unsigned long long)a.bs * a.bs)
         err |= WV_DERR_TABLE;
       else {
         bytes += e - s;
         recs += (e - s) / a.rs;
       }
     }
-  }
-  const bool missing = sel && !was;
-  unsigned long long newb = missing ? bytes : 0ull;
-  const bool emit = !a.account_only && (sel || prev);
-  uint32_t emask = __ballot_sync(0xFFFFFFFFu, emit);
-  uint32_t base = 0;
-  if (lane == 0 && emask) base = atomicAdd(a.list_count, (uint32_t)__popc(emask));
-  base = __shfl_sync(0xFFFFFFFFu, base, 0);
-  if (emit) a.list[base + __popc(emask & ((1u << lane) - 1u))] = sel ? (uint32_t)b : ((uint32_t)b | ZERO_FLAG);
-  uint32_t nmiss = __popc(__ballot_sync(0xFFFFFFFFu, missing));
-  for (int o = 16; o; o >>= 1) {
-    recs += __shfl_xor_sync(0xFFFFFFFFu, recs, o);
-    newb += __shfl_xor_sync(0xFFFFFFFFu, newb, o);
-    err |= __shfl_xor_sync(0xFFFFFFFFu, err, o);
-  }
-  if (lane == 0) {
-    a.sel[word] = selmask;
-    if (!a.account_only) a.prev_sel[word] = selmask;
-    a.loaded[word] = loadw | selmask;
-    if (recs) atomicAdd(&a.res->records, recs);
-    if (newb) {
-      atomicAdd(&a.res->new_bytes, newb);
-      atomicAdd(a.set_bytes, newb);
+    for (int o = 16; o; o >>= 1) {
+      bytes += __shfl_xor_sync(0xFFFFFFFFu, bytes, o);
+      recs += __shfl_xor_sync(0xFFFFFFFFu, recs, o);
+      err |= __shfl_xor_sync(0xFFFFFFFFu, err, o);
     }
-    if (nmiss) atomicAdd(&a.res->n_missing, nmiss);
-    if (selmask) atomicAdd(&a.res->n_selected, (uint32_t)__popc(selmask));
-    if (err) atomicOr(&a.res->error, err);
+  }
+  __syncthreads();
+  const uint32_t word = (uint32_t)b >> 5, bit = 1u << (b & 31);
+  if (lane == 0 && b < a.NB) {
+    const bool prev = (a.prev_sel[word] & bit) != 0;
+    const bool was = (a.loaded[word] & bit) != 0;
+    s_sel[wi] = sel;
+    s_emit[wi] = !a.account_only && (sel || prev);
+    if (sel) {
+      atomicOr(&a.sel[word], bit);
+      if (!was) {
+        atomicOr(&a.loaded[word], bit);
+        atomicAdd(&s_newb, bytes);
+        atomicAdd(&s_miss, 1u);
+      }
+      atomicAdd(&s_recs, recs);
+      if (err) atomicOr(&s_err, err);
+    } else {
+      atomicAnd(&a.sel[word], ~bit);
+    }
+    if (!a.account_only) {
+      if (sel) atomicOr(&a.prev_sel[word], bit);
+      else if (prev) atomicAnd(&a.prev_sel[word], ~bit);
+    }
+  } else if (lane == 0) {
+    s_sel[wi] = 0;
+    s_emit[wi] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t ne = 0, ns = 0;
+    for (int i = 0; i < BLK_WARPS; ++i) { ne += s_emit[i]; ns += s_sel[i]; }
+    s_base = ne ? atomicAdd(a.list_count, ne) : 0u;
+    uint32_t pos = s_base;
+    for (int i = 0; i < BLK_WARPS; ++i) {
+      if (!s_emit[i]) continue;
+      const uint32_t bb = (uint32_t)(blockIdx.x * BLK_WARPS + i);
+      a.list[pos++] = s_sel[i] ? bb : (bb | ZERO_FLAG);
+    }
+    if (s_recs) atomicAdd(&a.res->records, s_recs);
+    if (s_newb) {
+      atomicAdd(&a.res->new_bytes, s_newb);
+      atomicAdd(a.set_bytes, s_newb);
+    }
+    if (s_miss) atomicAdd(&a.res->n_missing, s_miss);
+    if (ns) atomicAdd(&a.res->n_selected, ns);
+    if (s_err) atomicOr(&a.res->error, s_err);
   }
 }
 
 // -------------------------------------------------------------- tile lists
+// Level 1 (output pixels): a 64x64 tile is needed iff it touches the request;
+// tiles needed last frame but not now are listed with ZERO_FLAG so the
+// canvas is cleared there.  Level k >= 2: tile u is needed iff a needed
+// level-(k-1) tile reads its rows; unrolled to level 1 this is the need-bit
+// rectangle [2^m u - (2^m-1), 2^m u + 2(2^m-1)] (m = k-1) in each axis.
 struct TileArgs {
-  int L, H, W, mh;
+  int L, H, W;
   int wpr0;
   const uint32_t* R;
+  const uint32_t* rowmap;
   int full;
   int nty[WV_MAX_LEVELS + 1], ntx[WV_MAX_LEVELS + 1];
-  uint8_t* need[WV_MAX_LEVELS + 1];
+  uint32_t* need1;                   // bit rows: nty[1] x nwords1
+  int nwords1;
   uint32_t* list[WV_MAX_LEVELS + 1];
   uint8_t* prev_need;
   uint32_t* counters;                // CNT_TILES + k
+  const unsigned long long* set_bytes;
+  wv_frame_result* res;
+  int base[WV_MAX_LEVELS + 2];       // flattened coarse-tile index ranges (levels 2..L)
 };
 
-__global__ void k_tiles(TileArgs a) {
-  __shared__ uint32_t cnt;
-  // level 1: tiles of the output pixels that touch the request
+__global__ void __launch_bounds__(256) k_tiles1(TileArgs a) {
   const int nt1 = a.nty[1] * a.ntx[1];
-  if (threadIdx.x == 0) cnt = 0;
-  __syncthreads();
-  for (int t = threadIdx.x; t < nt1; t += blockDim.x) {
-    int ty = t / a.ntx[1], tx = t % a.ntx[1];
-    bool nd = a.full != 0;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  bool nd = false, pv = false;
+  if (t < nt1) {
+    const int ty = t / a.ntx[1], tx = t % a.ntx[1];
+    nd = a.full != 0;
     if (!nd) {
-      int y0 = ty * OUT_H, y1 = min(y0 + OUT_H, a.H);
-      int c0 = tx * OUT_W, c1 = min(c0 + OUT_W, a.W);
-      int m0 = (int)((long long)y0 * a.mh / a.H), m1 = (int)((long long)(y1 - 1) * a.mh / a.H);
-      for (int m = m0; m <= m1 && !nd; ++m) {
+      const int y0 = ty * OUT_H, y1 = min(y0 + OUT_H, a.H);
+      const int c0 = tx * OUT_W, c1 = min(c0 + OUT_W, a.W);
+      const uint32_t m0 = a.rowmap[y0], m1 = a.rowmap[y1 - 1];
+      for (uint32_t m = m0; m <= m1 && !nd; ++m) {
         const uint32_t* row = a.R + (uint64_t)m * a.wpr0;
         for (int w = c0 >> 5; w <= ((c1 - 1) >> 5); ++w)
           if (row[w] & range_mask(c0, c1, w)) { nd = true; break; }
       }
     }
-    bool pv = a.prev_need[t] != 0;
-    a.need[1][t] = nd;
+    pv = a.prev_need[t] != 0;
     a.prev_need[t] = nd;
-    if (nd || pv) {
-      uint32_t pos = atomicAdd(&cnt, 1u);
-      a.list[1][pos] = (uint32_t)t | (nd ? 0u : ZERO_FLAG);
-    }
+    if (nd) atomicOr(&a.need1[ty * a.nwords1 + (tx >> 5)], 1u << (tx & 31));
+    else atomicAnd(&a.need1[ty * a.nwords1 + (tx >> 5)], ~(1u << (tx & 31)));
   }
-  __syncthreads();
-  if (threadIdx.x == 0) a.counters[CNT_TILES + 1] = cnt;
-  // coarser levels: a tile is needed if a needed finer tile reads its rows
-  for (int k = 2; k <= a.L; ++k) {
-    __syncthreads();
-    if (threadIdx.x == 0) cnt = 0;
-    __syncthreads();
-    const int nt = a.nty[k] * a.ntx[k];
-    const int fy = a.nty[k - 1], fx = a.ntx[k - 1];
-    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
-      int u = t / a.ntx[k], v = t % a.ntx[k];
-      bool nd = false;
-      for (int ty = max(2 * u - 1, 0); ty <= min(2 * u + 2, fy - 1) && !nd; ++ty)
-        for (int tx = max(2 * v - 1, 0); tx <= min(2 * v + 2, fx - 1); ++tx)
-          if (a.need[k - 1][ty * fx + tx]) { nd = true; break; }
-      a.need[k][t] = nd;
-      if (nd) a.list[k][atomicAdd(&cnt, 1u)] = (uint32_t)t;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) a.counters[CNT_TILES + k] = cnt;
-  }
+  const bool emit = nd || pv;
+  const uint32_t m = __ballot_sync(0xFFFFFFFFu, emit);
+  const uint32_t mn = __ballot_sync(0xFFFFFFFFu, nd);
+  const int lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == 0 && m) base = atomicAdd(&a.counters[CNT_TILES + 1], (uint32_t)__popc(m));
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  if (emit) a.list[1][base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)t | (nd ? 0u : ZERO_FLAG);
+  if (lane == 0 && mn) atomicAdd(&a.res->n_tiles, (uint32_t)__popc(mn));
+  if (t == 0) a.res->set_bytes = *a.set_bytes;
 }
 
-// result finalisation: cache-entry total after this call, level-1 tile count
-__global__ void k_finalize(const uint8_t* need1, int nt1, const unsigned long long* set_bytes,
-                           wv_frame_result* res) {
-  __shared__ uint32_t c;
-  if (threadIdx.x == 0) c = 0;
-  __syncthreads();
-  uint32_t mine = 0;
-  if (need1)
-    for (int t = threadIdx.x; t < nt1; t += blockDim.x) mine += need1[t] != 0;
-  atomicAdd(&c, mine);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    res->n_tiles = c;
-    res->set_bytes = *set_bytes;
+__global__ void __launch_bounds__(256) k_tiles_up(TileArgs a) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.base[a.L + 1]) return;
+  int k = 2;
+  while (g >= a.base[k + 1]) ++k;
+  const int t = g - a.base[k];
+  const int u = t / a.ntx[k], v = t % a.ntx[k];
+  const int m = k - 1, s = 1 << m;
+  const int ylo = max(s * u - (s - 1), 0), yhi = min(s * u + 2 * (s - 1), a.nty[1] - 1);
+  const int xlo = max(s * v - (s - 1), 0), xhi = min(s * v + 2 * (s - 1), a.ntx[1] - 1);
+  bool nd = false;
+  for (int y = ylo; y <= yhi && !nd; ++y) {
+    const uint32_t* row = a.need1 + (uint64_t)y * a.nwords1;
+    for (int w = xlo >> 5; w <= (xhi >> 5); ++w)
+      if (row[w] & range_mask(xlo, xhi + 1, w)) { nd = true; break; }
   }
+  if (nd) a.list[k][atomicAdd(&a.counters[CNT_TILES + k], 1u)] = (uint32_t)t;
+}
+
+__global__ void k_finalize(const unsigned long long* set_bytes, wv_frame_result* res) {
+  res->set_bytes = *set_bytes;
 }
 
 }  // namespace
@@ -377,12 +440,14 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
   const bool acct = (a->flags & WV_FLAG_ACCOUNT_ONLY) != 0;
   if (!full && !a->d_mask) return WV_ERR_ARG;
   uint32_t* R = (uint32_t*)(ws + lo.mrows);
+  uint32_t* rowmap = (uint32_t*)(ws + lo.rowmap);
   uint32_t* counters = (uint32_t*)(ws + lo.counters);
   WV_CUDA(cudaMemsetAsync(counters, 0, 64 * 4, s));
   WV_CUDA(cudaMemsetAsync(a->d_result, 0, sizeof(wv_frame_result), s));
   {
-    int n = lo.mh * lo.wpr_[0];
-    k_mask_rows<<<cdiv(n, 256), 256, 0, s>>>(a->d_mask, R, lo.mh, lo.mw, W, lo.wpr_[0], full);
+    const int n = max(lo.mh * lo.wpr_[0], H);
+    k_mask_rows<<<cdiv(n, 256), 256, 0, s>>>(a->d_mask, R, rowmap, lo.mh, lo.mw, W, H,
+                                             lo.wpr_[0], full);
   }
   // level cascades (batch 0: request closure; batches k>=j: gaze windows)
   for (int j = 1; j <= L; ++j) {
@@ -392,7 +457,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
     c.prow_n = H >> (j - 1); c.pcols = W >> (j - 1); c.pwpr = lo.wpr_[j - 1];
     c.src = j > 1 ? (const uint32_t*)(ws + lo.stack[j - 1]) : nullptr;
     c.src_stride = j > 1 ? lo.stack_stride[j - 1] / 4 : 0;
-    c.R = R; c.mh = lo.mh;
+    c.R = R; c.rowmap = rowmap;
     c.dst = (uint32_t*)(ws + lo.stack[j]);
     c.dst_stride = lo.stack_stride[j] / 4;
     c.fov = fov;
@@ -403,8 +468,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
       for (int k = 1; k <= L; ++k)
         for (int q = 0; q < 4; ++q) c.rect[k][q] = a->fovea[k - 1][q];
     }
-    int n = c.rows * c.wpr;
-    dim3 grid(cdiv(n, 256), c.nbatch);
+    dim3 grid(cdiv(c.wpr, CT_W), c.nbatch, cdiv(c.rows, CT_R));
     k_cascade<<<grid, 256, 0, s>>>(c);
   }
   auto Dptr = [&](int k) -> uint32_t* {
@@ -419,9 +483,9 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
     f.V = j == L ? nullptr : (const uint32_t*)(ws + lo.fp[j]);
     f.D = Dptr(j);
     f.out = j == 1 ? a->d_footprint : (uint32_t*)(ws + lo.fp[j - 1]);
-    f.R = R; f.mh = lo.mh;
-    int n = f.rows * f.wpr;
-    k_footprint<<<cdiv(n, 256), 256, 0, s>>>(f);
+    f.R = R; f.rowmap = rowmap;
+    dim3 grid(cdiv(f.wpr, CT_W), 1, cdiv(f.rows, CT_R));
+    k_footprint<<<grid, 256, 0, s>>>(f);
   }
   {
     BlockArgs b{};
@@ -440,24 +504,28 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
     b.set_bytes = a->d_set_bytes;
     b.res = a->d_result;
     b.account_only = acct;
-    int warps = cdiv(lo.NB, 32);
-    k_blocks<<<cdiv(warps * 32, 256), 256, 0, s>>>(b);
+    k_blocks<<<cdiv(lo.NB, BLK_WARPS), 32 * BLK_WARPS, 0, s>>>(b);
   }
   if (acct) {
-    k_finalize<<<1, 32, 0, s>>>(nullptr, 0, a->d_set_bytes, a->d_result);
+    k_finalize<<<1, 1, 0, s>>>(a->d_set_bytes, a->d_result);
   } else {
     TileArgs t{};
-    t.L = L; t.H = H; t.W = W; t.mh = lo.mh; t.wpr0 = lo.wpr_[0]; t.R = R; t.full = full;
+    t.L = L; t.H = H; t.W = W; t.wpr0 = lo.wpr_[0]; t.R = R; t.rowmap = rowmap; t.full = full;
     for (int k = 1; k <= L; ++k) {
       t.nty[k] = lo.nty[k]; t.ntx[k] = lo.ntx[k];
-      t.need[k] = ws + lo.need[k];
       t.list[k] = (uint32_t*)(ws + lo.tlist[k]);
     }
+    t.need1 = (uint32_t*)(ws + lo.need[1]);
+    t.nwords1 = wpr(lo.ntx[1]);
     t.prev_need = ws + lo.prev_need;
     t.counters = counters;
-    k_tiles<<<1, 1024, 0, s>>>(t);
-    k_finalize<<<1, 256, 0, s>>>(ws + lo.need[1], lo.nty[1] * lo.ntx[1], a->d_set_bytes,
-                                 a->d_result);
+    t.set_bytes = a->d_set_bytes;
+    t.res = a->d_result;
+    t.base[2] = 0;
+    for (int k = 2; k <= L; ++k) t.base[k + 1] = t.base[k] + lo.nty[k] * lo.ntx[k];
+    const int nt1 = lo.nty[1] * lo.ntx[1];
+    k_tiles1<<<cdiv(nt1, 256), 256, 0, s>>>(t);
+    if (L >= 2) k_tiles_up<<<cdiv(max(t.base[L + 1], 1), 256), 256, 0, s>>>(t);
   }
   WV_CUDA(cudaGetLastError());
   return WV_OK;

@@ -146,7 +146,7 @@ class _Pending:
 
 
 class DeviceFrame:
-    """Device-resident decode result.  ``canvas`` (H, W, C) u8 and
+    """Device-resident decode result.  ``canvas`` planar (C, H, W) u8 and
     ``footprint_bits`` (H, ceil(W/32)) int32 are the session's buffers and
     stay valid until the next decode call on the session."""
 
@@ -196,7 +196,8 @@ class DecodeSession:
             N.check(self._lib.wv_workspace_reset(C.byref(self._geom), C.c_void_p(self._ws.data_ptr()),
                                                  C.c_void_p(self.stream.cuda_stream)),
                     "wv_workspace_reset")
-            self._canvas = torch.zeros((h.height, h.width, h.channels), dtype=torch.uint8,
+            # planar (C, H, W): K3 writes each channel plane with coalesced stores
+            self._canvas = torch.zeros((h.channels, h.height, h.width), dtype=torch.uint8,
                                        device=self.device)
             self._footprint = torch.zeros((h.height, wpr0), dtype=torch.int32, device=self.device)
             self._mask_dev = torch.zeros((_RING, h.mask_h * h.mask_w), dtype=torch.uint8,
@@ -434,7 +435,10 @@ class DecodeSession:
         p = self._launch(frame, mode, mask, schedule, time_stages=self.time_stages)
         self._settle_until(p)
         h = self.header
-        pixels = self._canvas.cpu().numpy()
+        with torch.cuda.stream(self.stream):
+            hwc = self._canvas.permute(1, 2, 0).contiguous()
+        self.stream.synchronize()
+        pixels = hwc.cpu().numpy()
         footprint = unpack_footprint(self._footprint.cpu().numpy(), h.width)
         return pixels, footprint, p.stats
 

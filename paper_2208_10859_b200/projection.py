@@ -121,12 +121,14 @@ def stereo_mask(pose: CameraPose, dims) -> np.ndarray:
 def view_args(canvas: torch.Tensor, footprint_bits: torch.Tensor, row0: int, rows: int,
               width: int, channels: int, pose: CameraPose, out: torch.Tensor,
               uncovered: torch.Tensor) -> N.ViewArgs:
+    """K4 arguments for one view of a planar (C, H, W) u8 canvas."""
     if not (pose.fov_h < 180 and pose.fov_v < 180):
         raise ProjectionError("perspective rendering requires FOV < 180 degrees")
     v = N.ViewArgs()
     v.d_canvas = canvas.data_ptr()
     v.d_footprint = footprint_bits.data_ptr()
     v.row0, v.rows, v.width, v.channels = row0, rows, width, channels
+    v.canvas_h = int(canvas.shape[-2])
     rot = pose.rotation().reshape(-1)
     for i in range(9):
         v.rot[i] = float(rot[i])
@@ -171,7 +173,7 @@ def render_perspective(region: np.ndarray, footprint: np.ndarray, pose: CameraPo
     mono = region.ndim == 2
     reg = region[..., None] if mono else region
     m, n, c = reg.shape
-    canvas = torch.from_numpy(np.ascontiguousarray(reg, np.uint8)).to(dev)
+    canvas = torch.from_numpy(np.ascontiguousarray(reg, np.uint8)).to(dev).permute(2, 0, 1).contiguous()
     fpb = torch.from_numpy(pack_footprint(np.asarray(footprint, bool))).to(dev)
     out = torch.empty((out_h, out_w, c), dtype=torch.uint8, device=dev)
     unc = torch.zeros(1, dtype=torch.int32, device=dev)
