@@ -18,7 +18,7 @@ namespace wv {
 namespace {
 
 struct TemporalArgs {
-  int L, H, W, C, bs, nbx, n, t, rs, float_mode;
+  int L, H, W, C, bs, bs_log2, nbx, n, t, rs, float_mode;
   const unsigned long long* ends;   // (n, NB)
   const uint8_t* recs;              // records region
   const float* extrema;             // (n, C, 4)
@@ -32,109 +32,194 @@ struct TemporalArgs {
 };
 
 // inclusion bit of plane position (y, x) (LevelMaskSet.inclusion_grid)
-__device__ __forceinline__ bool included(const TemporalArgs& a, int y, int x) {
+__device__ __forceinline__ uint32_t included(const TemporalArgs& a, int y, int x) {
   for (int k = 1; k <= a.L; ++k) {
-    int bh = a.H >> k, bw = a.W >> k;
+    const int bh = a.H >> k, bw = a.W >> k;
     if (y >= bh || x >= bw) {
-      int r = y >= bh ? y - bh : y;
-      int c = x >= bw ? x - bw : x;
+      const int r = y >= bh ? y - bh : y;
+      const int c = x >= bw ? x - bw : x;
       return (a.D[k][(uint64_t)r * a.dwpr[k] + (c >> 5)] >> (c & 31)) & 1u;
     }
   }
-  return true;  // approximation band: always included
+  return 1u;  // approximation band: always included
+}
+
+// Where a whole block sits inside one subband quadrant of one level (or in
+// the approximation band) its inclusion bits are a straight slice of that
+// level's mask rows; blocks straddling quadrants use the per-position path.
+struct BlockIncl {
+  int mode;            // 0: all included, 1: slice of D[k], 2: per position
+  const uint32_t* rows;
+  int wpr, r0, c0;
+};
+
+__device__ __forceinline__ BlockIncl classify(const TemporalArgs& a, int y0, int x0) {
+  BlockIncl bi{2, nullptr, 0, 0, 0};
+  const int y1 = y0 + a.bs, x1 = x0 + a.bs;
+  if (y1 <= (a.H >> a.L) && x1 <= (a.W >> a.L)) { bi.mode = 0; return bi; }
+  for (int k = 1; k <= a.L; ++k) {
+    const int bh = a.H >> k, bw = a.W >> k;
+    const bool top = y1 <= bh, bot = y0 >= bh && y1 <= 2 * bh;
+    const bool left = x1 <= bw, right = x0 >= bw && x1 <= 2 * bw;
+    if ((top && right) || (bot && (left || right))) {
+      bi.mode = 1;
+      bi.rows = a.D[k];
+      bi.wpr = a.dwpr[k];
+      bi.r0 = bot ? y0 - bh : y0;
+      bi.c0 = right ? x0 - bw : x0;
+      return bi;
+    }
+    if (!(y1 <= bh && x1 <= bw)) return bi;   // straddles this level's quadrants
+  }
+  return bi;
 }
 
 // temporal Mallat index ti contributes to display time t with sign
 // (+1/-1) or not at all (0) (encoding.py:187-195, decoding.py:72-80)
 __device__ __forceinline__ int tweight(int ti, int t, int n) {
   if (ti == 0) return 1;
-  int big = 31 - __clz(n);
-  int lvl = big - (31 - __clz(ti));
+  const int big = 31 - __clz(n);
+  const int lvl = big - (31 - __clz(ti));
   if ((t >> lvl) != ti - (1 << (big - lvl))) return 0;
   return ((t >> (lvl - 1)) & 1) ? -1 : 1;
 }
 
-__global__ void __launch_bounds__(256) k_temporal(TemporalArgs a) {
-  extern __shared__ float acc[];        // C x bs*bs
-  const int npos = a.bs * a.bs;
-  const uint32_t count = *a.count;
+// One CTA (128 threads) per work-list block.  All records of the block (all
+// temporal indices, for offset validation) are fetched in rounds of 128 with
+// one record per thread, so a sparse block costs one dependent load; the
+// shared-memory accumulation then runs temporal index by temporal index in
+// ascending order (the np.add.at order), and the inclusion-masked block is
+// written with 16-byte stores.
+constexpr int K2_THREADS = 128;
+constexpr int K2_MAXN = 32;
+
+__global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
+  extern __shared__ float4 smem4[];
+  float* acc = reinterpret_cast<float*>(smem4);              // C x bs*bs
+  __shared__ unsigned long long s_start[K2_MAXN];
+  __shared__ int s_pre[K2_MAXN + 1];
+  __shared__ int s_w[K2_MAXN];
   const int tid = threadIdx.x;
+  const int npos = a.bs * a.bs;
+  const int nq = (a.C * npos) >> 2;                           // float4 per block
+  const uint32_t count = *a.count;
   const int ah = a.H >> a.L, aw = a.W >> a.L;
+  const int bmask = a.bs - 1;
   uint32_t err = 0;
   for (uint32_t item = blockIdx.x; item < count; item += gridDim.x) {
     const uint32_t e = a.list[item];
     const int b = (int)(e & ~ZERO_FLAG);
-    const int y0 = (b / a.nbx) * a.bs, x0 = (b % a.nbx) * a.bs;
-    const bool zero_only = (e & ZERO_FLAG) != 0;
-    if (!zero_only) {
-      for (int i = tid; i < a.C * npos; i += blockDim.x) acc[i] = 0.0f;
-      __syncthreads();
-      for (int ti = 0; ti < a.n; ++ti) {
-        const int wgt = tweight(ti, a.t, a.n);
-        const uint64_t fi = (uint64_t)ti * a.NB + b;
-        const unsigned long long s = fi ? a.ends[fi - 1] : 0ull;
-        const unsigned long long en = a.ends[fi];
-        if (en < s || (en - s) % a.rs) continue;  // flagged by K1
-        const int cnt = (int)min((en - s) / a.rs, (unsigned long long)npos);
-        const uint8_t* base = a.recs + s;
-        for (int r = tid; r < cnt; r += blockDim.x) {
-          const uint8_t* rp = base + (uint64_t)r * a.rs;
-          const int off = (int)rp[0] | ((int)rp[1] << 8);
-          if (off >= npos) { err |= WV_DERR_OFFSET; continue; }
-          if (!wgt) continue;
-          const int yy = y0 + off / a.bs, xx = x0 + off % a.bs;
+    const int by = b / a.nbx;
+    const int y0 = by * a.bs, x0 = (b - by * a.nbx) * a.bs;
+    if (e & ZERO_FLAG) {
+      for (int q = tid; q < nq; q += K2_THREADS) {
+        const int c = (q << 2) / npos, i = (q << 2) - c * npos;
+        float* dst = a.plane + ((uint64_t)c * a.H + y0 + (i >> a.bs_log2)) * a.W + x0 + (i & bmask);
+        *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      continue;
+    }
+    if (tid < a.n) {
+      const uint64_t fi = (uint64_t)tid * a.NB + b;
+      const unsigned long long en = a.ends[fi];
+      const unsigned long long st = fi ? a.ends[fi - 1] : 0ull;
+      int cnt = 0;
+      if (en >= st && (en - st) % a.rs == 0) cnt = (int)min((en - st) / a.rs, (unsigned long long)npos);
+      s_start[tid] = st;
+      s_pre[tid + 1] = cnt;        // prefix-summed below
+      s_w[tid] = tweight(tid, a.t, a.n);
+    }
+    for (int q = tid; q < nq; q += K2_THREADS)
+      smem4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    if (tid == 0) {
+      s_pre[0] = 0;
+      for (int t = 1; t <= a.n; ++t) s_pre[t] += s_pre[t - 1];
+    }
+    __syncthreads();
+    const int total = s_pre[a.n];
+    for (int base = 0; base < total; base += K2_THREADS) {
+      const int i = base + tid;
+      int ti = -1, off = 0;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (i < total) {
+        ti = 0;
+        while (s_pre[ti + 1] <= i) ++ti;
+        const uint8_t* rp = a.recs + s_start[ti] + (uint64_t)(i - s_pre[ti]) * a.rs;
+        off = (int)rp[0] | ((int)rp[1] << 8);
+        if (off >= npos) {
+          err |= WV_DERR_OFFSET;
+          ti = -1;
+        } else if (!s_w[ti]) {
+          ti = -1;
+        } else {
+          const int yy = y0 + (off >> a.bs_log2), xx = x0 + (off & bmask);
           const bool appr = yy < ah && xx < aw;
-          for (int c = 0; c < a.C; ++c) {
-            float v;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float x = 0.0f;
+            if (c < a.C) {
             if (a.float_mode) {
-              uint32_t u = (uint32_t)rp[2 + 4 * c] | ((uint32_t)rp[3 + 4 * c] << 8) |
-                           ((uint32_t)rp[4 + 4 * c] << 16) | ((uint32_t)rp[5 + 4 * c] << 24);
-              v = __uint_as_float(u);
+              const uint8_t* q = rp + 2 + 4 * c;
+              x = __uint_as_float((uint32_t)q[0] | ((uint32_t)q[1] << 8) |
+                                  ((uint32_t)q[2] << 16) | ((uint32_t)q[3] << 24));
             } else {
               const float* ex = a.extrema + ((uint64_t)ti * a.C + c) * 4 + (appr ? 0 : 2);
               const float lo = ex[0], hi = ex[1];
-              v = __fadd_rn(lo, __fmul_rn(__fdiv_rn((float)rp[2 + c], 255.0f), __fsub_rn(hi, lo)));
+              x = __fadd_rn(lo, __fmul_rn(__fdiv_rn((float)rp[2 + c], 255.0f), __fsub_rn(hi, lo)));
             }
-            float* cell = acc + c * npos + off;
-            *cell = __fadd_rn(*cell, wgt > 0 ? v : -v);
+            }
+            v[c] = s_w[ti] > 0 ? x : -x;
           }
         }
-        if (wgt) __syncthreads();
       }
-    }
-    // write the block: 4 consecutive positions per thread-step
-    for (int i = tid * 4; i < npos; i += blockDim.x * 4) {
-      const int yy = y0 + i / a.bs, xx = x0 + i % a.bs;
-      float4 m;
-      if (zero_only) {
-        m = make_float4(0.f, 0.f, 0.f, 0.f);
-      } else {
-        m.x = included(a, yy, xx) ? 1.0f : 0.0f;
-        m.y = included(a, yy, xx + 1) ? 1.0f : 0.0f;
-        m.z = included(a, yy, xx + 2) ? 1.0f : 0.0f;
-        m.w = included(a, yy, xx + 3) ? 1.0f : 0.0f;
-      }
-      for (int c = 0; c < a.C; ++c) {
-        float4 v;
-        if (zero_only) {
-          v = m;
-        } else {
-          const float* p = acc + c * npos + i;
-          v = make_float4(__fmul_rn(p[0], m.x), __fmul_rn(p[1], m.y), __fmul_rn(p[2], m.z),
-                          __fmul_rn(p[3], m.w));
+      // accumulate this round's records in ascending temporal index
+      const int last = min(base + K2_THREADS, total) - 1;
+      int t_lo = 0, t_hi = 0;
+      while (s_pre[t_lo + 1] <= base) ++t_lo;
+      while (s_pre[t_hi + 1] <= last) ++t_hi;
+      for (int tt = t_lo; tt <= t_hi; ++tt) {
+        if (ti == tt) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (c < a.C) acc[c * npos + off] = __fadd_rn(acc[c * npos + off], v[c]);
         }
-        float* dst = a.plane + ((uint64_t)c * a.H + yy) * a.W + xx;
-        *reinterpret_cast<float4*>(dst) = v;
+        if (s_w[tt] && tt < t_hi) __syncthreads();
       }
+      __syncthreads();
+    }
+    // write: inclusion-masked, 4 consecutive positions per thread-step
+    const BlockIncl bi = classify(a, y0, x0);
+    for (int q = tid; q < nq; q += K2_THREADS) {
+      const int c = (q << 2) / npos, i = (q << 2) - c * npos;
+      const int ly = i >> a.bs_log2, lx = i & bmask;
+      const int yy = y0 + ly, xx = x0 + lx;
+      uint32_t m4;
+      if (bi.mode == 0) {
+        m4 = 0xFu;
+      } else if (bi.mode == 1) {
+        const int cc = bi.c0 + lx;
+        const uint32_t* row = bi.rows + (uint64_t)(bi.r0 + ly) * bi.wpr;
+        const uint32_t lo = row[cc >> 5];
+        const uint32_t hi = (cc & 31) > 28 ? row[(cc >> 5) + 1] : 0u;
+        m4 = (uint32_t)(((((uint64_t)hi) << 32) | lo) >> (cc & 31)) & 0xFu;
+      } else {
+        m4 = included(a, yy, xx) | (included(a, yy, xx + 1) << 1) |
+             (included(a, yy, xx + 2) << 2) | (included(a, yy, xx + 3) << 3);
+      }
+      const float4 v = smem4[q];
+      float4 o;
+      o.x = __fmul_rn(v.x, (m4 & 1u) ? 1.0f : 0.0f);
+      o.y = __fmul_rn(v.y, (m4 & 2u) ? 1.0f : 0.0f);
+      o.z = __fmul_rn(v.z, (m4 & 4u) ? 1.0f : 0.0f);
+      o.w = __fmul_rn(v.w, (m4 & 8u) ? 1.0f : 0.0f);
+      *reinterpret_cast<float4*>(a.plane + ((uint64_t)c * a.H + yy) * a.W + xx) = o;
     }
     __syncthreads();
   }
   for (int o = 16; o; o >>= 1) err |= __shfl_xor_sync(0xFFFFFFFFu, err, o);
   if ((tid & 31) == 0 && err) atomicOr(&a.res->error, err);
 }
-
-// block_size < 4: scalar writer (tiny test geometries only)
-
 
 }  // namespace
 
@@ -144,6 +229,7 @@ int launch_temporal(const Layout& lo, const wv_geometry* g, const wv_frame_args*
   if (a->t < 0 || a->t >= lo.n) return WV_ERR_ARG;
   TemporalArgs t{};
   t.L = lo.L; t.H = lo.H; t.W = lo.W; t.C = lo.C; t.bs = lo.bs; t.nbx = lo.nbx; t.n = lo.n;
+  t.bs_log2 = 31 - __builtin_clz((unsigned)lo.bs);
   t.t = a->t; t.float_mode = g->float_mode; t.rs = 2 + lo.C * (g->float_mode ? 4 : 1);
   t.NB = lo.NB;
   t.ends = (const unsigned long long*)a->d_payload;
@@ -161,11 +247,14 @@ int launch_temporal(const Layout& lo, const wv_geometry* g, const wv_frame_args*
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  size_t smem = (size_t)lo.C * lo.bs * lo.bs * 4;
+  if (lo.n > K2_MAXN) return WV_ERR_UNSUPPORTED;
+  const size_t smem = (size_t)lo.C * lo.bs * lo.bs * 4;
   if (smem > 48 * 1024)
     WV_CUDA(cudaFuncSetAttribute(k_temporal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int grid = min(lo.NB, sms * 8);
-  k_temporal<<<grid, 256, smem, s>>>(t);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_temporal, K2_THREADS, smem);
+  const int grid = max(1, min(lo.NB, sms * max(occ, 1)));
+  k_temporal<<<grid, K2_THREADS, smem, s>>>(t);
   WV_CUDA(cudaGetLastError());
   return WV_OK;
 }
