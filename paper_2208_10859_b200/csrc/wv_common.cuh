@@ -35,6 +35,7 @@ struct Layout {
   uint64_t stack[WV_MAX_LEVELS + 1];     // level j (1..L): (L+1) masks
   uint64_t stack_stride[WV_MAX_LEVELS + 1];
   uint64_t fp[WV_MAX_LEVELS + 1];        // footprint intermediates, level 1..L-1
+  uint64_t pooled[WV_MAX_LEVELS + 1];    // D_j pooled to 32x32 cells: one word per 32x1024 tile
   uint64_t sel, prev_sel;                // NB-bit bitmaps
   uint64_t blist;                        // NB u32 entries
   int nty[WV_MAX_LEVELS + 1], ntx[WV_MAX_LEVELS + 1];  // tile grid of synthesis level k
@@ -60,6 +61,9 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
       g->mask_w < 1 || g->mask_h < 1 || (bs & (bs - 1)) || (n & (n - 1)))
     return WV_ERR_ARG;
   if ((W % 4) != 0) return WV_ERR_UNSUPPORTED;  // TMA row strides need 16-B multiples
+  // 32-bit index maps in the mask kernels
+  if ((uint64_t)W * g->mask_w >= (1ull << 32) || (uint64_t)H * g->mask_h >= (1ull << 32))
+    return WV_ERR_UNSUPPORTED;
   o->L = L; o->C = C; o->H = H; o->W = W; o->bs = bs; o->n = n;
   o->nbx = W / bs; o->NB = (W / bs) * (H / bs);
   o->mh = g->mask_h; o->mw = g->mask_w;
@@ -75,6 +79,8 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
     o->stack[j] = take(one * (L + 1));
   }
   for (int j = 1; j < L; ++j) o->fp[j] = take(uint64_t(H >> j) * o->wpr_[j] * 4);
+  for (int j = 1; j <= L; ++j)
+    o->pooled[j] = take(uint64_t(cdiv(H >> j, 32)) * cdiv(o->wpr_[j], 32) * 4);
   o->sel = take(uint64_t(wpr(o->NB)) * 4);
   o->prev_sel = take(uint64_t(wpr(o->NB)) * 4);
   o->blist = take(uint64_t(o->NB) * 4);

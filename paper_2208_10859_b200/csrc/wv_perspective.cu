@@ -54,55 +54,88 @@ __device__ __forceinline__ int wrapx(int x, int n) { return x < 0 ? x + n : (x >
 // float64 reference geometry evaluated for the pixel.
 constexpr float kNear = 4e-3f;
 
+// bits [x0, x0+len) of a footprint row (len <= 4), wrapping in longitude
+__device__ __forceinline__ uint32_t fp_bits(const uint32_t* row, int x0, int len, int n) {
+  if (x0 >= 0 && x0 + len <= n) {
+    const int w = x0 >> 5, sh = x0 & 31;
+    uint64_t v = row[w];
+    if (sh + len > 32) v |= (uint64_t)row[w + 1] << 32;
+    return (uint32_t)(v >> sh) & ((1u << len) - 1u);
+  }
+  uint32_t r = 0;
+  for (int i = 0; i < len; ++i) {
+    int xx = x0 + i;
+    xx = xx < 0 ? xx + n : (xx >= n ? xx - n : xx);
+    r |= ((row[xx >> 5] >> (xx & 31)) & 1u) << i;
+  }
+  return r;
+}
+
+struct ViewConst {
+  float r[9];
+  float tan_h, tan_v, inv_w, inv_h, sx, sy;
+};
+
 __global__ void __launch_bounds__(256) k_perspective(const __grid_constant__ Views views) {
+  __shared__ ViewConst vc;
   const wv_view_args& v = views.v[blockIdx.z];
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    for (int i = 0; i < 9; ++i) vc.r[i] = (float)v.rot[i];
+    vc.tan_h = (float)v.tan_h;
+    vc.tan_v = (float)v.tan_v;
+    vc.inv_w = 2.0f / (float)v.out_w;
+    vc.inv_h = 2.0f / (float)v.out_h;
+    vc.sx = (float)v.width * (1.0f / 360.0f);
+    vc.sy = (float)v.rows * (1.0f / 180.0f);
+  }
+  __syncthreads();
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
-  const bool live = x < v.out_w && y < v.out_h;
+  const int out_w = v.out_w, out_h = v.out_h;
+  const bool live = x < out_w && y < out_h;
   bool uncovered = false;
   if (live) {
     const int m = v.rows, n = v.width;
-    const float u = ((float)x + 0.5f) / (float)v.out_w * 2.0f - 1.0f;
-    const float w = 1.0f - ((float)y + 0.5f) / (float)v.out_h * 2.0f;
-    const float rx = u * (float)v.tan_h, ry = w * (float)v.tan_v;
+    const float u = ((float)x + 0.5f) * vc.inv_w - 1.0f;
+    const float w = 1.0f - ((float)y + 0.5f) * vc.inv_h;
+    const float rx = u * vc.tan_h, ry = w * vc.tan_v;
     const float inv = rsqrtf(rx * rx + ry * ry + 1.0f);
-    const double* R = v.rot;
-    const float wx = rx * (float)R[0] + ry * (float)R[1] + (float)R[2];
-    const float wy = rx * (float)R[3] + ry * (float)R[4] + (float)R[5];
-    const float wz = rx * (float)R[6] + ry * (float)R[7] + (float)R[8];
+    const float wx = rx * vc.r[0] + ry * vc.r[1] + vc.r[2];
+    const float wy = rx * vc.r[3] + ry * vc.r[4] + vc.r[5];
+    const float wz = rx * vc.r[6] + ry * vc.r[7] + vc.r[8];
     const float lon = atan2f(wx, wz) * 57.29577951308232f;
     const float lat = asinf(fminf(fmaxf(wy * inv, -1.0f), 1.0f)) * 57.29577951308232f;
-    const float fx = (lon + 180.0f) * ((float)n * (1.0f / 360.0f)) - 0.5f;
-    const float fy = (90.0f - lat) * ((float)m * (1.0f / 180.0f)) - 0.5f;
-    int x0 = (int)floorf(fx), y0 = (int)floorf(fy);
-    float ax = fx - floorf(fx), ay = fy - floorf(fy);
+    const float fx = (lon + 180.0f) * vc.sx - 0.5f;
+    const float fy = (90.0f - lat) * vc.sy - 0.5f;
+    const float flx = floorf(fx), fly = floorf(fy);
+    int x0 = (int)flx, y0 = (int)fly;
+    float ax = fx - flx, ay = fy - fly;
     const int wpr0 = (n + 31) >> 5;
     const uint32_t* F = v.d_footprint + (uint64_t)v.row0 * wpr0;
-    auto fp = [&](int yy, int xx) {
-      yy = min(max(yy, 0), m - 1);
-      xx = wrapx(xx, n);
-      return (F[(uint64_t)yy * wpr0 + (xx >> 5)] >> (xx & 31)) & 1u;
-    };
     const int xl = ax < kNear ? x0 - 1 : x0, xh = ax > 1.0f - kNear ? x0 + 2 : x0 + 1;
     const int yl = ay < kNear ? y0 - 1 : y0, yh = ay > 1.0f - kNear ? y0 + 2 : y0 + 1;
+    const int len = xh - xl + 1;
+    const uint32_t full = (1u << len) - 1u;
     bool ok = true;
     for (int yy = yl; yy <= yh; ++yy)
-      for (int xx = xl; xx <= xh; ++xx) ok = ok && fp(yy, xx);
+      ok = ok && fp_bits(F + (uint64_t)min(max(yy, 0), m - 1) * wpr0, xl, len, n) == full;
     if (!ok) {
       taps_f64(v, x, y, x0, y0, ax, ay);
-      uncovered = !(fp(y0, x0) & fp(y0, x0 + 1) & fp(y0 + 1, x0) & fp(y0 + 1, x0 + 1));
+      const uint32_t* r0 = F + (uint64_t)min(max(y0, 0), m - 1) * wpr0;
+      const uint32_t* r1 = F + (uint64_t)min(max(y0 + 1, 0), m - 1) * wpr0;
+      uncovered = (fp_bits(r0, x0, 2, n) & fp_bits(r1, x0, 2, n)) != 3u;
     }
     const int xa = wrapx(x0, n), xb = wrapx(x0 + 1, n);
     const int ya = min(max(y0, 0), m - 1), yb = min(max(y0 + 1, 0), m - 1);
     const int C = v.channels;
     const uint32_t plane = (uint32_t)v.canvas_h * (uint32_t)n;
-    const uint8_t* img = v.d_canvas + (uint64_t)v.row0 * n;
+    const uint8_t* img = v.d_canvas + (uint32_t)v.row0 * (uint32_t)n;
     const float one_x = __fsub_rn(1.0f, ax), one_y = __fsub_rn(1.0f, ay);
-    uint8_t* out = v.d_out + ((uint64_t)y * v.out_w + x) * C;
+    uint8_t* out = v.d_out + ((uint32_t)y * out_w + x) * C;
     const uint32_t o00 = (uint32_t)ya * n + xa, o01 = (uint32_t)ya * n + xb;
     const uint32_t o10 = (uint32_t)yb * n + xa, o11 = (uint32_t)yb * n + xb;
     for (int c = 0; c < C; ++c) {
-      const uint8_t* pc = img + (uint64_t)c * plane;
+      const uint8_t* pc = img + c * plane;
       const float p00 = pc[o00], p01 = pc[o01], p10 = pc[o10], p11 = pc[o11];
       const float top = __fadd_rn(__fmul_rn(p00, one_x), __fmul_rn(p01, ax));
       const float bot = __fadd_rn(__fmul_rn(p10, one_x), __fmul_rn(p11, ax));

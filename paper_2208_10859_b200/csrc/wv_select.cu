@@ -75,24 +75,27 @@ __global__ void k_mask_rows(const uint8_t* __restrict__ mask, uint32_t* __restri
                             uint32_t* __restrict__ rowmap, int mh, int mw, int W, int H, int wpr0,
                             int full) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx < H) rowmap[idx] = (uint32_t)(((uint64_t)idx * mh) / H);
+  if (idx < H) rowmap[idx] = ((uint32_t)idx * (uint32_t)mh) / (uint32_t)H;
   if (idx >= mh * wpr0) return;
   const int my = idx / wpr0, w = idx % wpr0;
   uint32_t bits = 0;
   for (int i = 0; i < 32; ++i) {
     const int x = 32 * w + i;
     if (x >= W) break;
-    const int mx = (int)(((uint64_t)x * mw) / W);
+    const int mx = (int)(((uint32_t)x * (uint32_t)mw) / (uint32_t)W);   // < 2^32 (checked on host)
     if (full || mask[(uint64_t)my * mw + mx]) bits |= 1u << i;
   }
   R[idx] = bits;
 }
 
 // ------------------------------------------------------------- cascade step
-// C_j = dilate4(downmap2(C_{j-1})) on a 32-row x 8-word output tile: the
-// pooled words of the tile plus a 4-row / 1-word apron are staged in shared
-// memory once, then each thread ORs its 9x3 neighbourhood.
-constexpr int CT_R = 32, CT_W = 8;
+// C_j = dilate4(downmap2(C_{j-1})) on a 32-row x 32-word output tile (each
+// thread 4 words of one row): the pooled words of the tile plus a 4-row /
+// 1-word apron are staged in shared memory once, then each thread ORs its
+// 9-row neighbourhood.  The CTA that produces the final detail mask D_j also
+// pools it into one bit per 32x32 cell (used by the block selection when
+// block_size is 32).
+constexpr int CT_R = 32, CT_W = 32, CT_TW = 8;   // tile rows, tile words, threads per row
 
 struct CascadeArgs {
   int j, L, H;
@@ -108,6 +111,8 @@ struct CascadeArgs {
   int batch[WV_MAX_LEVELS + 1];
   int rect[WV_MAX_LEVELS + 1][4];  // j == 1 foveated windows, by batch id
   int fov;                         // foveated: batch j also ANDs with batch 0
+  uint32_t* pooled;                // one word per tile: bit w = any bit in (32 rows x word w)
+  int pool_wpr;                    // tiles per row of the level
 };
 
 __device__ __forceinline__ uint32_t cas_src(const CascadeArgs& a, int b, int rr, int ww) {
@@ -133,9 +138,12 @@ __device__ __forceinline__ uint32_t cas_down(const CascadeArgs& a, int b, int r,
 
 __global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
   __shared__ uint32_t dm[2][CT_R + 2 * DIL][CT_W + 2];
+  __shared__ uint32_t pool[CT_W];
   const int b = a.batch[blockIdx.y];
   const bool both = a.fov && b == a.j;
+  const bool final_mask = a.fov ? (b == a.j) : (b == 0);
   const int r0 = blockIdx.z * CT_R, w0 = blockIdx.x * CT_W;
+  if (threadIdx.x < CT_W) pool[threadIdx.x] = 0;
   for (int e = threadIdx.x; e < (CT_R + 2 * DIL) * (CT_W + 2); e += blockDim.x) {
     const int lr = e / (CT_W + 2), lw = e % (CT_W + 2);
     const int r = r0 - DIL + lr, w = w0 - 1 + lw;
@@ -145,25 +153,46 @@ __global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
       if (both) v1 = cas_down(a, 0, r, w);
     }
     dm[0][lr][lw] = v0;
-    dm[1][lr][lw] = v1;
+    if (both) dm[1][lr][lw] = v1;
   }
   __syncthreads();
-  const int tr = threadIdx.x / CT_W, tw = threadIdx.x % CT_W;
-  const int r = r0 + tr, w = w0 + tw;
-  if (r >= a.rows || w >= a.wpr) return;
-  uint32_t p = 0, c = 0, n = 0, p1 = 0, c1 = 0, n1 = 0;
+  const int tr = threadIdx.x / CT_TW, tq = threadIdx.x % CT_TW;
+  const int r = r0 + tr;
+  if (r < a.rows) {
 #pragma unroll
-  for (int k = 0; k <= 2 * DIL; ++k) {
-    p |= dm[0][tr + k][tw];
-    c |= dm[0][tr + k][tw + 1];
-    n |= dm[0][tr + k][tw + 2];
-    p1 |= dm[1][tr + k][tw];
-    c1 |= dm[1][tr + k][tw + 1];
-    n1 |= dm[1][tr + k][tw + 2];
+    for (int q = 0; q < CT_W / CT_TW; ++q) {
+      const int lw = tq + q * CT_TW, w = w0 + lw;
+      if (w >= a.wpr) break;
+      uint32_t p = 0, c = 0, n = 0;
+#pragma unroll
+      for (int k = 0; k <= 2 * DIL; ++k) {
+        p |= dm[0][tr + k][lw];
+        c |= dm[0][tr + k][lw + 1];
+        n |= dm[0][tr + k][lw + 2];
+      }
+      uint32_t v = spread(p, c, n);
+      if (both) {
+        uint32_t p1 = 0, c1 = 0, n1 = 0;
+#pragma unroll
+        for (int k = 0; k <= 2 * DIL; ++k) {
+          p1 |= dm[1][tr + k][lw];
+          c1 |= dm[1][tr + k][lw + 1];
+          n1 |= dm[1][tr + k][lw + 2];
+        }
+        v &= spread(p1, c1, n1);
+      }
+      v &= last_word_mask(a.cols, w);
+      a.dst[(uint64_t)b * a.dst_stride + (uint64_t)r * a.wpr + w] = v;
+      if (final_mask && v) atomicOr(&pool[lw], 1u);
+    }
   }
-  uint32_t v = spread(p, c, n);
-  if (both) v &= spread(p1, c1, n1);
-  a.dst[(uint64_t)b * a.dst_stride + (uint64_t)r * a.wpr + w] = v & last_word_mask(a.cols, w);
+  if (final_mask && a.pooled) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const uint32_t bits = __ballot_sync(0xFFFFFFFFu, threadIdx.x < CT_W && pool[threadIdx.x]);
+      if (threadIdx.x == 0) a.pooled[(uint64_t)blockIdx.z * a.pool_wpr + blockIdx.x] = bits;
+    }
+  }
 }
 
 // ----------------------------------------------------------- footprint step
@@ -182,7 +211,7 @@ struct FootArgs {
 };
 
 constexpr int FP_SR = CT_R / 2 + DIL + 1;  // source rows staged per tile (21)
-constexpr int FP_SW = CT_W / 2 + 2;        // source words staged per tile (6)
+constexpr int FP_SW = CT_W / 2 + 2;        // source words staged per tile (18)
 
 __global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
   __shared__ uint32_t sv[FP_SR][FP_SW];
@@ -199,25 +228,31 @@ __global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
     sv[lr][lw] = v;
   }
   __syncthreads();
-  const int tr = threadIdx.x / CT_W, tw = threadIdx.x % CT_W;
-  const int r = r0 + tr, w = w0 + tw;
-  if (r >= a.rows || w >= a.wpr) return;
+  const int tr = threadIdx.x / CT_TW, tq = threadIdx.x % CT_TW;
+  const int r = r0 + tr;
+  if (r >= a.rows) return;
   const int s_lo = ((r - DIL) >> 1) - sr0, s_hi = ((r + DIL) >> 1) - sr0;
-  uint32_t nb[3];
+  const uint32_t req_row = a.j == 1 ? a.rowmap[r] : 0u;
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    const int ww = w - 1 + q;
-    if (ww < 0 || ww >= a.wpr) {
-      nb[q] = 0xFFFFFFFFu;
-      continue;
+  for (int q = 0; q < CT_W / CT_TW; ++q) {
+    const int w = w0 + tq + q * CT_TW;
+    if (w >= a.wpr) break;
+    uint32_t nb[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int ww = w - 1 + d;
+      if (ww < 0 || ww >= a.wpr) {
+        nb[d] = 0xFFFFFFFFu;
+        continue;
+      }
+      uint32_t v = 0xFFFFFFFFu;
+      for (int k = s_lo; k <= s_hi; ++k) v &= sv[k][(ww >> 1) - sw0];
+      nb[d] = double_bits(v >> (16 * (ww & 1))) | ~last_word_mask(a.cols, ww);
     }
-    uint32_t v = 0xFFFFFFFFu;
-    for (int k = s_lo; k <= s_hi; ++k) v &= sv[k][(ww >> 1) - sw0];
-    nb[q] = double_bits(v >> (16 * (ww & 1))) | ~last_word_mask(a.cols, ww);
+    uint32_t v = shrink(nb[0], nb[1], nb[2]) & last_word_mask(a.cols, w);
+    if (a.j == 1) v &= a.R[(uint64_t)req_row * a.wpr + w];
+    a.out[(uint64_t)r * a.wpr + w] = v;
   }
-  uint32_t v = shrink(nb[0], nb[1], nb[2]) & last_word_mask(a.cols, w);
-  if (a.j == 1) v &= a.R[(uint64_t)a.rowmap[r] * a.wpr + w];
-  a.out[(uint64_t)r * a.wpr + w] = v;
 }
 
 // -------------------------------------------------------------- block select
@@ -238,6 +273,8 @@ struct BlockArgs {
   unsigned long long* set_bytes;
   wv_frame_result* res;
   int account_only;
+  const uint32_t* pooled[WV_MAX_LEVELS + 1];   // nullptr: scan rows
+  int pool_wpr[WV_MAX_LEVELS + 1];
 };
 
 __device__ __forceinline__ bool row_any(const uint32_t* row, int c0, int c1) {
@@ -263,90 +300,93 @@ __device__ bool incl_row_any(const BlockArgs& a, int y, int x0, int x1) {
   return false;
 }
 
-constexpr int BLK_WARPS = 8;
-
-__global__ void __launch_bounds__(32 * BLK_WARPS) k_blocks(BlockArgs a) {
-  __shared__ uint32_t s_sel[BLK_WARPS], s_emit[BLK_WARPS], s_base, s_miss;
-  __shared__ unsigned long long s_recs, s_newb;
-  __shared__ uint32_t s_err;
-  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const int b = blockIdx.x * BLK_WARPS + wi;
-  if (threadIdx.x == 0) { s_recs = 0; s_newb = 0; s_err = 0; s_miss = 0; }
-  bool sel = false;
-  if (b < a.NB) {
-    const int by = b / a.nbx, bx = b % a.nbx;
-    const int x0 = bx * a.bs, x1 = x0 + a.bs;
-    bool any = false;
-    for (int r = lane; r < a.bs; r += 32) any |= incl_row_any(a, by * a.bs + r, x0, x1);
-    sel = __any_sync(0xFFFFFFFFu, any);
+// Thread per block.  A block lying inside one subband quadrant of one level
+// reads its "any" bit from the level's 32x32-pooled mask (block_size 32 with
+// 32-aligned subbands: every block at the 8K configuration); other blocks
+// scan their rows.  A warp owns 32 consecutive blocks = one bitmap word.
+__device__ bool block_any(const BlockArgs& a, int b) {
+  const int by = b / a.nbx, bx = b - (b / a.nbx) * a.nbx;
+  const int y0 = by * a.bs, x0 = bx * a.bs, y1 = y0 + a.bs, x1 = x0 + a.bs;
+  if (y0 < (a.H >> a.L) && x0 < (a.W >> a.L)) return true;
+  for (int k = 1; k <= a.L; ++k) {
+    const int bh = a.H >> k, bw = a.W >> k;
+    const bool top = y1 <= bh, bot = y0 >= bh && y1 <= 2 * bh;
+    const bool left = x1 <= bw, right = x0 >= bw && x1 <= 2 * bw;
+    if ((top && right) || (bot && (left || right))) {
+      const int r0 = bot ? y0 - bh : y0, c0 = right ? x0 - bw : x0;
+      if (a.pooled[k] && !(r0 & 31) && !(c0 & 31)) {
+        const int w = c0 >> 5;
+        return (a.pooled[k][(uint64_t)(r0 >> 5) * a.pool_wpr[k] + (w >> 5)] >> (w & 31)) & 1u;
+      }
+      break;
+    }
+    if (!(y1 <= bh && x1 <= bw)) break;   // straddles quadrants: scan rows
   }
+  for (int r = y0; r < y1; ++r)
+    if (incl_row_any(a, r, x0, x1)) return true;
+  return false;
+}
+
+__global__ void __launch_bounds__(256) k_blocks(BlockArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = b < a.NB;
+  const bool sel = valid && block_any(a, b);
   unsigned long long bytes = 0, recs = 0;
   uint32_t err = 0;
   if (sel) {
-    for (int t = lane; t < a.n; t += 32) {
+    unsigned long long prev = b ? a.ends[b - 1] : 0ull;
+    for (int t = 0; t < a.n; ++t) {
       const uint64_t i = (uint64_t)t * a.NB + b;
       const unsigned long long e = a.ends[i];
-      const unsigned long long s = i ? a.ends[i - 1] : 0ull;
-      if (e < s || e > a.rec_bytes || (e - s) % a.rs ||
-          (e - s) / a.rs > (unsigned long long)a.bs * a.bs)
+      const unsigned long long st = t ? a.ends[i - 1] : prev;
+      if (e < st || e > a.rec_bytes || (e - st) % a.rs ||
+          (e - st) / a.rs > (unsigned long long)a.bs * a.bs)
         err |= WV_DERR_TABLE;
       else {
-        bytes += e - s;
-        recs += (e - s) / a.rs;
+        bytes += e - st;
+        recs += (e - st) / a.rs;
       }
     }
-    for (int o = 16; o; o >>= 1) {
-      bytes += __shfl_xor_sync(0xFFFFFFFFu, bytes, o);
-      recs += __shfl_xor_sync(0xFFFFFFFFu, recs, o);
-      err |= __shfl_xor_sync(0xFFFFFFFFu, err, o);
-    }
   }
-  __syncthreads();
-  const uint32_t word = (uint32_t)b >> 5, bit = 1u << (b & 31);
-  if (lane == 0 && b < a.NB) {
-    const bool prev = (a.prev_sel[word] & bit) != 0;
-    const bool was = (a.loaded[word] & bit) != 0;
-    s_sel[wi] = sel;
-    s_emit[wi] = !a.account_only && (sel || prev);
-    if (sel) {
-      atomicOr(&a.sel[word], bit);
-      if (!was) {
-        atomicOr(&a.loaded[word], bit);
-        atomicAdd(&s_newb, bytes);
-        atomicAdd(&s_miss, 1u);
-      }
-      atomicAdd(&s_recs, recs);
-      if (err) atomicOr(&s_err, err);
-    } else {
-      atomicAnd(&a.sel[word], ~bit);
-    }
-    if (!a.account_only) {
-      if (sel) atomicOr(&a.prev_sel[word], bit);
-      else if (prev) atomicAnd(&a.prev_sel[word], ~bit);
-    }
-  } else if (lane == 0) {
-    s_sel[wi] = 0;
-    s_emit[wi] = 0;
+  const uint32_t word = (uint32_t)(blockIdx.x * blockDim.x + (threadIdx.x & ~31)) >> 5;
+  const uint32_t selmask = __ballot_sync(0xFFFFFFFFu, sel);
+  uint32_t prevw = 0, loadw = 0;
+  if (lane == 0 && (word << 5) < (uint32_t)a.NB) {
+    prevw = a.prev_sel[word];
+    loadw = a.loaded[word];
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t ne = 0, ns = 0;
-    for (int i = 0; i < BLK_WARPS; ++i) { ne += s_emit[i]; ns += s_sel[i]; }
-    s_base = ne ? atomicAdd(a.list_count, ne) : 0u;
-    uint32_t pos = s_base;
-    for (int i = 0; i < BLK_WARPS; ++i) {
-      if (!s_emit[i]) continue;
-      const uint32_t bb = (uint32_t)(blockIdx.x * BLK_WARPS + i);
-      a.list[pos++] = s_sel[i] ? bb : (bb | ZERO_FLAG);
+  prevw = __shfl_sync(0xFFFFFFFFu, prevw, 0);
+  loadw = __shfl_sync(0xFFFFFFFFu, loadw, 0);
+  const bool prev = valid && ((prevw >> lane) & 1u);
+  const bool was = (loadw >> lane) & 1u;
+  const bool missing = sel && !was;
+  const bool emit = !a.account_only && (sel || prev);
+  const uint32_t emask = __ballot_sync(0xFFFFFFFFu, emit);
+  uint32_t base = 0;
+  if (lane == 0 && emask) base = atomicAdd(a.list_count, (uint32_t)__popc(emask));
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  if (emit)
+    a.list[base + __popc(emask & ((1u << lane) - 1u))] = sel ? (uint32_t)b : ((uint32_t)b | ZERO_FLAG);
+  unsigned long long newb = missing ? bytes : 0ull;
+  const uint32_t nmiss = __popc(__ballot_sync(0xFFFFFFFFu, missing));
+  for (int o = 16; o; o >>= 1) {
+    recs += __shfl_xor_sync(0xFFFFFFFFu, recs, o);
+    newb += __shfl_xor_sync(0xFFFFFFFFu, newb, o);
+    err |= __shfl_xor_sync(0xFFFFFFFFu, err, o);
+  }
+  if (lane == 0 && (word << 5) < (uint32_t)a.NB) {
+    a.sel[word] = selmask;
+    if (!a.account_only) a.prev_sel[word] = selmask;
+    a.loaded[word] = loadw | selmask;
+    if (recs) atomicAdd(&a.res->records, recs);
+    if (newb) {
+      atomicAdd(&a.res->new_bytes, newb);
+      atomicAdd(a.set_bytes, newb);
     }
-    if (s_recs) atomicAdd(&a.res->records, s_recs);
-    if (s_newb) {
-      atomicAdd(&a.res->new_bytes, s_newb);
-      atomicAdd(a.set_bytes, s_newb);
-    }
-    if (s_miss) atomicAdd(&a.res->n_missing, s_miss);
-    if (ns) atomicAdd(&a.res->n_selected, ns);
-    if (s_err) atomicOr(&a.res->error, s_err);
+    if (nmiss) atomicAdd(&a.res->n_missing, nmiss);
+    if (selmask) atomicAdd(&a.res->n_selected, (uint32_t)__popc(selmask));
+    if (err) atomicOr(&a.res->error, err);
   }
 }
 
@@ -407,23 +447,38 @@ __global__ void __launch_bounds__(256) k_tiles1(TileArgs a) {
   if (t == 0) a.res->set_bytes = *a.set_bytes;
 }
 
-__global__ void __launch_bounds__(256) k_tiles_up(TileArgs a) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= a.base[a.L + 1]) return;
-  int k = 2;
-  while (g >= a.base[k + 1]) ++k;
-  const int t = g - a.base[k];
-  const int u = t / a.ntx[k], v = t % a.ntx[k];
-  const int m = k - 1, s = 1 << m;
-  const int ylo = max(s * u - (s - 1), 0), yhi = min(s * u + 2 * (s - 1), a.nty[1] - 1);
-  const int xlo = max(s * v - (s - 1), 0), xhi = min(s * v + 2 * (s - 1), a.ntx[1] - 1);
-  bool nd = false;
-  for (int y = ylo; y <= yhi && !nd; ++y) {
-    const uint32_t* row = a.need1 + (uint64_t)y * a.nwords1;
-    for (int w = xlo >> 5; w <= (xhi >> 5); ++w)
-      if (row[w] & range_mask(xlo, xhi + 1, w)) { nd = true; break; }
+// Coarser levels in one CTA: need maps live as bit rows in shared memory and
+// level k is derived from level k-1 (rows 2u-1..2u+2 x cols 2v-1..2v+2).
+__global__ void __launch_bounds__(1024) k_tiles_up(TileArgs a) {
+  extern __shared__ uint32_t nbits[];
+  __shared__ uint32_t cnt;
+  int off[WV_MAX_LEVELS + 2];
+  off[1] = 0;
+  for (int k = 1; k <= a.L; ++k) off[k + 1] = off[k] + a.nty[k] * wpr(a.ntx[k]);
+  for (int i = threadIdx.x; i < off[a.L + 1]; i += blockDim.x)
+    nbits[i] = i < off[2] ? a.need1[i] : 0u;
+  __syncthreads();
+  for (int k = 2; k <= a.L; ++k) {
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    const int ntx = a.ntx[k], nt = a.nty[k] * ntx;
+    const int fy = a.nty[k - 1], fx = a.ntx[k - 1], fw = wpr(fx);
+    const uint32_t* prev = nbits + off[k - 1];
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+      const int u = t / ntx, v = t - (t / ntx) * ntx;
+      const int x0 = max(2 * v - 1, 0), x1 = min(2 * v + 2, fx - 1);
+      bool nd = false;
+      for (int ty = max(2 * u - 1, 0); ty <= min(2 * u + 2, fy - 1) && !nd; ++ty)
+        for (int w = x0 >> 5; w <= (x1 >> 5); ++w)
+          if (prev[ty * fw + w] & range_mask(x0, x1 + 1, w)) { nd = true; break; }
+      if (nd) {
+        atomicOr(&nbits[off[k] + u * wpr(ntx) + (v >> 5)], 1u << (v & 31));
+        a.list[k][atomicAdd(&cnt, 1u)] = (uint32_t)t;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) a.counters[CNT_TILES + k] = cnt;
   }
-  if (nd) a.list[k][atomicAdd(&a.counters[CNT_TILES + k], 1u)] = (uint32_t)t;
 }
 
 __global__ void k_finalize(const unsigned long long* set_bytes, wv_frame_result* res) {
@@ -468,6 +523,8 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
       for (int k = 1; k <= L; ++k)
         for (int q = 0; q < 4; ++q) c.rect[k][q] = a->fovea[k - 1][q];
     }
+    c.pooled = lo.bs == 32 ? (uint32_t*)(ws + lo.pooled[j]) : nullptr;
+    c.pool_wpr = cdiv(c.wpr, CT_W);
     dim3 grid(cdiv(c.wpr, CT_W), c.nbatch, cdiv(c.rows, CT_R));
     k_cascade<<<grid, 256, 0, s>>>(c);
   }
@@ -504,7 +561,12 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
     b.set_bytes = a->d_set_bytes;
     b.res = a->d_result;
     b.account_only = acct;
-    k_blocks<<<cdiv(lo.NB, BLK_WARPS), 32 * BLK_WARPS, 0, s>>>(b);
+    for (int k = 1; k <= L; ++k) {
+      const bool ok = lo.bs == 32 && ((H >> k) % 32) == 0 && ((W >> k) % 32) == 0;
+      b.pooled[k] = ok ? (const uint32_t*)(ws + lo.pooled[k]) : nullptr;
+      b.pool_wpr[k] = cdiv(lo.wpr_[k], CT_W);
+    }
+    k_blocks<<<cdiv(lo.NB, 256), 256, 0, s>>>(b);
   }
   if (acct) {
     k_finalize<<<1, 1, 0, s>>>(a->d_set_bytes, a->d_result);
@@ -525,7 +587,15 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
     for (int k = 2; k <= L; ++k) t.base[k + 1] = t.base[k] + lo.nty[k] * lo.ntx[k];
     const int nt1 = lo.nty[1] * lo.ntx[1];
     k_tiles1<<<cdiv(nt1, 256), 256, 0, s>>>(t);
-    if (L >= 2) k_tiles_up<<<cdiv(max(t.base[L + 1], 1), 256), 256, 0, s>>>(t);
+    if (L >= 2) {
+      size_t words = 0;
+      for (int k = 1; k <= L; ++k) words += (size_t)lo.nty[k] * wpr(lo.ntx[k]);
+      if (words * 4 > 200 * 1024) return WV_ERR_UNSUPPORTED;
+      if (words * 4 > 48 * 1024)
+        WV_CUDA(cudaFuncSetAttribute(k_tiles_up, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(words * 4)));
+      k_tiles_up<<<1, 1024, words * 4, s>>>(t);
+    }
   }
   WV_CUDA(cudaGetLastError());
   return WV_OK;

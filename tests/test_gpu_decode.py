@@ -1,0 +1,319 @@
+"""GPU decode path: perspective parity, reference-suite behaviours
+(pkg/tests/test_decoding.py, test_acceptance.py, test_projection.py) and
+larger-frame parity against the CPU oracle."""
+import os
+import shutil
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, unpack_mask
+from oracle import wavevid_oracle as wo
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def wv():
+    import paper_2208_10859_b200 as p
+    from paper_2208_10859_b200 import build
+    build.build()
+    return p
+
+
+@pytest.fixture(scope="module")
+def clip512():
+    from paper_2208_10859_b200.synthetic import make_synthetic_clip
+    return make_synthetic_clip(16, 512)
+
+
+@pytest.fixture(scope="module")
+def hq512(wv, clip512, tmp_path_factory):
+    """test_acceptance.py hq_file: 512^2, 16 frames, L5, HQ params."""
+    path = tmp_path_factory.mktemp("acc") / "hq.wvv"
+    p = wv.EncodeParams(levels=5, mapping=wv.MappingKind.NONE, alpha=0.1, inter_threshold=0.005)
+    wv.write_video(wv.encode_video(clip512, p), path)
+    return path
+
+
+# ------------------------------------------------------------ perspective
+
+def test_perspective_matches_reference_fixtures(wv):
+    want = np.load(os.path.join(GOLDEN, "projection.npz"))
+    for fname in ("smooth_hq.wvv", "golden_stereo.wvv"):
+        sess = wv.DecodeSession(os.path.join(GOLDEN, fname))
+        h = sess.header
+        done = set()
+        for k in sorted(k for k in want.files if k.startswith(f"persp|{fname}|")):
+            _, _, i, e = k.split("|")
+            i, e = int(i), int(e)
+            yaw, pitch, roll, fh, fv = want[f"pose|{i}"]
+            pose = wv.CameraPose(float(yaw), float(pitch), float(roll), float(fh), float(fv))
+            key = f"{'smask' if h.stereo else 'vmask'}|{i}|{h.mask_w}x{h.mask_h}"
+            mk = unpack_mask(want[key], (h.mask_h, h.mask_w))
+            if (i, 0) not in done:
+                pix, fp, _ = sess.decode_viewport(i % h.frame_count, mk)
+                done.add((i, 0))
+            half = h.height // 2 if h.stereo else h.height
+            reg, f = pix[e * half:(e + 1) * half], fp[e * half:(e + 1) * half]
+            ref = want[k]
+            if ref.dtype.kind == "U":
+                with pytest.raises(wv.CoverageError):
+                    wv.render_perspective(reg, f, pose, (40, 24))
+            else:
+                got = wv.render_perspective(reg, f, pose, (40, 24))
+                d = np.abs(got.astype(int) - ref.astype(int))
+                assert d.max() <= 1, (fname, i, e, d.max())
+        sess.close()
+
+
+def test_perspective_against_oracle_random_poses(wv):
+    rng = np.random.default_rng(5)
+    region = rng.integers(0, 256, (256, 512, 3), dtype=np.uint8)
+    fp = np.ones((256, 512), bool)
+    for _ in range(25):
+        pose = wv.CameraPose(yaw=rng.uniform(-180, 180), pitch=rng.uniform(-89, 89),
+                             roll=rng.uniform(-30, 30), fov_h=rng.uniform(30, 150),
+                             fov_v=rng.uniform(30, 150))
+        got = wv.render_perspective(region, fp, pose, (97, 61))
+        ref = wo.perspective(region, fp, pose.rotation(), pose.fov_h, pose.fov_v, 97, 61)
+        assert np.abs(got.astype(int) - ref.astype(int)).max() <= 1
+
+
+def test_perspective_coverage_matches_oracle(wv):
+    """Partial footprints: CoverageError exactly when the oracle raises."""
+    rng = np.random.default_rng(9)
+    region = rng.integers(0, 256, (128, 256, 3), dtype=np.uint8)
+    for _ in range(30):
+        fp = np.zeros((128, 256), bool)
+        y, x = rng.integers(0, 100), rng.integers(0, 220)
+        fp[y:y + rng.integers(10, 128), x:x + rng.integers(10, 256)] = True
+        pose = wv.CameraPose(yaw=rng.uniform(-180, 180), pitch=rng.uniform(-60, 60),
+                             fov_h=rng.uniform(20, 90), fov_v=rng.uniform(20, 90))
+        try:
+            ref = wo.perspective(region, fp, pose.rotation(), pose.fov_h, pose.fov_v, 48, 32)
+        except wo.Uncovered:
+            with pytest.raises(wv.CoverageError):
+                wv.render_perspective(region, fp, pose, (48, 32))
+            continue
+        got = wv.render_perspective(region, fp, pose, (48, 32))
+        assert np.abs(got.astype(int) - ref.astype(int)).max() <= 1
+
+
+def test_perspective_constant_and_identity(wv):
+    # test_projection.py:139-155
+    region = np.full((128, 256, 3), 77, np.uint8)
+    fp = np.ones((128, 256), bool)
+    out = wv.render_perspective(region, fp, wv.CameraPose(yaw=12, pitch=-5), (64, 64))
+    assert (out == 77).all()
+    region = np.zeros((128, 256, 3), np.uint8)
+    region[63:65, 127:129] = (200, 10, 30)
+    out = wv.render_perspective(region, fp, wv.CameraPose(), (65, 65))
+    assert tuple(out[32, 32]) == (200, 10, 30)
+
+
+def test_perspective_errors(wv):
+    region = np.zeros((64, 128), np.uint8)
+    with pytest.raises(wv.ProjectionError):
+        wv.render_perspective(region, np.ones((64, 128), bool), wv.CameraPose(fov_h=180), (32, 32))
+    with pytest.raises(wv.CoverageError):
+        wv.render_perspective(np.zeros((64, 128, 3), np.uint8), np.zeros((64, 128), bool),
+                              wv.CameraPose(), (16, 16))
+
+
+def test_hundred_random_poses_covered(wv):
+    # test_projection.py:159-176 on the conftest quantized file
+    rng = np.random.default_rng(42)
+    sess = wv.DecodeSession(os.path.join(GOLDEN, "smooth_hq.wvv"))
+    h = sess.header
+    for _ in range(100):
+        pose = wv.CameraPose(yaw=rng.uniform(-180, 180), pitch=rng.uniform(-85, 85),
+                             roll=rng.uniform(-10, 10), fov_h=rng.uniform(60, 120),
+                             fov_v=rng.uniform(60, 120))
+        mask = wv.viewport_to_mask(pose, (h.mask_w, h.mask_h))
+        sess.decode_viewport_device(0, mask)
+        sess.render_views(pose, (32, 32))       # raises CoverageError if not covered
+    sess.close()
+
+
+# --------------------------------------------------- reference behaviours
+
+def test_roi_exactness_hundred_masks(wv, hq512):
+    """test_acceptance.py:96-117, plus every pixel == oracle."""
+    rng = np.random.default_rng(99)
+    full, _, _ = wv.DecodeSession(hq512).decode_full(3)
+    sess = wv.DecodeSession(hq512)
+    ref = wo.OracleSession(hq512)
+    for i in range(100):
+        mask = np.zeros((64, 64), bool)
+        w, h = rng.integers(4, 40, 2)
+        x, y = rng.integers(0, 64 - w), rng.integers(0, 64 - h)
+        mask[y:y + h, x:x + w] = True
+        pix, fp, st = sess.decode_viewport(3, mask)
+        assert (pix[fp] == full[fp]).all()
+        rp, rf, rs = ref.decode(3, "viewport", mask)     # same call history: same stats
+        assert (st.bytes_loaded, st.records_processed) == (rs.bytes_loaded, rs.records_processed)
+        if i % 10 == 0:
+            np.testing.assert_array_equal(pix, rp)
+            np.testing.assert_array_equal(fp, rf)
+
+
+def test_quantized_psnr_and_oracle_psnr_equal(wv, clip512, hq512):
+    """PSNR >= 40 dB (test_acceptance.py:84-93) and identical to the oracle's
+    PSNR to 0.01 dB (north-star parity bar)."""
+    sess = wv.DecodeSession(hq512)
+    ref = wo.OracleSession(hq512)
+    for f in (0, 8, 15):
+        pix, _, _ = sess.decode_full(f)
+        rp, _, _ = ref.decode(f, "full")
+        a, b = wv.psnr(pix, clip512[f]), wv.psnr(rp, clip512[f])
+        assert a >= 40.0 and abs(a - b) < 0.01
+
+
+def test_lossless_path(wv, clip512, tmp_path):
+    path = tmp_path / "lossless.wvv"
+    p = wv.EncodeParams(levels=5, mapping=wv.MappingKind.NONE, alpha=0.0, inter_threshold=0.0,
+                        quantize=False)
+    wv.write_video(wv.encode_video(clip512, p), path)
+    sess = wv.DecodeSession(path)
+    for f in (0, 7, 15):
+        pix, _, _ = sess.decode_full(f)
+        assert np.abs(pix.astype(int) - clip512[f].astype(int)).max() <= 1
+        assert wv.psnr(pix, clip512[f]) >= 60.0
+
+
+def test_foveation_savings(wv, hq512):
+    # test_acceptance.py:183-197
+    pose = wv.CameraPose(yaw=30, pitch=10, fov_h=90, fov_v=90)
+    mask = wv.viewport_to_mask(pose, (64, 64))
+    _, _, vs = wv.DecodeSession(hq512).decode_viewport(0, mask)
+    s = wv.DecodeSession(hq512)
+    _, _, fs = s.decode_foveated(0, mask, wv.FoveationSchedule.default(s.header.levels))
+    assert 1.0 - fs.bytes_loaded / vs.bytes_loaded >= 0.5
+
+
+def test_keyframe_freedom_and_cache(wv, hq512):
+    mask = np.ones((64, 64), bool)
+    sess = wv.DecodeSession(hq512)
+    n = sess.header.inter_size
+    for frame in [13, 2, 9, 0, 15, 6]:
+        before = len(sess.reader.io_trace)
+        sess.decode_viewport(frame, mask)
+        assert {e[0] for e in sess.reader.io_trace[before:]} <= {frame // n}
+    sess2 = wv.DecodeSession(hq512)
+    for frame in (0, 4, 0, 4, 0):
+        sess2.decode_viewport(frame, mask)
+        assert len(sess2._cache) <= 2
+
+
+def test_stats_monotone_and_errors(wv):
+    path = os.path.join(GOLDEN, "smooth_hq.wvv")
+    mask = np.zeros((64, 64), bool)
+    mask[10:50, 10:50] = True
+    with wv.DecodeSession(path) as s:
+        seen = []
+        for frame in range(4):
+            s.decode_viewport(frame, mask)
+            st = s.stats
+            seen.append((st.bytes_loaded, st.records_processed, st.frames_decoded))
+        assert seen == sorted(seen)
+        with pytest.raises(wv.DecodeError):
+            s.decode_viewport(0, np.ones((32, 32), bool))
+        with pytest.raises(wv.DecodeError):
+            s.decode_full(99)
+        with pytest.raises(wv.DecodeError):
+            wv.FoveationSchedule((1.0, 0.2, 0.5))
+
+
+def test_prefetch_mask_enlarged(wv):
+    # test_decoding.py:233-247
+    path = os.path.join(GOLDEN, "smooth_hq.wvv")
+    small = np.zeros((64, 64), bool)
+    small[24:40, 24:40] = True
+    large = np.zeros((64, 64), bool)
+    large[8:56, 8:56] = True
+    with wv.DecodeSession(path) as s:
+        s.decode_viewport(0, small)
+        s.advance(0, small)
+        s.join_prefetch()
+        grown, gf, gs = s.decode_viewport(4, large)
+    with wv.DecodeSession(path) as f:
+        want, wf, ws = f.decode_viewport(4, large)
+    np.testing.assert_array_equal(gf, wf)
+    np.testing.assert_array_equal(grown, want)
+    # the prefetched blocks were already accounted: fewer new bytes
+    assert gs.bytes_loaded < ws.bytes_loaded
+
+
+def test_corrupt_offset_raises(wv, tmp_path):
+    src = os.path.join(GOLDEN, "golden_quantized.wvv")
+    dst = tmp_path / "corrupt.wvv"
+    shutil.copy(src, dst)
+    raw = bytearray(open(dst, "rb").read())
+    from paper_2208_10859_b200.fileio import read_header
+    h, metas = read_header(src)
+    rec0 = metas[0].payload_offset + h.table_bytes
+    raw[rec0:rec0 + 2] = (0xFFFF).to_bytes(2, "little")   # offset 65535 >= 32*32
+    open(dst, "wb").write(bytes(raw))
+    with wv.DecodeSession(dst) as s:
+        with pytest.raises(wv.CorruptStreamError):
+            s.decode_full(0)
+
+
+# ------------------------------------------------------ larger frames
+
+@pytest.mark.parametrize("mode", ["viewport", "foveated", "full"])
+def test_stereo_2048_vs_oracle(wv, tmp_path_factory, mode):
+    """8K-shaped path at 2048^2 stereo (L4, 256^2 mask grid): GPU == oracle."""
+    import torch
+    d = tmp_path_factory.mktemp("s2048")
+    path = d / "s.wvv"
+    if not path.exists():
+        from paper_2208_10859_b200.synthetic import make_synthetic_clip_torch
+        clip = make_synthetic_clip_torch(4, 2048, 2048, 3, device="cuda")
+        p = wv.EncodeParams(stereo=True, fps=120.0, mask_w=256, mask_h=256)
+        wv.write_video(wv.encode_video(clip, p, device="cuda"), path)
+    sess = wv.DecodeSession(path)
+    ref = wo.OracleSession(path)
+    h = sess.header
+    pose = wv.CameraPose(yaw=30, pitch=10)
+    mask = wv.stereo_mask(pose, (h.mask_w, h.mask_h))
+    for frame in (0, 2):
+        if mode == "full":
+            pix, fp, st = sess.decode_full(frame)
+            rp, rf, rs = ref.decode(frame, "full")
+        elif mode == "viewport":
+            pix, fp, st = sess.decode_viewport(frame, mask)
+            rp, rf, rs = ref.decode(frame, "viewport", mask)
+        else:
+            sc = wv.FoveationSchedule.default(h.levels, 0.3, 0.6)
+            pix, fp, st = sess.decode_foveated(frame, mask, sc)
+            rp, rf, rs = ref.decode(frame, "foveated", mask, fractions=sc.fractions,
+                                    gaze=(0.3, 0.6))
+        np.testing.assert_array_equal(pix, rp)
+        np.testing.assert_array_equal(fp, rf)
+        assert (st.bytes_loaded, st.records_processed) == (rs.bytes_loaded, rs.records_processed)
+    if mode == "viewport":
+        out = sess.render_views(pose, (500, 500)).cpu().numpy()
+        half = h.height // 2
+        for e in range(2):
+            r = wo.perspective(rp[e * half:(e + 1) * half], rf[e * half:(e + 1) * half],
+                               pose.rotation(), 90.0, 90.0, 500, 500)
+            assert np.abs(out[e].astype(int) - r.astype(int)).max() <= 1
+    torch.cuda.synchronize()
+
+
+def test_c1_full_decode_vs_oracle(wv, tmp_path):
+    """BASELINE configs[0]: 1024x512, 16 frames, L3 full decode."""
+    from paper_2208_10859_b200.synthetic import make_synthetic_clip
+    clip = make_synthetic_clip(16, height=512, width=1024)
+    path = tmp_path / "c1.wvv"
+    wv.write_video(wv.encode_video(clip, wv.EncodeParams(levels=3)), path)
+    sess = wv.DecodeSession(path)
+    ref = wo.OracleSession(path)
+    for f in (0, 5, 15):
+        pix, fp, st = sess.decode_full(f)
+        rp, rf, rs = ref.decode(f, "full")
+        np.testing.assert_array_equal(pix, rp)
+        assert abs(wv.psnr(pix, clip[f]) - wv.psnr(rp, clip[f])) < 0.01
+        assert (st.bytes_loaded, st.records_processed) == (rs.bytes_loaded, rs.records_processed)
