@@ -1,0 +1,210 @@
+"""CPU-only checks: the C ABI library loads and exports every declared
+symbol (no compute calls), the .wvv reader, the package encoder's byte
+exactness against reference-produced files, host-side mask geometry, and the
+foveation window arithmetic against the oracle."""
+import ctypes as C
+import hashlib
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT, unpack_mask
+from oracle import wavevid_oracle as wo
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2208_10859_b200 import _native, build
+    build.build()
+    return _native.load()
+
+
+def _declared_functions():
+    text = open(os.path.join(ROOT, "include", "wavevid_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(wv_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol(lib):
+    names = _declared_functions()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(lib, n), n
+    from paper_2208_10859_b200 import _native
+    assert sorted(_native.EXPORTS) == names
+
+
+def test_abi_host_functions(lib):
+    from paper_2208_10859_b200 import _native as N
+    assert lib.wv_abi_version() == 1
+    assert lib.wv_status_string(0) == b"ok"
+    g = N.Geometry(8192, 8192, 3, 6, 4, 32, 0, 256, 256)
+    b = C.c_uint64()
+    assert lib.wv_workspace_bytes(C.byref(g), C.byref(b)) == 0
+    # plane 805 MB + level buffers + masks: about 1.1 GB at 8K
+    assert 1.0e9 < b.value < 1.3e9
+    bad = N.Geometry(100, 64, 3, 6, 4, 32, 0, 64, 64)          # not divisible by 2^6
+    assert lib.wv_workspace_bytes(C.byref(bad), C.byref(b)) == N.WV_ERR_ARG
+    # decode entry points reject missing pointers before touching the GPU
+    a = N.FrameArgs()
+    assert lib.wv_decode_frame(C.byref(g), C.byref(a), None, None) == N.WV_ERR_ARG
+
+
+def test_struct_layouts_match_header():
+    from paper_2208_10859_b200 import _native as N
+    assert C.sizeof(N.Geometry) == 36
+    assert C.sizeof(N.FrameResult) == 40
+    assert N.FrameArgs.d_mask.offset == 16
+    assert N.FrameArgs.d_payload.offset == 16 + 8 + 12 * 4 * 4
+
+
+@pytest.mark.parametrize("name", ["golden_quantized.wvv", "golden_float.wvv",
+                                  "golden_stereo.wvv", "noise_bs16.wvv", "smooth_n8.wvv"])
+def test_reader_parses_fixture(manifest, name):
+    from paper_2208_10859_b200.fileio import VideoReader
+    with VideoReader(os.path.join(GOLDEN, name)) as r:
+        h = r.header
+        assert list(r.header.__dict__.keys())[:4] == ["width", "height", "frame_count", "fps"]
+        assert h.num_sets == len(r.set_meta)
+        total = 0
+        for si in range(h.num_sets):
+            buf = r.read_set_payload(si)
+            t = r.block_table(si)
+            assert len(buf) == r.set_meta[si].payload_length
+            assert t.total_bytes() + h.table_bytes == len(buf)
+            total += r.set_meta[si].record_count
+        assert total > 0
+
+
+def test_golden_header_fields():
+    # pkg/tests/data/golden.json header entries
+    from paper_2208_10859_b200.fileio import VideoReader
+    with VideoReader(os.path.join(GOLDEN, "golden_stereo.wvv")) as r:
+        h = r.header
+        assert (h.width, h.height, h.channels, h.levels, h.inter_size, h.block_size) == \
+            (128, 128, 3, 3, 4, 32)
+        assert h.stereo and not h.float_mode and h.fps == 60.0
+    with VideoReader(os.path.join(GOLDEN, "golden_quantized.wvv")) as r:
+        assert [m.record_count for m in r.set_meta] == [16383]
+        assert [m.payload_offset for m in r.set_meta] == [280]
+        assert [m.payload_length for m in r.set_meta] == [82043]
+
+
+def _clip(spec_name):
+    from paper_2208_10859_b200.synthetic import make_synthetic_clip
+
+    def noise(seed, frames, size, channels):
+        return np.random.default_rng(seed).integers(0, 256, (frames, size, size, channels),
+                                                    dtype=np.uint8)
+    return {
+        "golden_quantized.wvv": lambda: noise(11, 4, 64, 3),
+        "golden_float.wvv": lambda: noise(12, 2, 64, 1),
+        "golden_stereo.wvv": lambda: noise(13, 4, 128, 3),
+        "smooth_hq.wvv": lambda: make_synthetic_clip(8, 128),
+        "smooth_lossless.wvv": lambda: make_synthetic_clip(4, 64),
+        "noise_bs16.wvv": lambda: noise(5, 4, 128, 3),
+        "smooth_n8.wvv": lambda: make_synthetic_clip(10, 64),
+        "smooth_n1_mono.wvv": lambda: make_synthetic_clip(3, 64, 1),
+        "wide_equirect.wvv": lambda: make_synthetic_clip(4, 128)[:, :64],
+    }[spec_name]()
+
+
+@pytest.mark.parametrize("name", ["golden_quantized.wvv", "golden_float.wvv",
+                                  "golden_stereo.wvv", "smooth_hq.wvv", "smooth_lossless.wvv",
+                                  "noise_bs16.wvv", "smooth_n8.wvv", "smooth_n1_mono.wvv",
+                                  "wide_equirect.wvv"])
+def test_encoder_reproduces_reference_bytes(manifest, name, tmp_path):
+    """The package encoder (torch, CPU here) writes the reference encoder's
+    exact bytes; the first three digests are pkg/tests/data/golden.json's."""
+    from paper_2208_10859_b200.encoding import EncodeParams, MappingKind, encode_video
+    from paper_2208_10859_b200.fileio import write_video
+    spec = dict(manifest[name]["params"])
+    spec["mapping"] = MappingKind[spec.get("mapping", "EQUIRECTANGULAR")]
+    out = tmp_path / "x.wvv"
+    write_video(encode_video(_clip(name), EncodeParams(**spec)), out)
+    assert hashlib.sha256(out.read_bytes()).hexdigest() == manifest[name]["sha256"]
+
+
+def test_synthetic_clip_matches_reference():
+    from paper_2208_10859_b200.synthetic import make_synthetic_clip
+    want = json.load(open(os.path.join(GOLDEN, "synthetic.json")))
+    for k, v in want.items():
+        f, size, c, seed = (int(x) for x in k.split("x"))
+        got = make_synthetic_clip(f, size, c, seed)
+        assert hashlib.sha256(got.tobytes()).hexdigest() == v
+
+
+def test_viewport_and_stereo_masks_match_reference():
+    from paper_2208_10859_b200.projection import CameraPose, stereo_mask, viewport_to_mask
+    want = np.load(os.path.join(GOLDEN, "projection.npz"))
+    n = 0
+    for k in want.files:
+        if not (k.startswith("vmask|") or k.startswith("smask|")):
+            continue
+        kind, i, dims = k.split("|")
+        mw, mh = (int(x) for x in dims.split("x"))
+        yaw, pitch, roll, fh, fv = want[f"pose|{i}"]
+        pose = CameraPose(float(yaw), float(pitch), float(roll), float(fh), float(fv))
+        fn = viewport_to_mask if kind == "vmask" else stereo_mask
+        got = fn(pose, (mw, mh))
+        np.testing.assert_array_equal(got, unpack_mask(want[k], (mh, mw)), err_msg=k)
+        n += 1
+    assert n >= 100
+
+
+def test_mask_bbox_and_fovea_rects_match_oracle(rng):
+    from paper_2208_10859_b200.decoding import FoveationSchedule, fovea_rects, mask_bbox
+    for H, W, mh, mw in [(128, 128, 64, 64), (8192, 8192, 256, 256), (512, 1024, 32, 64),
+                         (96, 64, 128, 128)]:
+        for _ in range(20):
+            m = np.zeros((mh, mw), bool)
+            y, x = rng.integers(0, mh), rng.integers(0, mw)
+            m[y:y + rng.integers(1, mh), x:x + rng.integers(1, mw)] = True
+            pm = wo.upscale(m, W, H)
+            want = wo.pixel_bbox(pm)
+            assert mask_bbox(m, W, H) == want
+            if want is None:
+                continue
+            L = 3
+            sc = FoveationSchedule.default(L, float(rng.uniform()), float(rng.uniform()))
+            assert fovea_rects(want, H, W, sc, L) == wo.fovea_rects(
+                want, H, W, sc.fractions, sc.gaze_u, sc.gaze_v, L)
+
+
+def test_schedule_and_pose_validation():
+    from paper_2208_10859_b200 import CameraPose, DecodeError, FoveationSchedule, ProjectionError
+    assert FoveationSchedule.default(6).fractions == (1.0, 0.65, 0.40, 0.22, 0.10, 0.04, 0.02)
+    for levels in range(1, 8):
+        f = FoveationSchedule.default(levels).fractions
+        assert f[0] == 1.0 and all(a >= b for a, b in zip(f, f[1:]))
+    for bad in [((1.0, 0.2, 0.5),), ((0.9, 0.5),)]:
+        with pytest.raises(DecodeError):
+            FoveationSchedule(*bad)
+    with pytest.raises(DecodeError):
+        FoveationSchedule((1.0, 0.5), gaze_u=1.5)
+    with pytest.raises(ProjectionError):
+        CameraPose(fov_h=0)
+    with pytest.raises(ProjectionError):
+        CameraPose(pitch=95)
+    r = CameraPose(yaw=33, pitch=-20, roll=7).rotation()
+    np.testing.assert_allclose(r @ r.T, np.eye(3), atol=1e-12)
+    np.testing.assert_allclose(r, wo.pose_rotation(33, -20, 7), atol=0)
+
+
+def test_footprint_bit_packing_roundtrip(rng):
+    from paper_2208_10859_b200.projection import pack_footprint, unpack_footprint
+    for shape in [(5, 7), (64, 64), (33, 100)]:
+        fp = rng.random(shape) < 0.5
+        np.testing.assert_array_equal(unpack_footprint(pack_footprint(fp), shape[1]), fp)
+
+
+def test_decode_session_requires_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2208_10859_b200 import DecodeSession
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        DecodeSession(os.path.join(GOLDEN, "golden_quantized.wvv"))
