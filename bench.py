@@ -230,12 +230,9 @@ def run_ours(args):
         pose, mask, gaze = pm[f]
         if args.mode == "full":
             ss.decode_full_device(f)
-        elif args.mode == "foveated":
-            ss.decode_foveated_device(f, mask, FoveationSchedule.default(h.levels, *gaze))
         else:
-            ss.decode_viewport_device(f, mask)
-        if args.mode != "full":
-            ss.render_views(pose, (OUT_W, OUT_H), out=ob, check=False)
+            sc = FoveationSchedule.default(h.levels, *gaze) if args.mode == "foveated" else None
+            ss.decode_render_device(f, args.mode, mask, pose, (OUT_W, OUT_H), ob, schedule=sc)
 
     def gather(ss=None, ob=None):
         if world > 1:
@@ -289,7 +286,7 @@ def run_ours(args):
     max_ms = float(tp.item())
     for ss in sessions:
         ss._settle_until(None)
-    unc = sum(int(ss._uncovered.item()) for ss in sessions)
+    unc = sum(ss.uncovered() for ss in sessions)
 
     # serial latency view: one stream, L2 flushed (256 MiB write) before each
     # step, each step bracketed by events

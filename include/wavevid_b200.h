@@ -135,6 +135,17 @@ int wv_synthesize_level(const wv_geometry* g, const wv_frame_args* a, void* d_wo
 
 int wv_render_perspective(const wv_view_args* views, int n_views, void* stream);
 
+/* Graph-capturable variants.  Per-frame inputs live in device memory: the
+ * frame arguments in the workspace descriptor slot (wv_desc_view; a
+ * wv_frame_args followed by room for 4 wv_view_args), so the launch sequence
+ * of a mode is fixed and can be recorded once in a CUDA graph and replayed
+ * after a single H2D copy of the slot per frame. */
+int wv_desc_view(const wv_geometry* g, void* d_workspace, void** d_desc);
+int wv_decode_frame_desc(const wv_geometry* g, int mode, int flags, void* d_workspace,
+                         void* stream);
+int wv_render_perspective_desc(const wv_view_args* d_views, int n_views, int max_out_w,
+                               int max_out_h, void* stream);
+
 /* Views into the workspace for parity tests (no launches). */
 int wv_plane_view(const wv_geometry* g, void* d_workspace, float** d_plane);
 int wv_level_mask_view(const wv_geometry* g, void* d_workspace, int level,

@@ -21,7 +21,8 @@ EXPORTS = ["wv_abi_version", "wv_status_string", "wv_workspace_bytes", "wv_works
            "wv_select", "wv_dequant_temporal", "wv_synthesize", "wv_decode_frame",
            "wv_synthesize_level",
            "wv_render_perspective", "wv_plane_view", "wv_level_mask_view",
-           "wv_block_list_view"]
+           "wv_block_list_view", "wv_desc_view", "wv_decode_frame_desc",
+           "wv_render_perspective_desc"]
 
 
 class Geometry(C.Structure):
@@ -85,6 +86,10 @@ def load(path: str = LIB_PATH):
                                        C.POINTER(C.c_int32)]
     lib.wv_block_list_view.argtypes = [G, C.c_void_p, C.POINTER(C.c_void_p),
                                        C.POINTER(C.c_void_p)]
+    lib.wv_desc_view.argtypes = [G, C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.wv_decode_frame_desc.argtypes = [G, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+    lib.wv_render_perspective_desc.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                               C.c_void_p]
     for fn in EXPORTS[2:]:
         getattr(lib, fn).restype = C.c_int
     if lib.wv_abi_version() != 1:

@@ -56,48 +56,91 @@ int wv_workspace_reset(const wv_geometry* g, void* ws, void* stream) {
   return WV_OK;
 }
 
-int wv_select(const wv_geometry* g, const wv_frame_args* a, void* ws, void* stream) {
-  Layout lo;
-  int st = check(g, a, &lo);
+// Host-argument entry points: copy the arguments into the workspace
+// descriptor slot (stream-ordered) and run the launch sequence reading it.
+static int stage(const wv_geometry* g, const wv_frame_args* a, void* ws, void* stream,
+                 Layout* lo, wv_frame_args** d_fa) {
+  int st = check(g, a, lo);
   if (st != WV_OK) return st;
   if (!ws) return WV_ERR_ARG;
-  return launch_select(lo, g, a, (uint8_t*)ws, (cudaStream_t)stream);
+  if (a->payload_bytes < (uint64_t)lo->n * lo->NB * 8) return WV_ERR_ARG;
+  *d_fa = (wv_frame_args*)((uint8_t*)ws + lo->desc);
+  WV_CUDA(cudaMemcpyAsync(*d_fa, a, sizeof(wv_frame_args), cudaMemcpyHostToDevice,
+                          (cudaStream_t)stream));
+  return WV_OK;
+}
+
+int wv_select(const wv_geometry* g, const wv_frame_args* a, void* ws, void* stream) {
+  Layout lo;
+  wv_frame_args* d;
+  int st = stage(g, a, ws, stream, &lo, &d);
+  if (st != WV_OK) return st;
+  return launch_select(lo, g, a->mode, a->flags, d, (uint8_t*)ws, (cudaStream_t)stream);
 }
 
 int wv_dequant_temporal(const wv_geometry* g, const wv_frame_args* a, void* ws, void* stream) {
   Layout lo;
-  int st = check(g, a, &lo);
+  wv_frame_args* d;
+  int st = stage(g, a, ws, stream, &lo, &d);
   if (st != WV_OK) return st;
-  if (!ws) return WV_ERR_ARG;
-  return launch_temporal(lo, g, a, (uint8_t*)ws, (cudaStream_t)stream);
+  return launch_temporal(lo, g, a->mode, d, (uint8_t*)ws, (cudaStream_t)stream);
 }
 
 int wv_synthesize(const wv_geometry* g, const wv_frame_args* a, void* ws, void* stream) {
   Layout lo;
-  int st = check(g, a, &lo);
+  wv_frame_args* d;
+  int st = stage(g, a, ws, stream, &lo, &d);
   if (st != WV_OK) return st;
-  if (!ws) return WV_ERR_ARG;
-  return launch_synthesis(lo, g, a, (uint8_t*)ws, (cudaStream_t)stream);
+  return launch_synthesis(lo, g, d, (uint8_t*)ws, (cudaStream_t)stream);
 }
 
 int wv_decode_frame(const wv_geometry* g, const wv_frame_args* a, void* ws, void* stream) {
   Layout lo;
-  int st = check(g, a, &lo);
+  wv_frame_args* d;
+  int st = stage(g, a, ws, stream, &lo, &d);
   if (st != WV_OK) return st;
-  if (!ws) return WV_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  if ((st = launch_select(lo, g, a, (uint8_t*)ws, s)) != WV_OK) return st;
-  if ((st = launch_temporal(lo, g, a, (uint8_t*)ws, s)) != WV_OK) return st;
-  return launch_synthesis(lo, g, a, (uint8_t*)ws, s);
+  if ((st = launch_select(lo, g, a->mode, a->flags, d, (uint8_t*)ws, s)) != WV_OK) return st;
+  if (a->flags & WV_FLAG_ACCOUNT_ONLY) return WV_OK;
+  if ((st = launch_temporal(lo, g, a->mode, d, (uint8_t*)ws, s)) != WV_OK) return st;
+  return launch_synthesis(lo, g, d, (uint8_t*)ws, s);
 }
 
 int wv_synthesize_level(const wv_geometry* g, const wv_frame_args* a, void* ws, int level,
                         void* stream) {
   Layout lo;
-  int st = check(g, a, &lo);
+  wv_frame_args* d;
+  int st = stage(g, a, ws, stream, &lo, &d);
   if (st != WV_OK) return st;
-  if (!ws || level < 1 || level > lo.L) return WV_ERR_ARG;
-  return launch_synthesis(lo, g, a, (uint8_t*)ws, (cudaStream_t)stream, level);
+  if (level < 1 || level > lo.L) return WV_ERR_ARG;
+  return launch_synthesis(lo, g, d, (uint8_t*)ws, (cudaStream_t)stream, level);
+}
+
+int wv_desc_view(const wv_geometry* g, void* ws, void** d_desc) {
+  Layout lo;
+  int st = build_layout(g, &lo);
+  if (st != WV_OK) return st;
+  if (!ws || !d_desc) return WV_ERR_ARG;
+  *d_desc = (uint8_t*)ws + lo.desc;
+  return WV_OK;
+}
+
+int wv_decode_frame_desc(const wv_geometry* g, int mode, int flags, void* ws, void* stream) {
+  Layout lo;
+  int st = build_layout(g, &lo);
+  if (st != WV_OK) return st;
+  if (!ws || mode < WV_MODE_FULL || mode > WV_MODE_FOVEATED) return WV_ERR_ARG;
+  const wv_frame_args* d = (const wv_frame_args*)((uint8_t*)ws + lo.desc);
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((st = launch_select(lo, g, mode, flags, d, (uint8_t*)ws, s)) != WV_OK) return st;
+  if (flags & WV_FLAG_ACCOUNT_ONLY) return WV_OK;
+  if ((st = launch_temporal(lo, g, mode, d, (uint8_t*)ws, s)) != WV_OK) return st;
+  return launch_synthesis(lo, g, d, (uint8_t*)ws, s);
+}
+
+int wv_render_perspective_desc(const wv_view_args* d_views, int n_views, int max_out_w,
+                               int max_out_h, void* stream) {
+  return launch_perspective_dev(d_views, n_views, max_out_w, max_out_h, (cudaStream_t)stream);
 }
 
 int wv_render_perspective(const wv_view_args* views, int n_views, void* stream) {

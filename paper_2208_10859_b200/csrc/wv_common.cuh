@@ -43,6 +43,7 @@ struct Layout {
   uint64_t prev_need;                    // level 1, u8 per tile
   uint64_t tlist[WV_MAX_LEVELS + 1];     // u32 per tile
   uint64_t counters;                     // u32[64]
+  uint64_t desc;                         // device wv_frame_args + 4 wv_view_args (per-frame inputs)
   uint64_t plane;                        // C x H x W f32
   uint64_t ybuf[WV_MAX_LEVELS + 1];      // level k (1..L-1): C x (H>>k) x pitch[k] f32
   int ypitch[WV_MAX_LEVELS + 1];
@@ -94,6 +95,7 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
   }
   o->prev_need = take(uint64_t(o->nty[1]) * o->ntx[1]);
   o->counters = take(64 * 4);
+  o->desc = take(sizeof(wv_frame_args) + 4 * sizeof(wv_view_args));
   o->plane = take(uint64_t(C) * H * W * 4);
   for (int k = 1; k < L; ++k) {
     int cols = W >> k;
@@ -111,12 +113,17 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
   } while (0)
 
 // ---- kernel launchers (defined in the .cu files) ----
-int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
-                  cudaStream_t s);
-int launch_temporal(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
-                    cudaStream_t s);
-int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
-                     cudaStream_t s, int only_level = 0);
+// Launchers take the frame arguments as a DEVICE pointer (the descriptor slot
+// of the workspace): kernels read every per-frame value from it, so the launch
+// sequence of a mode is fixed and can be captured in a CUDA graph.
+int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
+                  const wv_frame_args* d_fa, uint8_t* ws, cudaStream_t s);
+int launch_temporal(const Layout& lo, const wv_geometry* g, int mode, const wv_frame_args* d_fa,
+                    uint8_t* ws, cudaStream_t s);
+int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* d_fa,
+                     uint8_t* ws, cudaStream_t s, int only_level = 0);
 int launch_perspective(const wv_view_args* v, int n, cudaStream_t s);
+int launch_perspective_dev(const wv_view_args* d_views, int n, int max_w, int max_h,
+                           cudaStream_t s);
 
 }  // namespace wv

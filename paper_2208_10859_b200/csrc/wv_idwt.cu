@@ -144,7 +144,7 @@ struct LevelArgs {
   const uint32_t* count;
   float* out;          // non-final: Y_{k-1} planar C x 2bh x out_pitch
   int out_pitch;       // floats
-  uint8_t* canvas;     // final: planar C x H x W u8
+  const wv_frame_args* fa;   // final: fa->d_canvas, planar C x H x W u8
   const uint32_t* R;   // final: requested-mask rows (mh x wpr0)
   const uint32_t* rowmap;  // final: pixel row -> mask row
   int wpr0;
@@ -153,35 +153,64 @@ struct LevelArgs {
   const float* plane; int plane_w, plane_h;
 };
 
-// Items are (tile, channel).  Column pass: 2 segments x BOX_W columns (each
-// segment lifts 16 output row pairs from its own 2-row halo); row pass: 2
-// segments x TY row pairs.  Store pass: coalesced f32 (mid levels) or packed
-// u8 with the request mask applied (finest level).
+// Items are (tile, channel).  Boxes are double-buffered: while one item is
+// lifted, the next item's four TMA boxes are already in flight into the other
+// buffer.  Column pass: 2 segments x BOX_W columns (each segment lifts 16
+// output row pairs from its own 2-row halo); row pass: 2 segments x TY row
+// pairs.  Store pass: coalesced f32 (mid levels) or packed u8 with the
+// request mask applied (finest level).
+constexpr int BOXSET = 4 * BOX_SLOT;
+constexpr int NBUF = 1;
+
 template <bool FINAL>
 __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUtensorMap tm_ll,
                                                     const __grid_constant__ CUtensorMap tm_det,
                                                     LevelArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  float* box = reinterpret_cast<float*>(smem);                      // 4 slots
-  float2* colL = reinterpret_cast<float2*>(smem + 4 * BOX_SLOT);    // [TY][CB_PITCH]
+  uint8_t* canvas = FINAL ? a.fa->d_canvas : nullptr;
+  float2* colL = reinterpret_cast<float2*>(smem + NBUF * BOXSET);  // [TY][CB_PITCH]
   float2* colH = colL + TY * CB_PITCH;
-  float2* outb = reinterpret_cast<float2*>(smem);                   // aliases boxes
-  __shared__ uint64_t bar;
-  const float* bLL = box;
-  const float* bHL = box + BOX_SLOT / 4;
-  const float* bLH = box + 2 * BOX_SLOT / 4;
-  const float* bHH = box + 3 * BOX_SLOT / 4;
+  uint32_t* req = reinterpret_cast<uint32_t*>(colH + TY * CB_PITCH);  // FINAL: [OUT_H][2]
+  __shared__ uint64_t bar[2];
   constexpr int SEG = TY / 2;   // == TX / 2
 
   const int tid = threadIdx.x;
-  if (tid == 0) mbar_init(&bar, 1);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
   __syncthreads();
-  uint32_t phase = 0;
+  uint32_t phases = 0u;   // bit b = parity of buffer b's barrier
   const int C = a.C;
   const uint32_t nitems = *a.count * (uint32_t)C;
   const int H = 2 * a.bh, W = 2 * a.bw;
 
-  for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+  // issue the four box loads of an item into buffer b (elected thread)
+  auto issue = [&](uint32_t it, int b) {
+    if (!a.use_tma || tid != 0) return;
+    const uint32_t e = a.list[it / C];
+    if (FINAL && (e & ZERO_FLAG)) return;
+    const uint32_t tile = e & ~ZERO_FLAG;
+    const int ty = tile / a.ntx, tx = tile - (tile / a.ntx) * a.ntx;
+    // TMA faults on unaligned/negative innermost box coordinates (observed on
+    // B200, driver 580): x starts at ax-4 clamped to 0
+    const int oy = max(ty * TY - HALO, 0), ox = max(tx * TX - XPAD, 0);
+    const int c = (int)(it % C);
+    float* box = reinterpret_cast<float*>(smem + b * BOXSET);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bar[b], 4u * BOX_FLOATS * 4u);
+    tma_load_3d(box, &tm_ll, ox, oy, c, &bar[b]);
+    tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar[b]);
+    tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar[b]);
+    tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar[b]);
+  };
+
+  // NBUF == 2 prefetches the next item's boxes while lifting the current one;
+  // NBUF == 1 keeps shared memory at 44 KB (5 CTAs/SM), which measured faster
+  int buf = 0;
+  if (NBUF == 2 && blockIdx.x < nitems) issue(blockIdx.x, 0);
+  for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x, buf ^= (NBUF - 1)) {
+    const uint32_t next = item + gridDim.x;
     const uint32_t entry = a.list[item / C];
     const int c = (int)(item % C);
     const uint32_t tile = entry & ~ZERO_FLAG;
@@ -190,29 +219,28 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     const int by = min(ay + TY, a.bh), bx = min(ax + TX, a.bw);
     const int ny = 2 * (by - ay), nx = 2 * (bx - ax);
     if (FINAL && (entry & ZERO_FLAG)) {
+      if (NBUF == 2 && next < nitems) issue(next, buf ^ 1);
       // tile left the request: clear what an earlier frame wrote there
       const int qw = nx >> 2;
       for (int idx = tid; idx < ny * qw; idx += NTHREADS) {
         const int r = idx / qw, q = idx % qw;
-        *reinterpret_cast<uint32_t*>(a.canvas + ((uint64_t)c * H + 2 * ay + r) * W + 2 * ax +
+        *reinterpret_cast<uint32_t*>(canvas + ((uint64_t)c * H + 2 * ay + r) * W + 2 * ax +
                                      4 * q) = 0u;
       }
       continue;
     }
-    // box origin: TMA faults on unaligned/negative innermost coordinates
-    // (observed on B200, driver 580), so x starts at ax-4 clamped to 0
+    float* box = reinterpret_cast<float*>(smem + buf * BOXSET);
+    const float* bLL = box;
+    const float* bHL = box + BOX_SLOT / 4;
+    const float* bLH = box + 2 * BOX_SLOT / 4;
+    const float* bHH = box + 3 * BOX_SLOT / 4;
+    float2* outb = reinterpret_cast<float2*>(box);                  // aliases this item's boxes
     const int oy = max(ay - HALO, 0), ox = max(ax - XPAD, 0);
     if (a.use_tma) {
-      if (tid == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar, 4u * BOX_FLOATS * 4u);
-        tma_load_3d(box, &tm_ll, ox, oy, c, &bar);
-        tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar);
-        tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar);
-        tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar);
-      }
-      mbar_wait(&bar, phase);
-      phase ^= 1u;
+      if (NBUF == 1) issue(item, 0);
+      mbar_wait(&bar[buf], (phases >> buf) & 1u);
+      phases ^= 1u << buf;
+      if (NBUF == 2 && next < nitems) issue(next, buf ^ 1);
     } else {
       // tiny levels whose subband width is not a multiple of 4 floats
       for (int i = tid; i < 4 * BOX_FLOATS; i += NTHREADS) {
@@ -230,6 +258,13 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         box[q * (BOX_SLOT / 4) + e] = v;
       }
       __syncthreads();
+    }
+    if (FINAL && tid < ny) {
+      // request-mask words of this tile's output rows (used by the store pass)
+      const int gx = 2 * ax;
+      const uint32_t* row = a.R + (uint64_t)a.rowmap[2 * ay + tid] * a.wpr0 + (gx >> 5);
+      req[2 * tid] = row[0];
+      req[2 * tid + 1] = nx > 32 ? row[1] : 0u;
     }
 
     // column pass: (segment, box column) per thread, L and H halves packed
@@ -291,9 +326,8 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         const int gx = 2 * ax + 4 * q;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int gy = 2 * ay + 2 * i + h;
-          const uint32_t rbits =
-              (a.R[(uint64_t)a.rowmap[gy] * a.wpr0 + (gx >> 5)] >> (gx & 31)) & 0xFu;
+          const int r = 2 * i + h;
+          const uint32_t rbits = (req[2 * r + (q >> 3)] >> ((4 * q) & 31)) & 0xFu;
           uint32_t word = 0;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -303,7 +337,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
             const uint32_t b = ((rbits >> e) & 1u) ? (uint32_t)v : 0u;
             word |= b << (8 * e);
           }
-          *reinterpret_cast<uint32_t*>(a.canvas + ((uint64_t)c * H + gy) * W + gx) = word;
+          *reinterpret_cast<uint32_t*>(canvas + ((uint64_t)c * H + 2 * ay + r) * W + gx) = word;
         }
       }
     }
@@ -335,7 +369,7 @@ int make_map(CUtensorMap* m, const float* base, int cols, int rows, int pitch, i
 
 }  // namespace
 
-int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
+int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* fa, uint8_t* ws,
                      cudaStream_t s, int only_level) {
   (void)g;
   const int L = lo.L, C = lo.C;
@@ -344,8 +378,8 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem_mid = 4 * BOX_SLOT + 2 * TY * CB_PITCH * 8;
-  const size_t smem_fin = smem_mid;
+  const size_t smem_mid = NBUF * BOXSET + 2 * TY * CB_PITCH * 8;
+  const size_t smem_fin = smem_mid + OUT_H * 2 * 4;
   WV_CUDA(cudaFuncSetAttribute(k_level<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem_mid));
   WV_CUDA(cudaFuncSetAttribute(k_level<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -379,7 +413,7 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
       int grid = max(1, min(ntiles * C, sms * occ_mid));
       k_level<false><<<grid, NTHREADS, smem_mid, s>>>(tm_ll, tm_plane, la);
     } else {
-      la.canvas = a->d_canvas;
+      la.fa = fa;
       la.R = (const uint32_t*)(ws + lo.mrows);
       la.rowmap = (const uint32_t*)(ws + lo.rowmap);
       la.wpr0 = lo.wpr_[0];

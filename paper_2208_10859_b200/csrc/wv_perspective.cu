@@ -76,9 +76,13 @@ struct ViewConst {
   float tan_h, tan_v, inv_w, inv_h, sx, sy;
 };
 
-__global__ void __launch_bounds__(256) k_perspective(const __grid_constant__ Views views) {
+// DEV: views come from device memory (graph-capturable launch); otherwise
+// they are passed by value as a kernel parameter.
+template <bool DEV>
+__global__ void __launch_bounds__(256) k_perspective(const __grid_constant__ Views views,
+                                                     const wv_view_args* __restrict__ d_views) {
   __shared__ ViewConst vc;
-  const wv_view_args& v = views.v[blockIdx.z];
+  const wv_view_args& v = DEV ? d_views[blockIdx.z] : views.v[blockIdx.z];
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     for (int i = 0; i < 9; ++i) vc.r[i] = (float)v.rot[i];
     vc.tan_h = (float)v.tan_h;
@@ -166,7 +170,18 @@ int launch_perspective(const wv_view_args* views, int n, cudaStream_t s) {
   }
   dim3 block(32, 8);
   dim3 grid(cdiv(mw, 32), cdiv(mh, 8), n);
-  k_perspective<<<grid, block, 0, s>>>(pv);
+  k_perspective<false><<<grid, block, 0, s>>>(pv, nullptr);
+  WV_CUDA(cudaGetLastError());
+  return WV_OK;
+}
+
+int launch_perspective_dev(const wv_view_args* d_views, int n, int max_w, int max_h,
+                           cudaStream_t s) {
+  if (!d_views || n < 1 || n > kMaxViews || max_w < 1 || max_h < 1) return WV_ERR_ARG;
+  Views none{};
+  dim3 block(32, 8);
+  dim3 grid(cdiv(max_w, 32), cdiv(max_h, 8), n);
+  k_perspective<true><<<grid, block, 0, s>>>(none, d_views);
   WV_CUDA(cudaGetLastError());
   return WV_OK;
 }

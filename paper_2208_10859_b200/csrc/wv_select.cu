@@ -71,10 +71,12 @@ __device__ __forceinline__ uint32_t shrink(uint32_t p, uint32_t c, uint32_t n) {
 // ---------------------------------------------------------------- mask rows
 // Distinct pixel-mask rows R[my] (nearest column map, fileio.py:435) and the
 // row map rowmap[y] = (y*mh)/H (fileio.py:434).
-__global__ void k_mask_rows(const uint8_t* __restrict__ mask, uint32_t* __restrict__ R,
+__global__ void k_mask_rows(const wv_frame_args* __restrict__ fa, uint32_t* __restrict__ R,
                             uint32_t* __restrict__ rowmap, int mh, int mw, int W, int H, int wpr0,
                             int full) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint8_t* __restrict__ mask = fa->d_mask;
+  if (idx == 0) *fa->d_result = wv_frame_result{};
   if (idx < H) rowmap[idx] = ((uint32_t)idx * (uint32_t)mh) / (uint32_t)H;
   if (idx >= mh * wpr0) return;
   const int my = idx / wpr0, w = idx % wpr0;
@@ -109,20 +111,20 @@ struct CascadeArgs {
   uint64_t dst_stride;
   int nbatch;
   int batch[WV_MAX_LEVELS + 1];
-  int rect[WV_MAX_LEVELS + 1][4];  // j == 1 foveated windows, by batch id
+  const wv_frame_args* fa;         // j == 1 foveated windows: fa->fovea[batch id - 1]
   int fov;                         // foveated: batch j also ANDs with batch 0
   uint32_t* pooled;                // one word per tile: bit w = any bit in (32 rows x word w)
   int pool_wpr;                    // tiles per row of the level
 };
 
-__device__ __forceinline__ uint32_t cas_src(const CascadeArgs& a, int b, int rr, int ww) {
+__device__ __forceinline__ uint32_t cas_src(const CascadeArgs& a, const int4& rect, int b,
+                                            int rr, int ww) {
   if (ww >= a.pwpr || rr >= a.prow_n) return 0u;
   if (a.j == 1) {
     uint32_t v = a.R[(uint64_t)a.rowmap[rr] * a.pwpr + ww];
     if (b > 0) {
-      const int* r = a.rect[b];
-      if (rr < r[0] || rr >= r[1]) return 0u;
-      v &= range_mask(r[2], r[3], ww);
+      if (rr < rect.x || rr >= rect.y) return 0u;
+      v &= range_mask(rect.z, rect.w, ww);
     }
     return v;
   }
@@ -130,9 +132,11 @@ __device__ __forceinline__ uint32_t cas_src(const CascadeArgs& a, int b, int rr,
 }
 
 // downmapped word at output level (row r, word w), both in range
-__device__ __forceinline__ uint32_t cas_down(const CascadeArgs& a, int b, int r, int w) {
-  const uint32_t lo = cas_src(a, b, 2 * r, 2 * w) | cas_src(a, b, 2 * r + 1, 2 * w);
-  const uint32_t hi = cas_src(a, b, 2 * r, 2 * w + 1) | cas_src(a, b, 2 * r + 1, 2 * w + 1);
+__device__ __forceinline__ uint32_t cas_down(const CascadeArgs& a, const int4& rect, int b,
+                                             int r, int w) {
+  const uint32_t lo = cas_src(a, rect, b, 2 * r, 2 * w) | cas_src(a, rect, b, 2 * r + 1, 2 * w);
+  const uint32_t hi =
+      cas_src(a, rect, b, 2 * r, 2 * w + 1) | cas_src(a, rect, b, 2 * r + 1, 2 * w + 1);
   return pool_pairs((uint64_t)lo | ((uint64_t)hi << 32));
 }
 
@@ -143,14 +147,20 @@ __global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
   const bool both = a.fov && b == a.j;
   const bool final_mask = a.fov ? (b == a.j) : (b == 0);
   const int r0 = blockIdx.z * CT_R, w0 = blockIdx.x * CT_W;
+  int4 rect = make_int4(0, 0, 0, 0);
+  if (a.j == 1 && b > 0) {
+    const int32_t* f = a.fa->fovea[b - 1];
+    rect = make_int4(f[0], f[1], f[2], f[3]);
+  }
+  const int4 none = make_int4(0, 0, 0, 0);
   if (threadIdx.x < CT_W) pool[threadIdx.x] = 0;
   for (int e = threadIdx.x; e < (CT_R + 2 * DIL) * (CT_W + 2); e += blockDim.x) {
     const int lr = e / (CT_W + 2), lw = e % (CT_W + 2);
     const int r = r0 - DIL + lr, w = w0 - 1 + lw;
     uint32_t v0 = 0, v1 = 0;
     if (r >= 0 && r < a.rows && w >= 0 && w < a.wpr) {
-      v0 = cas_down(a, b, r, w);
-      if (both) v1 = cas_down(a, 0, r, w);
+      v0 = cas_down(a, rect, b, r, w);
+      if (both) v1 = cas_down(a, none, 0, r, w);
     }
     dm[0][lr][lw] = v0;
     if (both) dm[1][lr][lw] = v1;
@@ -205,9 +215,10 @@ struct FootArgs {
   int srows, swpr;            // source level j
   const uint32_t* V;          // valid at level j (nullptr: all ones)
   const uint32_t* D;          // detail mask level j
-  uint32_t* out;              // level j-1
+  uint32_t* out;              // level j-1 (j == 1: fa->d_footprint)
   const uint32_t* R;          // j == 1: requested rows
   const uint32_t* rowmap;
+  const wv_frame_args* fa;
 };
 
 constexpr int FP_SR = CT_R / 2 + DIL + 1;  // source rows staged per tile (21)
@@ -251,7 +262,7 @@ __global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
     }
     uint32_t v = shrink(nb[0], nb[1], nb[2]) & last_word_mask(a.cols, w);
     if (a.j == 1) v &= a.R[(uint64_t)req_row * a.wpr + w];
-    a.out[(uint64_t)r * a.wpr + w] = v;
+    (a.j == 1 ? a.fa->d_footprint : a.out)[(uint64_t)r * a.wpr + w] = v;
   }
 }
 
@@ -263,15 +274,12 @@ struct BlockArgs {
   int L, H, W, bs, nbx, NB, n, rs;
   const uint32_t* D[WV_MAX_LEVELS + 1];
   int dwpr[WV_MAX_LEVELS + 1];
-  const unsigned long long* ends;   // (n, NB) u64
-  unsigned long long rec_bytes;     // bytes after the table
+  const wv_frame_args* fa;          // payload / cache entry / result of this call
+  unsigned long long table_bytes;   // n * NB * 8
   uint32_t* sel;
   uint32_t* prev_sel;
-  uint32_t* loaded;
   uint32_t* list;
   uint32_t* list_count;
-  unsigned long long* set_bytes;
-  wv_frame_result* res;
   int account_only;
   const uint32_t* pooled[WV_MAX_LEVELS + 1];   // nullptr: scan rows
   int pool_wpr[WV_MAX_LEVELS + 1];
@@ -328,6 +336,11 @@ __device__ bool block_any(const BlockArgs& a, int b) {
 }
 
 __global__ void __launch_bounds__(256) k_blocks(BlockArgs a) {
+  const unsigned long long* __restrict__ ends = (const unsigned long long*)a.fa->d_payload;
+  const unsigned long long rec_bytes = a.fa->payload_bytes - a.table_bytes;
+  uint32_t* loaded = a.fa->d_set_loaded;
+  unsigned long long* set_bytes = a.fa->d_set_bytes;
+  wv_frame_result* res = a.fa->d_result;
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = b < a.NB;
@@ -335,12 +348,12 @@ __global__ void __launch_bounds__(256) k_blocks(BlockArgs a) {
   unsigned long long bytes = 0, recs = 0;
   uint32_t err = 0;
   if (sel) {
-    unsigned long long prev = b ? a.ends[b - 1] : 0ull;
+    unsigned long long prev = b ? ends[b - 1] : 0ull;
     for (int t = 0; t < a.n; ++t) {
       const uint64_t i = (uint64_t)t * a.NB + b;
-      const unsigned long long e = a.ends[i];
-      const unsigned long long st = t ? a.ends[i - 1] : prev;
-      if (e < st || e > a.rec_bytes || (e - st) % a.rs ||
+      const unsigned long long e = ends[i];
+      const unsigned long long st = t ? ends[i - 1] : prev;
+      if (e < st || e > rec_bytes || (e - st) % a.rs ||
           (e - st) / a.rs > (unsigned long long)a.bs * a.bs)
         err |= WV_DERR_TABLE;
       else {
@@ -354,7 +367,7 @@ __global__ void __launch_bounds__(256) k_blocks(BlockArgs a) {
   uint32_t prevw = 0, loadw = 0;
   if (lane == 0 && (word << 5) < (uint32_t)a.NB) {
     prevw = a.prev_sel[word];
-    loadw = a.loaded[word];
+    loadw = loaded[word];
   }
   prevw = __shfl_sync(0xFFFFFFFFu, prevw, 0);
   loadw = __shfl_sync(0xFFFFFFFFu, loadw, 0);
@@ -378,15 +391,15 @@ __global__ void __launch_bounds__(256) k_blocks(BlockArgs a) {
   if (lane == 0 && (word << 5) < (uint32_t)a.NB) {
     a.sel[word] = selmask;
     if (!a.account_only) a.prev_sel[word] = selmask;
-    a.loaded[word] = loadw | selmask;
-    if (recs) atomicAdd(&a.res->records, recs);
+    loaded[word] = loadw | selmask;
+    if (recs) atomicAdd(&res->records, recs);
     if (newb) {
-      atomicAdd(&a.res->new_bytes, newb);
-      atomicAdd(a.set_bytes, newb);
+      atomicAdd(&res->new_bytes, newb);
+      atomicAdd(set_bytes, newb);
     }
-    if (nmiss) atomicAdd(&a.res->n_missing, nmiss);
-    if (selmask) atomicAdd(&a.res->n_selected, (uint32_t)__popc(selmask));
-    if (err) atomicOr(&a.res->error, err);
+    if (nmiss) atomicAdd(&res->n_missing, nmiss);
+    if (selmask) atomicAdd(&res->n_selected, (uint32_t)__popc(selmask));
+    if (err) atomicOr(&res->error, err);
   }
 }
 
@@ -408,9 +421,7 @@ struct TileArgs {
   uint32_t* list[WV_MAX_LEVELS + 1];
   uint8_t* prev_need;
   uint32_t* counters;                // CNT_TILES + k
-  const unsigned long long* set_bytes;
-  wv_frame_result* res;
-  int base[WV_MAX_LEVELS + 2];       // flattened coarse-tile index ranges (levels 2..L)
+  const wv_frame_args* fa;
 };
 
 __global__ void __launch_bounds__(256) k_tiles1(TileArgs a) {
@@ -443,8 +454,8 @@ __global__ void __launch_bounds__(256) k_tiles1(TileArgs a) {
   if (lane == 0 && m) base = atomicAdd(&a.counters[CNT_TILES + 1], (uint32_t)__popc(m));
   base = __shfl_sync(0xFFFFFFFFu, base, 0);
   if (emit) a.list[1][base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)t | (nd ? 0u : ZERO_FLAG);
-  if (lane == 0 && mn) atomicAdd(&a.res->n_tiles, (uint32_t)__popc(mn));
-  if (t == 0) a.res->set_bytes = *a.set_bytes;
+  if (lane == 0 && mn) atomicAdd(&a.fa->d_result->n_tiles, (uint32_t)__popc(mn));
+  if (t == 0) a.fa->d_result->set_bytes = *a.fa->d_set_bytes;
 }
 
 // Coarser levels in one CTA: need maps live as bit rows in shared memory and
@@ -481,28 +492,25 @@ __global__ void __launch_bounds__(1024) k_tiles_up(TileArgs a) {
   }
 }
 
-__global__ void k_finalize(const unsigned long long* set_bytes, wv_frame_result* res) {
-  res->set_bytes = *set_bytes;
+__global__ void k_finalize(const wv_frame_args* fa) {
+  fa->d_result->set_bytes = *fa->d_set_bytes;
 }
 
 }  // namespace
 
-int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
-                  cudaStream_t s) {
+int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
+                  const wv_frame_args* fa, uint8_t* ws, cudaStream_t s) {
   const int L = lo.L, H = lo.H, W = lo.W;
-  const bool full = a->mode == WV_MODE_FULL;
-  const bool fov = a->mode == WV_MODE_FOVEATED;
-  const bool acct = (a->flags & WV_FLAG_ACCOUNT_ONLY) != 0;
-  if (!full && !a->d_mask) return WV_ERR_ARG;
+  const bool full = mode == WV_MODE_FULL;
+  const bool fov = mode == WV_MODE_FOVEATED;
+  const bool acct = (flags & WV_FLAG_ACCOUNT_ONLY) != 0;
   uint32_t* R = (uint32_t*)(ws + lo.mrows);
   uint32_t* rowmap = (uint32_t*)(ws + lo.rowmap);
   uint32_t* counters = (uint32_t*)(ws + lo.counters);
   WV_CUDA(cudaMemsetAsync(counters, 0, 64 * 4, s));
-  WV_CUDA(cudaMemsetAsync(a->d_result, 0, sizeof(wv_frame_result), s));
   {
     const int n = max(lo.mh * lo.wpr_[0], H);
-    k_mask_rows<<<cdiv(n, 256), 256, 0, s>>>(a->d_mask, R, rowmap, lo.mh, lo.mw, W, H,
-                                             lo.wpr_[0], full);
+    k_mask_rows<<<cdiv(n, 256), 256, 0, s>>>(fa, R, rowmap, lo.mh, lo.mw, W, H, lo.wpr_[0], full);
   }
   // level cascades (batch 0: request closure; batches k>=j: gaze windows)
   for (int j = 1; j <= L; ++j) {
@@ -516,13 +524,11 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
     c.dst = (uint32_t*)(ws + lo.stack[j]);
     c.dst_stride = lo.stack_stride[j] / 4;
     c.fov = fov;
+    c.fa = fa;
     c.nbatch = 0;
     c.batch[c.nbatch++] = 0;
-    if (fov) {
+    if (fov)
       for (int k = j; k <= L; ++k) c.batch[c.nbatch++] = k;
-      for (int k = 1; k <= L; ++k)
-        for (int q = 0; q < 4; ++q) c.rect[k][q] = a->fovea[k - 1][q];
-    }
     c.pooled = lo.bs == 32 ? (uint32_t*)(ws + lo.pooled[j]) : nullptr;
     c.pool_wpr = cdiv(c.wpr, CT_W);
     dim3 grid(cdiv(c.wpr, CT_W), c.nbatch, cdiv(c.rows, CT_R));
@@ -539,8 +545,8 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
     f.srows = H >> j; f.swpr = lo.wpr_[j];
     f.V = j == L ? nullptr : (const uint32_t*)(ws + lo.fp[j]);
     f.D = Dptr(j);
-    f.out = j == 1 ? a->d_footprint : (uint32_t*)(ws + lo.fp[j - 1]);
-    f.R = R; f.rowmap = rowmap;
+    f.out = j == 1 ? nullptr : (uint32_t*)(ws + lo.fp[j - 1]);
+    f.R = R; f.rowmap = rowmap; f.fa = fa;
     dim3 grid(cdiv(f.wpr, CT_W), 1, cdiv(f.rows, CT_R));
     k_footprint<<<grid, 256, 0, s>>>(f);
   }
@@ -549,17 +555,12 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
     b.L = L; b.H = H; b.W = W; b.bs = lo.bs; b.nbx = lo.nbx; b.NB = lo.NB; b.n = lo.n;
     b.rs = 2 + lo.C * (g->float_mode ? 4 : 1);
     for (int k = 1; k <= L; ++k) { b.D[k] = Dptr(k); b.dwpr[k] = lo.wpr_[k]; }
-    uint64_t table = (uint64_t)lo.n * lo.NB * 8;
-    if (a->payload_bytes < table) return WV_ERR_ARG;
-    b.ends = (const unsigned long long*)a->d_payload;
-    b.rec_bytes = a->payload_bytes - table;
+    b.fa = fa;
+    b.table_bytes = (unsigned long long)lo.n * lo.NB * 8;
     b.sel = (uint32_t*)(ws + lo.sel);
     b.prev_sel = (uint32_t*)(ws + lo.prev_sel);
-    b.loaded = a->d_set_loaded;
     b.list = (uint32_t*)(ws + lo.blist);
     b.list_count = counters + CNT_BLOCKS;
-    b.set_bytes = a->d_set_bytes;
-    b.res = a->d_result;
     b.account_only = acct;
     for (int k = 1; k <= L; ++k) {
       const bool ok = lo.bs == 32 && ((H >> k) % 32) == 0 && ((W >> k) % 32) == 0;
@@ -569,7 +570,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
     k_blocks<<<cdiv(lo.NB, 256), 256, 0, s>>>(b);
   }
   if (acct) {
-    k_finalize<<<1, 1, 0, s>>>(a->d_set_bytes, a->d_result);
+    k_finalize<<<1, 1, 0, s>>>(fa);
   } else {
     TileArgs t{};
     t.L = L; t.H = H; t.W = W; t.wpr0 = lo.wpr_[0]; t.R = R; t.rowmap = rowmap; t.full = full;
@@ -581,10 +582,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, const wv_frame_args* a
     t.nwords1 = wpr(lo.ntx[1]);
     t.prev_need = ws + lo.prev_need;
     t.counters = counters;
-    t.set_bytes = a->d_set_bytes;
-    t.res = a->d_result;
-    t.base[2] = 0;
-    for (int k = 2; k <= L; ++k) t.base[k + 1] = t.base[k] + lo.nty[k] * lo.ntx[k];
+    t.fa = fa;
     const int nt1 = lo.nty[1] * lo.ntx[1];
     k_tiles1<<<cdiv(nt1, 256), 256, 0, s>>>(t);
     if (L >= 2) {

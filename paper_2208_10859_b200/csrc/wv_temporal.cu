@@ -18,17 +18,15 @@ namespace wv {
 namespace {
 
 struct TemporalArgs {
-  int L, H, W, C, bs, bs_log2, nbx, n, t, rs, float_mode;
-  const unsigned long long* ends;   // (n, NB)
-  const uint8_t* recs;              // records region
-  const float* extrema;             // (n, C, 4)
+  int L, H, W, C, bs, bs_log2, nbx, n, rs, float_mode;
+  const wv_frame_args* fa;          // t, payload (table + records), extrema, result
+  unsigned long long table_bytes;
   const uint32_t* D[WV_MAX_LEVELS + 1];
   int dwpr[WV_MAX_LEVELS + 1];
   const uint32_t* list;
   const uint32_t* count;
   int NB;
   float* plane;
-  wv_frame_result* res;
 };
 
 // inclusion bit of plane position (y, x) (LevelMaskSet.inclusion_grid)
@@ -94,6 +92,10 @@ constexpr int K2_THREADS = 128;
 constexpr int K2_MAXN = 32;
 
 __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
+  const int t_disp = a.fa->t;
+  const unsigned long long* __restrict__ ends = (const unsigned long long*)a.fa->d_payload;
+  const uint8_t* __restrict__ recs = (const uint8_t*)a.fa->d_payload + a.table_bytes;
+  const float* __restrict__ extrema = a.fa->d_extrema;
   extern __shared__ float4 smem4[];
   float* acc = reinterpret_cast<float*>(smem4);              // C x bs*bs
   __shared__ unsigned long long s_start[K2_MAXN];
@@ -121,13 +123,13 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
     }
     if (tid < a.n) {
       const uint64_t fi = (uint64_t)tid * a.NB + b;
-      const unsigned long long en = a.ends[fi];
-      const unsigned long long st = fi ? a.ends[fi - 1] : 0ull;
+      const unsigned long long en = ends[fi];
+      const unsigned long long st = fi ? ends[fi - 1] : 0ull;
       int cnt = 0;
       if (en >= st && (en - st) % a.rs == 0) cnt = (int)min((en - st) / a.rs, (unsigned long long)npos);
       s_start[tid] = st;
       s_pre[tid + 1] = cnt;        // prefix-summed below
-      s_w[tid] = tweight(tid, a.t, a.n);
+      s_w[tid] = tweight(tid, t_disp, a.n);
     }
     for (int q = tid; q < nq; q += K2_THREADS)
       smem4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -145,7 +147,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
       if (i < total) {
         ti = 0;
         while (s_pre[ti + 1] <= i) ++ti;
-        const uint8_t* rp = a.recs + s_start[ti] + (uint64_t)(i - s_pre[ti]) * a.rs;
+        const uint8_t* rp = recs + s_start[ti] + (uint64_t)(i - s_pre[ti]) * a.rs;
         off = (int)rp[0] | ((int)rp[1] << 8);
         if (off >= npos) {
           err |= WV_DERR_OFFSET;
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
               x = __uint_as_float((uint32_t)q[0] | ((uint32_t)q[1] << 8) |
                                   ((uint32_t)q[2] << 16) | ((uint32_t)q[3] << 24));
             } else {
-              const float* ex = a.extrema + ((uint64_t)ti * a.C + c) * 4 + (appr ? 0 : 2);
+              const float* ex = extrema + ((uint64_t)ti * a.C + c) * 4 + (appr ? 0 : 2);
               const float lo = ex[0], hi = ex[1];
               x = __fadd_rn(lo, __fmul_rn(__fdiv_rn((float)rp[2 + c], 255.0f), __fsub_rn(hi, lo)));
             }
@@ -218,24 +220,23 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
     __syncthreads();
   }
   for (int o = 16; o; o >>= 1) err |= __shfl_xor_sync(0xFFFFFFFFu, err, o);
-  if ((tid & 31) == 0 && err) atomicOr(&a.res->error, err);
+  if ((tid & 31) == 0 && err) atomicOr(&a.fa->d_result->error, err);
 }
 
 }  // namespace
 
-int launch_temporal(const Layout& lo, const wv_geometry* g, const wv_frame_args* a, uint8_t* ws,
-                    cudaStream_t s) {
+int launch_temporal(const Layout& lo, const wv_geometry* g, int mode, const wv_frame_args* fa,
+                    uint8_t* ws, cudaStream_t s) {
   if (lo.bs < 4) return WV_ERR_UNSUPPORTED;
-  if (a->t < 0 || a->t >= lo.n) return WV_ERR_ARG;
+  if (lo.n > K2_MAXN) return WV_ERR_UNSUPPORTED;
   TemporalArgs t{};
   t.L = lo.L; t.H = lo.H; t.W = lo.W; t.C = lo.C; t.bs = lo.bs; t.nbx = lo.nbx; t.n = lo.n;
   t.bs_log2 = 31 - __builtin_clz((unsigned)lo.bs);
-  t.t = a->t; t.float_mode = g->float_mode; t.rs = 2 + lo.C * (g->float_mode ? 4 : 1);
+  t.float_mode = g->float_mode; t.rs = 2 + lo.C * (g->float_mode ? 4 : 1);
   t.NB = lo.NB;
-  t.ends = (const unsigned long long*)a->d_payload;
-  t.recs = (const uint8_t*)a->d_payload + (uint64_t)lo.n * lo.NB * 8;
-  t.extrema = a->d_extrema;
-  const bool fov = a->mode == WV_MODE_FOVEATED;
+  t.fa = fa;
+  t.table_bytes = (unsigned long long)lo.n * lo.NB * 8;
+  const bool fov = mode == WV_MODE_FOVEATED;
   for (int k = 1; k <= lo.L; ++k) {
     t.D[k] = (const uint32_t*)(ws + lo.stack[k] + (fov ? (uint64_t)k * lo.stack_stride[k] : 0));
     t.dwpr[k] = lo.wpr_[k];
@@ -243,11 +244,9 @@ int launch_temporal(const Layout& lo, const wv_geometry* g, const wv_frame_args*
   t.list = (const uint32_t*)(ws + lo.blist);
   t.count = (const uint32_t*)(ws + lo.counters) + CNT_BLOCKS;
   t.plane = (float*)(ws + lo.plane);
-  t.res = a->d_result;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (lo.n > K2_MAXN) return WV_ERR_UNSUPPORTED;
   const size_t smem = (size_t)lo.C * lo.bs * lo.bs * 4;
   if (smem > 48 * 1024)
     WV_CUDA(cudaFuncSetAttribute(k_temporal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
