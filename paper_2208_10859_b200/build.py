@@ -20,8 +20,11 @@ SOURCES = ["wv_select.cu", "wv_temporal.cu", "wv_idwt.cu", "wv_perspective.cu", 
 HEADERS = ["wv_common.cuh"]
 LIB = os.path.join(HERE, "_wvb200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC,-O2",
-         "-shared", "-cudart", "static", "-diag-suppress", "177"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-diag-suppress", "177"]
+# Bit-exact arithmetic (dequantisation, temporal sums, lifting) forbids FMA
+# contraction; the perspective writeout's float32 geometry is approximate by
+# design (+-1 LSB bar) and keeps it.
+FMAD = {"wv_perspective.cu": "true"}
 
 
 def nvcc() -> str:
@@ -43,9 +46,19 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
+    objdir = os.path.join(HERE, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    objs = []
+    for f in SOURCES:
+        obj = os.path.join(objdir, f.replace(".cu", ".o"))
+        cmd = [nvcc(), *ARCH, *FLAGS, f"--fmad={FMAD.get(f, 'false')}", "-I",
+               os.path.join(ROOT, "include"), "-c", "-o", obj, os.path.join(CSRC, f)]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp,
-           *[os.path.join(CSRC, f) for f in SOURCES]]
+    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

@@ -208,3 +208,21 @@ def test_decode_session_requires_gpu():
     from paper_2208_10859_b200 import DecodeSession
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         DecodeSession(os.path.join(GOLDEN, "golden_quantized.wvv"))
+
+
+def test_lifting_kernels_have_no_fused_multiply_add(lib):
+    """Bit-exact synthesis needs every product rounded before its add: the
+    K3 kernels' SASS must contain no FFMA/FFMA2 (ptxas contracts paired f32x2
+    mul/add otherwise)."""
+    import subprocess
+    from paper_2208_10859_b200 import _native
+    sass = subprocess.run(["cuobjdump", "-sass", _native.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    fn, bad = None, []
+    for line in sass.splitlines():
+        if "Function :" in line:
+            fn = line.split(":")[1].strip()
+        elif fn and "k_level" in fn and ("FFMA" in line):
+            bad.append((fn, line.strip()[:60]))
+    assert "k_level" in sass and not bad, bad[:3]
+    assert "UTMALDG" in sass      # the synthesis tiles are TMA-fed
