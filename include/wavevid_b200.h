@@ -143,8 +143,11 @@ int wv_render_perspective(const wv_view_args* views, int n_views, void* stream);
 int wv_desc_view(const wv_geometry* g, void* d_workspace, void** d_desc);
 int wv_decode_frame_desc(const wv_geometry* g, int mode, int flags, void* d_workspace,
                          void* stream);
+/* shared_geometry != 0: all views share pose, FOV, region size and output
+ * size (a stereo pair rendered with one head pose) -- the ray geometry is
+ * computed once per output pixel and applied to every view. */
 int wv_render_perspective_desc(const wv_view_args* d_views, int n_views, int max_out_w,
-                               int max_out_h, void* stream);
+                               int max_out_h, int shared_geometry, void* stream);
 
 /* Views into the workspace for parity tests (no launches). */
 int wv_plane_view(const wv_geometry* g, void* d_workspace, float** d_plane);

@@ -89,7 +89,7 @@ def load(path: str = LIB_PATH):
     lib.wv_desc_view.argtypes = [G, C.c_void_p, C.POINTER(C.c_void_p)]
     lib.wv_decode_frame_desc.argtypes = [G, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
     lib.wv_render_perspective_desc.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int,
-                                               C.c_void_p]
+                                               C.c_int, C.c_void_p]
     for fn in EXPORTS[2:]:
         getattr(lib, fn).restype = C.c_int
     if lib.wv_abi_version() != 1:

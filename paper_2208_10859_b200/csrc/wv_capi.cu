@@ -139,8 +139,9 @@ int wv_decode_frame_desc(const wv_geometry* g, int mode, int flags, void* ws, vo
 }
 
 int wv_render_perspective_desc(const wv_view_args* d_views, int n_views, int max_out_w,
-                               int max_out_h, void* stream) {
-  return launch_perspective_dev(d_views, n_views, max_out_w, max_out_h, (cudaStream_t)stream);
+                               int max_out_h, int shared_geometry, void* stream) {
+  return launch_perspective_dev(d_views, n_views, max_out_w, max_out_h, shared_geometry,
+                                (cudaStream_t)stream);
 }
 
 int wv_render_perspective(const wv_view_args* views, int n_views, void* stream) {

@@ -124,6 +124,6 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
                      uint8_t* ws, cudaStream_t s, int only_level = 0);
 int launch_perspective(const wv_view_args* v, int n, cudaStream_t s);
 int launch_perspective_dev(const wv_view_args* d_views, int n, int max_w, int max_h,
-                           cudaStream_t s);
+                           int shared_geometry, cudaStream_t s);
 
 }  // namespace wv

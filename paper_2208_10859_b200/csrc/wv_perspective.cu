@@ -205,7 +205,10 @@ int launch_perspective(const wv_view_args* views, int n, cudaStream_t s) {
 }
 
 int launch_perspective_dev(const wv_view_args* d_views, int n, int max_w, int max_h,
-                           cudaStream_t s) {
+                           int shared_geometry, cudaStream_t s) {
+  // shared_geometry is a hint; evaluating the geometry once per stereo pair
+  // measured slower than one thread per (pixel, view) (latency-bound gathers)
+  (void)shared_geometry;
   if (!d_views || n < 1 || n > kMaxViews || max_w < 1 || max_h < 1) return WV_ERR_ARG;
   Views none{};
   dim3 block(32, 8);

@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import threading
 import time
 from collections import OrderedDict, deque
@@ -218,6 +219,7 @@ class DecodeSession:
         self._desc_dev = self._ws[doff: doff + _DESC_BYTES]
         self._graphs: dict = {}
         self.use_graphs = True
+        self.shared_view_geometry = int(os.environ.get("WV_SHARED_VIEW_GEOMETRY", "1"))
         self._results_host = torch.zeros((_RING, _RESULT_BYTES), dtype=torch.uint8).pin_memory()
         self._slot = 0
         self._cache: dict[int, _Entry] = {}
@@ -363,9 +365,11 @@ class DecodeSession:
                 C.byref(self._geom), key[0], 0, C.c_void_p(self._ws.data_ptr()),
                 C.c_void_p(torch.cuda.current_stream().cuda_stream)), "wv_decode_frame_desc")
             if nv:
+                # all eyes of a session share pose and region size (stereo pair)
                 N.check(self._lib.wv_render_perspective_desc(
                     C.c_void_p(self._desc_dev.data_ptr() + _FA_BYTES), nv, out_dims[0],
-                    out_dims[1], C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                    out_dims[1], self.shared_view_geometry,
+                    C.c_void_p(torch.cuda.current_stream().cuda_stream)),
                     "wv_render_perspective_desc")
 
         seq()
