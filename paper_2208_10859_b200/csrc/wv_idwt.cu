@@ -259,12 +259,15 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       }
       __syncthreads();
     }
+    bool row_req_full = true;
     if (FINAL && tid < ny) {
       // request-mask words of this tile's output rows (used by the store pass)
       const int gx = 2 * ax;
       const uint32_t* row = a.R + (uint64_t)a.rowmap[2 * ay + tid] * a.wpr0 + (gx >> 5);
-      req[2 * tid] = row[0];
-      req[2 * tid + 1] = nx > 32 ? row[1] : 0u;
+      const uint32_t w0 = row[0], w1 = nx > 32 ? row[1] : 0u;
+      req[2 * tid] = w0;
+      req[2 * tid + 1] = w1;
+      row_req_full = nx == OUT_W && w0 == 0xFFFFFFFFu && w1 == 0xFFFFFFFFu;
     }
 
     // column pass: (segment, box column) per thread, L and H halves packed
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
             });
       }
     }
-    __syncthreads();
+    const bool tile_req_full = __syncthreads_and(row_req_full) && FINAL && ny == OUT_H;
     // row pass: (segment, output row pair) per thread, two rows packed
     if (tid < 2 * TY) {
       const int i = tid % TY, sg = tid / TY;
@@ -309,36 +312,56 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     __syncthreads();
     if (!FINAL) {
       float* base = a.out + ((uint64_t)c * H + 2 * ay) * a.out_pitch + 2 * ax;
-      const int half = nx >> 1;   // float2 columns per row
-      for (int idx = tid; idx < (ny >> 1) * half; idx += NTHREADS) {
-        const int i = idx / half, x2 = idx % half;
-        const float2 u = outb[i * OB_PITCH + 2 * x2];
-        const float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
-        float* r0 = base + (uint64_t)(2 * i) * a.out_pitch + 2 * x2;
-        *reinterpret_cast<float2*>(r0) = make_float2(u.x, v.x);
-        *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
+      if (nx == OUT_W && ny == OUT_H) {
+        // full tile: 32 row pairs x 32 float2 columns, shifts only
+        for (int idx = tid; idx < TY * TX; idx += NTHREADS) {
+          const int i = idx >> 5, x2 = idx & 31;
+          const float2 u = outb[i * OB_PITCH + 2 * x2];
+          const float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
+          float* r0 = base + (uint64_t)(2 * i) * a.out_pitch + 2 * x2;
+          *reinterpret_cast<float2*>(r0) = make_float2(u.x, v.x);
+          *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
+        }
+      } else {
+        const int half = nx >> 1;   // float2 columns per row
+        for (int idx = tid; idx < (ny >> 1) * half; idx += NTHREADS) {
+          const int i = idx / half, x2 = idx % half;
+          const float2 u = outb[i * OB_PITCH + 2 * x2];
+          const float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
+          float* r0 = base + (uint64_t)(2 * i) * a.out_pitch + 2 * x2;
+          *reinterpret_cast<float2*>(r0) = make_float2(u.x, v.x);
+          *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
+        }
       }
     } else {
-      // clip(rint(x*255)) (decoding.py:301), zero outside the request
+      // clip(rint(x*255)) (decoding.py:301), zero outside the request; rint is
+      // round-half-even, as __float2uint_rn (which also saturates below 0)
+      uint8_t* base = canvas + ((uint64_t)c * H + 2 * ay) * W + 2 * ax;
       const int qw = nx >> 2;     // 4-pixel groups per row
-      for (int idx = tid; idx < (ny >> 1) * qw; idx += NTHREADS) {
-        const int i = idx / qw, q = idx % qw;
-        const int gx = 2 * ax + 4 * q;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int r = 2 * i + h;
-          const uint32_t rbits = (req[2 * r + (q >> 3)] >> ((4 * q) & 31)) & 0xFu;
-          uint32_t word = 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 u = outb[i * OB_PITCH + 4 * q + e];
-            float v = rintf(__fmul_rn(h ? u.y : u.x, 255.0f));
-            v = fminf(fmaxf(v, 0.0f), 255.0f);
-            const uint32_t b = ((rbits >> e) & 1u) ? (uint32_t)v : 0u;
-            word |= b << (8 * e);
-          }
-          *reinterpret_cast<uint32_t*>(canvas + ((uint64_t)c * H + 2 * ay + r) * W + gx) = word;
+      const int ngroups = (ny >> 1) * qw;
+      for (int idx = tid; idx < ngroups; idx += NTHREADS) {
+        const int i = tile_req_full ? (idx >> 4) : idx / qw;
+        const int q = tile_req_full ? (idx & 15) : idx % qw;
+        const float2 e0 = outb[i * OB_PITCH + 4 * q];
+        const float2 e1 = outb[i * OB_PITCH + 4 * q + 1];
+        const float2 e2 = outb[i * OB_PITCH + 4 * q + 2];
+        const float2 e3 = outb[i * OB_PITCH + 4 * q + 3];
+        auto cv = [](float v) { return min(__float2uint_rn(__fmul_rn(v, 255.0f)), 255u); };
+        uint32_t w0 = cv(e0.x) | (cv(e1.x) << 8) | (cv(e2.x) << 16) | (cv(e3.x) << 24);
+        uint32_t w1 = cv(e0.y) | (cv(e1.y) << 8) | (cv(e2.y) << 16) | (cv(e3.y) << 24);
+        if (!tile_req_full) {
+          const int sh = (4 * q) & 31;
+          const uint32_t b0 = (req[2 * (2 * i) + (q >> 3)] >> sh) & 0xFu;
+          const uint32_t b1 = (req[2 * (2 * i + 1) + (q >> 3)] >> sh) & 0xFu;
+          // expand 4 request bits to 4 byte masks
+          w0 &= ((b0 & 1u) * 0xFFu | ((b0 >> 1) & 1u) * 0xFF00u | ((b0 >> 2) & 1u) * 0xFF0000u |
+                 ((b0 >> 3) & 1u) * 0xFF000000u);
+          w1 &= ((b1 & 1u) * 0xFFu | ((b1 >> 1) & 1u) * 0xFF00u | ((b1 >> 2) & 1u) * 0xFF0000u |
+                 ((b1 >> 3) & 1u) * 0xFF000000u);
         }
+        uint8_t* r0 = base + (uint64_t)(2 * i) * W + 4 * q;
+        *reinterpret_cast<uint32_t*>(r0) = w0;
+        *reinterpret_cast<uint32_t*>(r0 + W) = w1;
       }
     }
     __syncthreads();

@@ -219,6 +219,7 @@ class DecodeSession:
         self._desc_dev = self._ws[doff: doff + _DESC_BYTES]
         self._graphs: dict = {}
         self.use_graphs = True
+        self._ones_fp = None
         self.shared_view_geometry = int(os.environ.get("WV_SHARED_VIEW_GEOMETRY", "1"))
         self._results_host = torch.zeros((_RING, _RESULT_BYTES), dtype=torch.uint8).pin_memory()
         self._slot = 0
@@ -534,7 +535,14 @@ class DecodeSession:
         h = self.header
         if mode == "foveated" and schedule is None:
             schedule = FoveationSchedule.default(h.levels)
-        views = [view_args(self._canvas, self._footprint, r0, rows, h.width, h.channels, pose,
+        # a foveated frame is exact only near the gaze; its callers render with
+        # an all-ones footprint (cli.py:177, service.py:135)
+        fp = self._footprint
+        if mode == "foveated":
+            if self._ones_fp is None:
+                self._ones_fp = torch.full_like(self._footprint, -1)
+            fp = self._ones_fp
+        views = [view_args(self._canvas, fp, r0, rows, h.width, h.channels, pose,
                            out[i], self._uncovered) for i, (r0, rows) in enumerate(self._eyes())]
         p = self._launch(frame, mode, mask, schedule, views=views, out_dims=tuple(out_dims))
         return DeviceFrame(self, p, self._canvas, self._footprint)
