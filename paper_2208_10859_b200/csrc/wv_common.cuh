@@ -8,7 +8,10 @@
 namespace wv {
 
 // synthesis tile: TY x TX coefficients per subband -> (2TY) x (2TX) outputs
-constexpr int TY = 32;
+#ifndef WV_TILE_Y
+#define WV_TILE_Y 32
+#endif
+constexpr int TY = WV_TILE_Y;
 constexpr int TX = 32;
 constexpr int HALO = 2;               // lifting support per side
 // TMA box: the innermost box coordinate must be 16-byte aligned (unaligned or

@@ -35,10 +35,20 @@ constexpr int BOX_FLOATS = BOX_W * BOX_H;
 constexpr int BOX_SLOT = ((BOX_FLOATS * 4 + 127) / 128) * 128;  // bytes
 constexpr int CB_PITCH = BOX_W + 1;   // float2 units, odd -> conflict-free row pass
 constexpr int OB_PITCH = OUT_W + 1;   // float2 units (row pairs), odd
-constexpr int NTHREADS = 128;
+// line segments: every lifting stream covers 16 output pairs (+ its halo)
+constexpr int SEGLEN = 16;
+constexpr int COL_SEGS = TY / SEGLEN, ROW_SEGS = TX / SEGLEN;
+constexpr int NTHREADS = (COL_SEGS * BOX_W > ROW_SEGS * TY ? COL_SEGS * BOX_W : ROW_SEGS * TY) <= 64
+                             ? 64 : 128;
 static_assert(TY * OB_PITCH * 8 <= 4 * BOX_SLOT, "output tile must fit in the box region");
 
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+// d * (1/K) feeds the packed add (d[i-1] + d[i]) of the next lifting step; a
+// packed multiply there would be contracted into FFMA2 by ptxas, so the
+// scale is two scalar round-to-nearest multiplies (never contracted).
+__device__ __forceinline__ float2 dscale(float2 d, float2 ik) {
+  return make_float2(__fmul_rn(d.x, ik.x), __fmul_rn(d.y, ik.y));
+}
 // x - k*(y1 + y2), written as x + (-k)*(y1+y2): identical rounding.  The
 // final add is issued as two scalar FADDs: ptxas contracts a paired
 // mul.rn.f32x2 feeding add.rn.f32x2 into FFMA2 (observed with CUDA 12.9),
@@ -64,13 +74,13 @@ __device__ __forceinline__ void lift_line(int g0, int g1, int N, int a, int b, L
   float2 sr, dr;
   // j = g0 (at the left border d1[-1] = d1[0]; elsewhere the value is a halo)
   load(g0, sr, dr);
-  float2 d1m = __fmul2_rn(dr, IK);
+  float2 d1m = dscale(dr, IK);
   float2 s2m = lstep(__fmul2_rn(sr, KS), ND, d1m, d1m);
   float2 d2mm = d1m, s3mm = s2m;
   if (g1 - g0 >= 2) {
     // j = g0 + 1 (at the left border d2[-1] = d2[0])
     load(g0 + 1, sr, dr);
-    float2 d1 = __fmul2_rn(dr, IK);
+    float2 d1 = dscale(dr, IK);
     float2 s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);
     float2 d2 = lstep(d1m, NG, s2m, s2);
     s3mm = lstep(s2m, NB, d2, d2);
@@ -80,7 +90,7 @@ __device__ __forceinline__ void lift_line(int g0, int g1, int N, int a, int b, L
 #pragma unroll 4
     for (int j = g0 + 2; j < g1; ++j) {
       load(j, sr, dr);
-      d1 = __fmul2_rn(dr, IK);
+      d1 = dscale(dr, IK);
       s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);   // s2[j]
       d2 = lstep(d1m, NG, s2m, s2);                   // d2[j-1]
       float2 s3 = lstep(s2m, NB, d2mm, d2);           // s3[j-1]
@@ -98,6 +108,44 @@ __device__ __forceinline__ void lift_line(int g0, int g1, int N, int a, int b, L
     float2 s3 = lstep(s2m, NB, N == 1 ? d2 : d2mm, d2);       // s3[N-1]
     if (N >= 2 && N - 2 >= a && N - 2 < b) emit(N - 2, s3mm, lstep(d2mm, NA, s3mm, s3));
     if (N - 1 >= a && N - 1 < b) emit(N - 1, s3, lstep(d2, NA, s3, s3));
+  }
+}
+
+// Interior segment (no level border inside [g0, g0 + LEN + 4)): the same
+// stream with a compile-time trip count, fully unrolled -- no loop counter,
+// no emission tests, constant shared-memory offsets.  Local indices: inputs
+// 0 .. LEN+3, emitted pairs 2 .. LEN+1.
+template <int LEN, class Load, class Emit>
+__device__ __forceinline__ void lift_interior(Load load, Emit emit) {
+  const float2 KS = f2(__uint_as_float(0x3f9d7658u));
+  const float2 IK = f2(__uint_as_float(0x3f5019c3u));
+  const float2 ND = f2(-__uint_as_float(0x3ee31355u));
+  const float2 NG = f2(-__uint_as_float(0x3f620676u));
+  const float2 NB = f2(-__uint_as_float(0xbd5901aeu));
+  const float2 NA = f2(-__uint_as_float(0xbfcb0673u));
+  float2 sr, dr;
+  load(0, sr, dr);
+  float2 d1m = dscale(dr, IK);
+  float2 s2m = __fmul2_rn(sr, KS);         // s2[0] is a halo value: never emitted
+  load(1, sr, dr);
+  float2 d1 = dscale(dr, IK);
+  float2 s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);
+  float2 d2mm = lstep(d1m, NG, s2m, s2);   // d2[0] (halo)
+  float2 s3mm = s2;                        // s3[0] (halo)
+  d1m = d1;
+  s2m = s2;
+#pragma unroll
+  for (int j = 2; j < LEN + 4; ++j) {
+    load(j, sr, dr);
+    d1 = dscale(dr, IK);
+    s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);   // s2[j]
+    const float2 d2 = lstep(d1m, NG, s2m, s2);      // d2[j-1]
+    const float2 s3 = lstep(s2m, NB, d2mm, d2);     // s3[j-1]
+    if (j >= 4) emit(j - 2, s3mm, lstep(d2mm, NA, s3mm, s3));   // d3[j-2]
+    d2mm = d2;
+    s3mm = s3;
+    d1m = d1;
+    s2m = s2;
   }
 }
 
@@ -160,6 +208,8 @@ struct LevelArgs {
 // pairs.  Store pass: coalesced f32 (mid levels) or packed u8 with the
 // request mask applied (finest level).
 constexpr int BOXSET = 4 * BOX_SLOT;
+constexpr int O8_PITCH = OUT_W + 4;   // bytes; 4-aligned rows for the word copy
+static_assert(OUT_H * O8_PITCH <= BOXSET, "u8 tile must fit in the box region");
 constexpr int NBUF = 1;
 
 template <bool FINAL>
@@ -172,7 +222,6 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   float2* colH = colL + TY * CB_PITCH;
   uint32_t* req = reinterpret_cast<uint32_t*>(colH + TY * CB_PITCH);  // FINAL: [OUT_H][2]
   __shared__ uint64_t bar[2];
-  constexpr int SEG = TY / 2;   // == TX / 2
 
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -235,6 +284,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     const float* bLH = box + 2 * BOX_SLOT / 4;
     const float* bHH = box + 3 * BOX_SLOT / 4;
     float2* outb = reinterpret_cast<float2*>(box);                  // aliases this item's boxes
+    uint8_t* out8 = reinterpret_cast<uint8_t*>(box);                // FINAL: [OUT_H][O8_PITCH]
     const int oy = max(ay - HALO, 0), ox = max(ax - XPAD, 0);
     if (a.use_tma) {
       if (NBUF == 1) issue(item, 0);
@@ -271,42 +321,78 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     }
 
     // column pass: (segment, box column) per thread, L and H halves packed
-    if (tid < 2 * BOX_W) {
+    if (tid < COL_SEGS * BOX_W) {
       const int lc = tid % BOX_W, sg = tid / BOX_W;
       const int cg = ox + lc;
-      const int pa = ay + sg * SEG, pb = sg ? by : min(ay + SEG, by);
+      const int pa = ay + sg * SEGLEN, pb = min(pa + SEGLEN, by);
       if (pa < pb && cg >= max(ax - HALO, 0) && cg < min(bx + HALO, a.bw)) {
-        lift_line(
-            max(pa - HALO, 0), min(pb + HALO, a.bh), a.bh, pa, pb,
-            [&](int j, float2& s, float2& d) {
-              const int o = (j - oy) * BOX_W + lc;
-              s = make_float2(bLL[o], bHL[o]);
-              d = make_float2(bLH[o], bHH[o]);
-            },
-            [&](int p, float2 s3, float2 d3) {
-              const int q = p - ay;
-              colL[q * CB_PITCH + lc] = make_float2(s3.x, d3.x);
-              colH[q * CB_PITCH + lc] = make_float2(s3.y, d3.y);
-            });
+        if (pa >= HALO && pb + HALO <= a.bh && pb - pa == SEGLEN) {
+          const int rb = pa - HALO - oy;          // local box row of input 0
+          const int qb = pa - HALO - ay;          // output pair of input 0
+          lift_interior<SEGLEN>(
+              [&](int j, float2& s, float2& d) {
+                const int o = (rb + j) * BOX_W + lc;
+                s = make_float2(bLL[o], bHL[o]);
+                d = make_float2(bLH[o], bHH[o]);
+              },
+              [&](int p, float2 s3, float2 d3) {
+                colL[(qb + p) * CB_PITCH + lc] = make_float2(s3.x, d3.x);
+                colH[(qb + p) * CB_PITCH + lc] = make_float2(s3.y, d3.y);
+              });
+        } else {
+          lift_line(
+              max(pa - HALO, 0), min(pb + HALO, a.bh), a.bh, pa, pb,
+              [&](int j, float2& s, float2& d) {
+                const int o = (j - oy) * BOX_W + lc;
+                s = make_float2(bLL[o], bHL[o]);
+                d = make_float2(bLH[o], bHH[o]);
+              },
+              [&](int p, float2 s3, float2 d3) {
+                const int q = p - ay;
+                colL[q * CB_PITCH + lc] = make_float2(s3.x, d3.x);
+                colH[q * CB_PITCH + lc] = make_float2(s3.y, d3.y);
+              });
+        }
       }
     }
     const bool tile_req_full = __syncthreads_and(row_req_full) && FINAL && ny == OUT_H;
     // row pass: (segment, output row pair) per thread, two rows packed
-    if (tid < 2 * TY) {
+    if (tid < ROW_SEGS * TY) {
       const int i = tid % TY, sg = tid / TY;
-      const int pa = ax + sg * SEG, pb = sg ? bx : min(ax + SEG, bx);
+      const int pa = ax + sg * SEGLEN, pb = min(pa + SEGLEN, bx);
       if (i < by - ay && pa < pb) {
-        lift_line(
-            max(pa - HALO, 0), min(pb + HALO, a.bw), a.bw, pa, pb,
-            [&](int j, float2& s, float2& d) {
-              s = colL[i * CB_PITCH + (j - ox)];
-              d = colH[i * CB_PITCH + (j - ox)];
-            },
-            [&](int p, float2 s3, float2 d3) {
-              const int q = p - ax;
-              outb[i * OB_PITCH + 2 * q] = s3;
-              outb[i * OB_PITCH + 2 * q + 1] = d3;
-            });
+        // mid levels: f32 pairs into outb; finest level: clip(rint(x*255))
+        // (decoding.py:301; rint is round-half-even like __float2uint_rn,
+        // which also saturates below 0) straight into a u8 tile
+        auto emit_out = [&](int q, float2 s3, float2 d3) {
+          if (!FINAL) {
+            outb[i * OB_PITCH + 2 * q] = s3;
+            outb[i * OB_PITCH + 2 * q + 1] = d3;
+          } else {
+            auto cv = [](float v) { return min(__float2uint_rn(__fmul_rn(v, 255.0f)), 255u); };
+            *reinterpret_cast<uint16_t*>(out8 + (2 * i) * O8_PITCH + 2 * q) =
+                (uint16_t)(cv(s3.x) | (cv(d3.x) << 8));
+            *reinterpret_cast<uint16_t*>(out8 + (2 * i + 1) * O8_PITCH + 2 * q) =
+                (uint16_t)(cv(s3.y) | (cv(d3.y) << 8));
+          }
+        };
+        if (pa >= HALO && pb + HALO <= a.bw && pb - pa == SEGLEN) {
+          const int cb = pa - HALO - ox, qb = pa - HALO - ax;
+          lift_interior<SEGLEN>(
+              [&](int j, float2& s, float2& d) {
+                s = colL[i * CB_PITCH + cb + j];
+                d = colH[i * CB_PITCH + cb + j];
+              },
+              [&](int p, float2 s3, float2 d3) { emit_out(qb + p, s3, d3); });
+        } else {
+          lift_line(
+              max(pa - HALO, 0), min(pb + HALO, a.bw), a.bw, pa, pb,
+              [&](int j, float2& s, float2& d) {
+                s = colL[i * CB_PITCH + (j - ox)];
+                d = colH[i * CB_PITCH + (j - ox)];
+              },
+              [&](int p, float2 s3, float2 d3) { emit_out(p - ax, s3, d3); });
+        }
       }
     }
     __syncthreads();
@@ -315,7 +401,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       if (nx == OUT_W && ny == OUT_H) {
         // full tile: 32 row pairs x 32 float2 columns, shifts only
         for (int idx = tid; idx < TY * TX; idx += NTHREADS) {
-          const int i = idx >> 5, x2 = idx & 31;
+          const int i = idx / TX, x2 = idx % TX;
           const float2 u = outb[i * OB_PITCH + 2 * x2];
           const float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
           float* r0 = base + (uint64_t)(2 * i) * a.out_pitch + 2 * x2;
@@ -334,34 +420,19 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         }
       }
     } else {
-      // clip(rint(x*255)) (decoding.py:301), zero outside the request; rint is
-      // round-half-even, as __float2uint_rn (which also saturates below 0)
+      // u8 rows -> canvas plane c, zero outside the request
       uint8_t* base = canvas + ((uint64_t)c * H + 2 * ay) * W + 2 * ax;
-      const int qw = nx >> 2;     // 4-pixel groups per row
-      const int ngroups = (ny >> 1) * qw;
-      for (int idx = tid; idx < ngroups; idx += NTHREADS) {
-        const int i = tile_req_full ? (idx >> 4) : idx / qw;
-        const int q = tile_req_full ? (idx & 15) : idx % qw;
-        const float2 e0 = outb[i * OB_PITCH + 4 * q];
-        const float2 e1 = outb[i * OB_PITCH + 4 * q + 1];
-        const float2 e2 = outb[i * OB_PITCH + 4 * q + 2];
-        const float2 e3 = outb[i * OB_PITCH + 4 * q + 3];
-        auto cv = [](float v) { return min(__float2uint_rn(__fmul_rn(v, 255.0f)), 255u); };
-        uint32_t w0 = cv(e0.x) | (cv(e1.x) << 8) | (cv(e2.x) << 16) | (cv(e3.x) << 24);
-        uint32_t w1 = cv(e0.y) | (cv(e1.y) << 8) | (cv(e2.y) << 16) | (cv(e3.y) << 24);
+      const int qw = nx >> 2;     // 4-pixel words per row
+      for (int idx = tid; idx < ny * qw; idx += NTHREADS) {
+        const int r = tile_req_full ? idx / (OUT_W / 4) : idx / qw;
+        const int q = tile_req_full ? idx % (OUT_W / 4) : idx % qw;
+        uint32_t w = *reinterpret_cast<const uint32_t*>(out8 + r * O8_PITCH + 4 * q);
         if (!tile_req_full) {
-          const int sh = (4 * q) & 31;
-          const uint32_t b0 = (req[2 * (2 * i) + (q >> 3)] >> sh) & 0xFu;
-          const uint32_t b1 = (req[2 * (2 * i + 1) + (q >> 3)] >> sh) & 0xFu;
-          // expand 4 request bits to 4 byte masks
-          w0 &= ((b0 & 1u) * 0xFFu | ((b0 >> 1) & 1u) * 0xFF00u | ((b0 >> 2) & 1u) * 0xFF0000u |
-                 ((b0 >> 3) & 1u) * 0xFF000000u);
-          w1 &= ((b1 & 1u) * 0xFFu | ((b1 >> 1) & 1u) * 0xFF00u | ((b1 >> 2) & 1u) * 0xFF0000u |
-                 ((b1 >> 3) & 1u) * 0xFF000000u);
+          const uint32_t b = (req[2 * r + (q >> 3)] >> ((4 * q) & 31)) & 0xFu;
+          w &= (b & 1u) * 0xFFu | ((b >> 1) & 1u) * 0xFF00u | ((b >> 2) & 1u) * 0xFF0000u |
+               ((b >> 3) & 1u) * 0xFF000000u;
         }
-        uint8_t* r0 = base + (uint64_t)(2 * i) * W + 4 * q;
-        *reinterpret_cast<uint32_t*>(r0) = w0;
-        *reinterpret_cast<uint32_t*>(r0 + W) = w1;
+        *reinterpret_cast<uint32_t*>(base + (uint64_t)r * W + 4 * q) = w;
       }
     }
     __syncthreads();
