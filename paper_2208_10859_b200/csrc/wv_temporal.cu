@@ -27,6 +27,7 @@ struct TemporalArgs {
   const uint32_t* count;
   int NB;
   float* plane;
+  int all_included;                 // full-frame decode: every inclusion bit is set
 };
 
 // inclusion bit of plane position (y, x) (LevelMaskSet.inclusion_grid)
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
   __shared__ unsigned long long s_start[K2_MAXN];
   __shared__ int s_pre[K2_MAXN + 1];
   __shared__ int s_w[K2_MAXN];
+  __shared__ uint32_t s_mrow[32];
   const int tid = threadIdx.x;
   const int npos = a.bs * a.bs;
   const int nq = (a.C * npos) >> 2;                           // float4 per block
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
     const int y0 = by * a.bs, x0 = (b - by * a.nbx) * a.bs;
     if (e & ZERO_FLAG) {
       for (int q = tid; q < nq; q += K2_THREADS) {
-        const int c = (q << 2) / npos, i = (q << 2) - c * npos;
+        const int c = (q << 2) >> (2 * a.bs_log2), i = (q << 2) & (npos - 1);
         float* dst = a.plane + ((uint64_t)c * a.H + y0 + (i >> a.bs_log2)) * a.W + x0 + (i & bmask);
         *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -130,6 +132,14 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
       s_start[tid] = st;
       s_pre[tid + 1] = cnt;        // prefix-summed below
       s_w[tid] = tweight(tid, t_disp, a.n);
+    }
+    const BlockIncl bi = a.all_included ? BlockIncl{0, nullptr, 0, 0, 0} : classify(a, y0, x0);
+    if (bi.mode == 1 && a.bs <= 32 && tid < a.bs) {
+      const int cc = bi.c0;
+      const uint32_t* row = bi.rows + (uint64_t)(bi.r0 + tid) * bi.wpr;
+      const uint32_t lo = row[cc >> 5];
+      const uint32_t hi = ((cc & 31) + a.bs > 32) ? row[(cc >> 5) + 1] : 0u;
+      s_mrow[tid] = (uint32_t)(((((uint64_t)hi) << 32) | lo) >> (cc & 31));
     }
     for (int q = tid; q < nq; q += K2_THREADS)
       smem4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -190,15 +200,19 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
       }
       __syncthreads();
     }
-    // write: inclusion-masked, 4 consecutive positions per thread-step
-    const BlockIncl bi = classify(a, y0, x0);
+    // write: inclusion-masked, 4 consecutive positions per thread-step; the
+    // block's mask rows (bs <= 32) were staged in shared memory up front
+    const int npos_log2 = 2 * a.bs_log2;
     for (int q = tid; q < nq; q += K2_THREADS) {
-      const int c = (q << 2) / npos, i = (q << 2) - c * npos;
+      const int e4 = q << 2;
+      const int c = e4 >> npos_log2, i = e4 & (npos - 1);
       const int ly = i >> a.bs_log2, lx = i & bmask;
       const int yy = y0 + ly, xx = x0 + lx;
       uint32_t m4;
       if (bi.mode == 0) {
         m4 = 0xFu;
+      } else if (bi.mode == 1 && a.bs <= 32) {
+        m4 = (s_mrow[ly] >> lx) & 0xFu;
       } else if (bi.mode == 1) {
         const int cc = bi.c0 + lx;
         const uint32_t* row = bi.rows + (uint64_t)(bi.r0 + ly) * bi.wpr;
@@ -237,6 +251,7 @@ int launch_temporal(const Layout& lo, const wv_geometry* g, int mode, const wv_f
   t.fa = fa;
   t.table_bytes = (unsigned long long)lo.n * lo.NB * 8;
   const bool fov = mode == WV_MODE_FOVEATED;
+  t.all_included = mode == WV_MODE_FULL;
   for (int k = 1; k <= lo.L; ++k) {
     t.D[k] = (const uint32_t*)(ws + lo.stack[k] + (fov ? (uint64_t)k * lo.stack_stride[k] : 0));
     t.dwpr[k] = lo.wpr_[k];
