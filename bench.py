@@ -476,6 +476,11 @@ def cpu_baseline_sample(path, frame, pm_entry, mode):
                        f"numpy oracle, single process, {el:.1f} s")}
 
 
+def _init_worker():
+    import numpy  # noqa: F401
+    from oracle import wavevid_oracle  # noqa: F401
+
+
 def _worker(a):
     path, frame, pose_t, mask, mode = a
     return _oracle_frame(path, frame, pose_t, mask, mode)
@@ -511,9 +516,10 @@ def run_reference(args):
     jobs = [(path, f, (pm[f][0].yaw, pm[f][0].pitch, pm[f][0].roll), pm[f][1], args.mode)
             for f in frames]
     ctx = mp.get_context("spawn")
-    with ctx.Pool(procs) as pool:
-        wj = [jobs[i % len(jobs)] for i in range(max(1, min(args.warmup, procs)))]
-        pool.map(_worker, wj)
+    with ctx.Pool(procs, initializer=_init_worker) as pool:
+        # warm every worker (imports, first-touch allocations) before timing
+        wj = [jobs[i % len(jobs)] for i in range(max(procs, args.warmup))]
+        pool.map(_worker, wj, chunksize=1)
         tj = [jobs[i % len(jobs)] for i in range(args.steps)]
         t0 = time.perf_counter()
         pool.map(_worker, tj, chunksize=1)
