@@ -281,6 +281,7 @@ struct BlockArgs {
   uint32_t* list;
   uint32_t* list_count;
   int account_only;
+  int full;                                    // decode_full: every block selected
   const uint32_t* pooled[WV_MAX_LEVELS + 1];   // nullptr: scan rows
   int pool_wpr[WV_MAX_LEVELS + 1];
 };
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(256) k_blocks(BlockArgs a) {
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = b < a.NB;
-  const bool sel = valid && block_any(a, b);
+  const bool sel = valid && (a.full || block_any(a, b));
   unsigned long long bytes = 0, recs = 0;
   uint32_t err = 0;
   if (sel) {
@@ -492,6 +493,16 @@ __global__ void __launch_bounds__(1024) k_tiles_up(TileArgs a) {
   }
 }
 
+// decode_full: the footprint is the whole frame (LevelMaskSet.full,
+// wavelets.py:267-270), no mask cascades are needed
+__global__ void k_fill_footprint(const wv_frame_args* __restrict__ fa, int rows, int cols,
+                                 int wpr) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * wpr) return;
+  const int w = idx % wpr;
+  fa->d_footprint[idx] = last_word_mask(cols, w);
+}
+
 __global__ void k_finalize(const wv_frame_args* fa) {
   fa->d_result->set_bytes = *fa->d_set_bytes;
 }
@@ -512,8 +523,9 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     const int n = max(lo.mh * lo.wpr_[0], H);
     k_mask_rows<<<cdiv(n, 256), 256, 0, s>>>(fa, R, rowmap, lo.mh, lo.mw, W, H, lo.wpr_[0], full);
   }
-  // level cascades (batch 0: request closure; batches k>=j: gaze windows)
-  for (int j = 1; j <= L; ++j) {
+  // level cascades (batch 0: request closure; batches k>=j: gaze windows);
+  // a full-frame decode needs none of them
+  for (int j = 1; j <= L && !full; ++j) {
     CascadeArgs c{};
     c.j = j; c.L = L; c.H = H;
     c.rows = H >> j; c.cols = W >> j; c.wpr = lo.wpr_[j];
@@ -538,7 +550,9 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     return (uint32_t*)(ws + lo.stack[k] + (fov ? (uint64_t)k * lo.stack_stride[k] : 0));
   };
   // footprint: V_L = ones; V_{j-1} = shrink(up(V_j & D_j)); last & request
-  for (int j = L; j >= 1 && !acct; --j) {
+  if (full && !acct)
+    k_fill_footprint<<<cdiv(H * lo.wpr_[0], 256), 256, 0, s>>>(fa, H, W, lo.wpr_[0]);
+  for (int j = L; j >= 1 && !acct && !full; --j) {
     FootArgs f{};
     f.j = j; f.L = L; f.H = H;
     f.rows = H >> (j - 1); f.cols = W >> (j - 1); f.wpr = lo.wpr_[j - 1];
@@ -562,6 +576,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     b.list = (uint32_t*)(ws + lo.blist);
     b.list_count = counters + CNT_BLOCKS;
     b.account_only = acct;
+    b.full = full;
     for (int k = 1; k <= L; ++k) {
       const bool ok = lo.bs == 32 && ((H >> k) % 32) == 0 && ((W >> k) % 32) == 0;
       b.pooled[k] = ok ? (const uint32_t*)(ws + lo.pooled[k]) : nullptr;
