@@ -41,6 +41,7 @@ struct Layout {
   uint64_t pooled[WV_MAX_LEVELS + 1];    // D_j pooled to 32x32 cells: one word per 32x1024 tile
   uint64_t sel, prev_sel;                // NB-bit bitmaps
   uint64_t blist;                        // NB u32 entries
+  uint64_t bstate;                       // u8[NB]: plane block may hold nonzeros (K2)
   int nty[WV_MAX_LEVELS + 1], ntx[WV_MAX_LEVELS + 1];  // tile grid of synthesis level k
   uint64_t need[WV_MAX_LEVELS + 1];      // u8 per tile
   uint64_t prev_need;                    // level 1, u8 per tile
@@ -88,6 +89,7 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
   o->sel = take(uint64_t(wpr(o->NB)) * 4);
   o->prev_sel = take(uint64_t(wpr(o->NB)) * 4);
   o->blist = take(uint64_t(o->NB) * 4);
+  o->bstate = take(uint64_t(o->NB));
   for (int k = 1; k <= L; ++k) {
     o->nty[k] = cdiv(H >> k, TY);
     o->ntx[k] = cdiv(W >> k, TX);

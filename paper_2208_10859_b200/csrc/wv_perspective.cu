@@ -55,10 +55,21 @@ __device__ __forceinline__ int wrapx(int x, int n) { return x < 0 ? x + n : (x >
 // atan2 for finite arguments, not both zero: octant reduction + degree-15 odd
 // minimax polynomial (max error 1.1e-7 rad in float32, i.e. < 2e-4 px of the
 // 8K source; the coverage margin kNear is 4e-3 px).
+__device__ __forceinline__ float rcp_approx(float x) {   // MUFU.RCP, no denormal fix-up
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ float fast_atan2(float y, float x) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-  const float a = __fdividef(mn, mx);
+  const float a = mx > 1e-30f ? mn * rcp_approx(mx) : 0.0f;   // atan2(0, 0) = 0
   const float s = a * a;
   float p = -0.004054488614201546f;
   p = fmaf(p, s, 0.021862687543034554f);
@@ -88,9 +99,6 @@ __device__ __forceinline__ uint32_t range_bits(int c0, int c1, int w) {
 // tap sets is tested, and only if that union is not fully covered is the
 // float64 reference geometry evaluated for the pixel.
 constexpr float kNear = 4e-3f;
-#ifndef K4_MIN_BLOCKS
-#define K4_MIN_BLOCKS 8
-#endif
 
 __device__ __noinline__ uint32_t fp_bits_wrap(const uint32_t* row, int x0, int len, int n) {
   uint32_t r = 0;
@@ -124,18 +132,171 @@ struct ViewConst {
   uint32_t* uncovered;
   int xmin, xmax, ymin, ymax;   // candidate-tap bounding box of the CTA
   int covered;                  // that whole box lies inside the footprint
+  int use_win;                  // the box is staged in shared memory
 };
 
-// This translation unit is compiled with FMA contraction enabled: the float32
-// geometry is approximate by design, and the bilinear blend's lerps may round
-// differently from the reference by < 1e-4 LSB; both stay inside the +-1 LSB
-// bar.  The float64 fallback uses explicit __d*_rn intrinsics.
+// One CTA renders a K4_TY x K4_TX output tile (256 threads, K4_PPT pixels per
+// thread, rows ty + 8k).  Phases: (1) float32 geometry of every pixel and the
+// CTA's candidate-tap box; (2) one warp tests the box against the footprint;
+// (3) the box of all C canvas planes is read with 4-byte loads and stored
+// channel-interleaved (one 32-bit word per source pixel) in shared memory;
+// (4) four shared loads per pixel feed the bilinear blend; (5) the tile's
+// (rows, K4_TX*C) bytes are staged and written with 16-byte stores.  Boxes
+// that wrap in longitude, clamp at a pole or exceed the window use direct
+// global gathers (projection.py:146-149 semantics).
+constexpr int K4_TX = 32, K4_TY = 32, K4_PPT = K4_TY / 8;
+constexpr int WIN_W = 128, WIN_H = 80;          // source pixels (32-bit words)
+constexpr int OST_PITCH = K4_TX * 4;            // bytes per staged output row (C <= 4)
+#ifndef K4_MIN_BLOCKS
+#define K4_MIN_BLOCKS 4
+#endif
+
+
+// clip(rint(v)) of the bilinear blend (projection.py:150-170) from the four
+// taps' biased channel values.  v is a convex combination of bytes, rounded
+// once per FMA, so it lies in [0, 255] up to 1e-5 and needs no clamp;
+// adding 2^23 rounds half-to-even like np.rint and leaves the byte in the
+// low mantissa bits.
+__device__ __forceinline__ uint32_t blend(float b00, float b01, float b10, float b11, float ax,
+                                          float ay) {
+  const float top = fmaf(ax, b01 - b00, b00 - 8388608.0f);
+  const float bot = fmaf(ax, b11 - b10, b10 - 8388608.0f);
+  return __float_as_uint(fmaf(ay, bot - top, top) + 8388608.0f) & 0xFFu;
+}
+
+// Phases 3-5 for CT channels (CT = 0: any C in 1..4, read at run time).
+template <int CT>
+__device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& v, uint32_t* win,
+                                       uint8_t* ost, const int (&x0)[K4_PPT],
+                                       const int (&y0)[K4_PPT], const float (&ax)[K4_PPT],
+                                       const float (&ay)[K4_PPT], int x, int ybase, int xl, int yl,
+                                       int yh, int wx0, int ww, int tid) {
+  const int C = CT ? CT : vc.C;
+  const int m = vc.m, n = vc.n, out_w = vc.out_w, out_h = vc.out_h;
+  const bool use_win = vc.use_win;
+  // (3) stage the box, channels interleaved (byte c of word = channel c)
+  if (use_win) {
+    const uint8_t* img = vc.img;
+    const uint32_t plane = vc.plane;
+    const int rows = yh - yl + 1;
+    for (int idx = tid; idx < rows * ww; idx += 256) {
+      const int r = idx / ww, q = idx - (idx / ww) * ww;
+      const uint32_t off = (uint32_t)(yl + r) * n + wx0 + 4 * q;
+      const uint32_t R = __ldg(reinterpret_cast<const uint32_t*>(img + off));
+      const uint32_t G = C > 1 ? __ldg(reinterpret_cast<const uint32_t*>(img + plane + off)) : 0u;
+      const uint32_t B = C > 2 ? __ldg(reinterpret_cast<const uint32_t*>(img + 2 * plane + off)) : 0u;
+      const uint32_t A = C > 3 ? __ldg(reinterpret_cast<const uint32_t*>(img + 3 * plane + off)) : 0u;
+      const uint32_t rg_lo = __byte_perm(R, G, 0x5140), rg_hi = __byte_perm(R, G, 0x7362);
+      const uint32_t ba_lo = __byte_perm(B, A, 0x5140), ba_hi = __byte_perm(B, A, 0x7362);
+      *reinterpret_cast<uint4*>(win + r * WIN_W + 4 * q) =
+          make_uint4(__byte_perm(rg_lo, ba_lo, 0x5410), __byte_perm(rg_lo, ba_lo, 0x7632),
+                     __byte_perm(rg_hi, ba_hi, 0x5410), __byte_perm(rg_hi, ba_hi, 0x7632));
+    }
+  }
+  __syncthreads();
+  // (4) per-pixel coverage (only when the box test failed) and blend
+  const bool covered = vc.covered;
+  unsigned n_unc = 0;
+  const uint32_t K = 0x4B000000u;
+#pragma unroll
+  for (int k = 0; k < K4_PPT; ++k) {
+    const int y = ybase + 8 * k;
+    const bool live = x < out_w && y < out_h;
+    bool uncovered = false;
+    if (live) {
+      int tx0 = x0[k], ty0 = y0[k];
+      float tax = ax[k], tay = ay[k];
+      if (!covered) {
+        const uint32_t* F = vc.F;
+        const int wpr0 = vc.wpr0;
+        const int cl = tax < kNear ? tx0 - 1 : tx0, ch = tax > 1.0f - kNear ? tx0 + 2 : tx0 + 1;
+        const int rl = tay < kNear ? ty0 - 1 : ty0, rh = tay > 1.0f - kNear ? ty0 + 2 : ty0 + 1;
+        const int len = ch - cl + 1;
+        const uint32_t full = (1u << len) - 1u;
+        bool ok = true;
+        for (int yy = rl; yy <= rh; ++yy)
+          ok = ok && fp_bits(F + (uint32_t)min(max(yy, 0), m - 1) * wpr0, cl, len, n) == full;
+        if (!ok) {
+          const Taps t = taps_f64(v, x, y);
+          tx0 = t.x0;
+          ty0 = t.y0;
+          tax = t.ax;
+          tay = t.ay;
+          const uint32_t* r0 = F + (uint32_t)min(max(ty0, 0), m - 1) * wpr0;
+          const uint32_t* r1 = F + (uint32_t)min(max(ty0 + 1, 0), m - 1) * wpr0;
+          uncovered = (fp_bits(r0, tx0, 2, n) & fp_bits(r1, tx0, 2, n)) != 3u;
+        }
+      }
+      uint32_t w00, w01, w10, w11;
+      if (use_win) {
+        const uint32_t* p = win + (ty0 - yl) * WIN_W + (tx0 - wx0);
+        w00 = p[0];
+        w01 = p[1];
+        w10 = p[WIN_W];
+        w11 = p[WIN_W + 1];
+      } else {
+        // longitude wrap / pole clamp (projection.py:146-149)
+        const int xa = wrapx(tx0, n), xb = wrapx(tx0 + 1, n);
+        const int ya = min(max(ty0, 0), m - 1), yb = min(max(ty0 + 1, 0), m - 1);
+        const uint32_t o00 = (uint32_t)ya * n + xa, o01 = (uint32_t)ya * n + xb;
+        const uint32_t o10 = (uint32_t)yb * n + xa, o11 = (uint32_t)yb * n + xb;
+        w00 = w01 = w10 = w11 = 0u;
+        const uint8_t* pc = vc.img;
+        for (int c = 0; c < C; ++c, pc += vc.plane) {
+          w00 |= (uint32_t)__ldg(pc + o00) << (8 * c);
+          w01 |= (uint32_t)__ldg(pc + o01) << (8 * c);
+          w10 |= (uint32_t)__ldg(pc + o10) << (8 * c);
+          w11 |= (uint32_t)__ldg(pc + o11) << (8 * c);
+        }
+      }
+      uint8_t* o = ost + (threadIdx.y + 8 * k) * OST_PITCH + threadIdx.x * C;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < C) {
+          // 2^23 + byte c of each tap (selector: byte c of the tap, zeros, 0x4B)
+          const uint32_t sel = 0x3004u + c;
+          const float b00 = __uint_as_float(__byte_perm(K, w00, sel));
+          const float b01 = __uint_as_float(__byte_perm(K, w01, sel));
+          const float b10 = __uint_as_float(__byte_perm(K, w10, sel));
+          const float b11 = __uint_as_float(__byte_perm(K, w11, sel));
+          o[c] = (uint8_t)blend(b00, b01, b10, b11, tax, tay);
+        }
+      }
+    }
+    n_unc += __popc(__ballot_sync(0xFFFFFFFFu, uncovered));
+  }
+  if (threadIdx.x == 0 && n_unc) atomicAdd(vc.uncovered, n_unc);
+  __syncthreads();
+  // (5) tile rows -> (out_h, out_w, C) with 16-byte stores where aligned
+  const int nx = min(K4_TX, out_w - (int)blockIdx.x * K4_TX);
+  const int ny = min(K4_TY, out_h - (int)blockIdx.y * K4_TY);
+  const int rowb = nx * C;
+  uint8_t* gbase = vc.out + ((uint64_t)blockIdx.y * K4_TY * out_w + blockIdx.x * K4_TX) * C;
+  const uint64_t gpitch = (uint64_t)out_w * C;
+  if (((reinterpret_cast<uintptr_t>(gbase) | gpitch | rowb) & 15) == 0) {
+    const int nv = rowb >> 4;
+    for (int idx = tid; idx < ny * nv; idx += 256) {
+      const int r = idx / nv, q = idx - (idx / nv) * nv;
+      __stcs(reinterpret_cast<uint4*>(gbase + r * gpitch) + q,
+             *reinterpret_cast<const uint4*>(ost + r * OST_PITCH + 16 * q));
+    }
+  } else {
+    for (int idx = tid; idx < ny * rowb; idx += 256) {
+      const int r = idx / rowb, b = idx - (idx / rowb) * rowb;
+      gbase[r * gpitch + b] = ost[r * OST_PITCH + b];
+    }
+  }
+}
+
 template <bool DEV>
 __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid_constant__ Views views,
                                                      const wv_view_args* __restrict__ d_views) {
   __shared__ ViewConst vc;
+  __shared__ __align__(16) uint32_t win[WIN_H * WIN_W];
+  __shared__ __align__(16) uint8_t ost[K4_TY * OST_PITCH];
   const wv_view_args& v = DEV ? d_views[blockIdx.z] : views.v[blockIdx.z];
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  if (tid == 0) {
     for (int i = 0; i < 9; ++i) vc.r[i] = (float)v.rot[i];
     vc.tan_h = (float)v.tan_h;
     vc.tan_v = (float)v.tan_v;
@@ -158,41 +319,55 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
     vc.xmax = vc.ymax = -0x7FFFFFFF;
   }
   __syncthreads();
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y * blockDim.y + threadIdx.y;
-  const bool live = x < vc.out_w && y < vc.out_h;
-  bool uncovered = false;
-  const int m = vc.m, n = vc.n, wpr0 = vc.wpr0;
-  int x0 = 0, y0 = 0;
-  float ax = 0.f, ay = 0.f;
-  if (live) {
+  const int out_w = vc.out_w, out_h = vc.out_h;
+  if ((int)blockIdx.x * K4_TX >= out_w || (int)blockIdx.y * K4_TY >= out_h) return;  // smaller view
+  const int m = vc.m, n = vc.n;
+  const int x = blockIdx.x * K4_TX + threadIdx.x;
+  const int ybase = blockIdx.y * K4_TY + threadIdx.y;
+
+  // (1) geometry
+  int x0[K4_PPT], y0[K4_PPT];
+  float ax[K4_PPT], ay[K4_PPT];
+  int bx0 = 0x7FFFFFFF, bx1 = -0x7FFFFFFF, by0 = 0x7FFFFFFF, by1 = -0x7FFFFFFF;
+  {
     const float u = ((float)x + 0.5f) * vc.inv_w - 1.0f;
-    const float w = 1.0f - ((float)y + 0.5f) * vc.inv_h;
-    const float rx = u * vc.tan_h, ry = w * vc.tan_v;
-    const float wx = rx * vc.r[0] + ry * vc.r[1] + vc.r[2];
-    const float wy = rx * vc.r[3] + ry * vc.r[4] + vc.r[5];
-    const float wz = rx * vc.r[6] + ry * vc.r[7] + vc.r[8];
-    // lon = atan2(x, z); lat = asin(y/|w|) = atan2(y, hypot(x, z))
-    const float lon = fast_atan2(wx, wz) * 57.29577951308232f;
-    const float hz = wx * wx + wz * wz;
-    const float lat = (hz > 0.0f ? fast_atan2(wy, hz * rsqrtf(hz)) : copysignf(1.5707963f, wy)) *
-                      57.29577951308232f;
-    const float fx = (lon + 180.0f) * vc.sx - 0.5f;
-    const float fy = (90.0f - lat) * vc.sy - 0.5f;
-    const float flx = floorf(fx), fly = floorf(fy);
-    x0 = (int)flx;
-    y0 = (int)fly;
-    ax = fx - flx;
-    ay = fy - fly;
+    const float rx = u * vc.tan_h;
+    const float cx = rx * vc.r[0] + vc.r[2], cy = rx * vc.r[3] + vc.r[5], cz = rx * vc.r[6] + vc.r[8];
+    const float r1 = vc.r[1], r4 = vc.r[4], r7 = vc.r[7], tv = vc.tan_v, ih = vc.inv_h;
+    const float sx = vc.sx, sy = vc.sy;
+#pragma unroll
+    for (int k = 0; k < K4_PPT; ++k) {
+      const int y = ybase + 8 * k;
+      const float w = 1.0f - ((float)y + 0.5f) * ih;
+      const float ry = w * tv;
+      const float wx = fmaf(ry, r1, cx), wy = fmaf(ry, r4, cy), wz = fmaf(ry, r7, cz);
+      // lon = atan2(x, z); lat = asin(y/|w|) = atan2(y, hypot(x, z))
+      const float lon = fast_atan2(wx, wz) * 57.29577951308232f;
+      const float hz = wx * wx + wz * wz;
+      const float lat = (hz > 1e-30f ? fast_atan2(wy, hz * rsqrt_approx(hz)) : copysignf(1.5707963f, wy)) *
+                        57.29577951308232f;
+      const float fx = (lon + 180.0f) * sx - 0.5f;
+      const float fy = (90.0f - lat) * sy - 0.5f;
+      const float flx = floorf(fx), fly = floorf(fy);
+      x0[k] = (int)flx;
+      y0[k] = (int)fly;
+      ax[k] = fx - flx;
+      ay[k] = fy - fly;
+      if (x < out_w && y < out_h) {
+        bx0 = min(bx0, x0[k] - 1);
+        bx1 = max(bx1, x0[k] + 2);
+        by0 = min(by0, y0[k] - 1);
+        by1 = max(by1, y0[k] + 2);
+      }
+    }
   }
   {
-    // candidate-tap box of the CTA (both tap choices near integer boundaries):
-    // warp reductions, one shared atomic per warp, one warp tests its rows
-    const int bx0 = __reduce_min_sync(0xFFFFFFFFu, live ? x0 - 1 : 0x7FFFFFFF);
-    const int bx1 = __reduce_max_sync(0xFFFFFFFFu, live ? x0 + 2 : -0x7FFFFFFF);
-    const int by0 = __reduce_min_sync(0xFFFFFFFFu, live ? y0 - 1 : 0x7FFFFFFF);
-    const int by1 = __reduce_max_sync(0xFFFFFFFFu, live ? y0 + 2 : -0x7FFFFFFF);
-    if ((threadIdx.x & 31) == 0) {
+    // candidate-tap box of the CTA (both tap choices near integer boundaries)
+    bx0 = __reduce_min_sync(0xFFFFFFFFu, bx0);
+    bx1 = __reduce_max_sync(0xFFFFFFFFu, bx1);
+    by0 = __reduce_min_sync(0xFFFFFFFFu, by0);
+    by1 = __reduce_max_sync(0xFFFFFFFFu, by1);
+    if (threadIdx.x == 0) {
       atomicMin(&vc.xmin, bx0);
       atomicMax(&vc.xmax, bx1);
       atomicMin(&vc.ymin, by0);
@@ -200,81 +375,30 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
     }
   }
   __syncthreads();
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  // (2) footprint test of the box; window eligibility
+  const int xl = vc.xmin, xh = vc.xmax, yl = vc.ymin, yh = vc.ymax;
+  const bool inside = xl >= 0 && xh < n && yl >= 0 && yh < m && xl <= xh;
+  const int wx0 = xl & ~3;
+  const int ww = ((xh | 3) - wx0 + 1) >> 2;   // 4-pixel words per window row
   if (tid < 32) {
-    const int xl = vc.xmin, xh = vc.xmax, yl = vc.ymin, yh = vc.ymax;
-    bool ok = xl >= 0 && xh < n && yl >= 0 && yh < m && xl <= xh && (xh - xl) < 96;
+    const int wpr0 = vc.wpr0;
+    bool ok = inside && (xh - xl) < WIN_W;
     for (int yy = yl + tid; ok && yy <= yh; yy += 32) {
       const uint32_t* row = vc.F + (uint32_t)yy * wpr0;
       for (int wd = xl >> 5; ok && wd <= (xh >> 5); ++wd)
         ok = (__ldg(row + wd) | ~range_bits(xl, xh + 1, wd)) == 0xFFFFFFFFu;
     }
     const bool all = __all_sync(0xFFFFFFFFu, ok);
-    if (tid == 0) vc.covered = all;
+    if (tid == 0) {
+      vc.covered = all;
+      vc.use_win = inside && (n & 3) == 0 && 4 * ww <= WIN_W && (yh - yl + 1) <= WIN_H;
+    }
   }
   __syncthreads();
-  if (live) {
-    if (!vc.covered) {
-      const uint32_t* F = vc.F;
-      const int xl = ax < kNear ? x0 - 1 : x0, xh = ax > 1.0f - kNear ? x0 + 2 : x0 + 1;
-      const int yl = ay < kNear ? y0 - 1 : y0, yh = ay > 1.0f - kNear ? y0 + 2 : y0 + 1;
-      const int len = xh - xl + 1;
-      const uint32_t full = (1u << len) - 1u;
-      bool ok = true;
-      for (int yy = yl; yy <= yh; ++yy)
-        ok = ok && fp_bits(F + (uint32_t)min(max(yy, 0), m - 1) * wpr0, xl, len, n) == full;
-      if (!ok) {
-        const Taps t = taps_f64(v, x, y);
-        x0 = t.x0;
-        y0 = t.y0;
-        ax = t.ax;
-        ay = t.ay;
-        const uint32_t* r0 = F + (uint32_t)min(max(y0, 0), m - 1) * wpr0;
-        const uint32_t* r1 = F + (uint32_t)min(max(y0 + 1, 0), m - 1) * wpr0;
-        uncovered = (fp_bits(r0, x0, 2, n) & fp_bits(r1, x0, 2, n)) != 3u;
-      }
-    }
-    const int C = vc.C;
-    uint8_t* out = vc.out + ((uint32_t)y * vc.out_w + x) * C;
-    // u8 <-> f32 without the conversion pipe: 2^23 + b has b in its mantissa
-    auto u2f = [](uint32_t b) { return __uint_as_float(0x4B000000u | b) - 8388608.0f; };
-    auto f2u = [](float v) {   // clip(rint(v)), round-half-even like np.rint
-      return __float_as_uint(fminf(fmaxf(v, 0.0f), 255.0f) + 8388608.0f) & 0xFFu;
-    };
-    if (x0 >= 0 && x0 + 1 < n && y0 >= 0 && y0 + 1 < m) {
-      // interior taps: (y0, x0), (y0, x0+1), (y0+1, x0), (y0+1, x0+1)
-      const uint8_t* p0 = vc.img + (uint32_t)y0 * n + x0;
-      const uint8_t* p1 = p0 + n;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (c < C) {
-          const float p00 = u2f(__ldg(p0)), p01 = u2f(__ldg(p0 + 1));
-          const float p10 = u2f(__ldg(p1)), p11 = u2f(__ldg(p1 + 1));
-          const float top = fmaf(ax, p01 - p00, p00);
-          const float bot = fmaf(ax, p11 - p10, p10);
-          __stcs(out + c, (unsigned char)f2u(fmaf(ay, bot - top, top)));
-          p0 += vc.plane;
-          p1 += vc.plane;
-        }
-      }
-    } else {
-      // longitude wrap / pole clamp (projection.py:146-149)
-      const int xa = wrapx(x0, n), xb = wrapx(x0 + 1, n);
-      const int ya = min(max(y0, 0), m - 1), yb = min(max(y0 + 1, 0), m - 1);
-      const uint32_t o00 = (uint32_t)ya * n + xa, o01 = (uint32_t)ya * n + xb;
-      const uint32_t o10 = (uint32_t)yb * n + xa, o11 = (uint32_t)yb * n + xb;
-      const uint8_t* pc = vc.img;
-      for (int c = 0; c < C; ++c, pc += vc.plane) {
-        const float p00 = u2f(__ldg(pc + o00)), p01 = u2f(__ldg(pc + o01));
-        const float p10 = u2f(__ldg(pc + o10)), p11 = u2f(__ldg(pc + o11));
-        const float top = fmaf(ax, p01 - p00, p00);
-        const float bot = fmaf(ax, p11 - p10, p10);
-        __stcs(out + c, (unsigned char)f2u(fmaf(ay, bot - top, top)));
-      }
-    }
-  }
-  const unsigned cnt = __popc(__ballot_sync(0xFFFFFFFFu, uncovered));
-  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(vc.uncovered, cnt);
+  if (vc.C == 3)
+    finish<3>(vc, v, win, ost, x0, y0, ax, ay, x, ybase, xl, yl, yh, wx0, ww, tid);
+  else
+    finish<0>(vc, v, win, ost, x0, y0, ax, ay, x, ybase, xl, yl, yh, wx0, ww, tid);
 }
 
 }  // namespace
@@ -294,7 +418,7 @@ int launch_perspective(const wv_view_args* views, int n, cudaStream_t s) {
     mh = max(mh, v.out_h);
   }
   dim3 block(32, 8);
-  dim3 grid(cdiv(mw, 32), cdiv(mh, 8), n);
+  dim3 grid(cdiv(mw, K4_TX), cdiv(mh, K4_TY), n);
   k_perspective<false><<<grid, block, 0, s>>>(pv, nullptr);
   WV_CUDA(cudaGetLastError());
   return WV_OK;
@@ -308,7 +432,7 @@ int launch_perspective_dev(const wv_view_args* d_views, int n, int max_w, int ma
   if (!d_views || n < 1 || n > kMaxViews || max_w < 1 || max_h < 1) return WV_ERR_ARG;
   Views none{};
   dim3 block(32, 8);
-  dim3 grid(cdiv(max_w, 32), cdiv(max_h, 8), n);
+  dim3 grid(cdiv(max_w, K4_TX), cdiv(max_h, K4_TY), n);
   k_perspective<true><<<grid, block, 0, s>>>(none, d_views);
   WV_CUDA(cudaGetLastError());
   return WV_OK;

@@ -27,6 +27,7 @@ struct TemporalArgs {
   const uint32_t* count;
   int NB;
   float* plane;
+  uint8_t* bstate;                  // per block: the plane block may hold nonzeros
   int all_included;                 // full-frame decode: every inclusion bit is set
 };
 
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
   __shared__ int s_pre[K2_MAXN + 1];
   __shared__ int s_w[K2_MAXN];
   __shared__ uint32_t s_mrow[32];
+  __shared__ int s_live;
   const int tid = threadIdx.x;
   const int npos = a.bs * a.bs;
   const int nq = (a.C * npos) >> 2;                           // float4 per block
@@ -115,23 +117,67 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
     const int b = (int)(e & ~ZERO_FLAG);
     const int by = b / a.nbx;
     const int y0 = by * a.bs, x0 = (b - by * a.nbx) * a.bs;
-    if (e & ZERO_FLAG) {
+    const bool dirty = a.bstate[b] != 0;
+    auto zero_block = [&]() {
       for (int q = tid; q < nq; q += K2_THREADS) {
         const int c = (q << 2) >> (2 * a.bs_log2), i = (q << 2) & (npos - 1);
         float* dst = a.plane + ((uint64_t)c * a.H + y0 + (i >> a.bs_log2)) * a.W + x0 + (i & bmask);
         *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
+    };
+    if (e & ZERO_FLAG) {
+      // block left the selection: clear it unless it is already all zero
+      if (dirty) {
+        zero_block();
+        __syncthreads();   // every thread has read the state byte
+        if (tid == 0) a.bstate[b] = 0;
+      }
       continue;
     }
-    if (tid < a.n) {
-      const uint64_t fi = (uint64_t)tid * a.NB + b;
-      const unsigned long long en = ends[fi];
-      const unsigned long long st = fi ? ends[fi - 1] : 0ull;
-      int cnt = 0;
-      if (en >= st && (en - st) % a.rs == 0) cnt = (int)min((en - st) / a.rs, (unsigned long long)npos);
-      s_start[tid] = st;
-      s_pre[tid + 1] = cnt;        // prefix-summed below
-      s_w[tid] = tweight(tid, t_disp, a.n);
+    // spans of the block's records per temporal index; warp 0 prefix-sums
+    // the counts (n <= 32) and the weights of display time t
+    if (tid < 32) {
+      int cnt = 0, w = 0;
+      unsigned long long st = 0;
+      if (tid < a.n) {
+        const uint64_t fi = (uint64_t)tid * a.NB + b;
+        const unsigned long long en = ends[fi];
+        st = fi ? ends[fi - 1] : 0ull;
+        if (en >= st && (en - st) % a.rs == 0) cnt = (int)min((en - st) / a.rs, (unsigned long long)npos);
+        w = tweight(tid, t_disp, a.n);
+      }
+      int inc = cnt, live = w ? cnt : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xFFFFFFFFu, inc, o), l = __shfl_up_sync(0xFFFFFFFFu, live, o);
+        if (tid >= o) {
+          inc += u;
+          live += l;
+        }
+      }
+      if (tid < a.n) {
+        s_start[tid] = st;
+        s_pre[tid + 1] = inc;
+        s_w[tid] = w;
+      }
+      if (tid == 0) s_pre[0] = 0;
+      if (tid == 31) s_live = live;
+    }
+    __syncthreads();
+    const int total = s_pre[a.n];
+    if (s_live == 0) {
+      // no record of a contributing temporal index: the block is zero
+      // (offsets of the other records are still validated, decoding.py:64-69)
+      for (int i = tid; i < total; i += K2_THREADS) {
+        int ti = 0;
+        while (s_pre[ti + 1] <= i) ++ti;
+        const uint8_t* rp = recs + s_start[ti] + (uint64_t)(i - s_pre[ti]) * a.rs;
+        if (((int)rp[0] | ((int)rp[1] << 8)) >= npos) err |= WV_DERR_OFFSET;
+      }
+      if (dirty) zero_block();
+      __syncthreads();
+      if (tid == 0 && dirty) a.bstate[b] = 0;
+      continue;
     }
     const BlockIncl bi = a.all_included ? BlockIncl{0, nullptr, 0, 0, 0} : classify(a, y0, x0);
     if (bi.mode == 1 && a.bs <= 32 && tid < a.bs) {
@@ -144,12 +190,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
     for (int q = tid; q < nq; q += K2_THREADS)
       smem4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
-    if (tid == 0) {
-      s_pre[0] = 0;
-      for (int t = 1; t <= a.n; ++t) s_pre[t] += s_pre[t - 1];
-    }
-    __syncthreads();
-    const int total = s_pre[a.n];
+    if (tid == 0 && !dirty) a.bstate[b] = 1;
     for (int base = 0; base < total; base += K2_THREADS) {
       const int i = base + tid;
       int ti = -1, off = 0;
@@ -259,6 +300,7 @@ int launch_temporal(const Layout& lo, const wv_geometry* g, int mode, const wv_f
   t.list = (const uint32_t*)(ws + lo.blist);
   t.count = (const uint32_t*)(ws + lo.counters) + CNT_BLOCKS;
   t.plane = (float*)(ws + lo.plane);
+  t.bstate = ws + lo.bstate;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
