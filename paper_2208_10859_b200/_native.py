@@ -62,11 +62,13 @@ class NativeError(RuntimeError):
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load the decode library (raises if it is absent: no fallback)."""
+def load(path: str | None = None):
+    """Load the decode library (raises if it is absent: no fallback).
+    ``WV_LIB`` selects an experimental build variant (build.build(out=...))."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("WV_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise NativeError(
             f"B200 decode library not built: {path} (run python -m paper_2208_10859_b200.build)")

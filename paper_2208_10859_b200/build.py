@@ -43,27 +43,31 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Build the library (``out``/``defines``: an experimental variant, e.g.
+    ``defines=["WV_SEGLEN_R=8"]``, loaded with ``WV_LIB=<out>``)."""
+    lib = out or LIB
+    if not out and not defines and not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build_obj")
+    objdir = os.path.join(HERE, "build_obj", os.path.basename(lib).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for f in SOURCES:
         obj = os.path.join(objdir, f.replace(".cu", ".o"))
         cmd = [nvcc(), *ARCH, *FLAGS, f"--fmad={FMAD.get(f, 'false')}", "-I",
-               os.path.join(ROOT, "include"), "-c", "-o", obj, os.path.join(CSRC, f)]
+               os.path.join(ROOT, "include"), *[f"-D{d}" for d in defines], "-c", "-o", obj,
+               os.path.join(CSRC, f)]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -35,11 +35,23 @@ constexpr int BOX_FLOATS = BOX_W * BOX_H;
 constexpr int BOX_SLOT = ((BOX_FLOATS * 4 + 127) / 128) * 128;  // bytes
 constexpr int CB_PITCH = BOX_W + 1;   // float2 units, odd -> conflict-free row pass
 constexpr int OB_PITCH = OUT_W + 1;   // float2 units (row pairs), odd
-// line segments: every lifting stream covers 16 output pairs (+ its halo)
-constexpr int SEGLEN = 16;
-constexpr int COL_SEGS = TY / SEGLEN, ROW_SEGS = TX / SEGLEN;
-constexpr int NTHREADS = (COL_SEGS * BOX_W > ROW_SEGS * TY ? COL_SEGS * BOX_W : ROW_SEGS * TY) <= 64
-                             ? 64 : 128;
+// line segments: every column (row) lifting stream covers SEGLEN_C
+// (SEGLEN_R) output pairs plus its own 2-pair halo on each side
+#ifndef WV_SEGLEN_C
+#define WV_SEGLEN_C 8
+#endif
+#ifndef WV_SEGLEN_R
+#define WV_SEGLEN_R 8
+#endif
+constexpr int SEGLEN_C = WV_SEGLEN_C, SEGLEN_R = WV_SEGLEN_R;
+constexpr int COL_SEGS = TY / SEGLEN_C, ROW_SEGS = TX / SEGLEN_R;
+constexpr int NTHREADS_MIN = (COL_SEGS * BOX_W > ROW_SEGS * TY ? COL_SEGS * BOX_W : ROW_SEGS * TY);
+#ifdef WV_K3_THREADS
+constexpr int NTHREADS = WV_K3_THREADS;
+#else
+constexpr int NTHREADS = NTHREADS_MIN <= 64 ? 64 : (NTHREADS_MIN <= 128 ? 128 : (NTHREADS_MIN + 31) / 32 * 32);
+#endif
+static_assert(NTHREADS >= NTHREADS_MIN, "every segment needs a thread");
 static_assert(TY * OB_PITCH * 8 <= 4 * BOX_SLOT, "output tile must fit in the box region");
 
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
@@ -201,16 +213,19 @@ struct LevelArgs {
   const float* plane; int plane_w, plane_h;
 };
 
-// Items are (tile, channel).  Boxes are double-buffered: while one item is
-// lifted, the next item's four TMA boxes are already in flight into the other
-// buffer.  Column pass: 2 segments x BOX_W columns (each segment lifts 16
-// output row pairs from its own 2-row halo); row pass: 2 segments x TY row
-// pairs.  Store pass: coalesced f32 (mid levels) or packed u8 with the
-// request mask applied (finest level).
+// Items are (tile, channel).  Column pass: 2 segments x BOX_W columns (each
+// segment lifts 16 output row pairs from its own 2-row halo); row pass: 2
+// segments x TY row pairs.  Mid levels stage the f32 output tile in the box
+// region (dead after the column pass) and store it coalesced.  The finest
+// level keeps its u8 tile in a separate 4 KB buffer, so the box region is
+// free as soon as the column pass ends: the next item's four TMA boxes are
+// issued there and load while this item's row and store passes run.  Its
+// store pass writes 16-byte vectors with the request mask applied.
 constexpr int BOXSET = 4 * BOX_SLOT;
-constexpr int O8_PITCH = OUT_W + 4;   // bytes; 4-aligned rows for the word copy
-static_assert(OUT_H * O8_PITCH <= BOXSET, "u8 tile must fit in the box region");
-constexpr int NBUF = 1;
+constexpr int O8_PITCH = OUT_W + 4;   // bytes; 17 words: conflict-light row-pass stores
+constexpr int COL_BYTES = 2 * TY * CB_PITCH * 8;
+constexpr int SMEM_MID = BOXSET + COL_BYTES;
+constexpr int SMEM_FIN = BOXSET + COL_BYTES + OUT_H * O8_PITCH + OUT_H * 2 * 4;
 
 template <bool FINAL>
 __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUtensorMap tm_ll,
@@ -218,48 +233,45 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
                                                     LevelArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* canvas = FINAL ? a.fa->d_canvas : nullptr;
-  float2* colL = reinterpret_cast<float2*>(smem + NBUF * BOXSET);  // [TY][CB_PITCH]
+  float* box = reinterpret_cast<float*>(smem);
+  const float* bLL = box;
+  const float* bHL = box + BOX_SLOT / 4;
+  const float* bLH = box + 2 * BOX_SLOT / 4;
+  const float* bHH = box + 3 * BOX_SLOT / 4;
+  float2* colL = reinterpret_cast<float2*>(smem + BOXSET);  // [TY][CB_PITCH]
   float2* colH = colL + TY * CB_PITCH;
-  uint32_t* req = reinterpret_cast<uint32_t*>(colH + TY * CB_PITCH);  // FINAL: [OUT_H][2]
-  __shared__ uint64_t bar[2];
+  float2* outb = reinterpret_cast<float2*>(smem);                     // mid: aliases the boxes
+  uint8_t* out8 = smem + BOXSET + COL_BYTES;                          // final: [OUT_H][O8_PITCH]
+  uint32_t* req = reinterpret_cast<uint32_t*>(out8 + OUT_H * O8_PITCH);  // final: [OUT_H][2]
+  __shared__ uint64_t bar;
 
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-  }
+  if (tid == 0) mbar_init(&bar, 1);
   __syncthreads();
-  uint32_t phases = 0u;   // bit b = parity of buffer b's barrier
+  uint32_t phase = 0u;
   const int C = a.C;
   const uint32_t nitems = *a.count * (uint32_t)C;
   const int H = 2 * a.bh, W = 2 * a.bw;
 
-  // issue the four box loads of an item into buffer b (elected thread)
-  auto issue = [&](uint32_t it, int b) {
-    if (!a.use_tma || tid != 0) return;
-    const uint32_t e = a.list[it / C];
-    if (FINAL && (e & ZERO_FLAG)) return;
-    const uint32_t tile = e & ~ZERO_FLAG;
+  // issue the four box loads of an item (elected thread)
+  auto issue = [&](uint32_t it) {
+    if (tid != 0) return;
+    const uint32_t tile = a.list[it / C] & ~ZERO_FLAG;
     const int ty = tile / a.ntx, tx = tile - (tile / a.ntx) * a.ntx;
     // TMA faults on unaligned/negative innermost box coordinates (observed on
     // B200, driver 580): x starts at ax-4 clamped to 0
     const int oy = max(ty * TY - HALO, 0), ox = max(tx * TX - XPAD, 0);
     const int c = (int)(it % C);
-    float* box = reinterpret_cast<float*>(smem + b * BOXSET);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&bar[b], 4u * BOX_FLOATS * 4u);
-    tma_load_3d(box, &tm_ll, ox, oy, c, &bar[b]);
-    tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar[b]);
-    tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar[b]);
-    tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar[b]);
+    mbar_expect_tx(&bar, 4u * BOX_FLOATS * 4u);
+    tma_load_3d(box, &tm_ll, ox, oy, c, &bar);
+    tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar);
+    tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar);
+    tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar);
   };
 
-  // NBUF == 2 prefetches the next item's boxes while lifting the current one;
-  // NBUF == 1 keeps shared memory at 44 KB (5 CTAs/SM), which measured faster
-  int buf = 0;
-  if (NBUF == 2 && blockIdx.x < nitems) issue(blockIdx.x, 0);
-  for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x, buf ^= (NBUF - 1)) {
-    const uint32_t next = item + gridDim.x;
+  bool issued = false;   // the current item's boxes are already in flight
+  for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
     const uint32_t entry = a.list[item / C];
     const int c = (int)(item % C);
     const uint32_t tile = entry & ~ZERO_FLAG;
@@ -268,7 +280,6 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     const int by = min(ay + TY, a.bh), bx = min(ax + TX, a.bw);
     const int ny = 2 * (by - ay), nx = 2 * (bx - ax);
     if (FINAL && (entry & ZERO_FLAG)) {
-      if (NBUF == 2 && next < nitems) issue(next, buf ^ 1);
       // tile left the request: clear what an earlier frame wrote there
       const int qw = nx >> 2;
       for (int idx = tid; idx < ny * qw; idx += NTHREADS) {
@@ -278,19 +289,11 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       }
       continue;
     }
-    float* box = reinterpret_cast<float*>(smem + buf * BOXSET);
-    const float* bLL = box;
-    const float* bHL = box + BOX_SLOT / 4;
-    const float* bLH = box + 2 * BOX_SLOT / 4;
-    const float* bHH = box + 3 * BOX_SLOT / 4;
-    float2* outb = reinterpret_cast<float2*>(box);                  // aliases this item's boxes
-    uint8_t* out8 = reinterpret_cast<uint8_t*>(box);                // FINAL: [OUT_H][O8_PITCH]
     const int oy = max(ay - HALO, 0), ox = max(ax - XPAD, 0);
     if (a.use_tma) {
-      if (NBUF == 1) issue(item, 0);
-      mbar_wait(&bar[buf], (phases >> buf) & 1u);
-      phases ^= 1u << buf;
-      if (NBUF == 2 && next < nitems) issue(next, buf ^ 1);
+      if (!issued) issue(item);
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
     } else {
       // tiny levels whose subband width is not a multiple of 4 floats
       for (int i = tid; i < 4 * BOX_FLOATS; i += NTHREADS) {
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       }
       __syncthreads();
     }
+    issued = false;
     bool row_req_full = true;
     if (FINAL && tid < ny) {
       // request-mask words of this tile's output rows (used by the store pass)
@@ -324,12 +328,12 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     if (tid < COL_SEGS * BOX_W) {
       const int lc = tid % BOX_W, sg = tid / BOX_W;
       const int cg = ox + lc;
-      const int pa = ay + sg * SEGLEN, pb = min(pa + SEGLEN, by);
+      const int pa = ay + sg * SEGLEN_C, pb = min(pa + SEGLEN_C, by);
       if (pa < pb && cg >= max(ax - HALO, 0) && cg < min(bx + HALO, a.bw)) {
-        if (pa >= HALO && pb + HALO <= a.bh && pb - pa == SEGLEN) {
+        if (pa >= HALO && pb + HALO <= a.bh && pb - pa == SEGLEN_C) {
           const int rb = pa - HALO - oy;          // local box row of input 0
           const int qb = pa - HALO - ay;          // output pair of input 0
-          lift_interior<SEGLEN>(
+          lift_interior<SEGLEN_C>(
               [&](int j, float2& s, float2& d) {
                 const int o = (rb + j) * BOX_W + lc;
                 s = make_float2(bLL[o], bHL[o]);
@@ -356,14 +360,22 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       }
     }
     const bool tile_req_full = __syncthreads_and(row_req_full) && FINAL && ny == OUT_H;
+    if (FINAL && a.use_tma) {
+      // the boxes are consumed: start the next item's loads now
+      uint32_t nxt = item + gridDim.x;
+      if (nxt < nitems && !(a.list[nxt / C] & ZERO_FLAG)) {
+        issue(nxt);
+        issued = true;
+      }
+    }
     // row pass: (segment, output row pair) per thread, two rows packed
     if (tid < ROW_SEGS * TY) {
       const int i = tid % TY, sg = tid / TY;
-      const int pa = ax + sg * SEGLEN, pb = min(pa + SEGLEN, bx);
+      const int pa = ax + sg * SEGLEN_R, pb = min(pa + SEGLEN_R, bx);
       if (i < by - ay && pa < pb) {
         // mid levels: f32 pairs into outb; finest level: clip(rint(x*255))
         // (decoding.py:301; rint is round-half-even like __float2uint_rn,
-        // which also saturates below 0) straight into a u8 tile
+        // which also saturates below 0) straight into the u8 tile
         auto emit_out = [&](int q, float2 s3, float2 d3) {
           if (!FINAL) {
             outb[i * OB_PITCH + 2 * q] = s3;
@@ -376,9 +388,9 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
                 (uint16_t)(cv(s3.y) | (cv(d3.y) << 8));
           }
         };
-        if (pa >= HALO && pb + HALO <= a.bw && pb - pa == SEGLEN) {
+        if (pa >= HALO && pb + HALO <= a.bw && pb - pa == SEGLEN_R) {
           const int cb = pa - HALO - ox, qb = pa - HALO - ax;
-          lift_interior<SEGLEN>(
+          lift_interior<SEGLEN_R>(
               [&](int j, float2& s, float2& d) {
                 s = colL[i * CB_PITCH + cb + j];
                 d = colH[i * CB_PITCH + cb + j];
@@ -419,23 +431,40 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
           *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
         }
       }
+      __syncthreads();
     } else {
       // u8 rows -> canvas plane c, zero outside the request
       uint8_t* base = canvas + ((uint64_t)c * H + 2 * ay) * W + 2 * ax;
-      const int qw = nx >> 2;     // 4-pixel words per row
-      for (int idx = tid; idx < ny * qw; idx += NTHREADS) {
-        const int r = tile_req_full ? idx / (OUT_W / 4) : idx / qw;
-        const int q = tile_req_full ? idx % (OUT_W / 4) : idx % qw;
-        uint32_t w = *reinterpret_cast<const uint32_t*>(out8 + r * O8_PITCH + 4 * q);
-        if (!tile_req_full) {
-          const uint32_t b = (req[2 * r + (q >> 3)] >> ((4 * q) & 31)) & 0xFu;
-          w &= (b & 1u) * 0xFFu | ((b >> 1) & 1u) * 0xFF00u | ((b >> 2) & 1u) * 0xFF0000u |
-               ((b >> 3) & 1u) * 0xFF000000u;
+      if (((W | nx) & 15) == 0) {
+        const int vw = nx >> 4;     // 16-pixel vectors per row
+        for (int idx = tid; idx < ny * vw; idx += NTHREADS) {
+          const int r = tile_req_full ? idx >> 2 : idx / vw;
+          const int q = tile_req_full ? idx & 3 : idx - (idx / vw) * vw;
+          const uint32_t* src = reinterpret_cast<const uint32_t*>(out8 + r * O8_PITCH) + 4 * q;
+          uint4 w = make_uint4(src[0], src[1], src[2], src[3]);
+          if (!tile_req_full) {
+            const uint32_t bits = (req[2 * r + (q >> 1)] >> (16 * (q & 1))) & 0xFFFFu;
+            // 4 request bits -> 4 byte masks (bit k -> byte k)
+            auto bm = [](uint32_t b4) { return ((b4 * 0x00204081u) & 0x01010101u) * 0xFFu; };
+            w.x &= bm(bits & 0xFu);
+            w.y &= bm((bits >> 4) & 0xFu);
+            w.z &= bm((bits >> 8) & 0xFu);
+            w.w &= bm(bits >> 12);
+          }
+          *reinterpret_cast<uint4*>(base + (uint64_t)r * W + 16 * q) = w;
         }
-        *reinterpret_cast<uint32_t*>(base + (uint64_t)r * W + 4 * q) = w;
+      } else {
+        const int qw = nx >> 2;     // 4-pixel words per row
+        for (int idx = tid; idx < ny * qw; idx += NTHREADS) {
+          const int r = idx / qw, q = idx % qw;
+          uint32_t w = *reinterpret_cast<const uint32_t*>(out8 + r * O8_PITCH + 4 * q);
+          const uint32_t b = (req[2 * r + (q >> 3)] >> ((4 * q) & 31)) & 0xFu;
+          w &= ((b * 0x00204081u) & 0x01010101u) * 0xFFu;
+          *reinterpret_cast<uint32_t*>(base + (uint64_t)r * W + 4 * q) = w;
+        }
       }
+      __syncthreads();   // out8 and req are rewritten by the next item
     }
-    __syncthreads();
   }
 }
 
@@ -472,8 +501,8 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem_mid = NBUF * BOXSET + 2 * TY * CB_PITCH * 8;
-  const size_t smem_fin = smem_mid + OUT_H * 2 * 4;
+  const size_t smem_mid = SMEM_MID;
+  const size_t smem_fin = SMEM_FIN;
   WV_CUDA(cudaFuncSetAttribute(k_level<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem_mid));
   WV_CUDA(cudaFuncSetAttribute(k_level<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
