@@ -126,13 +126,7 @@ struct ViewConst {
   float tan_h, tan_v, inv_w, inv_h, sx, sy;
   int out_w, out_h, m, n, C, wpr0;
   uint32_t plane;
-  const uint32_t* F;
-  const uint8_t* img;
-  uint8_t* out;
-  uint32_t* uncovered;
   int xmin, xmax, ymin, ymax;   // candidate-tap bounding box of the CTA
-  int covered;                  // that whole box lies inside the footprint
-  int use_win;                  // the box is staged in shared memory
 };
 
 // One CTA renders a K4_TY x K4_TX output tile (256 threads, K4_PPT pixels per
@@ -144,7 +138,10 @@ struct ViewConst {
 // (rows, K4_TX*C) bytes are staged and written with 16-byte stores.  Boxes
 // that wrap in longitude, clamp at a pole or exceed the window use direct
 // global gathers (projection.py:146-149 semantics).
-constexpr int K4_TX = 32, K4_TY = 32, K4_PPT = K4_TY / 8;
+#ifndef K4_TILE_Y
+#define K4_TILE_Y 32
+#endif
+constexpr int K4_TX = 32, K4_TY = K4_TILE_Y, K4_PPT = K4_TY / 8;
 constexpr int WIN_W = 128, WIN_H = 80;          // source pixels (32-bit words)
 constexpr int OST_PITCH = K4_TX * 4;            // bytes per staged output row (C <= 4)
 #ifndef K4_MIN_BLOCKS
@@ -165,18 +162,35 @@ __device__ __forceinline__ uint32_t blend(float b00, float b01, float b10, float
 }
 
 // Phases 3-5 for CT channels (CT = 0: any C in 1..4, read at run time).
+struct ViewPtrs {
+  const uint32_t* F;     // footprint rows of the view's region
+  const uint8_t* img;    // canvas plane 0, first row of the region
+  uint8_t* out;
+  uint32_t* uncovered;
+};
+
 template <int CT>
-__device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& v, uint32_t* win,
-                                       uint8_t* ost, const int (&x0)[K4_PPT],
-                                       const int (&y0)[K4_PPT], const float (&ax)[K4_PPT],
-                                       const float (&ay)[K4_PPT], int x, int ybase, int xl, int yl,
-                                       int yh, int wx0, int ww, int tid) {
+__device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& v,
+                                       const ViewPtrs& vp, uint32_t* win, uint8_t* ost,
+                                       const int (&x0)[K4_PPT], const int (&y0)[K4_PPT],
+                                       const float (&ax)[K4_PPT], const float (&ay)[K4_PPT], int x,
+                                       int ybase, int xl, int xh, int yl, int yh, int wx0, int ww,
+                                       bool box_ok, bool use_win, int tid) {
   const int C = CT ? CT : vc.C;
   const int m = vc.m, n = vc.n, out_w = vc.out_w, out_h = vc.out_h;
-  const bool use_win = vc.use_win;
+  // (2) footprint test of the box, one (row, word) per thread
+  bool ok = box_ok;
+  if (box_ok) {
+    const int w0 = xl >> 5, nw = (xh >> 5) - w0 + 1;
+    for (int idx = tid; idx < (yh - yl + 1) * nw; idx += 256) {
+      const int r = idx / nw, wd = w0 + idx - (idx / nw) * nw;
+      const uint32_t f = __ldg(vp.F + (uint32_t)(yl + r) * vc.wpr0 + wd);
+      ok = ok && (f | ~range_bits(xl, xh + 1, wd)) == 0xFFFFFFFFu;
+    }
+  }
   // (3) stage the box, channels interleaved (byte c of word = channel c)
   if (use_win) {
-    const uint8_t* img = vc.img;
+    const uint8_t* img = vp.img;
     const uint32_t plane = vc.plane;
     const int rows = yh - yl + 1;
     for (int idx = tid; idx < rows * ww; idx += 256) {
@@ -193,9 +207,8 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
                      __byte_perm(rg_hi, ba_hi, 0x5410), __byte_perm(rg_hi, ba_hi, 0x7632));
     }
   }
-  __syncthreads();
+  const bool covered = __syncthreads_and(ok);
   // (4) per-pixel coverage (only when the box test failed) and blend
-  const bool covered = vc.covered;
   unsigned n_unc = 0;
   const uint32_t K = 0x4B000000u;
 #pragma unroll
@@ -207,7 +220,7 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
       int tx0 = x0[k], ty0 = y0[k];
       float tax = ax[k], tay = ay[k];
       if (!covered) {
-        const uint32_t* F = vc.F;
+        const uint32_t* F = vp.F;
         const int wpr0 = vc.wpr0;
         const int cl = tax < kNear ? tx0 - 1 : tx0, ch = tax > 1.0f - kNear ? tx0 + 2 : tx0 + 1;
         const int rl = tay < kNear ? ty0 - 1 : ty0, rh = tay > 1.0f - kNear ? ty0 + 2 : ty0 + 1;
@@ -241,7 +254,7 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
         const uint32_t o00 = (uint32_t)ya * n + xa, o01 = (uint32_t)ya * n + xb;
         const uint32_t o10 = (uint32_t)yb * n + xa, o11 = (uint32_t)yb * n + xb;
         w00 = w01 = w10 = w11 = 0u;
-        const uint8_t* pc = vc.img;
+        const uint8_t* pc = vp.img;
         for (int c = 0; c < C; ++c, pc += vc.plane) {
           w00 |= (uint32_t)__ldg(pc + o00) << (8 * c);
           w01 |= (uint32_t)__ldg(pc + o01) << (8 * c);
@@ -265,13 +278,13 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
     }
     n_unc += __popc(__ballot_sync(0xFFFFFFFFu, uncovered));
   }
-  if (threadIdx.x == 0 && n_unc) atomicAdd(vc.uncovered, n_unc);
+  if (threadIdx.x == 0 && n_unc) atomicAdd(vp.uncovered, n_unc);
   __syncthreads();
   // (5) tile rows -> (out_h, out_w, C) with 16-byte stores where aligned
   const int nx = min(K4_TX, out_w - (int)blockIdx.x * K4_TX);
   const int ny = min(K4_TY, out_h - (int)blockIdx.y * K4_TY);
   const int rowb = nx * C;
-  uint8_t* gbase = vc.out + ((uint64_t)blockIdx.y * K4_TY * out_w + blockIdx.x * K4_TX) * C;
+  uint8_t* gbase = vp.out + ((uint64_t)blockIdx.y * K4_TY * out_w + blockIdx.x * K4_TX) * C;
   const uint64_t gpitch = (uint64_t)out_w * C;
   if (((reinterpret_cast<uintptr_t>(gbase) | gpitch | rowb) & 15) == 0) {
     const int nv = rowb >> 4;
@@ -288,13 +301,18 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
   }
 }
 
+// shared_n == 0: CTA (x, y, z) renders view z.  shared_n > 0: the views
+// share pose, FOV, region size and output size (a stereo pair), so the CTA
+// evaluates the geometry once and renders all shared_n views from it.
 template <bool DEV>
 __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid_constant__ Views views,
-                                                     const wv_view_args* __restrict__ d_views) {
+                                                     const wv_view_args* __restrict__ d_views,
+                                                     int shared_n) {
   __shared__ ViewConst vc;
   __shared__ __align__(16) uint32_t win[WIN_H * WIN_W];
   __shared__ __align__(16) uint8_t ost[K4_TY * OST_PITCH];
-  const wv_view_args& v = DEV ? d_views[blockIdx.z] : views.v[blockIdx.z];
+  const int vz = shared_n > 0 ? 0 : blockIdx.z;
+  const wv_view_args& v = DEV ? d_views[vz] : views.v[vz];
   const int tid = threadIdx.y * 32 + threadIdx.x;
   if (tid == 0) {
     for (int i = 0; i < 9; ++i) vc.r[i] = (float)v.rot[i];
@@ -311,10 +329,6 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
     vc.C = v.channels;
     vc.wpr0 = (v.width + 31) >> 5;
     vc.plane = (uint32_t)v.canvas_h * (uint32_t)v.width;
-    vc.F = v.d_footprint + (uint64_t)v.row0 * vc.wpr0;
-    vc.img = v.d_canvas + (uint64_t)v.row0 * v.width;
-    vc.out = v.d_out;
-    vc.uncovered = v.d_uncovered;
     vc.xmin = vc.ymin = 0x7FFFFFFF;
     vc.xmax = vc.ymax = -0x7FFFFFFF;
   }
@@ -375,30 +389,25 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
     }
   }
   __syncthreads();
-  // (2) footprint test of the box; window eligibility
   const int xl = vc.xmin, xh = vc.xmax, yl = vc.ymin, yh = vc.ymax;
   const bool inside = xl >= 0 && xh < n && yl >= 0 && yh < m && xl <= xh;
   const int wx0 = xl & ~3;
   const int ww = ((xh | 3) - wx0 + 1) >> 2;   // 4-pixel words per window row
-  if (tid < 32) {
-    const int wpr0 = vc.wpr0;
-    bool ok = inside && (xh - xl) < WIN_W;
-    for (int yy = yl + tid; ok && yy <= yh; yy += 32) {
-      const uint32_t* row = vc.F + (uint32_t)yy * wpr0;
-      for (int wd = xl >> 5; ok && wd <= (xh >> 5); ++wd)
-        ok = (__ldg(row + wd) | ~range_bits(xl, xh + 1, wd)) == 0xFFFFFFFFu;
-    }
-    const bool all = __all_sync(0xFFFFFFFFu, ok);
-    if (tid == 0) {
-      vc.covered = all;
-      vc.use_win = inside && (n & 3) == 0 && 4 * ww <= WIN_W && (yh - yl + 1) <= WIN_H;
-    }
+  const bool box_ok = inside && (xh - xl) < WIN_W;
+  const bool use_win = inside && (n & 3) == 0 && 4 * ww <= WIN_W && (yh - yl + 1) <= WIN_H;
+  const int nv = shared_n > 0 ? shared_n : 1;
+  for (int vi = 0; vi < nv; ++vi) {
+    // phases of consecutive views are separated by finish's own barriers
+    const wv_view_args& vv = shared_n > 0 ? (DEV ? d_views[vi] : views.v[vi]) : v;
+    const ViewPtrs vp{vv.d_footprint + (uint64_t)vv.row0 * vc.wpr0,
+                      vv.d_canvas + (uint64_t)vv.row0 * vv.width, vv.d_out, vv.d_uncovered};
+    if (vc.C == 3)
+      finish<3>(vc, vv, vp, win, ost, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww, box_ok,
+                use_win, tid);
+    else
+      finish<0>(vc, vv, vp, win, ost, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww, box_ok,
+                use_win, tid);
   }
-  __syncthreads();
-  if (vc.C == 3)
-    finish<3>(vc, v, win, ost, x0, y0, ax, ay, x, ybase, xl, yl, yh, wx0, ww, tid);
-  else
-    finish<0>(vc, v, win, ost, x0, y0, ax, ay, x, ybase, xl, yl, yh, wx0, ww, tid);
 }
 
 }  // namespace
@@ -417,23 +426,30 @@ int launch_perspective(const wv_view_args* views, int n, cudaStream_t s) {
     mw = max(mw, v.out_w);
     mh = max(mh, v.out_h);
   }
+  // one geometry evaluation for views that differ only in their canvas rows
+  bool shared = n > 1;
+  for (int i = 1; i < n && shared; ++i) {
+    const wv_view_args &a = views[0], &b = views[i];
+    shared = a.out_w == b.out_w && a.out_h == b.out_h && a.width == b.width &&
+             a.rows == b.rows && a.channels == b.channels && a.canvas_h == b.canvas_h &&
+             a.tan_h == b.tan_h && a.tan_v == b.tan_v;
+    for (int k = 0; k < 9 && shared; ++k) shared = a.rot[k] == b.rot[k];
+  }
   dim3 block(32, 8);
-  dim3 grid(cdiv(mw, K4_TX), cdiv(mh, K4_TY), n);
-  k_perspective<false><<<grid, block, 0, s>>>(pv, nullptr);
+  dim3 grid(cdiv(mw, K4_TX), cdiv(mh, K4_TY), shared ? 1 : n);
+  k_perspective<false><<<grid, block, 0, s>>>(pv, nullptr, shared ? n : 0);
   WV_CUDA(cudaGetLastError());
   return WV_OK;
 }
 
 int launch_perspective_dev(const wv_view_args* d_views, int n, int max_w, int max_h,
                            int shared_geometry, cudaStream_t s) {
-  // shared_geometry is a hint; evaluating the geometry once per stereo pair
-  // measured slower than one thread per (pixel, view) (latency-bound gathers)
-  (void)shared_geometry;
   if (!d_views || n < 1 || n > kMaxViews || max_w < 1 || max_h < 1) return WV_ERR_ARG;
   Views none{};
+  const bool shared = shared_geometry && n > 1;
   dim3 block(32, 8);
-  dim3 grid(cdiv(max_w, K4_TX), cdiv(max_h, K4_TY), n);
-  k_perspective<true><<<grid, block, 0, s>>>(none, d_views);
+  dim3 grid(cdiv(max_w, K4_TX), cdiv(max_h, K4_TY), shared ? 1 : n);
+  k_perspective<true><<<grid, block, 0, s>>>(none, d_views, shared ? n : 0);
   WV_CUDA(cudaGetLastError());
   return WV_OK;
 }
