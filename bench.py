@@ -39,8 +39,8 @@ FPS = 120.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--size", type=int, default=8192, help="frame width = height")
     ap.add_argument("--sets", type=int, default=0, help="inter-frame sets (default max(2, N))")
@@ -336,6 +336,7 @@ def run_ours(args):
     k3m = mean([e[2].elapsed_time(e[3]) for e in ks])
     k3f = mean([e[3].elapsed_time(e[4]) for e in ks])
     k4 = mean([e[5].elapsed_time(e[6]) for e in ks]) if args.mode != "full" else 0.0
+    k2_items = int(len(sess.block_work()))   # last frame's K2 work list
     tiles = mean([fo.result().n_tiles for fo in frames_out])
     sel_blocks = mean([fo.result().n_selected for fo in frames_out])
     C = h.channels
@@ -431,7 +432,7 @@ def run_ours(args):
             "stage_ms": {"k1_select": round(k1, 4), "k2_dequant_temporal": round(k2, 4),
                          "k3_levels_L_to_2": round(k3m, 4), "k3_level1_final": round(k3f, 4),
                          "k4_perspective": round(k4, 4)},
-            "selected_blocks": sel_blocks, "level1_tiles": tiles,
+            "selected_blocks": sel_blocks, "k2_work_blocks": k2_items, "level1_tiles": tiles,
             "uncovered_pixels": unc,
             "cpu_baseline": cpu,
             "e2e": e2e,

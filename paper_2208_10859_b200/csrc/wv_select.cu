@@ -282,6 +282,7 @@ struct BlockArgs {
   uint32_t* list_count;
   int account_only;
   int full;                                    // decode_full: every block selected
+  const uint8_t* bstate;                       // K2's per-block "plane may be nonzero"
   const uint32_t* pooled[WV_MAX_LEVELS + 1];   // nullptr: scan rows
   int pool_wpr[WV_MAX_LEVELS + 1];
 };
@@ -375,7 +376,11 @@ __global__ void __launch_bounds__(256) k_blocks(BlockArgs a) {
   const bool prev = valid && ((prevw >> lane) & 1u);
   const bool was = (loadw >> lane) & 1u;
   const bool missing = sel && !was;
-  const bool emit = !a.account_only && (sel || prev);
+  // K2 work: selected blocks with records (all are offset-checked) or with
+  // stale nonzeros; blocks that left the selection and still hold nonzeros.
+  // A selected block without records whose plane block is zero needs nothing.
+  const bool dirty = valid && a.bstate[b] != 0;
+  const bool emit = !a.account_only && ((sel && (recs > 0 || dirty)) || (!sel && prev && dirty));
   const uint32_t emask = __ballot_sync(0xFFFFFFFFu, emit);
   uint32_t base = 0;
   if (lane == 0 && emask) base = atomicAdd(a.list_count, (uint32_t)__popc(emask));
@@ -577,6 +582,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     b.list_count = counters + CNT_BLOCKS;
     b.account_only = acct;
     b.full = full;
+    b.bstate = ws + lo.bstate;
     for (int k = 1; k <= L; ++k) {
       const bool ok = lo.bs == 32 && ((H >> k) % 32) == 0 && ((W >> k) % 32) == 0;
       b.pooled[k] = ok ? (const uint32_t*)(ws + lo.pooled[k]) : nullptr;

@@ -84,13 +84,15 @@ __device__ __forceinline__ int tweight(int ti, int t, int n) {
   return ((t >> (lvl - 1)) & 1) ? -1 : 1;
 }
 
-// One CTA (128 threads) per work-list block.  All records of the block (all
-// temporal indices, for offset validation) are fetched in rounds of 128 with
-// one record per thread, so a sparse block costs one dependent load; the
-// shared-memory accumulation then runs temporal index by temporal index in
-// ascending order (the np.add.at order), and the inclusion-masked block is
-// written with 16-byte stores.
-constexpr int K2_THREADS = 128;
+// One CTA (256 threads) per work-list block (K1 lists only blocks with
+// records or with stale nonzeros).  Warp 0 reads the block's BlockEnd spans
+// and prefix-sums them; blocks without a record of a contributing temporal
+// index are zero (cleared only if the plane block still holds nonzeros).
+// Otherwise the records are added into a shared-memory block temporal index
+// by temporal index (ascending, the np.add.at order), all records of one
+// index concurrently, and the inclusion-masked block is written with 16-byte
+// stores.
+constexpr int K2_THREADS = 256;
 constexpr int K2_MAXN = 32;
 
 __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
@@ -105,6 +107,8 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
   __shared__ int s_w[K2_MAXN];
   __shared__ uint32_t s_mrow[32];
   __shared__ int s_live;
+  __shared__ float s_q255[256];   // q / 255.0f, IEEE division (encoding.py:270-271)
+  for (int q = threadIdx.x; q < 256; q += blockDim.x) s_q255[q] = __fdiv_rn((float)q, 255.0f);
   const int tid = threadIdx.x;
   const int npos = a.bs * a.bs;
   const int nq = (a.C * npos) >> 2;                           // float4 per block
@@ -191,53 +195,60 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
       smem4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     if (tid == 0 && !dirty) a.bstate[b] = 1;
-    for (int base = 0; base < total; base += K2_THREADS) {
-      const int i = base + tid;
-      int ti = -1, off = 0;
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
-      if (i < total) {
-        ti = 0;
-        while (s_pre[ti + 1] <= i) ++ti;
-        const uint8_t* rp = recs + s_start[ti] + (uint64_t)(i - s_pre[ti]) * a.rs;
-        off = (int)rp[0] | ((int)rp[1] << 8);
+    // temporal index by temporal index, ascending (the np.add.at order);
+    // within one index every position has at most one record, so its
+    // records are added concurrently
+    for (int tt = 0; tt < a.n; ++tt) {
+      const int cnt = s_pre[tt + 1] - s_pre[tt];
+      if (cnt == 0) continue;
+      const int w = s_w[tt];
+      const uint8_t* rbase = recs + s_start[tt];
+      if (!w) {
+        // not summed for this display time; offsets are still validated
+        for (int i = tid; i < cnt; i += K2_THREADS) {
+          const uint8_t* rp = rbase + (uint64_t)i * a.rs;
+          if (((int)rp[0] | ((int)rp[1] << 8)) >= npos) err |= WV_DERR_OFFSET;
+        }
+        continue;
+      }
+      float lo_a[4], d_a[4], lo_d[4], d_d[4];   // cmin, cmax - cmin: approx / detail
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        lo_a[c] = d_a[c] = lo_d[c] = d_d[c] = 0.0f;
+        if (c < a.C && !a.float_mode) {
+          const float* ex = extrema + ((uint64_t)tt * a.C + c) * 4;
+          lo_a[c] = ex[0];
+          d_a[c] = __fsub_rn(ex[1], ex[0]);
+          lo_d[c] = ex[2];
+          d_d[c] = __fsub_rn(ex[3], ex[2]);
+        }
+      }
+#pragma unroll 4
+      for (int i = tid; i < cnt; i += K2_THREADS) {
+        const uint8_t* rp = rbase + (uint64_t)i * a.rs;
+        const int off = (int)rp[0] | ((int)rp[1] << 8);
         if (off >= npos) {
           err |= WV_DERR_OFFSET;
-          ti = -1;
-        } else if (!s_w[ti]) {
-          ti = -1;
-        } else {
-          const int yy = y0 + (off >> a.bs_log2), xx = x0 + (off & bmask);
-          const bool appr = yy < ah && xx < aw;
+          continue;
+        }
+        const int yy = y0 + (off >> a.bs_log2), xx = x0 + (off & bmask);
+        const bool appr = yy < ah && xx < aw;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float x = 0.0f;
-            if (c < a.C) {
+        for (int c = 0; c < 4; ++c) {
+          if (c < a.C) {
+            float x;
             if (a.float_mode) {
               const uint8_t* q = rp + 2 + 4 * c;
               x = __uint_as_float((uint32_t)q[0] | ((uint32_t)q[1] << 8) |
                                   ((uint32_t)q[2] << 16) | ((uint32_t)q[3] << 24));
             } else {
-              const float* ex = extrema + ((uint64_t)ti * a.C + c) * 4 + (appr ? 0 : 2);
-              const float lo = ex[0], hi = ex[1];
-              x = __fadd_rn(lo, __fmul_rn(__fdiv_rn((float)rp[2 + c], 255.0f), __fsub_rn(hi, lo)));
+              // cmin + (q / 255) * (cmax - cmin), q / 255 from the IEEE table
+              x = __fadd_rn(appr ? lo_a[c] : lo_d[c],
+                            __fmul_rn(s_q255[rp[2 + c]], appr ? d_a[c] : d_d[c]));
             }
-            }
-            v[c] = s_w[ti] > 0 ? x : -x;
+            acc[c * npos + off] = __fadd_rn(acc[c * npos + off], w > 0 ? x : -x);
           }
         }
-      }
-      // accumulate this round's records in ascending temporal index
-      const int last = min(base + K2_THREADS, total) - 1;
-      int t_lo = 0, t_hi = 0;
-      while (s_pre[t_lo + 1] <= base) ++t_lo;
-      while (s_pre[t_hi + 1] <= last) ++t_hi;
-      for (int tt = t_lo; tt <= t_hi; ++tt) {
-        if (ti == tt) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (c < a.C) acc[c * npos + off] = __fadd_rn(acc[c * npos + off], v[c]);
-        }
-        if (s_w[tt] && tt < t_hi) __syncthreads();
       }
       __syncthreads();
     }

@@ -590,6 +590,18 @@ class DecodeSession:
         n = h.channels * h.height * h.width
         return self._ws[off: off + 4 * n].view(torch.float32).view(h.channels, h.height, h.width)
 
+    def block_work(self) -> np.ndarray:
+        """K2 work list of the last decode (block ids; ZERO_FLAG bit = clear
+        only), after the stream has finished."""
+        lst, cnt = C.c_void_p(), C.c_void_p()
+        N.check(self._lib.wv_block_list_view(C.byref(self._geom), C.c_void_p(self._ws.data_ptr()),
+                                             C.byref(lst), C.byref(cnt)), "wv_block_list_view")
+        self.stream.synchronize()
+        base = self._ws.data_ptr()
+        n = int(self._ws[cnt.value - base: cnt.value - base + 4].view(torch.int32).item())
+        off = lst.value - base
+        return self._ws[off: off + 4 * n].view(torch.int32).cpu().numpy().view(np.uint32)
+
     # -- prefetch (decoding.py:335-354) -------------------------------------------
 
     def advance(self, current_frame: int, next_mask: np.ndarray) -> None:

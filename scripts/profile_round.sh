@@ -1,0 +1,24 @@
+#!/bin/bash
+# ncu evidence for one round (run on the GPU box from the repo root):
+#   scripts/profile_round.sh TAG
+# 1) the profiled command must first exit 0 without ncu; 2) launch list
+# (gpu__time_duration per launch, 4 frames); 3) one --set full capture per
+# hot kernel (viewport and full-frame).  Output: gpurun_out/prof/.
+set -e
+tag=${1:-rXX}
+out=gpurun_out/prof; mkdir -p $out
+cmd="python bench.py --profile-only --warmup 4 --steps 1 --pipeline 1"
+$cmd
+$cmd --mode full
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_${tag}.csv $cmd > /dev/null
+cap() {  # name, kernel regex, skip, extra bench args
+  ncu --set full --import-source on --clock-control none -k regex:$2 -s $3 -c 1 -o $out/${tag}_$1 $cmd $4 > $out/${tag}_$1.log 2>&1 || tail -5 $out/${tag}_$1.log
+}
+cap k3_final k_level 11 ""
+cap k3_level2 k_level 10 ""
+cap k2 k_temporal 1 ""
+cap k4 persp 1 ""
+cap k1_cascade1 k_cascade 6 ""
+cap k3_final_full k_level 11 "--mode full"
+cap k2_full k_temporal 1 "--mode full"
+ls -la $out
