@@ -111,6 +111,38 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
   return WV_OK;
 }
 
+// Programmatic dependent launch (WV_PDL=1): kernels of the decode sequence
+// are launched with programmatic stream serialization; each first waits for
+// its predecessor grid (griddepcontrol.wait: completion + memory visibility)
+// and then lets its successor launch.  Measured slower end to end on B200
+// (serial frame latency +0.1-0.25 ms, early-resident successor CTAs), so it
+// is off by default; the launch path is shared.
+#ifndef WV_PDL
+#define WV_PDL 0
+#endif
+__device__ __forceinline__ void pdl_sync() {
+#if WV_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = WV_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
+
 #define WV_CUDA(x)                                   \
   do {                                               \
     cudaError_t e_ = (x);                            \

@@ -231,6 +231,7 @@ template <bool FINAL>
 __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUtensorMap tm_ll,
                                                     const __grid_constant__ CUtensorMap tm_det,
                                                     LevelArgs a) {
+  pdl_sync();
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* canvas = FINAL ? a.fa->d_canvas : nullptr;
   float* box = reinterpret_cast<float*>(smem);
@@ -534,14 +535,14 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
       la.out = (float*)(ws + lo.ybuf[k - 1]);
       la.out_pitch = lo.ypitch[k - 1];
       int grid = max(1, min(ntiles * C, sms * occ_mid));
-      k_level<false><<<grid, NTHREADS, smem_mid, s>>>(tm_ll, tm_plane, la);
+      WV_CUDA(launch_k(k_level<false>, dim3(grid), dim3(NTHREADS), smem_mid, s, tm_ll, tm_plane, la));
     } else {
       la.fa = fa;
       la.R = (const uint32_t*)(ws + lo.mrows);
       la.rowmap = (const uint32_t*)(ws + lo.rowmap);
       la.wpr0 = lo.wpr_[0];
       int grid = max(1, min(ntiles * C, sms * occ_fin));
-      k_level<true><<<grid, NTHREADS, smem_fin, s>>>(tm_ll, tm_plane, la);
+      WV_CUDA(launch_k(k_level<true>, dim3(grid), dim3(NTHREADS), smem_fin, s, tm_ll, tm_plane, la));
     }
     WV_CUDA(cudaGetLastError());
     if (getenv("WV_DEBUG_SYNC")) {

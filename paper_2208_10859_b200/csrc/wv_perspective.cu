@@ -308,6 +308,7 @@ template <bool DEV>
 __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid_constant__ Views views,
                                                      const wv_view_args* __restrict__ d_views,
                                                      int shared_n) {
+  pdl_sync();
   __shared__ ViewConst vc;
   __shared__ __align__(16) uint32_t win[WIN_H * WIN_W];
   __shared__ __align__(16) uint8_t ost[K4_TY * OST_PITCH];
@@ -437,7 +438,7 @@ int launch_perspective(const wv_view_args* views, int n, cudaStream_t s) {
   }
   dim3 block(32, 8);
   dim3 grid(cdiv(mw, K4_TX), cdiv(mh, K4_TY), shared ? 1 : n);
-  k_perspective<false><<<grid, block, 0, s>>>(pv, nullptr, shared ? n : 0);
+  WV_CUDA(launch_k(k_perspective<false>, dim3(grid), dim3(block), 0, s, pv, nullptr, shared ? n : 0));
   WV_CUDA(cudaGetLastError());
   return WV_OK;
 }
@@ -449,7 +450,7 @@ int launch_perspective_dev(const wv_view_args* d_views, int n, int max_w, int ma
   const bool shared = shared_geometry && n > 1;
   dim3 block(32, 8);
   dim3 grid(cdiv(max_w, K4_TX), cdiv(max_h, K4_TY), shared ? 1 : n);
-  k_perspective<true><<<grid, block, 0, s>>>(none, d_views, shared ? n : 0);
+  WV_CUDA(launch_k(k_perspective<true>, dim3(grid), dim3(block), 0, s, none, d_views, shared ? n : 0));
   WV_CUDA(cudaGetLastError());
   return WV_OK;
 }

@@ -72,11 +72,13 @@ __device__ __forceinline__ uint32_t shrink(uint32_t p, uint32_t c, uint32_t n) {
 // Distinct pixel-mask rows R[my] (nearest column map, fileio.py:435) and the
 // row map rowmap[y] = (y*mh)/H (fileio.py:434).
 __global__ void k_mask_rows(const wv_frame_args* __restrict__ fa, uint32_t* __restrict__ R,
-                            uint32_t* __restrict__ rowmap, int mh, int mw, int W, int H, int wpr0,
-                            int full) {
+                            uint32_t* __restrict__ rowmap, uint32_t* __restrict__ counters, int mh,
+                            int mw, int W, int H, int wpr0, int full) {
+  pdl_sync();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const uint8_t* __restrict__ mask = fa->d_mask;
   if (idx == 0) *fa->d_result = wv_frame_result{};
+  if (idx < 64) counters[idx] = 0u;   // work-list counters of this call
   if (idx < H) rowmap[idx] = ((uint32_t)idx * (uint32_t)mh) / (uint32_t)H;
   if (idx >= mh * wpr0) return;
   const int my = idx / wpr0, w = idx % wpr0;
@@ -141,6 +143,7 @@ __device__ __forceinline__ uint32_t cas_down(const CascadeArgs& a, const int4& r
 }
 
 __global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
+  pdl_sync();
   __shared__ uint32_t dm[2][CT_R + 2 * DIL][CT_W + 2];
   __shared__ uint32_t pool[CT_W];
   const int b = a.batch[blockIdx.y];
@@ -225,6 +228,7 @@ constexpr int FP_SR = CT_R / 2 + DIL + 1;  // source rows staged per tile (21)
 constexpr int FP_SW = CT_W / 2 + 2;        // source words staged per tile (18)
 
 __global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
+  pdl_sync();
   __shared__ uint32_t sv[FP_SR][FP_SW];
   const int r0 = blockIdx.z * CT_R, w0 = blockIdx.x * CT_W;
   const int sr0 = (r0 - DIL) >> 1, sw0 = (w0 >> 1) - 1;
@@ -338,6 +342,7 @@ __device__ bool block_any(const BlockArgs& a, int b) {
 }
 
 __global__ void __launch_bounds__(256) k_blocks(BlockArgs a) {
+  pdl_sync();
   const unsigned long long* __restrict__ ends = (const unsigned long long*)a.fa->d_payload;
   const unsigned long long rec_bytes = a.fa->payload_bytes - a.table_bytes;
   uint32_t* loaded = a.fa->d_set_loaded;
@@ -431,6 +436,7 @@ struct TileArgs {
 };
 
 __global__ void __launch_bounds__(256) k_tiles1(TileArgs a) {
+  pdl_sync();
   const int nt1 = a.nty[1] * a.ntx[1];
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   bool nd = false, pv = false;
@@ -467,6 +473,7 @@ __global__ void __launch_bounds__(256) k_tiles1(TileArgs a) {
 // Coarser levels in one CTA: need maps live as bit rows in shared memory and
 // level k is derived from level k-1 (rows 2u-1..2u+2 x cols 2v-1..2v+2).
 __global__ void __launch_bounds__(1024) k_tiles_up(TileArgs a) {
+  pdl_sync();
   extern __shared__ uint32_t nbits[];
   __shared__ uint32_t cnt;
   int off[WV_MAX_LEVELS + 2];
@@ -502,6 +509,7 @@ __global__ void __launch_bounds__(1024) k_tiles_up(TileArgs a) {
 // wavelets.py:267-270), no mask cascades are needed
 __global__ void k_fill_footprint(const wv_frame_args* __restrict__ fa, int rows, int cols,
                                  int wpr) {
+  pdl_sync();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= rows * wpr) return;
   const int w = idx % wpr;
@@ -509,6 +517,7 @@ __global__ void k_fill_footprint(const wv_frame_args* __restrict__ fa, int rows,
 }
 
 __global__ void k_finalize(const wv_frame_args* fa) {
+  pdl_sync();
   fa->d_result->set_bytes = *fa->d_set_bytes;
 }
 
@@ -523,10 +532,10 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
   uint32_t* R = (uint32_t*)(ws + lo.mrows);
   uint32_t* rowmap = (uint32_t*)(ws + lo.rowmap);
   uint32_t* counters = (uint32_t*)(ws + lo.counters);
-  WV_CUDA(cudaMemsetAsync(counters, 0, 64 * 4, s));
   {
     const int n = max(lo.mh * lo.wpr_[0], H);
-    k_mask_rows<<<cdiv(n, 256), 256, 0, s>>>(fa, R, rowmap, lo.mh, lo.mw, W, H, lo.wpr_[0], full);
+    WV_CUDA(launch_k(k_mask_rows, dim3(cdiv(n, 256)), dim3(256), 0, s, fa, R, rowmap, counters,
+                     lo.mh, lo.mw, W, H, lo.wpr_[0], (int)full));
   }
   // level cascades (batch 0: request closure; batches k>=j: gaze windows);
   // a full-frame decode needs none of them
@@ -549,14 +558,15 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     c.pooled = lo.bs == 32 ? (uint32_t*)(ws + lo.pooled[j]) : nullptr;
     c.pool_wpr = cdiv(c.wpr, CT_W);
     dim3 grid(cdiv(c.wpr, CT_W), c.nbatch, cdiv(c.rows, CT_R));
-    k_cascade<<<grid, 256, 0, s>>>(c);
+    WV_CUDA(launch_k(k_cascade, dim3(grid), dim3(256), 0, s, c));
   }
   auto Dptr = [&](int k) -> uint32_t* {
     return (uint32_t*)(ws + lo.stack[k] + (fov ? (uint64_t)k * lo.stack_stride[k] : 0));
   };
   // footprint: V_L = ones; V_{j-1} = shrink(up(V_j & D_j)); last & request
   if (full && !acct)
-    k_fill_footprint<<<cdiv(H * lo.wpr_[0], 256), 256, 0, s>>>(fa, H, W, lo.wpr_[0]);
+    WV_CUDA(launch_k(k_fill_footprint, dim3(cdiv(H * lo.wpr_[0], 256)), dim3(256), 0, s, fa, H, W,
+                     lo.wpr_[0]));
   for (int j = L; j >= 1 && !acct && !full; --j) {
     FootArgs f{};
     f.j = j; f.L = L; f.H = H;
@@ -567,7 +577,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     f.out = j == 1 ? nullptr : (uint32_t*)(ws + lo.fp[j - 1]);
     f.R = R; f.rowmap = rowmap; f.fa = fa;
     dim3 grid(cdiv(f.wpr, CT_W), 1, cdiv(f.rows, CT_R));
-    k_footprint<<<grid, 256, 0, s>>>(f);
+    WV_CUDA(launch_k(k_footprint, dim3(grid), dim3(256), 0, s, f));
   }
   {
     BlockArgs b{};
@@ -588,10 +598,10 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
       b.pooled[k] = ok ? (const uint32_t*)(ws + lo.pooled[k]) : nullptr;
       b.pool_wpr[k] = cdiv(lo.wpr_[k], CT_W);
     }
-    k_blocks<<<cdiv(lo.NB, 256), 256, 0, s>>>(b);
+    WV_CUDA(launch_k(k_blocks, dim3(cdiv(lo.NB, 256)), dim3(256), 0, s, b));
   }
   if (acct) {
-    k_finalize<<<1, 1, 0, s>>>(fa);
+    WV_CUDA(launch_k(k_finalize, dim3(1), dim3(1), 0, s, fa));
   } else {
     TileArgs t{};
     t.L = L; t.H = H; t.W = W; t.wpr0 = lo.wpr_[0]; t.R = R; t.rowmap = rowmap; t.full = full;
@@ -605,7 +615,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     t.counters = counters;
     t.fa = fa;
     const int nt1 = lo.nty[1] * lo.ntx[1];
-    k_tiles1<<<cdiv(nt1, 256), 256, 0, s>>>(t);
+    WV_CUDA(launch_k(k_tiles1, dim3(cdiv(nt1, 256)), dim3(256), 0, s, t));
     if (L >= 2) {
       size_t words = 0;
       for (int k = 1; k <= L; ++k) words += (size_t)lo.nty[k] * wpr(lo.ntx[k]);
@@ -613,7 +623,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
       if (words * 4 > 48 * 1024)
         WV_CUDA(cudaFuncSetAttribute(k_tiles_up, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(words * 4)));
-      k_tiles_up<<<1, 1024, words * 4, s>>>(t);
+      WV_CUDA(launch_k(k_tiles_up, dim3(1), dim3(1024), words * 4, s, t));
     }
   }
   WV_CUDA(cudaGetLastError());

@@ -96,6 +96,7 @@ constexpr int K2_THREADS = 256;
 constexpr int K2_MAXN = 32;
 
 __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
+  pdl_sync();
   const int t_disp = a.fa->t;
   const unsigned long long* __restrict__ ends = (const unsigned long long*)a.fa->d_payload;
   const uint8_t* __restrict__ recs = (const uint8_t*)a.fa->d_payload + a.table_bytes;
@@ -321,7 +322,7 @@ int launch_temporal(const Layout& lo, const wv_geometry* g, int mode, const wv_f
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_temporal, K2_THREADS, smem);
   const int grid = max(1, min(lo.NB, sms * max(occ, 1)));
-  k_temporal<<<grid, K2_THREADS, smem, s>>>(t);
+  WV_CUDA(launch_k(k_temporal, dim3(grid), dim3(K2_THREADS), smem, s, t));
   WV_CUDA(cudaGetLastError());
   return WV_OK;
 }
