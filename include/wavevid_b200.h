@@ -98,7 +98,10 @@ typedef struct wv_frame_args {
   uint32_t* d_set_loaded;         /* NB-bit block bitmap of the set's cache entry */
   unsigned long long* d_set_bytes;/* the entry's cumulative bytes */
   uint8_t* d_canvas;              /* planar (C, H, W) u8 output; must persist across calls of one workspace */
-  uint32_t* d_footprint;          /* (H, ceil(W/32)) bit rows output, bit i of word w = column 32w+i */
+  uint32_t* d_footprint;          /* (H, ceil(W/32)) bit rows output, bit i of word w = column 32w+i;
+                                     like d_canvas it is updated incrementally (only the 64x64 tiles
+                                     that touch or left the request are rewritten): zero it once and
+                                     pass the same buffer to every call of one workspace */
   wv_frame_result* d_result;
 } wv_frame_args;
 

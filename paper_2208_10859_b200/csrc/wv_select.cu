@@ -270,6 +270,66 @@ __global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
   }
 }
 
+// Finest footprint step restricted to the level-1 synthesis tiles: the
+// footprint is ANDed with the request, so it is zero outside the tiles that
+// touch the request; tiles that left the request (ZERO_FLAG) are cleared.
+// One CTA-iteration per 64x64-pixel tile (64 rows x 2 words, one word per
+// thread); source: 37 rows x 3 words of V_1 & D_1.
+constexpr int FT_SR = OUT_H / 2 + DIL + 1, FT_SW = 3;
+
+__global__ void __launch_bounds__(128) k_footprint_tiles(FootArgs a, const uint32_t* list,
+                                                         const uint32_t* count, int ntx1) {
+  pdl_sync();
+  __shared__ uint32_t sv[FT_SR][FT_SW];
+  const uint32_t n = *count;
+  uint32_t* out = a.fa->d_footprint;
+  const int tid = threadIdx.x;
+  for (uint32_t it = blockIdx.x; it < n; it += gridDim.x) {
+    const uint32_t e = list[it];
+    const int tile = (int)(e & ~ZERO_FLAG);
+    const int ty = tile / ntx1, tx = tile - (tile / ntx1) * ntx1;
+    const int r0 = ty * OUT_H, w0 = tx * (OUT_W / 32);
+    const int lr = tid >> 1, lw = tid & 1;
+    const int r = r0 + lr, w = w0 + lw;
+    const bool mine = r < a.rows && w < a.wpr;
+    if (e & ZERO_FLAG) {
+      if (mine) out[(uint64_t)r * a.wpr + w] = 0u;
+      continue;   // no shared memory touched
+    }
+    const int sr0 = (r0 - DIL) >> 1, sw0 = tx - 1;
+    for (int i = tid; i < FT_SR * FT_SW; i += blockDim.x) {
+      const int ir = i / FT_SW, iw = i - (i / FT_SW) * FT_SW;
+      const int sr = sr0 + ir, sw = sw0 + iw;
+      uint32_t v = 0xFFFFFFFFu;
+      if (sr >= 0 && sr < a.srows && sw >= 0 && sw < a.swpr) {
+        v = a.D[(uint64_t)sr * a.swpr + sw];
+        if (a.V) v &= a.V[(uint64_t)sr * a.swpr + sw];
+      }
+      sv[ir][iw] = v;
+    }
+    __syncthreads();
+    if (mine) {
+      const int s_lo = ((r - DIL) >> 1) - sr0, s_hi = ((r + DIL) >> 1) - sr0;
+      uint32_t nb[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int ww = w - 1 + d;
+        if (ww < 0 || ww >= a.wpr) {
+          nb[d] = 0xFFFFFFFFu;
+          continue;
+        }
+        uint32_t v = 0xFFFFFFFFu;
+        for (int k = s_lo; k <= s_hi; ++k) v &= sv[k][(ww >> 1) - sw0];
+        nb[d] = double_bits(v >> (16 * (ww & 1))) | ~last_word_mask(a.cols, ww);
+      }
+      uint32_t v = shrink(nb[0], nb[1], nb[2]) & last_word_mask(a.cols, w);
+      v &= a.R[(uint64_t)a.rowmap[r] * a.wpr + w];
+      out[(uint64_t)r * a.wpr + w] = v;
+    }
+    __syncthreads();
+  }
+}
+
 // -------------------------------------------------------------- block select
 // One warp per 32x32 coefficient block (lane = block row); 8 blocks per CTA
 // aggregate their list appends and statistics before touching global
@@ -567,14 +627,14 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
   if (full && !acct)
     WV_CUDA(launch_k(k_fill_footprint, dim3(cdiv(H * lo.wpr_[0], 256)), dim3(256), 0, s, fa, H, W,
                      lo.wpr_[0]));
-  for (int j = L; j >= 1 && !acct && !full; --j) {
+  for (int j = L; j >= 2 && !acct && !full; --j) {
     FootArgs f{};
     f.j = j; f.L = L; f.H = H;
     f.rows = H >> (j - 1); f.cols = W >> (j - 1); f.wpr = lo.wpr_[j - 1];
     f.srows = H >> j; f.swpr = lo.wpr_[j];
     f.V = j == L ? nullptr : (const uint32_t*)(ws + lo.fp[j]);
     f.D = Dptr(j);
-    f.out = j == 1 ? nullptr : (uint32_t*)(ws + lo.fp[j - 1]);
+    f.out = (uint32_t*)(ws + lo.fp[j - 1]);
     f.R = R; f.rowmap = rowmap; f.fa = fa;
     dim3 grid(cdiv(f.wpr, CT_W), 1, cdiv(f.rows, CT_R));
     WV_CUDA(launch_k(k_footprint, dim3(grid), dim3(256), 0, s, f));
@@ -616,6 +676,22 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     t.fa = fa;
     const int nt1 = lo.nty[1] * lo.ntx[1];
     WV_CUDA(launch_k(k_tiles1, dim3(cdiv(nt1, 256)), dim3(256), 0, s, t));
+    if (!full) {
+      // finest footprint step on the level-1 tiles only (zero elsewhere)
+      FootArgs f{};
+      f.j = 1; f.L = L; f.H = H;
+      f.rows = H; f.cols = W; f.wpr = lo.wpr_[0];
+      f.srows = H >> 1; f.swpr = lo.wpr_[1];
+      f.V = L == 1 ? nullptr : (const uint32_t*)(ws + lo.fp[1]);
+      f.D = Dptr(1);
+      f.R = R; f.rowmap = rowmap; f.fa = fa;
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      WV_CUDA(launch_k(k_footprint_tiles, dim3(min(nt1, 8 * sms)), dim3(128), 0, s, f,
+                       (const uint32_t*)t.list[1], (const uint32_t*)(counters + CNT_TILES + 1),
+                       lo.ntx[1]));
+    }
     if (L >= 2) {
       size_t words = 0;
       for (int k = 1; k <= L; ++k) words += (size_t)lo.nty[k] * wpr(lo.ntx[k]);
