@@ -557,10 +557,12 @@ class DecodeSession:
         return n
 
     def render_views(self, pose: CameraPose, out_dims, out: torch.Tensor | None = None,
-                     check: bool = True) -> torch.Tensor:
+                     check: bool = True, all_covered: bool = False) -> torch.Tensor:
         """Perspective writeout (K4) of the current canvas: one view, or one
         per eye for top-bottom stereo.  Returns
-        (views, out_h, out_w, C) u8 on the device."""
+        (views, out_h, out_w, C) u8 on the device.  ``all_covered``: coverage
+        against an all-ones footprint, as the reference's foveated callers do
+        (cli.py:177, service.py:135)."""
         h = self.header
         out_w, out_h = out_dims
         eyes = [(0, h.height)] if not h.stereo else [(0, h.height // 2),
@@ -570,7 +572,12 @@ class DecodeSession:
                               device=self.device)
         with torch.cuda.stream(self.stream):
             self._uncovered.zero_()
-            views = [view_args(self._canvas, self._footprint, r0, rows, h.width, h.channels,
+            fp = self._footprint
+            if all_covered:
+                if self._ones_fp is None:
+                    self._ones_fp = torch.full_like(self._footprint, -1)
+                fp = self._ones_fp
+            views = [view_args(self._canvas, fp, r0, rows, h.width, h.channels,
                                pose, out[i], self._uncovered) for i, (r0, rows) in enumerate(eyes)]
             launch_views(views, self.stream)
         if check:

@@ -81,9 +81,11 @@ def main():
     with open(os.path.join(ROOT, "profiles", f"ncu_summary_{tag}.json"), "w") as fh:
         json.dump(out, fh, indent=1)
     for k in out["kernels"]:
-        if k["report"].startswith(f"{tag}_k3_final.") or k["report"] == f"{tag}_k3_final.ncu-rep":
-            with open(os.path.join(ROOT, "profiles", f"ncu_k3_final_{tag}.json"), "w") as fh:
-                json.dump(k, fh, indent=1)
+        for name, dst in ((f"{tag}_k3_final.ncu-rep", f"ncu_k3_final_{tag}.json"),
+                          (f"{tag}_k3_final_full.ncu-rep", f"ncu_k3_final_full_{tag}.json")):
+            if k["report"] == name:
+                with open(os.path.join(ROOT, "profiles", dst), "w") as fh:
+                    json.dump(k, fh, indent=1)
     print(json.dumps(out, indent=1))
 
 
