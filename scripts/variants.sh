@@ -3,7 +3,7 @@
 # and the default build; one summary line per variant.  Usage: variants.sh [mode]
 mode=${1:-viewport}
 for lib in paper_2208_10859_b200/_wvb200.so paper_2208_10859_b200/variants/*.so; do
-  WV_LIB=$PWD/$lib python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --mode $mode \
+  WV_LIB=$PWD/$lib python bench.py --steps 200 --warmup 10 --no-cpu-baseline --no-e2e --mode $mode \
     > gpurun_out/var.json 2> gpurun_out/var.err
   python -c "import json,sys;d=json.load(open('gpurun_out/var.json'));print(sys.argv[1], d['value'], d['serial_ms_per_frame'], d['stage_ms'])" $(basename $lib)
 done
