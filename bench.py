@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--cache-dir", default="/tmp/wvb200_bench")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--pipeline", type=int, default=3,
+    ap.add_argument("--pipeline", type=int, default=8,
                     help="decode sessions (streams) per GPU; frames round-robin so one "
                          "frame's writeout overlaps the next frame's decode")
     ap.add_argument("--profile-only", action="store_true",
