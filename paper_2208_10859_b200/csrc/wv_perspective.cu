@@ -208,9 +208,31 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
     }
   }
   const bool covered = __syncthreads_and(ok);
-  // (4) per-pixel coverage (only when the box test failed) and blend
-  unsigned n_unc = 0;
   const uint32_t K = 0x4B000000u;
+  // (4a) common case, uniform over the CTA: whole tile inside the output, box
+  // covered by the footprint and staged -- taps straight from the window
+  if (covered && use_win && ((int)blockIdx.x + 1) * K4_TX <= out_w &&
+      ((int)blockIdx.y + 1) * K4_TY <= out_h) {
+#pragma unroll
+    for (int k = 0; k < K4_PPT; ++k) {
+      const uint32_t* p = win + (y0[k] - yl) * WIN_W + (x0[k] - wx0);
+      const uint32_t w00 = p[0], w01 = p[1], w10 = p[WIN_W], w11 = p[WIN_W + 1];
+      uint8_t* o = ost + (threadIdx.y + 8 * k) * OST_PITCH + threadIdx.x * C;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < C) {
+          const uint32_t sel = 0x3004u + c;
+          o[c] = (uint8_t)blend(__uint_as_float(__byte_perm(K, w00, sel)),
+                                __uint_as_float(__byte_perm(K, w01, sel)),
+                                __uint_as_float(__byte_perm(K, w10, sel)),
+                                __uint_as_float(__byte_perm(K, w11, sel)), ax[k], ay[k]);
+        }
+      }
+    }
+  } else {
+  // (4b) general case: per-pixel coverage (only when the box test failed),
+  // longitude wrap / pole clamp, partial tiles
+  unsigned n_unc = 0;
 #pragma unroll
   for (int k = 0; k < K4_PPT; ++k) {
     const int y = ybase + 8 * k;
@@ -279,6 +301,7 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
     n_unc += __popc(__ballot_sync(0xFFFFFFFFu, uncovered));
   }
   if (threadIdx.x == 0 && n_unc) atomicAdd(vp.uncovered, n_unc);
+  }
   __syncthreads();
   // (5) tile rows -> (out_h, out_w, C) with 16-byte stores where aligned
   const int nx = min(K4_TX, out_w - (int)blockIdx.x * K4_TX);

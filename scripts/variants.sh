@@ -2,6 +2,7 @@
 # Bench each experimental library variant (paper_2208_10859_b200/variants/*.so)
 # and the default build; one summary line per variant.  Usage: variants.sh [mode]
 mode=${1:-viewport}
+shopt -s nullglob
 for lib in paper_2208_10859_b200/_wvb200.so paper_2208_10859_b200/variants/*.so; do
   WV_LIB=$PWD/$lib python bench.py --steps 200 --warmup 10 --no-cpu-baseline --no-e2e --mode $mode \
     > gpurun_out/var.json 2> gpurun_out/var.err
