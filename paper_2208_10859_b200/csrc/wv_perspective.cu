@@ -178,33 +178,37 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
                                        bool box_ok, bool use_win, int tid) {
   const int C = CT ? CT : vc.C;
   const int m = vc.m, n = vc.n, out_w = vc.out_w, out_h = vc.out_h;
-  // (2) footprint test of the box, one (row, word) per thread
+  // (2) footprint test of the box and (3) staging of the box, channels
+  // interleaved (byte c of word = channel c).  Thread t owns word t % nwords
+  // of rows t / nwords + k * (256 / nwords): one division per CTA, not per word.
+  const int rows = yh - yl + 1;
   bool ok = box_ok;
   if (box_ok) {
     const int w0 = xl >> 5, nw = (xh >> 5) - w0 + 1;
-    for (int idx = tid; idx < (yh - yl + 1) * nw; idx += 256) {
-      const int r = idx / nw, wd = w0 + idx - (idx / nw) * nw;
-      const uint32_t f = __ldg(vp.F + (uint32_t)(yl + r) * vc.wpr0 + wd);
-      ok = ok && (f | ~range_bits(xl, xh + 1, wd)) == 0xFFFFFFFFu;
-    }
+    const int q = tid % nw, rstep = 256 / nw, wd = w0 + q;
+    const uint32_t m = ~range_bits(xl, xh + 1, wd);
+    const uint32_t* f = vp.F + (uint32_t)yl * vc.wpr0 + wd;
+    if (tid < rstep * nw)
+      for (int r = tid / nw; r < rows; r += rstep) ok = ok && (__ldg(f + (uint32_t)r * vc.wpr0) | m) == 0xFFFFFFFFu;
   }
-  // (3) stage the box, channels interleaved (byte c of word = channel c)
   if (use_win) {
-    const uint8_t* img = vp.img;
     const uint32_t plane = vc.plane;
-    const int rows = yh - yl + 1;
-    for (int idx = tid; idx < rows * ww; idx += 256) {
-      const int r = idx / ww, q = idx - (idx / ww) * ww;
-      const uint32_t off = (uint32_t)(yl + r) * n + wx0 + 4 * q;
-      const uint32_t R = __ldg(reinterpret_cast<const uint32_t*>(img + off));
-      const uint32_t G = C > 1 ? __ldg(reinterpret_cast<const uint32_t*>(img + plane + off)) : 0u;
-      const uint32_t B = C > 2 ? __ldg(reinterpret_cast<const uint32_t*>(img + 2 * plane + off)) : 0u;
-      const uint32_t A = C > 3 ? __ldg(reinterpret_cast<const uint32_t*>(img + 3 * plane + off)) : 0u;
-      const uint32_t rg_lo = __byte_perm(R, G, 0x5140), rg_hi = __byte_perm(R, G, 0x7362);
-      const uint32_t ba_lo = __byte_perm(B, A, 0x5140), ba_hi = __byte_perm(B, A, 0x7362);
-      *reinterpret_cast<uint4*>(win + r * WIN_W + 4 * q) =
-          make_uint4(__byte_perm(rg_lo, ba_lo, 0x5410), __byte_perm(rg_lo, ba_lo, 0x7632),
-                     __byte_perm(rg_hi, ba_hi, 0x5410), __byte_perm(rg_hi, ba_hi, 0x7632));
+    const int q = tid % ww, rstep = 256 / ww;
+    const uint8_t* img = vp.img + (uint32_t)yl * n + wx0 + 4 * q;
+    uint32_t* dst = win + 4 * q;
+    if (tid < rstep * ww) {
+      for (int r = tid / ww; r < rows; r += rstep) {
+        const uint8_t* src = img + (uint32_t)r * n;
+        const uint32_t R = __ldg(reinterpret_cast<const uint32_t*>(src));
+        const uint32_t G = C > 1 ? __ldg(reinterpret_cast<const uint32_t*>(src + plane)) : 0u;
+        const uint32_t B = C > 2 ? __ldg(reinterpret_cast<const uint32_t*>(src + 2 * plane)) : 0u;
+        const uint32_t A = C > 3 ? __ldg(reinterpret_cast<const uint32_t*>(src + 3 * plane)) : 0u;
+        const uint32_t rg_lo = __byte_perm(R, G, 0x5140), rg_hi = __byte_perm(R, G, 0x7362);
+        const uint32_t ba_lo = __byte_perm(B, A, 0x5140), ba_hi = __byte_perm(B, A, 0x7362);
+        *reinterpret_cast<uint4*>(dst + r * WIN_W) =
+            make_uint4(__byte_perm(rg_lo, ba_lo, 0x5410), __byte_perm(rg_lo, ba_lo, 0x7632),
+                       __byte_perm(rg_hi, ba_hi, 0x5410), __byte_perm(rg_hi, ba_hi, 0x7632));
+      }
     }
   }
   const bool covered = __syncthreads_and(ok);
