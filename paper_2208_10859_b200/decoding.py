@@ -31,7 +31,8 @@ import torch
 
 from . import _native as N
 from .fileio import VideoReader
-from .projection import CameraPose, CoverageError, launch_views, unpack_footprint, view_args
+from .projection import (CameraPose, CoverageError, launch_views, set_view_pose, unpack_footprint,
+                         view_args)
 
 
 class DecodeError(ValueError):
@@ -227,6 +228,8 @@ class DecodeSession:
         self._resident: OrderedDict = OrderedDict()
         self._max_resident = max(2, max_resident_sets)
         self._pending: deque = deque()
+        self._n_may_evict = 0          # pending launches whose settle may evict
+        self._view_cache = {}          # (footprint, out, out shape) -> eye ViewArgs
         self._stats = SessionStats()
         self._prefetch_thread: threading.Thread | None = None
         self._prefetch_job = None
@@ -302,7 +305,7 @@ class DecodeSession:
                 del self._cache[oldest]
 
     def _entry_for(self, set_index: int) -> tuple[_Entry, bool, bool]:
-        if any(p.may_evict for p in self._pending):
+        if self._n_may_evict:
             self._settle_until(None)
         entry = self._cache.get(set_index)
         if entry is None:
@@ -323,7 +326,7 @@ class DecodeSession:
         m = np.asarray(mask)
         if m.shape != (h.mask_h, h.mask_w):
             raise DecodeError(f"mask dims {m.shape} != header ({h.mask_h}, {h.mask_w})")
-        return m.astype(bool)
+        return m if m.dtype == np.bool_ else m.astype(bool)
 
     def _mode_args(self, mode: str, mask, schedule, slot: int):
         h = self.header
@@ -332,7 +335,7 @@ class DecodeSession:
             args.mode = N.WV_MODE_FULL
             return args
         m = self._check_mask(mask)
-        self._mask_host[slot].numpy()[:] = m.reshape(-1)
+        np.copyto(self._mask_host[slot].numpy(), m.reshape(-1), casting="unsafe")
         self._mask_dev[slot].copy_(self._mask_host[slot], non_blocking=True)
         args.d_mask = self._mask_dev[slot].data_ptr()
         args.mode = N.WV_MODE_VIEWPORT
@@ -448,6 +451,7 @@ class DecodeSession:
         p.slot, p.set_index, p.entry, p.existed, p.may_evict = slot, si, entry, existed, may_evict
         p.event, p.ev, p.account_only = done, (ev0, evs), account_only
         self._pending.append(p)
+        self._n_may_evict += bool(may_evict)
         return p
 
     def _settle_until(self, target: _Pending | None):
@@ -455,6 +459,7 @@ class DecodeSession:
         errors, cache store/eviction of existing entries)."""
         while self._pending:
             p = self._pending.popleft()
+            self._n_may_evict -= bool(p.may_evict)
             p.event.synchronize()
             r = N.FrameResult.from_buffer_copy(bytes(self._results_host[p.slot].numpy()))
             entry = p.entry
@@ -542,8 +547,14 @@ class DecodeSession:
             if self._ones_fp is None:
                 self._ones_fp = torch.full_like(self._footprint, -1)
             fp = self._ones_fp
-        views = [view_args(self._canvas, fp, r0, rows, h.width, h.channels, pose,
-                           out[i], self._uncovered) for i, (r0, rows) in enumerate(self._eyes())]
+        key = (fp.data_ptr(), out.data_ptr(), tuple(out.shape))
+        views = self._view_cache.get(key)
+        if views is None:
+            views = [view_args(self._canvas, fp, r0, rows, h.width, h.channels, pose,
+                               out[i], self._uncovered) for i, (r0, rows) in enumerate(self._eyes())]
+            self._view_cache[key] = views
+        else:
+            set_view_pose(views, pose)
         p = self._launch(frame, mode, mask, schedule, views=views, out_dims=tuple(out_dims))
         return DeviceFrame(self, p, self._canvas, self._footprint)
 

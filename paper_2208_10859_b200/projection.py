@@ -140,6 +140,18 @@ def view_args(canvas: torch.Tensor, footprint_bits: torch.Tensor, row0: int, row
     return v
 
 
+def set_view_pose(views: list, pose: CameraPose) -> None:
+    """Re-point cached K4 arguments at a new pose (one rotation for all views)."""
+    if not (pose.fov_h < 180 and pose.fov_v < 180):
+        raise ProjectionError("perspective rendering requires FOV < 180 degrees")
+    rot = pose.rotation().reshape(-1).tolist()
+    tan_h = math.tan(math.radians(pose.fov_h / 2.0))
+    tan_v = math.tan(math.radians(pose.fov_v / 2.0))
+    for v in views:
+        v.rot[:] = rot
+        v.tan_h, v.tan_v = tan_h, tan_v
+
+
 def launch_views(views: list, stream: torch.cuda.Stream | None = None) -> None:
     lib = N.load()
     arr = (N.ViewArgs * len(views))(*views)
