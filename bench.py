@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--pipeline", type=int, default=8,
                     help="decode sessions (streams) per GPU; frames round-robin so one "
                          "frame's writeout overlaps the next frame's decode")
+    ap.add_argument("--residency", choices=["set", "spans"], default="set",
+                    help="spans: only BlockEnd tables are uploaded; the GPU fetches the record "
+                         "spans of selected blocks from pinned host memory (load_blocks)")
     ap.add_argument("--profile-only", action="store_true",
                     help="a few decodes for ncu; prints nothing")
     return ap.parse_args()
@@ -213,7 +216,8 @@ def run_ours(args):
         dist.barrier()
 
     P = max(1, args.pipeline)
-    sessions = [wv.DecodeSession(path, device=dev, max_resident_sets=n_sets + 1) for _ in range(P)]
+    sessions = [wv.DecodeSession(path, device=dev, max_resident_sets=n_sets + 1,
+                                 residency=args.residency) for _ in range(P)]
     for s_ in sessions:
         s_.time_stages = False
     sess = sessions[0]
@@ -371,17 +375,21 @@ def run_ours(args):
         e_start.record(stream)
         for ss in sessions[1:]:
             ss.stream.wait_event(e_start)
+        fetched0 = sum(ss.bytes_fetched for ss in sessions)
         for i in range(args.steps):
             p_ = i % P
             ss = sessions[p_]
             f = frames[i % len(frames)]
             s = f // h.inter_size
+            # whole payload ("set") or BlockEnd table + spans fetched by the
+            # decode ("spans", counted after the run)
             ss.upload_set(s, pinned[s])
             step(i, ss, outs[p_])
             gather(ss, outs[p_])
             with torch.cuda.stream(ss.stream):
                 host_outs[p_].copy_(outs[p_], non_blocking=True)
-            bi += pinned[s].numel() + h.mask_w * h.mask_h
+            bi += (pinned[s].numel() if args.residency == "set" else h.table_bytes)
+            bi += h.mask_w * h.mask_h
             bo += host_outs[p_].numel()
         for ss in sessions[1:]:
             e = torch.cuda.Event()
@@ -392,6 +400,9 @@ def run_ours(args):
         te = torch.tensor([e_start.elapsed_time(e_end)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        for ss in sessions:
+            ss._settle_until(None)
+        bi += sum(ss.bytes_fetched for ss in sessions) - fetched0
         e2e = {"value": round(world * args.steps / (float(te.item()) / 1000.0), 2),
                "unit": "frames/s",
                "h2d_bytes_per_step": bi // args.steps, "d2h_bytes_per_step": bo // args.steps}
@@ -429,6 +440,7 @@ def run_ours(args):
                        "exceeds the 126 MB L2; serial_ms_per_frame: L2 flushed (256 MiB write) "
                        "before every step"),
                 "pipeline": f"{P} decode sessions (CUDA streams) per GPU, frames round-robin",
+                "residency": args.residency,
                 "parallelism": f"sets round-robin over {world} GPU(s), eye images gathered to rank 0",
             },
             "mpix_per_s": round(fps * out_px / 1e6, 1),

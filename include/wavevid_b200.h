@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define WV_ABI_VERSION 1
+#define WV_ABI_VERSION 2
 #define WV_MAX_LEVELS 12
 
 enum wv_status {
@@ -54,9 +54,14 @@ enum wv_mode { WV_MODE_FULL = 0, WV_MODE_VIEWPORT = 1, WV_MODE_FOVEATED = 2 };
 
 /* wv_frame_args.flags */
 enum wv_flags {
-  WV_FLAG_ACCOUNT_ONLY = 1   /* wv_select only: update the set's cache accounting
+  WV_FLAG_ACCOUNT_ONLY = 1,  /* wv_select only: update the set's cache accounting
                                 (DecodeSession.advance prefetch, decoding.py:335-354);
                                 no work lists, no footprint, dirty maps untouched */
+  WV_FLAG_FETCH = 2          /* span streaming (VideoReader.load_blocks, fileio.py:346-390):
+                                d_payload holds the BlockEnd table but records only for
+                                blocks whose d_fetched bit is set; the records of newly
+                                selected blocks are copied from h_payload (pinned host
+                                memory, read by the GPU over PCIe) before K2 runs */
 };
 
 /* device error word bits (wv_frame_result.error) */
@@ -82,6 +87,7 @@ typedef struct wv_frame_result {
   uint32_t n_selected;            /* blocks selected by the level masks */
   uint32_t error;                 /* WV_DERR_* bits */
   uint32_t n_tiles;               /* level-1 synthesis tiles computed */
+  unsigned long long fetched_bytes;/* WV_FLAG_FETCH: record bytes copied host -> HBM by this call */
 } wv_frame_result;
 
 typedef struct wv_frame_args {
@@ -103,6 +109,10 @@ typedef struct wv_frame_args {
                                      that touch or left the request are rewritten): zero it once and
                                      pass the same buffer to every call of one workspace */
   wv_frame_result* d_result;
+  const void* h_payload;          /* WV_FLAG_FETCH: the set payload in pinned host memory (UVA
+                                     pointer, same layout as d_payload) */
+  uint32_t* d_fetched;            /* WV_FLAG_FETCH: NB-bit bitmap, records of block b are in
+                                     d_payload; zero it when d_payload is (re)filled */
 } wv_frame_args;
 
 /* One perspective view (projection.py:111-172). */

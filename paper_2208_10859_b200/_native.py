@@ -13,7 +13,8 @@ LIB_PATH = os.path.join(HERE, "_wvb200.so")
 
 WV_OK, WV_ERR_ARG, WV_ERR_CUDA, WV_ERR_UNSUPPORTED = 0, 1, 2, 3
 WV_MODE_FULL, WV_MODE_VIEWPORT, WV_MODE_FOVEATED = 0, 1, 2
-WV_FLAG_ACCOUNT_ONLY = 1
+WV_FLAG_ACCOUNT_ONLY, WV_FLAG_FETCH = 1, 2
+WV_ABI_VERSION = 2
 WV_DERR_OFFSET, WV_DERR_TABLE = 1, 2
 WV_MAX_LEVELS = 12
 
@@ -33,7 +34,7 @@ class Geometry(C.Structure):
 class FrameResult(C.Structure):
     _fields_ = [("new_bytes", C.c_uint64), ("set_bytes", C.c_uint64), ("records", C.c_uint64),
                 ("n_missing", C.c_uint32), ("n_selected", C.c_uint32), ("error", C.c_uint32),
-                ("n_tiles", C.c_uint32)]
+                ("n_tiles", C.c_uint32), ("fetched_bytes", C.c_uint64)]
 
 
 class FrameArgs(C.Structure):
@@ -43,7 +44,8 @@ class FrameArgs(C.Structure):
                 ("d_payload", C.c_void_p), ("payload_bytes", C.c_uint64),
                 ("d_extrema", C.c_void_p), ("d_set_loaded", C.c_void_p),
                 ("d_set_bytes", C.c_void_p), ("d_canvas", C.c_void_p),
-                ("d_footprint", C.c_void_p), ("d_result", C.c_void_p)]
+                ("d_footprint", C.c_void_p), ("d_result", C.c_void_p),
+                ("h_payload", C.c_void_p), ("d_fetched", C.c_void_p)]
 
 
 class ViewArgs(C.Structure):
@@ -94,7 +96,7 @@ def load(path: str | None = None):
                                                C.c_int, C.c_void_p]
     for fn in EXPORTS[2:]:
         getattr(lib, fn).restype = C.c_int
-    if lib.wv_abi_version() != 1:
+    if lib.wv_abi_version() != WV_ABI_VERSION:
         raise NativeError("decode library ABI mismatch")
     _lib = lib
     return lib

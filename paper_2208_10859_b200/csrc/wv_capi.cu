@@ -19,6 +19,9 @@ int check(const wv_geometry* g, const wv_frame_args* a, Layout* lo) {
     return WV_ERR_ARG;
   if (reinterpret_cast<uintptr_t>(a->d_payload) & 15) return WV_ERR_ARG;
   if (a->mode != WV_MODE_FULL && !a->d_mask) return WV_ERR_ARG;
+  if ((a->flags & WV_FLAG_FETCH) &&
+      (!a->h_payload || !a->d_fetched || (reinterpret_cast<uintptr_t>(a->h_payload) & 15)))
+    return WV_ERR_ARG;
   return WV_OK;
 }
 

@@ -42,6 +42,7 @@ struct Layout {
   uint64_t sel, prev_sel;                // NB-bit bitmaps
   uint64_t blist;                        // NB u32 entries
   uint64_t bstate;                       // u8[NB]: plane block may hold nonzeros (K2)
+  uint64_t flist;                        // NB u32: blocks whose records are fetched (WV_FLAG_FETCH)
   int nty[WV_MAX_LEVELS + 1], ntx[WV_MAX_LEVELS + 1];  // tile grid of synthesis level k
   uint64_t need[WV_MAX_LEVELS + 1];      // u8 per tile
   uint64_t prev_need;                    // level 1, u8 per tile
@@ -55,7 +56,7 @@ struct Layout {
 };
 
 // counter slots
-enum { CNT_BLOCKS = 0, CNT_TILES = 1 /* + level */ };
+enum { CNT_BLOCKS = 0, CNT_TILES = 1 /* + level */, CNT_FETCH = 40 };
 
 inline int build_layout(const wv_geometry* g, Layout* o) {
   if (!g || !o) return WV_ERR_ARG;
@@ -90,6 +91,7 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
   o->prev_sel = take(uint64_t(wpr(o->NB)) * 4);
   o->blist = take(uint64_t(o->NB) * 4);
   o->bstate = take(uint64_t(o->NB));
+  o->flist = take(uint64_t(o->NB) * 4);
   for (int k = 1; k <= L; ++k) {
     o->nty[k] = cdiv(H >> k, TY);
     o->ntx[k] = cdiv(W >> k, TX);

@@ -347,6 +347,9 @@ struct BlockArgs {
   int account_only;
   int full;                                    // decode_full: every block selected
   const uint8_t* bstate;                       // K2's per-block "plane may be nonzero"
+  int fetch;                                   // WV_FLAG_FETCH: list blocks whose records are absent
+  uint32_t* flist;
+  uint32_t* fcount;
   const uint32_t* pooled[WV_MAX_LEVELS + 1];   // nullptr: scan rows
   int pool_wpr[WV_MAX_LEVELS + 1];
 };
@@ -459,6 +462,20 @@ __global__ void __launch_bounds__(256) k_blocks(BlockArgs a) {
     newb += __shfl_xor_sync(0xFFFFFFFFu, newb, o);
     err |= __shfl_xor_sync(0xFFFFFFFFu, err, o);
   }
+  if (a.fetch) {
+    // records of selected blocks not yet in HBM: list them for k_fetch
+    uint32_t fw = 0;
+    if (lane == 0 && (word << 5) < (uint32_t)a.NB) fw = a.fa->d_fetched[word];
+    fw = __shfl_sync(0xFFFFFFFFu, fw, 0);
+    const uint32_t need = selmask & ~fw;
+    uint32_t fb = 0;
+    if (lane == 0 && need) {
+      fb = atomicAdd(a.fcount, (uint32_t)__popc(need));
+      a.fa->d_fetched[word] = fw | need;
+    }
+    fb = __shfl_sync(0xFFFFFFFFu, fb, 0);
+    if ((need >> lane) & 1u) a.flist[fb + __popc(need & ((1u << lane) - 1u))] = (uint32_t)b;
+  }
   if (lane == 0 && (word << 5) < (uint32_t)a.NB) {
     a.sel[word] = selmask;
     if (!a.account_only) a.prev_sel[word] = selmask;
@@ -472,6 +489,40 @@ __global__ void __launch_bounds__(256) k_blocks(BlockArgs a) {
     if (selmask) atomicAdd(&res->n_selected, (uint32_t)__popc(selmask));
     if (err) atomicOr(&res->error, err);
   }
+}
+
+// --------------------------------------------------------------- span fetch
+// VideoReader.load_blocks (fileio.py:346-390) for one decode: copy the record
+// spans of the listed blocks, all temporal indices, from the set payload in
+// pinned host memory (read by the SMs over PCIe, UVA) to the same offsets of
+// the HBM payload.  One warp per (block, t) span; 16-byte chunks covering the
+// span (both payload buffers are padded to 16 bytes, and bytes outside the
+// span are the file's own bytes, so over-copying is harmless).
+__global__ void __launch_bounds__(256) k_fetch(const wv_frame_args* __restrict__ fa,
+                                               const uint32_t* __restrict__ flist,
+                                               const uint32_t* __restrict__ fcount, int n, int NB,
+                                               unsigned long long table_bytes) {
+  pdl_sync();
+  const uint32_t nspans = *fcount * (uint32_t)n;
+  const unsigned long long* __restrict__ ends = (const unsigned long long*)fa->d_payload;
+  const uint4* src = reinterpret_cast<const uint4*>(fa->h_payload);
+  uint4* dst = reinterpret_cast<uint4*>(const_cast<void*>(fa->d_payload));
+  const unsigned long long size = fa->payload_bytes;
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  unsigned long long copied = 0;
+  for (uint32_t sp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); sp < nspans; sp += warps) {
+    const uint32_t b = flist[sp / n];
+    const int t = (int)(sp % n);
+    const uint64_t fi = (uint64_t)t * NB + b;
+    const unsigned long long en = ends[fi], st = fi ? ends[fi - 1] : 0ull;
+    if (en <= st) continue;
+    const unsigned long long lo = table_bytes + st, hi = min(table_bytes + en, size);
+    if (lo >= hi) continue;   // (k_blocks flags inconsistent tables)
+    for (unsigned long long c = (lo >> 4) + lane; c < (hi + 15) >> 4; c += 32) dst[c] = src[c];
+    copied += hi - lo;
+  }
+  if (lane == 0 && copied) atomicAdd(&fa->d_result->fetched_bytes, copied);
 }
 
 // -------------------------------------------------------------- tile lists
@@ -653,12 +704,22 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     b.account_only = acct;
     b.full = full;
     b.bstate = ws + lo.bstate;
+    b.fetch = (flags & WV_FLAG_FETCH) != 0;
+    b.flist = (uint32_t*)(ws + lo.flist);
+    b.fcount = counters + CNT_FETCH;
     for (int k = 1; k <= L; ++k) {
       const bool ok = lo.bs == 32 && ((H >> k) % 32) == 0 && ((W >> k) % 32) == 0;
       b.pooled[k] = ok ? (const uint32_t*)(ws + lo.pooled[k]) : nullptr;
       b.pool_wpr[k] = cdiv(lo.wpr_[k], CT_W);
     }
     WV_CUDA(launch_k(k_blocks, dim3(cdiv(lo.NB, 256)), dim3(256), 0, s, b));
+    if (b.fetch) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      WV_CUDA(launch_k(k_fetch, dim3(4 * sms), dim3(256), 0, s, fa, (const uint32_t*)b.flist,
+                       (const uint32_t*)b.fcount, lo.n, lo.NB, b.table_bytes));
+    }
   }
   if (acct) {
     WV_CUDA(launch_k(k_finalize, dim3(1), dim3(1), 0, s, fa));

@@ -179,7 +179,15 @@ _MODES = {"full": N.WV_MODE_FULL, "viewport": N.WV_MODE_VIEWPORT, "foveated": N.
 class DecodeSession:
     """Single-owner decode session on one GPU stream with one-slot prefetch."""
 
-    def __init__(self, path, device=None, max_resident_sets: int = 4):
+    def __init__(self, path, device=None, max_resident_sets: int = 4, residency: str = "set"):
+        """``residency``: "set" uploads a set's whole payload to HBM when it is
+        first decoded; "spans" uploads only its BlockEnd table and, per decode,
+        the GPU copies the record spans of newly selected blocks from the set
+        payload in pinned host memory (VideoReader.load_blocks, fileio.py:346-390)."""
+        if residency not in ("set", "spans"):
+            raise ValueError(f"residency {residency!r} not in ('set', 'spans')")
+        self.residency = residency
+        self.bytes_fetched = 0         # spans residency: record bytes copied host -> HBM
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 decode path needs a CUDA device (no CPU fallback)")
         self._lib = N.load()
@@ -259,10 +267,12 @@ class DecodeSession:
     # -- set payloads -----------------------------------------------------------
 
     def _read_payload(self, set_index: int) -> torch.Tensor:
+        """The set payload in pinned host memory, zero-padded to 16 bytes (the
+        span fetch copies 16-byte chunks)."""
         n = self.reader.payload_length(set_index)
-        host = torch.empty(n, dtype=torch.uint8).pin_memory()
+        host = torch.zeros((n + 15) // 16 * 16, dtype=torch.uint8).pin_memory()
         with self._io_lock:
-            self.reader.read_set_payload(set_index, memoryview(host.numpy()))
+            self.reader.read_set_payload(set_index, memoryview(host.numpy()[:n]))
         return host
 
     def pinned_payload(self, set_index: int) -> torch.Tensor:
@@ -284,12 +294,23 @@ class DecodeSession:
             host = self._read_payload(set_index)
         meta = self.reader.set_meta[set_index]
         ext_host = torch.from_numpy(np.ascontiguousarray(meta.extrema, np.float32)).pin_memory()
+        fetched = None
         with torch.cuda.stream(self.stream):
             dev = torch.empty(host.numel(), dtype=torch.uint8, device=self.device)
-            dev.copy_(host, non_blocking=True)
+            if self.residency == "set":
+                dev.copy_(host, non_blocking=True)
+            else:
+                # BlockEnd table only; record bytes arrive per selected block.
+                # Unfetched bytes read as 0xFF (offset 65535: a decode reading
+                # them would report a corrupt stream).
+                tb = self.header.table_bytes
+                dev.fill_(0xFF)
+                dev[:tb].copy_(host[:tb], non_blocking=True)
+                fetched = torch.zeros(max(1, (self.header.num_blocks + 31) // 32),
+                                      dtype=torch.int32, device=self.device)
             ext = torch.empty(ext_host.shape, dtype=torch.float32, device=self.device)
             ext.copy_(ext_host, non_blocking=True)
-        self._resident[set_index] = (dev, ext, (host, ext_host))
+        self._resident[set_index] = (dev, ext, (host, ext_host, fetched))
         while len(self._resident) > self._max_resident:
             self._resident.popitem(last=False)
         return self._resident[set_index]
@@ -348,7 +369,8 @@ class DecodeSession:
                         args.fovea[k][q] = rect[q]
         return args
 
-    def _run_fast(self, slot: int, args: N.FrameArgs, mode: str, views=None, out_dims=None):
+    def _run_fast(self, slot: int, args: N.FrameArgs, mode: str, views=None, out_dims=None,
+                  flags: int = 0):
         """Per-frame inputs -> the workspace descriptor (one H2D from a pinned
         ring slot), then the fixed launch sequence of this mode -- replayed
         from a CUDA graph after its first direct run."""
@@ -358,7 +380,7 @@ class DecodeSession:
         for i in range(nv):
             C.memmove(host.data_ptr() + _FA_BYTES + i * _VA_BYTES, C.addressof(views[i]), _VA_BYTES)
         self._desc_dev.copy_(host, non_blocking=True)
-        key = (_MODES[mode], nv, tuple(out_dims) if nv else None)
+        key = (_MODES[mode], nv, tuple(out_dims) if nv else None, flags)
         g = self._graphs.get(key)
         if g is not None:
             g.replay()
@@ -366,7 +388,7 @@ class DecodeSession:
 
         def seq():
             N.check(self._lib.wv_decode_frame_desc(
-                C.byref(self._geom), key[0], 0, C.c_void_p(self._ws.data_ptr()),
+                C.byref(self._geom), key[0], flags, C.c_void_p(self._ws.data_ptr()),
                 C.c_void_p(torch.cuda.current_stream().cuda_stream)), "wv_decode_frame_desc")
             if nv:
                 # all eyes of a session share pose and region size (stereo pair)
@@ -400,13 +422,17 @@ class DecodeSession:
             ev0 = torch.cuda.Event(enable_timing=True) if time_stages else None
             if ev0 is not None:
                 ev0.record(s)
-            dev, ext, _ = self._make_resident(si)
+            dev, ext, keep = self._make_resident(si)
             args = self._mode_args(mode, mask, schedule, slot)
             entry, existed, may_evict = self._entry_for(si)
             args.t = t
             args.flags = N.WV_FLAG_ACCOUNT_ONLY if account_only else 0
+            if self.residency == "spans":
+                args.flags |= N.WV_FLAG_FETCH
+                args.h_payload = keep[0].data_ptr()
+                args.d_fetched = keep[2].data_ptr()
             args.d_payload = dev.data_ptr()
-            args.payload_bytes = dev.numel()
+            args.payload_bytes = self.reader.payload_length(si)
             args.d_extrema = ext.data_ptr()
             args.d_set_loaded = entry.loaded.data_ptr()
             args.d_set_bytes = entry.nbytes.data_ptr()
@@ -444,7 +470,7 @@ class DecodeSession:
                 N.check(self._lib.wv_synthesize(g, C.byref(args), ws, cs), "wv_synthesize")
                 evs[2].record(s)
             else:
-                self._run_fast(slot, args, mode, views, out_dims)
+                self._run_fast(slot, args, mode, views, out_dims, args.flags)
             self._results_host[slot].copy_(self._results[slot], non_blocking=True)
             done = torch.cuda.Event()
             done.record(s)
@@ -475,6 +501,7 @@ class DecodeSession:
                 st.synthesis_ms = evs[1].elapsed_time(evs[2])
             p.stats = st
             p.raw = r
+            self.bytes_fetched += int(r.fetched_bytes)
             if not p.account_only:
                 self._stats.bytes_loaded += st.bytes_loaded
                 self._stats.records_processed += st.records_processed

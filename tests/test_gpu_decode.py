@@ -446,3 +446,46 @@ def test_8k_viewport_and_foveated_equal_full_inside_footprint(wv, tmp_path):
             except wo.Uncovered as u:
                 want += u.args[0]
         assert got == want
+
+
+def test_span_streaming_residency(wv, tmp_path):
+    """residency="spans" (VideoReader.load_blocks, fileio.py:346-390): only the
+    BlockEnd table is uploaded per set and the GPU copies the record spans of
+    newly selected blocks from pinned host memory.  Results and statistics
+    equal the whole-set residency call by call; a block's spans are copied
+    once; unfetched HBM bytes are 0xFF, so reading one would fail loudly."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(9)
+    clip = torch.randint(0, 256, (8, 1024, 1024, 3), dtype=torch.uint8, device="cuda", generator=g)
+    path = tmp_path / "sp.wvv"
+    wv.write_video(wv.encode_video(clip, wv.EncodeParams(stereo=True, levels=4, mask_w=128,
+                                                         mask_h=128), device="cuda"), path)
+    rng = np.random.default_rng(3)
+    a = wv.DecodeSession(path)
+    b = wv.DecodeSession(path, residency="spans")
+    h = a.header
+    total_records = sum(m.payload_length - h.table_bytes for m in a.reader.set_meta)
+    for _ in range(12):
+        frame, mode, mask, sc, pose = _random_call(rng, h, wv)
+        pa, fa, sa = _decode(a, frame, mode, mask, sc)
+        before = b.bytes_fetched
+        pb, fb, sb = _decode(b, frame, mode, mask, sc)
+        np.testing.assert_array_equal(pb, pa, err_msg=f"{frame} {mode}")
+        np.testing.assert_array_equal(fb, fa)
+        assert (sb.bytes_loaded, sb.records_processed) == (sa.bytes_loaded, sa.records_processed)
+        assert b.bytes_fetched - before <= total_records
+        # the same request again: everything is already in HBM
+        again = b.bytes_fetched
+        _decode(b, frame, mode, mask, sc)
+        assert b.bytes_fetched == again
+    assert 0 < b.bytes_fetched <= total_records
+    # device path (graph replay with the fetch step)
+    out_a = torch.empty((2, 256, 256, 3), dtype=torch.uint8, device="cuda")
+    out_b = torch.empty_like(out_a)
+    for _ in range(4):
+        frame, mode, mask, sc, pose = _random_call(rng, h, wv)
+        mode = "viewport" if mode == "full" else mode
+        s_ = sc if mode == "foveated" else None
+        a.decode_render_device(frame, mode, mask, pose, (256, 256), out_a, schedule=s_).result()
+        b.decode_render_device(frame, mode, mask, pose, (256, 256), out_b, schedule=s_).result()
+        assert torch.equal(out_a, out_b)

@@ -39,7 +39,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_abi_host_functions(lib):
     from paper_2208_10859_b200 import _native as N
-    assert lib.wv_abi_version() == 1
+    assert lib.wv_abi_version() == 2
     assert lib.wv_status_string(0) == b"ok"
     g = N.Geometry(8192, 8192, 3, 6, 4, 32, 0, 256, 256)
     b = C.c_uint64()
@@ -56,7 +56,8 @@ def test_abi_host_functions(lib):
 def test_struct_layouts_match_header():
     from paper_2208_10859_b200 import _native as N
     assert C.sizeof(N.Geometry) == 36
-    assert C.sizeof(N.FrameResult) == 40
+    assert C.sizeof(N.FrameResult) == 48
+    assert N.FrameArgs.h_payload.offset == N.FrameArgs.d_result.offset + 8
     assert N.FrameArgs.d_mask.offset == 16
     assert N.FrameArgs.d_payload.offset == 16 + 8 + 12 * 4 * 4
 
