@@ -47,7 +47,9 @@ enum wv_status {
   WV_OK = 0,
   WV_ERR_ARG = 1,          /* invalid geometry / argument */
   WV_ERR_CUDA = 2,         /* a CUDA runtime call or launch failed */
-  WV_ERR_UNSUPPORTED = 3   /* geometry outside what the kernels handle */
+  WV_ERR_UNSUPPORTED = 3,  /* geometry outside what the kernels handle */
+  WV_ERR_FORMAT = 4,       /* malformed or unsupported .wvv data (FormatError, fileio.py:34) */
+  WV_ERR_IO = 5            /* file missing / truncated read */
 };
 
 enum wv_mode { WV_MODE_FULL = 0, WV_MODE_VIEWPORT = 1, WV_MODE_FOVEATED = 2 };
@@ -161,6 +163,32 @@ int wv_decode_frame_desc(const wv_geometry* g, int mode, int flags, void* d_work
  * computed once per output pixel and applied to every view. */
 int wv_render_perspective_desc(const wv_view_args* d_views, int n_views, int max_out_w,
                                int max_out_h, int shared_geometry, void* stream);
+
+/* ---- .wvv container reader (fileio.py:28-193, read_header :240-261) ----
+ * Host-only, stateless (each call opens, reads and closes the file), no
+ * allocation: a C-ABI consumer (e.g. a native player) gets the decode
+ * geometry, the set directory and set payloads without Python. */
+typedef struct wv_file_info {
+  wv_geometry geom;               /* decode geometry of the header */
+  int32_t frame_count, pad_frames, num_sets, stereo;
+  float fps;
+  uint32_t version;
+  uint64_t table_bytes;           /* BlockEnd table bytes per set: inter_size * num_blocks * 8 */
+} wv_file_info;
+
+typedef struct wv_set_info {
+  uint64_t payload_offset, payload_length, record_count;
+} wv_set_info;
+
+/* Parse and validate the 64-byte header and the SetMeta directory. */
+int wv_file_info_read(const char* path, wv_file_info* info);
+/* Directory entry of one set; its extrema (inter_size, C, 4) f32 into
+ * `extrema` when not NULL (fileio.py:118-138). */
+int wv_file_set_read(const char* path, int set_index, wv_set_info* set, float* extrema);
+/* One set's payload (BlockEnd table + packed records) into `buf`
+ * (>= payload_length bytes; pinned host memory serves both a whole-set
+ * upload and WV_FLAG_FETCH's h_payload). */
+int wv_file_payload_read(const char* path, int set_index, void* buf, uint64_t buf_bytes);
 
 /* Views into the workspace for parity tests (no launches). */
 int wv_plane_view(const wv_geometry* g, void* d_workspace, float** d_plane);

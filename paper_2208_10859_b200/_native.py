@@ -11,7 +11,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_wvb200.so")
 
-WV_OK, WV_ERR_ARG, WV_ERR_CUDA, WV_ERR_UNSUPPORTED = 0, 1, 2, 3
+WV_OK, WV_ERR_ARG, WV_ERR_CUDA, WV_ERR_UNSUPPORTED, WV_ERR_FORMAT, WV_ERR_IO = 0, 1, 2, 3, 4, 5
 WV_MODE_FULL, WV_MODE_VIEWPORT, WV_MODE_FOVEATED = 0, 1, 2
 WV_FLAG_ACCOUNT_ONLY, WV_FLAG_FETCH = 1, 2
 WV_ABI_VERSION = 2
@@ -23,12 +23,24 @@ EXPORTS = ["wv_abi_version", "wv_status_string", "wv_workspace_bytes", "wv_works
            "wv_synthesize_level",
            "wv_render_perspective", "wv_plane_view", "wv_level_mask_view",
            "wv_block_list_view", "wv_desc_view", "wv_decode_frame_desc",
-           "wv_render_perspective_desc"]
+           "wv_render_perspective_desc", "wv_file_info_read", "wv_file_set_read",
+           "wv_file_payload_read"]
 
 
 class Geometry(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("width", "height", "channels", "levels", "inter_size",
                                          "block_size", "float_mode", "mask_w", "mask_h")]
+
+
+class FileInfo(C.Structure):
+    _fields_ = [("geom", Geometry), ("frame_count", C.c_int32), ("pad_frames", C.c_int32),
+                ("num_sets", C.c_int32), ("stereo", C.c_int32), ("fps", C.c_float),
+                ("version", C.c_uint32), ("table_bytes", C.c_uint64)]
+
+
+class SetInfo(C.Structure):
+    _fields_ = [("payload_offset", C.c_uint64), ("payload_length", C.c_uint64),
+                ("record_count", C.c_uint64)]
 
 
 class FrameResult(C.Structure):
@@ -94,6 +106,9 @@ def load(path: str | None = None):
     lib.wv_decode_frame_desc.argtypes = [G, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
     lib.wv_render_perspective_desc.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int,
                                                C.c_int, C.c_void_p]
+    lib.wv_file_info_read.argtypes = [C.c_char_p, C.POINTER(FileInfo)]
+    lib.wv_file_set_read.argtypes = [C.c_char_p, C.c_int, C.POINTER(SetInfo), C.c_void_p]
+    lib.wv_file_payload_read.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_uint64]
     for fn in EXPORTS[2:]:
         getattr(lib, fn).restype = C.c_int
     if lib.wv_abi_version() != WV_ABI_VERSION:

@@ -16,7 +16,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["wv_select.cu", "wv_temporal.cu", "wv_idwt.cu", "wv_perspective.cu", "wv_capi.cu"]
+SOURCES = ["wv_select.cu", "wv_temporal.cu", "wv_idwt.cu", "wv_perspective.cu", "wv_capi.cu",
+           "wv_file.cpp"]
 HEADERS = ["wv_common.cuh"]
 LIB = os.path.join(HERE, "_wvb200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -53,7 +54,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for f in SOURCES:
-        obj = os.path.join(objdir, f.replace(".cu", ".o"))
+        obj = os.path.join(objdir, f.rsplit(".", 1)[0] + ".o")
         cmd = [nvcc(), *ARCH, *FLAGS, f"--fmad={FMAD.get(f, 'false')}", "-I",
                os.path.join(ROOT, "include"), *[f"-D{d}" for d in defines], "-c", "-o", obj,
                os.path.join(CSRC, f)]

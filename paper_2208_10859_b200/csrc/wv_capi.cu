@@ -37,6 +37,8 @@ const char* wv_status_string(int status) {
     case WV_ERR_ARG: return "invalid argument";
     case WV_ERR_CUDA: return "CUDA error";
     case WV_ERR_UNSUPPORTED: return "unsupported geometry";
+    case WV_ERR_FORMAT: return "malformed or unsupported .wvv data";
+    case WV_ERR_IO: return "file missing or truncated";
     default: return "unknown status";
   }
 }

@@ -227,3 +227,80 @@ def test_lifting_kernels_have_no_fused_multiply_add(lib):
             bad.append((fn, line.strip()[:60]))
     assert "k_level" in sass and not bad, bad[:3]
     assert "UTMALDG" in sass      # the synthesis tiles are TMA-fed
+
+
+# ------------------------------------------------ C++ .wvv reader (§8f row 3)
+
+@pytest.mark.parametrize("name", ["golden_quantized.wvv", "golden_float.wvv", "golden_stereo.wvv",
+                                  "smooth_hq.wvv", "smooth_lossless.wvv", "noise_bs16.wvv",
+                                  "smooth_n8.wvv", "smooth_n1_mono.wvv", "wide_equirect.wvv"])
+def test_native_reader_matches_python_reader(lib, name):
+    """wv_file_* (C++) parse every fixture exactly like fileio.VideoReader."""
+    from paper_2208_10859_b200 import _native as N
+    from paper_2208_10859_b200.fileio import VideoReader
+    path = os.path.join(GOLDEN, name).encode()
+    info = N.FileInfo()
+    assert lib.wv_file_info_read(path, C.byref(info)) == 0
+    with VideoReader(os.path.join(GOLDEN, name)) as r:
+        h = r.header
+        g = info.geom
+        assert (g.width, g.height, g.channels, g.levels, g.inter_size, g.block_size,
+                g.float_mode, g.mask_w, g.mask_h) == (h.width, h.height, h.channels, h.levels,
+                                                     h.inter_size, h.block_size, int(h.float_mode),
+                                                     h.mask_w, h.mask_h)
+        assert (info.frame_count, info.pad_frames, info.num_sets, bool(info.stereo)) == \
+            (h.frame_count, h.pad_frames, h.num_sets, h.stereo)
+        assert np.float32(info.fps) == np.float32(h.fps) and info.table_bytes == h.table_bytes
+        for si, m in enumerate(r.set_meta):
+            si_info = N.SetInfo()
+            ext = np.zeros((h.inter_size, h.channels, 4), np.float32)
+            assert lib.wv_file_set_read(path, si, C.byref(si_info), ext.ctypes.data) == 0
+            assert (si_info.payload_offset, si_info.payload_length, si_info.record_count) == \
+                (m.payload_offset, m.payload_length, m.record_count)
+            np.testing.assert_array_equal(ext, m.extrema)
+            buf = np.zeros(m.payload_length, np.uint8)
+            assert lib.wv_file_payload_read(path, si, buf.ctypes.data, buf.size) == 0
+            assert bytes(buf) == bytes(r.read_set_payload(si))
+            assert lib.wv_file_payload_read(path, si, buf.ctypes.data, buf.size - 1) == N.WV_ERR_ARG
+        assert lib.wv_file_set_read(path, h.num_sets, C.byref(N.SetInfo()), None) == N.WV_ERR_ARG
+
+
+def test_native_reader_rejects_malformed(lib, tmp_path):
+    """fileio.py:34 FormatError cases: bad magic, bad version, truncation,
+    non-contiguous payloads; missing file -> WV_ERR_IO."""
+    from paper_2208_10859_b200 import _native as N
+    raw = bytearray(open(os.path.join(GOLDEN, "smooth_n8.wvv"), "rb").read())
+    info = N.FileInfo()
+    cases = {
+        "magic": (lambda b: b.__setitem__(slice(0, 4), b"XXXX"), N.WV_ERR_FORMAT),
+        "version": (lambda b: b.__setitem__(slice(4, 6), (7).to_bytes(2, "little")), N.WV_ERR_FORMAT),
+        "truncated": (lambda b: b.__delitem__(slice(70, None)), N.WV_ERR_IO),
+        # second SetMeta entry (n 8, C 3: 408 bytes each) -> payload_offset moved
+        "contiguity": (lambda b: b.__setitem__(slice(64 + 408, 64 + 416),
+                                               (12345).to_bytes(8, "little")), N.WV_ERR_FORMAT),
+    }
+    for what, (mutate, want) in cases.items():
+        b = bytearray(raw)
+        mutate(b)
+        p = tmp_path / f"{what}.wvv"
+        p.write_bytes(bytes(b))
+        assert lib.wv_file_info_read(str(p).encode(), C.byref(info)) == want, what
+    assert lib.wv_file_info_read(str(tmp_path / "none.wvv").encode(), C.byref(info)) == N.WV_ERR_IO
+
+
+def test_c_only_consumer_builds_and_reads(lib, tmp_path):
+    """examples/c_consumer.c: a plain-C program linked against the library
+    reads a .wvv through the C ABI (no Python, no torch)."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    from paper_2208_10859_b200 import _native
+    exe = tmp_path / "c_consumer"
+    libdir = os.path.dirname(_native.LIB_PATH)
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "c_consumer.c"), "-L", libdir, "-l:_wvb200.so",
+                    f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), os.path.join(GOLDEN, "smooth_n8.wvv")], capture_output=True,
+                         text=True, check=True).stdout
+    assert "64x64 C3 L2 n8 bs32 frames 10 sets 2" in out and "set 1:" in out
