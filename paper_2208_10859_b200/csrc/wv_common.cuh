@@ -113,6 +113,20 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
   return WV_OK;
 }
 
+// Debug builds (-DWV_CHECK=1, e.g. build.build(defines=["WV_CHECK=1"], ...)
+// + WV_LIB) trap on out-of-range shared-memory indices in K3/K4; release
+// builds compile the checks away.
+#if defined(WV_CHECK) && WV_CHECK
+#define WV_ASSERT(c)                 \
+  do {                               \
+    if (!(c)) __trap();              \
+  } while (0)
+#else
+#define WV_ASSERT(c) \
+  do {               \
+  } while (0)
+#endif
+
 // Programmatic dependent launch (WV_PDL=1): kernels of the decode sequence
 // are launched with programmatic stream serialization; each first waits for
 // its predecessor grid (griddepcontrol.wait: completion + memory visibility)

@@ -337,10 +337,12 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
           lift_interior<SEGLEN_C>(
               [&](int j, float2& s, float2& d) {
                 const int o = (rb + j) * BOX_W + lc;
+                WV_ASSERT(o >= 0 && o < BOX_FLOATS);
                 s = make_float2(bLL[o], bHL[o]);
                 d = make_float2(bLH[o], bHH[o]);
               },
               [&](int p, float2 s3, float2 d3) {
+                WV_ASSERT(qb + p >= 0 && qb + p < TY && lc < CB_PITCH);
                 colL[(qb + p) * CB_PITCH + lc] = make_float2(s3.x, d3.x);
                 colH[(qb + p) * CB_PITCH + lc] = make_float2(s3.y, d3.y);
               });
@@ -349,11 +351,13 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
               max(pa - HALO, 0), min(pb + HALO, a.bh), a.bh, pa, pb,
               [&](int j, float2& s, float2& d) {
                 const int o = (j - oy) * BOX_W + lc;
+                WV_ASSERT(o >= 0 && o < BOX_FLOATS);
                 s = make_float2(bLL[o], bHL[o]);
                 d = make_float2(bLH[o], bHH[o]);
               },
               [&](int p, float2 s3, float2 d3) {
                 const int q = p - ay;
+                WV_ASSERT(q >= 0 && q < TY && lc < CB_PITCH);
                 colL[q * CB_PITCH + lc] = make_float2(s3.x, d3.x);
                 colH[q * CB_PITCH + lc] = make_float2(s3.y, d3.y);
               });
@@ -378,6 +382,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         // (decoding.py:301; rint is round-half-even like __float2uint_rn,
         // which also saturates below 0) straight into the u8 tile
         auto emit_out = [&](int q, float2 s3, float2 d3) {
+          WV_ASSERT(q >= 0 && q < TX && i < TY);
           if (!FINAL) {
             outb[i * OB_PITCH + 2 * q] = s3;
             outb[i * OB_PITCH + 2 * q + 1] = d3;
@@ -393,6 +398,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
           const int cb = pa - HALO - ox, qb = pa - HALO - ax;
           lift_interior<SEGLEN_R>(
               [&](int j, float2& s, float2& d) {
+                WV_ASSERT(cb + j >= 0 && cb + j < CB_PITCH);
                 s = colL[i * CB_PITCH + cb + j];
                 d = colH[i * CB_PITCH + cb + j];
               },
@@ -401,6 +407,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
           lift_line(
               max(pa - HALO, 0), min(pb + HALO, a.bw), a.bw, pa, pb,
               [&](int j, float2& s, float2& d) {
+                WV_ASSERT(j - ox >= 0 && j - ox < CB_PITCH);
                 s = colL[i * CB_PITCH + (j - ox)];
                 d = colH[i * CB_PITCH + (j - ox)];
               },

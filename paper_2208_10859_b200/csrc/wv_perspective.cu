@@ -205,6 +205,7 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
         const uint32_t A = C > 3 ? __ldg(reinterpret_cast<const uint32_t*>(src + 3 * plane)) : 0u;
         const uint32_t rg_lo = __byte_perm(R, G, 0x5140), rg_hi = __byte_perm(R, G, 0x7362);
         const uint32_t ba_lo = __byte_perm(B, A, 0x5140), ba_hi = __byte_perm(B, A, 0x7362);
+        WV_ASSERT(r < WIN_H && 4 * q + 3 < WIN_W);
         *reinterpret_cast<uint4*>(dst + r * WIN_W) =
             make_uint4(__byte_perm(rg_lo, ba_lo, 0x5410), __byte_perm(rg_lo, ba_lo, 0x7632),
                        __byte_perm(rg_hi, ba_hi, 0x5410), __byte_perm(rg_hi, ba_hi, 0x7632));
@@ -219,6 +220,8 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
       ((int)blockIdx.y + 1) * K4_TY <= out_h) {
 #pragma unroll
     for (int k = 0; k < K4_PPT; ++k) {
+      WV_ASSERT(y0[k] - yl >= 0 && y0[k] + 1 - yl < WIN_H && x0[k] - wx0 >= 0 &&
+                x0[k] + 1 - wx0 < WIN_W);
       const uint32_t* p = win + (y0[k] - yl) * WIN_W + (x0[k] - wx0);
       const uint32_t w00 = p[0], w01 = p[1], w10 = p[WIN_W], w11 = p[WIN_W + 1];
       uint8_t* o = ost + (threadIdx.y + 8 * k) * OST_PITCH + threadIdx.x * C;
@@ -268,6 +271,8 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
       }
       uint32_t w00, w01, w10, w11;
       if (use_win) {
+        WV_ASSERT(ty0 - yl >= 0 && ty0 + 1 - yl < WIN_H && tx0 - wx0 >= 0 &&
+                  tx0 + 1 - wx0 < WIN_W);
         const uint32_t* p = win + (ty0 - yl) * WIN_W + (tx0 - wx0);
         w00 = p[0];
         w01 = p[1];

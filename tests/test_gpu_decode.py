@@ -489,3 +489,22 @@ def test_span_streaming_residency(wv, tmp_path):
         a.decode_render_device(frame, mode, mask, pose, (256, 256), out_a, schedule=s_).result()
         b.decode_render_device(frame, mode, mask, pose, (256, 256), out_b, schedule=s_).result()
         assert torch.equal(out_a, out_b)
+
+
+def test_bounds_checked_build_runs_clean(wv):
+    """Debug build with shared-memory index checks (WV_CHECK=1: K3 box /
+    column / output tiles, K4 window) runs every mode, the render path and
+    span streaming on the golden files without trapping."""
+    import subprocess
+    import sys
+    from paper_2208_10859_b200 import build
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2208_10859_b200", "variants", "checked.so")
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    if build._stale(lib):
+        build.build(defines=["WV_CHECK=1"], out=lib)
+    env = dict(os.environ, WV_LIB=lib)
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "sanitize.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.count(" ok") == 4
