@@ -158,6 +158,28 @@ int wv_render_perspective(const wv_view_args* views, int n_views, void* stream);
 int wv_desc_view(const wv_geometry* g, void* d_workspace, void** d_desc);
 int wv_decode_frame_desc(const wv_geometry* g, int mode, int flags, void* d_workspace,
                          void* stream);
+/* Stages of one decode (bit mask) for callers that overlap independent
+ * stages on several streams (e.g. inside a CUDA graph).  Dependencies:
+ * CASCADES, TILES <- ROWS; FOOTPRINT, BLOCKS <- CASCADES; DEQUANT <- BLOCKS;
+ * SYNTH <- DEQUANT, TILES; FOOTPRINT_TILES <- FOOTPRINT, TILES.  The
+ * footprint (only the writeout needs it) and the tile lists can therefore run
+ * beside block selection -> K2.  wv_decode_frame_desc runs all stages in
+ * order. */
+enum wv_stage {
+  WV_STAGE_ROWS = 1,              /* distinct request-mask rows, row map, counters (K1) */
+  WV_STAGE_CASCADES = 2,          /* level-mask cascades (K1) */
+  WV_STAGE_FOOTPRINT = 4,         /* footprint cascade levels L..2 (K1) */
+  WV_STAGE_BLOCKS = 8,            /* block selection + accounting, span fetch (K1) */
+  WV_STAGE_TILES = 16,            /* synthesis tile lists (K1) */
+  WV_STAGE_FOOTPRINT_TILES = 32,  /* finest footprint on the level-1 tiles (K1) */
+  WV_STAGE_DEQUANT = 64,          /* K2 */
+  WV_STAGE_SYNTH = 128,           /* K3, all levels */
+  WV_STAGE_SELECT = 63,
+  WV_STAGE_ALL = 255
+};
+int wv_decode_stages_desc(const wv_geometry* g, int mode, int flags, int stages,
+                          void* d_workspace, void* stream);
+
 /* shared_geometry != 0: all views share pose, FOV, region size and output
  * size (a stereo pair rendered with one head pose) -- the ray geometry is
  * computed once per output pixel and applied to every view. */

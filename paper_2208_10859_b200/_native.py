@@ -15,6 +15,8 @@ WV_OK, WV_ERR_ARG, WV_ERR_CUDA, WV_ERR_UNSUPPORTED, WV_ERR_FORMAT, WV_ERR_IO = 0
 WV_MODE_FULL, WV_MODE_VIEWPORT, WV_MODE_FOVEATED = 0, 1, 2
 WV_FLAG_ACCOUNT_ONLY, WV_FLAG_FETCH = 1, 2
 WV_ABI_VERSION = 2
+(WV_STAGE_ROWS, WV_STAGE_CASCADES, WV_STAGE_FOOTPRINT, WV_STAGE_BLOCKS, WV_STAGE_TILES,
+ WV_STAGE_FOOTPRINT_TILES, WV_STAGE_DEQUANT, WV_STAGE_SYNTH) = 1, 2, 4, 8, 16, 32, 64, 128
 WV_DERR_OFFSET, WV_DERR_TABLE = 1, 2
 WV_MAX_LEVELS = 12
 
@@ -24,7 +26,7 @@ EXPORTS = ["wv_abi_version", "wv_status_string", "wv_workspace_bytes", "wv_works
            "wv_render_perspective", "wv_plane_view", "wv_level_mask_view",
            "wv_block_list_view", "wv_desc_view", "wv_decode_frame_desc",
            "wv_render_perspective_desc", "wv_file_info_read", "wv_file_set_read",
-           "wv_file_payload_read"]
+           "wv_file_payload_read", "wv_decode_stages_desc"]
 
 
 class Geometry(C.Structure):
@@ -106,6 +108,7 @@ def load(path: str | None = None):
     lib.wv_decode_frame_desc.argtypes = [G, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
     lib.wv_render_perspective_desc.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int,
                                                C.c_int, C.c_void_p]
+    lib.wv_decode_stages_desc.argtypes = [G, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
     lib.wv_file_info_read.argtypes = [C.c_char_p, C.POINTER(FileInfo)]
     lib.wv_file_set_read.argtypes = [C.c_char_p, C.c_int, C.POINTER(SetInfo), C.c_void_p]
     lib.wv_file_payload_read.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_uint64]

@@ -143,6 +143,27 @@ int wv_decode_frame_desc(const wv_geometry* g, int mode, int flags, void* ws, vo
   return launch_synthesis(lo, g, d, (uint8_t*)ws, s);
 }
 
+int wv_decode_stages_desc(const wv_geometry* g, int mode, int flags, int stages, void* ws,
+                          void* stream) {
+  Layout lo;
+  int st = build_layout(g, &lo);
+  if (st != WV_OK) return st;
+  if (!ws || mode < WV_MODE_FULL || mode > WV_MODE_FOVEATED || (stages & ~WV_STAGE_ALL))
+    return WV_ERR_ARG;
+  const wv_frame_args* d = (const wv_frame_args*)((uint8_t*)ws + lo.desc);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (stages & WV_STAGE_SELECT)
+    if ((st = launch_select(lo, g, mode, flags, d, (uint8_t*)ws, s, stages & WV_STAGE_SELECT)) !=
+        WV_OK)
+      return st;
+  if (flags & WV_FLAG_ACCOUNT_ONLY) return WV_OK;
+  if ((stages & WV_STAGE_DEQUANT) &&
+      (st = launch_temporal(lo, g, mode, d, (uint8_t*)ws, s)) != WV_OK)
+    return st;
+  if (stages & WV_STAGE_SYNTH) return launch_synthesis(lo, g, d, (uint8_t*)ws, s);
+  return WV_OK;
+}
+
 int wv_render_perspective_desc(const wv_view_args* d_views, int n_views, int max_out_w,
                                int max_out_h, int shared_geometry, void* stream) {
   return launch_perspective_dev(d_views, n_views, max_out_w, max_out_h, shared_geometry,

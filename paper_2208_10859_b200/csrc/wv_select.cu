@@ -578,7 +578,6 @@ __global__ void __launch_bounds__(256) k_tiles1(TileArgs a) {
   base = __shfl_sync(0xFFFFFFFFu, base, 0);
   if (emit) a.list[1][base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)t | (nd ? 0u : ZERO_FLAG);
   if (lane == 0 && mn) atomicAdd(&a.fa->d_result->n_tiles, (uint32_t)__popc(mn));
-  if (t == 0) a.fa->d_result->set_bytes = *a.fa->d_set_bytes;
 }
 
 // Coarser levels in one CTA: need maps live as bit rows in shared memory and
@@ -635,7 +634,7 @@ __global__ void k_finalize(const wv_frame_args* fa) {
 }  // namespace
 
 int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
-                  const wv_frame_args* fa, uint8_t* ws, cudaStream_t s) {
+                  const wv_frame_args* fa, uint8_t* ws, cudaStream_t s, int stages) {
   const int L = lo.L, H = lo.H, W = lo.W;
   const bool full = mode == WV_MODE_FULL;
   const bool fov = mode == WV_MODE_FOVEATED;
@@ -643,14 +642,17 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
   uint32_t* R = (uint32_t*)(ws + lo.mrows);
   uint32_t* rowmap = (uint32_t*)(ws + lo.rowmap);
   uint32_t* counters = (uint32_t*)(ws + lo.counters);
-  {
+  const bool st_rows = stages & WV_STAGE_ROWS, st_cas = stages & WV_STAGE_CASCADES;
+  const bool st_fp = stages & WV_STAGE_FOOTPRINT, st_blocks = stages & WV_STAGE_BLOCKS;
+  const bool st_tiles = stages & WV_STAGE_TILES, st_fpt = stages & WV_STAGE_FOOTPRINT_TILES;
+  if (st_rows) {
     const int n = max(lo.mh * lo.wpr_[0], H);
     WV_CUDA(launch_k(k_mask_rows, dim3(cdiv(n, 256)), dim3(256), 0, s, fa, R, rowmap, counters,
                      lo.mh, lo.mw, W, H, lo.wpr_[0], (int)full));
   }
   // level cascades (batch 0: request closure; batches k>=j: gaze windows);
   // a full-frame decode needs none of them
-  for (int j = 1; j <= L && !full; ++j) {
+  for (int j = 1; j <= L && !full && st_cas; ++j) {
     CascadeArgs c{};
     c.j = j; c.L = L; c.H = H;
     c.rows = H >> j; c.cols = W >> j; c.wpr = lo.wpr_[j];
@@ -675,10 +677,10 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     return (uint32_t*)(ws + lo.stack[k] + (fov ? (uint64_t)k * lo.stack_stride[k] : 0));
   };
   // footprint: V_L = ones; V_{j-1} = shrink(up(V_j & D_j)); last & request
-  if (full && !acct)
+  if (full && !acct && st_fp)
     WV_CUDA(launch_k(k_fill_footprint, dim3(cdiv(H * lo.wpr_[0], 256)), dim3(256), 0, s, fa, H, W,
                      lo.wpr_[0]));
-  for (int j = L; j >= 2 && !acct && !full; --j) {
+  for (int j = L; j >= 2 && !acct && !full && st_fp; --j) {
     FootArgs f{};
     f.j = j; f.L = L; f.H = H;
     f.rows = H >> (j - 1); f.cols = W >> (j - 1); f.wpr = lo.wpr_[j - 1];
@@ -690,7 +692,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     dim3 grid(cdiv(f.wpr, CT_W), 1, cdiv(f.rows, CT_R));
     WV_CUDA(launch_k(k_footprint, dim3(grid), dim3(256), 0, s, f));
   }
-  {
+  if (st_blocks) {
     BlockArgs b{};
     b.L = L; b.H = H; b.W = W; b.bs = lo.bs; b.nbx = lo.nbx; b.NB = lo.NB; b.n = lo.n;
     b.rs = 2 + lo.C * (g->float_mode ? 4 : 1);
@@ -721,9 +723,9 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
                        (const uint32_t*)b.fcount, lo.n, lo.NB, b.table_bytes));
     }
   }
-  if (acct) {
+  if (acct && st_blocks) {
     WV_CUDA(launch_k(k_finalize, dim3(1), dim3(1), 0, s, fa));
-  } else {
+  } else if (!acct) {
     TileArgs t{};
     t.L = L; t.H = H; t.W = W; t.wpr0 = lo.wpr_[0]; t.R = R; t.rowmap = rowmap; t.full = full;
     for (int k = 1; k <= L; ++k) {
@@ -736,8 +738,8 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     t.counters = counters;
     t.fa = fa;
     const int nt1 = lo.nty[1] * lo.ntx[1];
-    WV_CUDA(launch_k(k_tiles1, dim3(cdiv(nt1, 256)), dim3(256), 0, s, t));
-    if (!full) {
+    if (st_tiles) WV_CUDA(launch_k(k_tiles1, dim3(cdiv(nt1, 256)), dim3(256), 0, s, t));
+    if (!full && st_fpt) {
       // finest footprint step on the level-1 tiles only (zero elsewhere)
       FootArgs f{};
       f.j = 1; f.L = L; f.H = H;
@@ -753,7 +755,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
                        (const uint32_t*)t.list[1], (const uint32_t*)(counters + CNT_TILES + 1),
                        lo.ntx[1]));
     }
-    if (L >= 2) {
+    if (L >= 2 && st_tiles) {
       size_t words = 0;
       for (int k = 1; k <= L; ++k) words += (size_t)lo.nty[k] * wpr(lo.ntx[k]);
       if (words * 4 > 200 * 1024) return WV_ERR_UNSUPPORTED;

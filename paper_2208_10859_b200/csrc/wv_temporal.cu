@@ -114,6 +114,8 @@ __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
   const int npos = a.bs * a.bs;
   const int nq = (a.C * npos) >> 2;                           // float4 per block
   const uint32_t count = *a.count;
+  // cache entry total after this call's block selection (decoding.py:231)
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.fa->d_result->set_bytes = *a.fa->d_set_bytes;
   const int ah = a.H >> a.L, aw = a.W >> a.L;
   const int bmask = a.bs - 1;
   uint32_t err = 0;

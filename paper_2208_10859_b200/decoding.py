@@ -230,6 +230,9 @@ class DecodeSession:
         self.use_graphs = True
         self._ones_fp = None
         self.shared_view_geometry = int(os.environ.get("WV_SHARED_VIEW_GEOMETRY", "1"))
+        self.fork_footprint = int(os.environ.get("WV_FORK_FOOTPRINT", "1")) != 0
+        self._aux_stream = torch.cuda.Stream(self.device)
+        self._aux_stream2 = torch.cuda.Stream(self.device)
         self._results_host = torch.zeros((_RING, _RESULT_BYTES), dtype=torch.uint8).pin_memory()
         self._slot = 0
         self._cache: dict[int, _Entry] = {}
@@ -386,16 +389,47 @@ class DecodeSession:
             g.replay()
             return
 
+        def run(stages, stream):
+            N.check(self._lib.wv_decode_stages_desc(
+                C.byref(self._geom), key[0], flags, stages, C.c_void_p(self._ws.data_ptr()),
+                C.c_void_p(stream.cuda_stream)), "wv_decode_stages_desc")
+
         def seq():
-            N.check(self._lib.wv_decode_frame_desc(
-                C.byref(self._geom), key[0], flags, C.c_void_p(self._ws.data_ptr()),
-                C.c_void_p(torch.cuda.current_stream().cuda_stream)), "wv_decode_frame_desc")
+            cur = torch.cuda.current_stream()
+            if self.fork_footprint:
+                # rows -> {tile lists} || cascades -> {footprint chain} ||
+                # block selection -> K2; K3 joins the tile lists, the finest
+                # footprint step joins the footprint chain
+                aux, aux2 = self._aux_stream, self._aux_stream2
+                run(N.WV_STAGE_ROWS, cur)
+                ev_r = torch.cuda.Event()
+                ev_r.record(cur)
+                aux2.wait_event(ev_r)
+                run(N.WV_STAGE_TILES, aux2)
+                ev_t = torch.cuda.Event()
+                ev_t.record(aux2)
+                run(N.WV_STAGE_CASCADES, cur)
+                ev_c = torch.cuda.Event()
+                ev_c.record(cur)
+                aux.wait_event(ev_c)
+                run(N.WV_STAGE_FOOTPRINT, aux)
+                ev_f = torch.cuda.Event()
+                ev_f.record(aux)
+                run(N.WV_STAGE_BLOCKS | N.WV_STAGE_DEQUANT, cur)
+                cur.wait_event(ev_t)
+                run(N.WV_STAGE_SYNTH, cur)
+                cur.wait_event(ev_f)
+                run(N.WV_STAGE_FOOTPRINT_TILES, cur)
+            else:
+                N.check(self._lib.wv_decode_frame_desc(
+                    C.byref(self._geom), key[0], flags, C.c_void_p(self._ws.data_ptr()),
+                    C.c_void_p(cur.cuda_stream)), "wv_decode_frame_desc")
             if nv:
                 # all eyes of a session share pose and region size (stereo pair)
                 N.check(self._lib.wv_render_perspective_desc(
                     C.c_void_p(self._desc_dev.data_ptr() + _FA_BYTES), nv, out_dims[0],
                     out_dims[1], self.shared_view_geometry,
-                    C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                    C.c_void_p(cur.cuda_stream)),
                     "wv_render_perspective_desc")
 
         seq()
