@@ -172,6 +172,19 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def launches_per_frame(L: int, mode: str, residency: str) -> int:
+    """Kernels of one frame's graph (csrc launch sequence): K1 rows, L
+    cascades, L-1 footprint steps, blocks, tile lists (2), finest footprint;
+    K2; K3 L levels; K4 -- full frame: rows, footprint fill, blocks, tile
+    lists, K2, K3 (no cascades, footprint chain or writeout)."""
+    tiles = 1 + (1 if L >= 2 else 0)
+    if mode == "full":
+        n = 1 + 1 + 1 + tiles + 1 + L
+    else:
+        n = 1 + L + (L - 1) + 1 + tiles + 1 + 1 + L + 1
+    return n + (1 if residency == "spans" else 0)
+
+
 def ncu_traffic(mode: str):
     """DRAM bytes per launch of the K3 finest level from the latest committed
     `ncu --set full` capture of this mode (profiles/ncu_k3_final[_full]_<tag>.json)."""
@@ -459,7 +472,7 @@ def run_ours(args):
             "clocks": clk.summary(),
             # per frame: K1 2L+4 (mask rows, L cascades, L footprint, blocks,
             # tiles, finalize) + K2 1 + K3 L + K4 1 (not in full mode)
-            "gpu_launches": args.steps * (3 * h.levels + 5 + (1 if args.mode != "full" else 0)),
+            "gpu_launches": args.steps * launches_per_frame(h.levels, args.mode, args.residency),
         }
         print(json.dumps(line), flush=True)
     for ss in sessions:
