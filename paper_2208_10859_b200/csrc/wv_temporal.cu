@@ -92,7 +92,10 @@ __device__ __forceinline__ int tweight(int ti, int t, int n) {
 // by temporal index (ascending, the np.add.at order), all records of one
 // index concurrently, and the inclusion-masked block is written with 16-byte
 // stores.
-constexpr int K2_THREADS = 256;
+#ifndef WV_K2_THREADS
+#define WV_K2_THREADS 256
+#endif
+constexpr int K2_THREADS = WV_K2_THREADS;
 constexpr int K2_MAXN = 32;
 
 __global__ void __launch_bounds__(K2_THREADS) k_temporal(TemporalArgs a) {
