@@ -208,7 +208,8 @@ struct LevelArgs {
   const uint32_t* R;   // final: requested-mask rows (mh x wpr0)
   const uint32_t* rowmap;  // final: pixel row -> mask row
   int wpr0;
-  int use_tma;         // subband widths are 16-byte multiples
+  int use_tma;         // subband width is a multiple of 4 floats (TMA inner coordinate
+                       // alignment); else the boxes are filled with plain loads
   const float* ll_ptr; int ll_pitch, ll_rows;   // LDG fallback sources
   const float* plane; int plane_w, plane_h;
 };

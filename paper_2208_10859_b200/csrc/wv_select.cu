@@ -209,8 +209,9 @@ __global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
 }
 
 // ----------------------------------------------------------- footprint step
-// V_{j-1} = shrink4(upsample2(V_j & D_j)) (outside the grid counts as set);
-// the finest step also ANDs the request.  Upsampling duplicates rows, so the
+// V_{j-1} = shrink4(upsample2(V_j & D_j)) (outside the grid counts as set),
+// levels j = L..2; the finest step (j = 1, ANDed with the request) is
+// k_footprint_tiles.  Upsampling duplicates rows, so the
 // 9-row AND is taken over the 5 distinct source rows before bit doubling.
 struct FootArgs {
   int j, L, H;
@@ -218,8 +219,8 @@ struct FootArgs {
   int srows, swpr;            // source level j
   const uint32_t* V;          // valid at level j (nullptr: all ones)
   const uint32_t* D;          // detail mask level j
-  uint32_t* out;              // level j-1 (j == 1: fa->d_footprint)
-  const uint32_t* R;          // j == 1: requested rows
+  uint32_t* out;              // level j-1 (finest step: fa->d_footprint)
+  const uint32_t* R;          // finest step: requested rows
   const uint32_t* rowmap;
   const wv_frame_args* fa;
 };
@@ -247,7 +248,6 @@ __global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
   const int r = r0 + tr;
   if (r >= a.rows) return;
   const int s_lo = ((r - DIL) >> 1) - sr0, s_hi = ((r + DIL) >> 1) - sr0;
-  const uint32_t req_row = a.j == 1 ? a.rowmap[r] : 0u;
 #pragma unroll
   for (int q = 0; q < CT_W / CT_TW; ++q) {
     const int w = w0 + tq + q * CT_TW;
@@ -264,9 +264,7 @@ __global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
       for (int k = s_lo; k <= s_hi; ++k) v &= sv[k][(ww >> 1) - sw0];
       nb[d] = double_bits(v >> (16 * (ww & 1))) | ~last_word_mask(a.cols, ww);
     }
-    uint32_t v = shrink(nb[0], nb[1], nb[2]) & last_word_mask(a.cols, w);
-    if (a.j == 1) v &= a.R[(uint64_t)req_row * a.wpr + w];
-    (a.j == 1 ? a.fa->d_footprint : a.out)[(uint64_t)r * a.wpr + w] = v;
+    a.out[(uint64_t)r * a.wpr + w] = shrink(nb[0], nb[1], nb[2]) & last_word_mask(a.cols, w);
   }
 }
 
