@@ -226,7 +226,7 @@ constexpr int BOXSET = 4 * BOX_SLOT;
 constexpr int O8_PITCH = OUT_W + 4;   // bytes; 17 words: conflict-light row-pass stores
 constexpr int COL_BYTES = 2 * TY * CB_PITCH * 8;
 constexpr int SMEM_MID = BOXSET + COL_BYTES;
-constexpr int SMEM_FIN = BOXSET + COL_BYTES + OUT_H * O8_PITCH + OUT_H * 2 * 4;
+constexpr int SMEM_FIN = BOXSET + COL_BYTES;   // the u8 tile goes from registers to HBM
 
 template <bool FINAL>
 __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUtensorMap tm_ll,
@@ -243,8 +243,6 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   float2* colL = reinterpret_cast<float2*>(smem + BOXSET);  // [TY][CB_PITCH]
   float2* colH = colL + TY * CB_PITCH;
   float2* outb = reinterpret_cast<float2*>(smem);                     // mid: aliases the boxes
-  uint8_t* out8 = smem + BOXSET + COL_BYTES;                          // final: [OUT_H][O8_PITCH]
-  uint32_t* req = reinterpret_cast<uint32_t*>(out8 + OUT_H * O8_PITCH);  // final: [OUT_H][2]
   __shared__ uint64_t bar;
 
   const int tid = threadIdx.x;
@@ -315,16 +313,6 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       __syncthreads();
     }
     issued = false;
-    bool row_req_full = true;
-    if (FINAL && tid < ny) {
-      // request-mask words of this tile's output rows (used by the store pass)
-      const int gx = 2 * ax;
-      const uint32_t* row = a.R + (uint64_t)a.rowmap[2 * ay + tid] * a.wpr0 + (gx >> 5);
-      const uint32_t w0 = row[0], w1 = nx > 32 ? row[1] : 0u;
-      req[2 * tid] = w0;
-      req[2 * tid + 1] = w1;
-      row_req_full = nx == OUT_W && w0 == 0xFFFFFFFFu && w1 == 0xFFFFFFFFu;
-    }
 
     // column pass: (segment, box column) per thread, L and H halves packed
     if (tid < COL_SEGS * BOX_W) {
@@ -365,7 +353,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         }
       }
     }
-    const bool tile_req_full = __syncthreads_and(row_req_full) && FINAL && ny == OUT_H;
+    __syncthreads();
     if (FINAL && a.use_tma) {
       // the boxes are consumed: start the next item's loads now
       uint32_t nxt = item + gridDim.x;
@@ -379,21 +367,18 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       const int i = tid % TY, sg = tid / TY;
       const int pa = ax + sg * SEGLEN_R, pb = min(pa + SEGLEN_R, bx);
       if (i < by - ay && pa < pb) {
-        // mid levels: f32 pairs into outb; finest level: clip(rint(x*255))
-        // (decoding.py:301; rint is round-half-even like __float2uint_rn,
-        // which also saturates below 0) straight into the u8 tile
-        auto emit_out = [&](int q, float2 s3, float2 d3) {
+        // finest level: clip(rint(x*255)) (decoding.py:301; rint is
+        // round-half-even like __float2uint_rn, which also saturates below 0)
+        // of the segment's 2 x 16 output pixels, kept in registers and
+        // written to the canvas with the request mask applied
+        auto cv = [](float v) { return min(__float2uint_rn(__fmul_rn(v, 255.0f)), 255u); };
+        uint32_t w0[SEGLEN_R / 2] = {}, w1[SEGLEN_R / 2] = {};   // rows 2i, 2i+1
+        uint8_t* crow = FINAL ? canvas + ((uint64_t)c * H + 2 * ay + 2 * i) * W : nullptr;
+        // mid levels: f32 pairs into outb
+        auto emit_mid = [&](int q, float2 s3, float2 d3) {
           WV_ASSERT(q >= 0 && q < TX && i < TY);
-          if (!FINAL) {
-            outb[i * OB_PITCH + 2 * q] = s3;
-            outb[i * OB_PITCH + 2 * q + 1] = d3;
-          } else {
-            auto cv = [](float v) { return min(__float2uint_rn(__fmul_rn(v, 255.0f)), 255u); };
-            *reinterpret_cast<uint16_t*>(out8 + (2 * i) * O8_PITCH + 2 * q) =
-                (uint16_t)(cv(s3.x) | (cv(d3.x) << 8));
-            *reinterpret_cast<uint16_t*>(out8 + (2 * i + 1) * O8_PITCH + 2 * q) =
-                (uint16_t)(cv(s3.y) | (cv(d3.y) << 8));
-          }
+          outb[i * OB_PITCH + 2 * q] = s3;
+          outb[i * OB_PITCH + 2 * q + 1] = d3;
         };
         if (pa >= HALO && pb + HALO <= a.bw && pb - pa == SEGLEN_R) {
           const int cb = pa - HALO - ox, qb = pa - HALO - ax;
@@ -403,7 +388,40 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
                 s = colL[i * CB_PITCH + cb + j];
                 d = colH[i * CB_PITCH + cb + j];
               },
-              [&](int p, float2 s3, float2 d3) { emit_out(qb + p, s3, d3); });
+              [&](int p, float2 s3, float2 d3) {
+                if (!FINAL) {
+                  emit_mid(qb + p, s3, d3);
+                } else {
+                  // p - HALO is the segment-local pair: compile-time after unrolling
+                  const int lq = p - HALO;
+                  w0[lq >> 1] |= (cv(s3.x) | (cv(d3.x) << 8)) << (16 * (lq & 1));
+                  w1[lq >> 1] |= (cv(s3.y) | (cv(d3.y) << 8)) << (16 * (lq & 1));
+                }
+              });
+          if (FINAL) {
+            // 16 pixels of each row: request bits -> byte masks, 16-byte stores
+            const int px = 2 * pa;
+            auto bm = [](uint32_t b4) { return ((b4 * 0x00204081u) & 0x01010101u) * 0xFFu; };
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+              const uint32_t* wr = rr ? w1 : w0;
+              const int y = 2 * ay + 2 * i + rr;
+              const uint32_t bits =
+                  (a.R[(uint64_t)a.rowmap[y] * a.wpr0 + (px >> 5)] >> (px & 31)) & 0xFFFFu;
+              const uint4 v = make_uint4(wr[0] & bm(bits & 0xFu), wr[1] & bm((bits >> 4) & 0xFu),
+                                         wr[2] & bm((bits >> 8) & 0xFu), wr[3] & bm(bits >> 12));
+              uint8_t* dst = crow + (uint64_t)rr * W + px;
+              if ((W & 15) == 0) {
+                *reinterpret_cast<uint4*>(dst) = v;
+              } else {
+                uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+                d4[0] = v.x;
+                d4[1] = v.y;
+                d4[2] = v.z;
+                d4[3] = v.w;
+              }
+            }
+          }
         } else {
           lift_line(
               max(pa - HALO, 0), min(pb + HALO, a.bw), a.bw, pa, pb,
@@ -412,7 +430,23 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
                 s = colL[i * CB_PITCH + (j - ox)];
                 d = colH[i * CB_PITCH + (j - ox)];
               },
-              [&](int p, float2 s3, float2 d3) { emit_out(p - ax, s3, d3); });
+              [&](int p, float2 s3, float2 d3) {
+                if (!FINAL) {
+                  emit_mid(p - ax, s3, d3);
+                } else {
+                  // level borders: two pixels per row straight to the canvas
+                  const int px = 2 * p;
+#pragma unroll
+                  for (int rr = 0; rr < 2; ++rr) {
+                    const int y = 2 * ay + 2 * i + rr;
+                    const uint32_t bits =
+                        (a.R[(uint64_t)a.rowmap[y] * a.wpr0 + (px >> 5)] >> (px & 31)) & 3u;
+                    const uint32_t lo = rr ? cv(s3.y) : cv(s3.x), hi = rr ? cv(d3.y) : cv(d3.x);
+                    *reinterpret_cast<uint16_t*>(crow + (uint64_t)rr * W + px) =
+                        (uint16_t)(((bits & 1u) ? lo : 0u) | (((bits >> 1) & 1u) ? hi << 8 : 0u));
+                  }
+                }
+              });
         }
       }
     }
@@ -442,37 +476,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       }
       __syncthreads();
     } else {
-      // u8 rows -> canvas plane c, zero outside the request
-      uint8_t* base = canvas + ((uint64_t)c * H + 2 * ay) * W + 2 * ax;
-      if (((W | nx) & 15) == 0) {
-        const int vw = nx >> 4;     // 16-pixel vectors per row
-        for (int idx = tid; idx < ny * vw; idx += NTHREADS) {
-          const int r = tile_req_full ? idx >> 2 : idx / vw;
-          const int q = tile_req_full ? idx & 3 : idx - (idx / vw) * vw;
-          const uint32_t* src = reinterpret_cast<const uint32_t*>(out8 + r * O8_PITCH) + 4 * q;
-          uint4 w = make_uint4(src[0], src[1], src[2], src[3]);
-          if (!tile_req_full) {
-            const uint32_t bits = (req[2 * r + (q >> 1)] >> (16 * (q & 1))) & 0xFFFFu;
-            // 4 request bits -> 4 byte masks (bit k -> byte k)
-            auto bm = [](uint32_t b4) { return ((b4 * 0x00204081u) & 0x01010101u) * 0xFFu; };
-            w.x &= bm(bits & 0xFu);
-            w.y &= bm((bits >> 4) & 0xFu);
-            w.z &= bm((bits >> 8) & 0xFu);
-            w.w &= bm(bits >> 12);
-          }
-          *reinterpret_cast<uint4*>(base + (uint64_t)r * W + 16 * q) = w;
-        }
-      } else {
-        const int qw = nx >> 2;     // 4-pixel words per row
-        for (int idx = tid; idx < ny * qw; idx += NTHREADS) {
-          const int r = idx / qw, q = idx % qw;
-          uint32_t w = *reinterpret_cast<const uint32_t*>(out8 + r * O8_PITCH + 4 * q);
-          const uint32_t b = (req[2 * r + (q >> 3)] >> ((4 * q) & 31)) & 0xFu;
-          w &= ((b * 0x00204081u) & 0x01010101u) * 0xFFu;
-          *reinterpret_cast<uint32_t*>(base + (uint64_t)r * W + 4 * q) = w;
-        }
-      }
-      __syncthreads();   // out8 and req are rewritten by the next item
+      __syncthreads();   // colL / colH are rewritten by the next item
     }
   }
 }
