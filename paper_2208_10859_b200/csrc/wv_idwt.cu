@@ -18,8 +18,10 @@
 // the L-half (LL/LH) and H-half (HL/HH) lines packed as float2 and lifted with
 // Blackwell's paired FP32 ops (__fadd2_rn/__fmul2_rn, RN, no FMA); results land
 // row-pair-interleaved so the row pass again lifts two output rows per
-// thread as one float2 stream.  The output tile is staged in shared memory and
-// written with coalesced stores.
+// thread as one float2 stream.  Mid levels stage the f32 output tile in shared
+// memory and write it with coalesced stores; the finest level converts to u8
+// in registers and stores each 16-pixel row segment, request-masked, straight
+// to the canvas.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -214,16 +216,16 @@ struct LevelArgs {
   const float* plane; int plane_w, plane_h;
 };
 
-// Items are (tile, channel).  Column pass: 2 segments x BOX_W columns (each
-// segment lifts 16 output row pairs from its own 2-row halo); row pass: 2
-// segments x TY row pairs.  Mid levels stage the f32 output tile in the box
-// region (dead after the column pass) and store it coalesced.  The finest
-// level keeps its u8 tile in a separate 4 KB buffer, so the box region is
-// free as soon as the column pass ends: the next item's four TMA boxes are
-// issued there and load while this item's row and store passes run.  Its
-// store pass writes 16-byte vectors with the request mask applied.
+// Items are (tile, channel).  Column pass: TY/SEGLEN_C segments x BOX_W
+// columns (each segment lifts SEGLEN_C output row pairs from its own 2-row
+// halo); row pass: TX/SEGLEN_R segments x TY row pairs.  Mid levels stage the
+// f32 output tile in the box region (dead after the column pass) and store it
+// coalesced.  The finest level needs no output tile: each row-pass thread
+// keeps its 2 x 16 output bytes in registers and writes them with the
+// request mask applied, so the box region is free as soon as the column pass
+// ends and the next item's four TMA boxes are issued there, loading while
+// this item's row pass runs (43 KB of shared memory: 5 CTAs per SM).
 constexpr int BOXSET = 4 * BOX_SLOT;
-constexpr int O8_PITCH = OUT_W + 4;   // bytes; 17 words: conflict-light row-pass stores
 constexpr int COL_BYTES = 2 * TY * CB_PITCH * 8;
 constexpr int SMEM_MID = BOXSET + COL_BYTES;
 constexpr int SMEM_FIN = BOXSET + COL_BYTES;   // the u8 tile goes from registers to HBM
