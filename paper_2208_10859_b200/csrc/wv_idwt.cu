@@ -45,8 +45,12 @@ constexpr int OB_PITCH = OUT_W + 1;   // float2 units (row pairs), odd
 #ifndef WV_SEGLEN_R
 #define WV_SEGLEN_R 8
 #endif
-constexpr int SEGLEN_C = WV_SEGLEN_C, SEGLEN_R = WV_SEGLEN_R;
+#ifndef WV_SEGLEN_RF
+#define WV_SEGLEN_RF 8    // finest level row segments (16 measured slower)
+#endif
+constexpr int SEGLEN_C = WV_SEGLEN_C, SEGLEN_R = WV_SEGLEN_R, SEGLEN_RF = WV_SEGLEN_RF;
 constexpr int COL_SEGS = TY / SEGLEN_C, ROW_SEGS = TX / SEGLEN_R;
+static_assert(SEGLEN_RF % 8 == 0 && SEGLEN_RF <= TX, "finest row segments store 16-pixel chunks");
 constexpr int NTHREADS_MIN = (COL_SEGS * BOX_W > ROW_SEGS * TY ? COL_SEGS * BOX_W : ROW_SEGS * TY);
 #ifdef WV_K3_THREADS
 constexpr int NTHREADS = WV_K3_THREADS;
@@ -365,16 +369,17 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       }
     }
     // row pass: (segment, output row pair) per thread, two rows packed
-    if (tid < ROW_SEGS * TY) {
+    constexpr int SR = FINAL ? SEGLEN_RF : SEGLEN_R;
+    if (tid < (TX / SR) * TY) {
       const int i = tid % TY, sg = tid / TY;
-      const int pa = ax + sg * SEGLEN_R, pb = min(pa + SEGLEN_R, bx);
+      const int pa = ax + sg * SR, pb = min(pa + SR, bx);
       if (i < by - ay && pa < pb) {
         // finest level: clip(rint(x*255)) (decoding.py:301; rint is
         // round-half-even like __float2uint_rn, which also saturates below 0)
         // of the segment's 2 x 16 output pixels, kept in registers and
         // written to the canvas with the request mask applied
         auto cv = [](float v) { return min(__float2uint_rn(__fmul_rn(v, 255.0f)), 255u); };
-        uint32_t w0[SEGLEN_R / 2] = {}, w1[SEGLEN_R / 2] = {};   // rows 2i, 2i+1
+        uint32_t w0[SR / 2] = {}, w1[SR / 2] = {};   // rows 2i, 2i+1
         uint8_t* crow = FINAL ? canvas + ((uint64_t)c * H + 2 * ay + 2 * i) * W : nullptr;
         // mid levels: f32 pairs into outb
         auto emit_mid = [&](int q, float2 s3, float2 d3) {
@@ -382,9 +387,9 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
           outb[i * OB_PITCH + 2 * q] = s3;
           outb[i * OB_PITCH + 2 * q + 1] = d3;
         };
-        if (pa >= HALO && pb + HALO <= a.bw && pb - pa == SEGLEN_R) {
+        if (pa >= HALO && pb + HALO <= a.bw && pb - pa == SR) {
           const int cb = pa - HALO - ox, qb = pa - HALO - ax;
-          lift_interior<SEGLEN_R>(
+          lift_interior<SR>(
               [&](int j, float2& s, float2& d) {
                 WV_ASSERT(cb + j >= 0 && cb + j < CB_PITCH);
                 s = colL[i * CB_PITCH + cb + j];
@@ -401,26 +406,31 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
                 }
               });
           if (FINAL) {
-            // 16 pixels of each row: request bits -> byte masks, 16-byte stores
-            const int px = 2 * pa;
+            // 16-pixel chunks of each row: request bits -> byte masks, 16-byte stores
             auto bm = [](uint32_t b4) { return ((b4 * 0x00204081u) & 0x01010101u) * 0xFFu; };
 #pragma unroll
             for (int rr = 0; rr < 2; ++rr) {
               const uint32_t* wr = rr ? w1 : w0;
               const int y = 2 * ay + 2 * i + rr;
-              const uint32_t bits =
-                  (a.R[(uint64_t)a.rowmap[y] * a.wpr0 + (px >> 5)] >> (px & 31)) & 0xFFFFu;
-              const uint4 v = make_uint4(wr[0] & bm(bits & 0xFu), wr[1] & bm((bits >> 4) & 0xFu),
-                                         wr[2] & bm((bits >> 8) & 0xFu), wr[3] & bm(bits >> 12));
-              uint8_t* dst = crow + (uint64_t)rr * W + px;
-              if ((W & 15) == 0) {
-                *reinterpret_cast<uint4*>(dst) = v;
-              } else {
-                uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
-                d4[0] = v.x;
-                d4[1] = v.y;
-                d4[2] = v.z;
-                d4[3] = v.w;
+              const uint32_t* req = a.R + (uint64_t)a.rowmap[y] * a.wpr0;
+#pragma unroll
+              for (int k = 0; k < SR / 8; ++k) {
+                const int px = 2 * pa + 16 * k;
+                const uint32_t bits = (req[px >> 5] >> (px & 31)) & 0xFFFFu;
+                const uint4 v = make_uint4(wr[4 * k] & bm(bits & 0xFu),
+                                           wr[4 * k + 1] & bm((bits >> 4) & 0xFu),
+                                           wr[4 * k + 2] & bm((bits >> 8) & 0xFu),
+                                           wr[4 * k + 3] & bm(bits >> 12));
+                uint8_t* dst = crow + (uint64_t)rr * W + px;
+                if ((W & 15) == 0) {
+                  *reinterpret_cast<uint4*>(dst) = v;
+                } else {
+                  uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+                  d4[0] = v.x;
+                  d4[1] = v.y;
+                  d4[2] = v.z;
+                  d4[3] = v.w;
+                }
               }
             }
           }
