@@ -82,12 +82,15 @@ __global__ void k_mask_rows(const wv_frame_args* __restrict__ fa, uint32_t* __re
   if (idx < H) rowmap[idx] = ((uint32_t)idx * (uint32_t)mh) / (uint32_t)H;
   if (idx >= mh * wpr0) return;
   const int my = idx / wpr0, w = idx % wpr0;
+  // the word's pixels map to a few runs of mask columns: pixel x -> floor(x*mw/W)
+  // (fileio.py:435); mask column mx starts at pixel ceil(mx*W/mw)
+  const int x0 = 32 * w, x1 = min(x0 + 32, W);
   uint32_t bits = 0;
-  for (int i = 0; i < 32; ++i) {
-    const int x = 32 * w + i;
-    if (x >= W) break;
-    const int mx = (int)(((uint32_t)x * (uint32_t)mw) / (uint32_t)W);   // < 2^32 (checked on host)
-    if (full || mask[(uint64_t)my * mw + mx]) bits |= 1u << i;
+  int mx = (int)(((uint32_t)x0 * (uint32_t)mw) / (uint32_t)W);   // < 2^32 (checked on host)
+  for (int xs = x0; xs < x1; ++mx) {
+    const int nx = min(x1, (int)(((uint64_t)(mx + 1) * W + mw - 1) / mw));
+    if (full || mask[(uint64_t)my * mw + mx]) bits |= range_mask(xs, nx, w);
+    xs = nx;
   }
   R[idx] = bits;
 }
@@ -145,6 +148,7 @@ __device__ __forceinline__ uint32_t cas_down(const CascadeArgs& a, const int4& r
 __global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
   pdl_sync();
   __shared__ uint32_t dm[2][CT_R + 2 * DIL][CT_W + 2];
+  __shared__ uint32_t vor[2][CT_R][CT_W + 2];
   __shared__ uint32_t pool[CT_W];
   const int b = a.batch[blockIdx.y];
   const bool both = a.fov && b == a.j;
@@ -169,6 +173,20 @@ __global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
     if (both) dm[1][lr][lw] = v1;
   }
   __syncthreads();
+  // vertical 9-row OR of every apron column, once (the horizontal spread
+  // then reads 3 of them per output word)
+  for (int e = threadIdx.x; e < CT_R * (CT_W + 2); e += blockDim.x) {
+    const int lr = e / (CT_W + 2), lw = e % (CT_W + 2);
+    uint32_t v0 = 0, v1 = 0;
+#pragma unroll
+    for (int k = 0; k <= 2 * DIL; ++k) {
+      v0 |= dm[0][lr + k][lw];
+      if (both) v1 |= dm[1][lr + k][lw];
+    }
+    vor[0][lr][lw] = v0;
+    if (both) vor[1][lr][lw] = v1;
+  }
+  __syncthreads();
   const int tr = threadIdx.x / CT_TW, tq = threadIdx.x % CT_TW;
   const int r = r0 + tr;
   if (r < a.rows) {
@@ -176,24 +194,8 @@ __global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
     for (int q = 0; q < CT_W / CT_TW; ++q) {
       const int lw = tq + q * CT_TW, w = w0 + lw;
       if (w >= a.wpr) break;
-      uint32_t p = 0, c = 0, n = 0;
-#pragma unroll
-      for (int k = 0; k <= 2 * DIL; ++k) {
-        p |= dm[0][tr + k][lw];
-        c |= dm[0][tr + k][lw + 1];
-        n |= dm[0][tr + k][lw + 2];
-      }
-      uint32_t v = spread(p, c, n);
-      if (both) {
-        uint32_t p1 = 0, c1 = 0, n1 = 0;
-#pragma unroll
-        for (int k = 0; k <= 2 * DIL; ++k) {
-          p1 |= dm[1][tr + k][lw];
-          c1 |= dm[1][tr + k][lw + 1];
-          n1 |= dm[1][tr + k][lw + 2];
-        }
-        v &= spread(p1, c1, n1);
-      }
+      uint32_t v = spread(vor[0][tr][lw], vor[0][tr][lw + 1], vor[0][tr][lw + 2]);
+      if (both) v &= spread(vor[1][tr][lw], vor[1][tr][lw + 1], vor[1][tr][lw + 2]);
       v &= last_word_mask(a.cols, w);
       a.dst[(uint64_t)b * a.dst_stride + (uint64_t)r * a.wpr + w] = v;
       if (final_mask && v) atomicOr(&pool[lw], 1u);
@@ -244,10 +246,20 @@ __global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
     sv[lr][lw] = v;
   }
   __syncthreads();
+  // AND over each output row's 4-5 source rows, once per staged source word
+  __shared__ uint32_t va[CT_R][FP_SW];
+  for (int e = threadIdx.x; e < CT_R * FP_SW; e += blockDim.x) {
+    const int lr = e / FP_SW, lw = e - (e / FP_SW) * FP_SW;
+    const int rr = r0 + lr;
+    const int s_lo = ((rr - DIL) >> 1) - sr0, s_hi = ((rr + DIL) >> 1) - sr0;
+    uint32_t v = 0xFFFFFFFFu;
+    for (int k = s_lo; k <= s_hi; ++k) v &= sv[k][lw];
+    va[lr][lw] = v;
+  }
+  __syncthreads();
   const int tr = threadIdx.x / CT_TW, tq = threadIdx.x % CT_TW;
   const int r = r0 + tr;
   if (r >= a.rows) return;
-  const int s_lo = ((r - DIL) >> 1) - sr0, s_hi = ((r + DIL) >> 1) - sr0;
 #pragma unroll
   for (int q = 0; q < CT_W / CT_TW; ++q) {
     const int w = w0 + tq + q * CT_TW;
@@ -260,8 +272,7 @@ __global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
         nb[d] = 0xFFFFFFFFu;
         continue;
       }
-      uint32_t v = 0xFFFFFFFFu;
-      for (int k = s_lo; k <= s_hi; ++k) v &= sv[k][(ww >> 1) - sw0];
+      const uint32_t v = va[tr][(ww >> 1) - sw0];
       nb[d] = double_bits(v >> (16 * (ww & 1))) | ~last_word_mask(a.cols, ww);
     }
     a.out[(uint64_t)r * a.wpr + w] = shrink(nb[0], nb[1], nb[2]) & last_word_mask(a.cols, w);

@@ -228,7 +228,9 @@ class DecodeSession:
         self._desc_dev = self._ws[doff: doff + _DESC_BYTES]
         self._graphs: dict = {}
         self.use_graphs = True
-        self._ones_fp = None
+        with torch.cuda.stream(self.stream):
+            # all-ones footprint for foveated writeout (cli.py:177, service.py:135)
+            self._ones_fp = torch.full_like(self._footprint, -1)
         self.shared_view_geometry = int(os.environ.get("WV_SHARED_VIEW_GEOMETRY", "1"))
         self.fork_footprint = int(os.environ.get("WV_FORK_FOOTPRINT", "1")) != 0
         self._aux_stream = torch.cuda.Stream(self.device)
@@ -629,7 +631,8 @@ class DecodeSession:
         return n
 
     def render_views(self, pose: CameraPose, out_dims, out: torch.Tensor | None = None,
-                     check: bool = True, all_covered: bool = False) -> torch.Tensor:
+                     check: bool = True, all_covered: bool = False,
+                     events: tuple | None = None) -> torch.Tensor:
         """Perspective writeout (K4) of the current canvas: one view, or one
         per eye for top-bottom stereo.  Returns
         (views, out_h, out_w, C) u8 on the device.  ``all_covered``: coverage
@@ -651,7 +654,11 @@ class DecodeSession:
                 fp = self._ones_fp
             views = [view_args(self._canvas, fp, r0, rows, h.width, h.channels,
                                pose, out[i], self._uncovered) for i, (r0, rows) in enumerate(eyes)]
+            if events is not None:   # (start, end) CUDA events around the K4 launch only
+                events[0].record(self.stream)
             launch_views(views, self.stream)
+            if events is not None:
+                events[1].record(self.stream)
         if check:
             self.stream.synchronize()
             missing = int(self._uncovered.item())
