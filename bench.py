@@ -336,6 +336,12 @@ def run_ours(args):
     # a GPU-side sleep before each timed stage keeps the stream busy while the
     # host enqueues the stage, so the event intervals hold kernel time only
     busy = int(4e5)   # clock cycles (~0.2 ms)
+    if args.mode != "full":
+        # first use of the by-value K4 launch path loads its kernel (lazy module
+        # loading): keep that out of the timed frames
+        sess.render_views(pm[frames[0]][0], (OUT_W, OUT_H), out=out, check=False,
+                          all_covered=args.mode == "foveated")
+        torch.cuda.synchronize()
     for i in range(R):
         with torch.cuda.stream(stream):
             flush.zero_()

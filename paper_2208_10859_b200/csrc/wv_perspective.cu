@@ -60,9 +60,9 @@ __device__ __forceinline__ float rcp_approx(float x) {   // MUFU.RCP, no denorma
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-__device__ __forceinline__ float rsqrt_approx(float x) {
+__device__ __forceinline__ float sqrt_approx(float x) {   // MUFU.SQRT; sqrt(0) = 0
   float r;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 
@@ -321,7 +321,8 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
   if (((reinterpret_cast<uintptr_t>(gbase) | gpitch | rowb) & 15) == 0) {
     const int nv = rowb >> 4;
     for (int idx = tid; idx < ny * nv; idx += 256) {
-      const int r = idx / nv, q = idx - (idx / nv) * nv;
+      // nv = 6 (RGB, full tile): constant divisor, no division instructions
+      const int r = nv == 6 ? idx / 6 : idx / nv, q = idx - r * nv;
       __stcs(reinterpret_cast<uint4*>(gbase + r * gpitch) + q,
              *reinterpret_cast<const uint4*>(ost + r * OST_PITCH + 16 * q));
     }
@@ -391,8 +392,8 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
       // lon = atan2(x, z); lat = asin(y/|w|) = atan2(y, hypot(x, z))
       const float lon = fast_atan2(wx, wz) * 57.29577951308232f;
       const float hz = wx * wx + wz * wz;
-      const float lat = (hz > 1e-30f ? fast_atan2(wy, hz * rsqrt_approx(hz)) : copysignf(1.5707963f, wy)) *
-                        57.29577951308232f;
+      // (at the poles hz = 0 and fast_atan2(wy, 0) = +-pi/2)
+      const float lat = fast_atan2(wy, sqrt_approx(hz)) * 57.29577951308232f;
       const float fx = (lon + 180.0f) * sx - 0.5f;
       const float fy = (90.0f - lat) * sy - 0.5f;
       const float flx = floorf(fx), fly = floorf(fy);
