@@ -162,6 +162,17 @@ __device__ __forceinline__ uint32_t blend(float b00, float b01, float b10, float
 }
 
 // Phases 3-5 for CT channels (CT = 0: any C in 1..4, read at run time).
+// t / d and t % d for 0 <= t <= 256 and 1 <= d <= 64 without an integer
+// division: (t + 0.5) / d is at least 1/128 away from an integer, far beyond
+// the float error, so the truncation is exact.
+struct SmallDiv {
+  int q, r;
+};
+__device__ __forceinline__ SmallDiv small_div(int t, int d, float inv_d) {
+  const int q = __float2int_rz(((float)t + 0.5f) * inv_d);
+  return SmallDiv{q, t - q * d};
+}
+
 struct ViewPtrs {
   const uint32_t* F;     // footprint rows of the view's region
   const uint8_t* img;    // canvas plane 0, first row of the region
@@ -185,19 +196,23 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
   bool ok = box_ok;
   if (box_ok) {
     const int w0 = xl >> 5, nw = (xh >> 5) - w0 + 1;
-    const int q = tid % nw, rstep = 256 / nw, wd = w0 + q;
+    const float inv = __frcp_rn((float)nw);
+    const SmallDiv dq = small_div(tid, nw, inv);
+    const int q = dq.r, rstep = small_div(256, nw, inv).q, wd = w0 + q;
     const uint32_t m = ~range_bits(xl, xh + 1, wd);
     const uint32_t* f = vp.F + (uint32_t)yl * vc.wpr0 + wd;
     if (tid < rstep * nw)
-      for (int r = tid / nw; r < rows; r += rstep) ok = ok && (__ldg(f + (uint32_t)r * vc.wpr0) | m) == 0xFFFFFFFFu;
+      for (int r = dq.q; r < rows; r += rstep) ok = ok && (__ldg(f + (uint32_t)r * vc.wpr0) | m) == 0xFFFFFFFFu;
   }
   if (use_win) {
     const uint32_t plane = vc.plane;
-    const int q = tid % ww, rstep = 256 / ww;
+    const float inv = __frcp_rn((float)ww);
+    const SmallDiv dq = small_div(tid, ww, inv);
+    const int q = dq.r, rstep = small_div(256, ww, inv).q;
     const uint8_t* img = vp.img + (uint32_t)yl * n + wx0 + 4 * q;
     uint32_t* dst = win + 4 * q;
     if (tid < rstep * ww) {
-      for (int r = tid / ww; r < rows; r += rstep) {
+      for (int r = dq.q; r < rows; r += rstep) {
         const uint8_t* src = img + (uint32_t)r * n;
         const uint32_t R = __ldg(reinterpret_cast<const uint32_t*>(src));
         const uint32_t G = C > 1 ? __ldg(reinterpret_cast<const uint32_t*>(src + plane)) : 0u;
