@@ -317,8 +317,17 @@ __global__ void __launch_bounds__(128) k_footprint_tiles(FootArgs a, const uint3
       sv[ir][iw] = v;
     }
     __syncthreads();
-    if (mine) {
+    // AND over each output row's 4-5 source rows, once per source word: the
+    // thread of output word lw = 0 needs source words 0, 1; lw = 1 needs 1, 2
+    uint32_t va0 = 0xFFFFFFFFu, va1 = 0xFFFFFFFFu;
+    {
       const int s_lo = ((r - DIL) >> 1) - sr0, s_hi = ((r + DIL) >> 1) - sr0;
+      for (int k = s_lo; k <= s_hi; ++k) {
+        va0 &= sv[k][lw];
+        va1 &= sv[k][lw + 1];
+      }
+    }
+    if (mine) {
       uint32_t nb[3];
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
@@ -327,8 +336,8 @@ __global__ void __launch_bounds__(128) k_footprint_tiles(FootArgs a, const uint3
           nb[d] = 0xFFFFFFFFu;
           continue;
         }
-        uint32_t v = 0xFFFFFFFFu;
-        for (int k = s_lo; k <= s_hi; ++k) v &= sv[k][(ww >> 1) - sw0];
+        // source word (ww >> 1) - sw0 is lw or lw + 1 for this thread
+        const uint32_t v = ((ww >> 1) - sw0) > lw ? va1 : va0;
         nb[d] = double_bits(v >> (16 * (ww & 1))) | ~last_word_mask(a.cols, ww);
       }
       uint32_t v = shrink(nb[0], nb[1], nb[2]) & last_word_mask(a.cols, w);
