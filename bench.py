@@ -495,6 +495,7 @@ def run_ours(args):
 
 def _oracle_frame(path, frame, pose_t, mask, mode):
     """One display frame through the CPU oracle (decode + per-eye render)."""
+    import numpy as np
     from oracle import wavevid_oracle as wo
     sess = wo.OracleSession(path)
     h = sess.header
@@ -502,6 +503,8 @@ def _oracle_frame(path, frame, pose_t, mask, mode):
     kind = {"viewport": "viewport", "foveated": "foveated", "full": "full"}[mode]
     pix, fp, _ = sess.decode(frame, kind, None if mode == "full" else mask)
     if mode != "full":
+        if mode == "foveated":   # the reference's foveated callers check coverage
+            fp = np.ones_like(fp)   # against an all-ones footprint (cli.py:177)
         yaw, pitch, roll = pose_t
         rot = wo.pose_rotation(yaw, pitch, roll)
         half = h.height // 2 if h.stereo else h.height

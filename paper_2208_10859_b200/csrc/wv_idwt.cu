@@ -296,6 +296,28 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       continue;
     }
     const int oy = max(ay - HALO, 0), ox = max(ax - XPAD, 0);
+    // finest level: fetch this thread's request-mask words (rowmap -> R, two
+    // dependent global loads) and the next item's list entry now, so their
+    // latency hides behind the box wait and the column pass
+    constexpr int SR = FINAL ? SEGLEN_RF : SEGLEN_R;
+    uint32_t rq[2][SR / 8];
+    uint32_t nxt_entry = ZERO_FLAG;
+    const uint32_t nxt = item + gridDim.x;
+    if (FINAL) {
+      const int i = tid % TY, pa = ax + (tid / TY) * SR;
+      if (tid < (TX / SR) * TY && i < by - ay && pa < bx) {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const uint32_t* req = a.R + (uint64_t)a.rowmap[2 * ay + 2 * i + rr] * a.wpr0;
+#pragma unroll
+          for (int k = 0; k < SR / 8; ++k) {
+            const int px = 2 * pa + 16 * k;
+            rq[rr][k] = px < W ? req[px >> 5] : 0u;
+          }
+        }
+      }
+      if (tid == 0 && a.use_tma && nxt < nitems) nxt_entry = a.list[nxt / C];
+    }
     if (a.use_tma) {
       if (!issued) issue(item);
       mbar_wait(&bar, phase);
@@ -361,15 +383,12 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     }
     __syncthreads();
     if (FINAL && a.use_tma) {
-      // the boxes are consumed: start the next item's loads now
-      uint32_t nxt = item + gridDim.x;
-      if (nxt < nitems && !(a.list[nxt / C] & ZERO_FLAG)) {
-        issue(nxt);
-        issued = true;
-      }
+      // the boxes are consumed: start the next item's loads now (only the
+      // elected thread read nxt_entry and issues)
+      issued = !(nxt_entry & ZERO_FLAG);   // meaningful for the elected thread only
+      if (issued) issue(nxt);
     }
     // row pass: (segment, output row pair) per thread, two rows packed
-    constexpr int SR = FINAL ? SEGLEN_RF : SEGLEN_R;
     if (tid < (TX / SR) * TY) {
       const int i = tid % TY, sg = tid / TY;
       const int pa = ax + sg * SR, pb = min(pa + SR, bx);
@@ -411,12 +430,10 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
 #pragma unroll
             for (int rr = 0; rr < 2; ++rr) {
               const uint32_t* wr = rr ? w1 : w0;
-              const int y = 2 * ay + 2 * i + rr;
-              const uint32_t* req = a.R + (uint64_t)a.rowmap[y] * a.wpr0;
 #pragma unroll
               for (int k = 0; k < SR / 8; ++k) {
                 const int px = 2 * pa + 16 * k;
-                const uint32_t bits = (req[px >> 5] >> (px & 31)) & 0xFFFFu;
+                const uint32_t bits = (rq[rr][k] >> (px & 31)) & 0xFFFFu;
                 const uint4 v = make_uint4(wr[4 * k] & bm(bits & 0xFu),
                                            wr[4 * k + 1] & bm((bits >> 4) & 0xFu),
                                            wr[4 * k + 2] & bm((bits >> 8) & 0xFu),
@@ -462,7 +479,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         }
       }
     }
-    __syncthreads();
+    __syncthreads();   // mid: outb complete; final: colL / colH free for the next item
     if (!FINAL) {
       float* base = a.out + ((uint64_t)c * H + 2 * ay) * a.out_pitch + 2 * ax;
       if (nx == OUT_W && ny == OUT_H) {
@@ -487,8 +504,6 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         }
       }
       __syncthreads();
-    } else {
-      __syncthreads();   // colL / colH are rewritten by the next item
     }
   }
 }
