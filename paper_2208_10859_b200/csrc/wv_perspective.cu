@@ -131,19 +131,23 @@ struct ViewConst {
 
 // One CTA renders a K4_TY x K4_TX output tile (256 threads, K4_PPT pixels per
 // thread, rows ty + 8k).  Phases: (1) float32 geometry of every pixel and the
-// CTA's candidate-tap box; (2) one warp tests the box against the footprint;
+// CTA's candidate-tap box; (2) the box is tested against the footprint;
 // (3) the box of all C canvas planes is read with 4-byte loads and stored
 // channel-interleaved (one 32-bit word per source pixel) in shared memory;
 // (4) four shared loads per pixel feed the bilinear blend; (5) the tile's
-// (rows, K4_TX*C) bytes are staged and written with 16-byte stores.  Boxes
-// that wrap in longitude, clamp at a pole or exceed the window use direct
-// global gathers (projection.py:146-149 semantics).
+// (rows, K4_TX*C) bytes are staged and written with 16-byte stores.  For a
+// stereo pair the window holds both eyes' boxes at once when they fit, so
+// phases (2)-(5) run once for the pair (one round of staging loads in flight,
+// half the barriers).  Boxes that wrap in longitude, clamp at a pole or exceed
+// the window use direct global gathers (projection.py:146-149 semantics).
 #ifndef K4_TILE_Y
 #define K4_TILE_Y 32
 #endif
 constexpr int K4_TX = 32, K4_TY = K4_TILE_Y, K4_PPT = K4_TY / 8;
-constexpr int WIN_W = 128, WIN_H = 80;          // source pixels (32-bit words)
+constexpr int WIN_WORDS = 9216;                 // window capacity, source pixels (32-bit words)
+constexpr int BOX_MAX_W = 128;                  // widest box the footprint test covers
 constexpr int OST_PITCH = K4_TX * 4;            // bytes per staged output row (C <= 4)
+constexpr int OST_VIEW = K4_TY * OST_PITCH;
 #ifndef K4_MIN_BLOCKS
 #define K4_MIN_BLOCKS 4
 #endif
@@ -161,7 +165,6 @@ __device__ __forceinline__ uint32_t blend(float b00, float b01, float b10, float
   return __float_as_uint(fmaf(ay, bot - top, top) + 8388608.0f) & 0xFFu;
 }
 
-// Phases 3-5 for CT channels (CT = 0: any C in 1..4, read at run time).
 // t / d and t % d for 0 <= t <= 256 and 1 <= d <= 64 without an integer
 // division: (t + 0.5) / d is at least 1/128 away from an integer, far beyond
 // the float error, so the truncation is exact.
@@ -180,173 +183,220 @@ struct ViewPtrs {
   uint32_t* uncovered;
 };
 
-template <int CT>
+// Phases 2-5 for NV views sharing the geometry (NV = 2: a stereo pair staged
+// together), CT channels (CT = 0: any C in 1..4, read at run time).
+template <int CT, int NV>
 __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& v,
-                                       const ViewPtrs& vp, uint32_t* win, uint8_t* ost,
-                                       const int (&x0)[K4_PPT], const int (&y0)[K4_PPT],
-                                       const float (&ax)[K4_PPT], const float (&ay)[K4_PPT], int x,
-                                       int ybase, int xl, int xh, int yl, int yh, int wx0, int ww,
-                                       bool box_ok, bool use_win, int tid) {
+                                       const ViewPtrs (&vp)[NV], uint32_t* win, uint8_t* ost,
+                                       uint32_t* s_ok, const int (&x0)[K4_PPT],
+                                       const int (&y0)[K4_PPT], const float (&ax)[K4_PPT],
+                                       const float (&ay)[K4_PPT], int x, int ybase, int xl,
+                                       int xh, int yl, int yh, int wx0, int ww, bool box_ok,
+                                       bool use_win, int tid) {
   const int C = CT ? CT : vc.C;
   const int m = vc.m, n = vc.n, out_w = vc.out_w, out_h = vc.out_h;
+  const int rows = yh - yl + 1;
+  const int P = 4 * ww;           // window pitch (words)
+  const int VW = rows * P;        // words per view in the window
   // (2) footprint test of the box and (3) staging of the box, channels
   // interleaved (byte c of word = channel c).  Thread t owns word t % nwords
   // of rows t / nwords + k * (256 / nwords): one division per CTA, not per word.
-  const int rows = yh - yl + 1;
-  bool ok = box_ok;
+  uint32_t okb = box_ok ? (1u << NV) - 1u : 0u;   // bit j: view j's box covered so far
   if (box_ok) {
     const int w0 = xl >> 5, nw = (xh >> 5) - w0 + 1;
     const float inv = __frcp_rn((float)nw);
     const SmallDiv dq = small_div(tid, nw, inv);
     const int q = dq.r, rstep = small_div(256, nw, inv).q, wd = w0 + q;
-    const uint32_t m = ~range_bits(xl, xh + 1, wd);
-    const uint32_t* f = vp.F + (uint32_t)yl * vc.wpr0 + wd;
+    const uint32_t mk = ~range_bits(xl, xh + 1, wd);
+    const uint32_t o = (uint32_t)yl * vc.wpr0 + wd;
     if (tid < rstep * nw)
-      for (int r = dq.q; r < rows; r += rstep) ok = ok && (__ldg(f + (uint32_t)r * vc.wpr0) | m) == 0xFFFFFFFFu;
+      for (int r = dq.q; r < rows; r += rstep) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          if ((__ldg(vp[j].F + o + (uint32_t)r * vc.wpr0) | mk) != 0xFFFFFFFFu) okb &= ~(1u << j);
+      }
   }
   if (use_win) {
     const uint32_t plane = vc.plane;
     const float inv = __frcp_rn((float)ww);
     const SmallDiv dq = small_div(tid, ww, inv);
     const int q = dq.r, rstep = small_div(256, ww, inv).q;
-    const uint8_t* img = vp.img + (uint32_t)yl * n + wx0 + 4 * q;
-    uint32_t* dst = win + 4 * q;
+    const uint32_t so = (uint32_t)yl * n + wx0 + 4 * q;
     if (tid < rstep * ww) {
       for (int r = dq.q; r < rows; r += rstep) {
-        const uint8_t* src = img + (uint32_t)r * n;
-        const uint32_t R = __ldg(reinterpret_cast<const uint32_t*>(src));
-        const uint32_t G = C > 1 ? __ldg(reinterpret_cast<const uint32_t*>(src + plane)) : 0u;
-        const uint32_t B = C > 2 ? __ldg(reinterpret_cast<const uint32_t*>(src + 2 * plane)) : 0u;
-        const uint32_t A = C > 3 ? __ldg(reinterpret_cast<const uint32_t*>(src + 3 * plane)) : 0u;
-        const uint32_t rg_lo = __byte_perm(R, G, 0x5140), rg_hi = __byte_perm(R, G, 0x7362);
-        const uint32_t ba_lo = __byte_perm(B, A, 0x5140), ba_hi = __byte_perm(B, A, 0x7362);
-        WV_ASSERT(r < WIN_H && 4 * q + 3 < WIN_W);
-        *reinterpret_cast<uint4*>(dst + r * WIN_W) =
-            make_uint4(__byte_perm(rg_lo, ba_lo, 0x5410), __byte_perm(rg_lo, ba_lo, 0x7632),
-                       __byte_perm(rg_hi, ba_hi, 0x5410), __byte_perm(rg_hi, ba_hi, 0x7632));
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          const uint8_t* src = vp[j].img + so + (uint32_t)r * n;
+          const uint32_t R = __ldg(reinterpret_cast<const uint32_t*>(src));
+          const uint32_t G = C > 1 ? __ldg(reinterpret_cast<const uint32_t*>(src + plane)) : 0u;
+          const uint32_t B = C > 2 ? __ldg(reinterpret_cast<const uint32_t*>(src + 2 * plane)) : 0u;
+          const uint32_t A = C > 3 ? __ldg(reinterpret_cast<const uint32_t*>(src + 3 * plane)) : 0u;
+          const uint32_t rg_lo = __byte_perm(R, G, 0x5140), rg_hi = __byte_perm(R, G, 0x7362);
+          const uint32_t ba_lo = __byte_perm(B, A, 0x5140), ba_hi = __byte_perm(B, A, 0x7362);
+          WV_ASSERT(j * VW + r * P + 4 * q + 3 < WIN_WORDS);
+          *reinterpret_cast<uint4*>(win + j * VW + r * P + 4 * q) =
+              make_uint4(__byte_perm(rg_lo, ba_lo, 0x5410), __byte_perm(rg_lo, ba_lo, 0x7632),
+                         __byte_perm(rg_hi, ba_hi, 0x5410), __byte_perm(rg_hi, ba_hi, 0x7632));
+        }
       }
     }
   }
-  const bool covered = __syncthreads_and(ok);
+  {
+    const uint32_t wb = __reduce_and_sync(0xFFFFFFFFu, okb);
+    if (threadIdx.x == 0) s_ok[threadIdx.y] = wb;
+  }
+  __syncthreads();
+  uint32_t cov;
+  {
+    const uint4 a = *reinterpret_cast<const uint4*>(s_ok);
+    const uint4 b = *reinterpret_cast<const uint4*>(s_ok + 4);
+    cov = a.x & a.y & a.z & a.w & b.x & b.y & b.z & b.w;
+  }
   const uint32_t K = 0x4B000000u;
-  // (4a) common case, uniform over the CTA: whole tile inside the output, box
-  // covered by the footprint and staged -- taps straight from the window
-  if (covered && use_win && ((int)blockIdx.x + 1) * K4_TX <= out_w &&
-      ((int)blockIdx.y + 1) * K4_TY <= out_h) {
+  const bool full_tile = ((int)blockIdx.x + 1) * K4_TX <= out_w && ((int)blockIdx.y + 1) * K4_TY <= out_h;
 #pragma unroll
-    for (int k = 0; k < K4_PPT; ++k) {
-      WV_ASSERT(y0[k] - yl >= 0 && y0[k] + 1 - yl < WIN_H && x0[k] - wx0 >= 0 &&
-                x0[k] + 1 - wx0 < WIN_W);
-      const uint32_t* p = win + (y0[k] - yl) * WIN_W + (x0[k] - wx0);
-      const uint32_t w00 = p[0], w01 = p[1], w10 = p[WIN_W], w11 = p[WIN_W + 1];
-      uint8_t* o = ost + (threadIdx.y + 8 * k) * OST_PITCH + threadIdx.x * C;
+  for (int j = 0; j < NV; ++j) {
+    const uint32_t* wj = win + j * VW;
+    uint8_t* oj = ost + j * OST_VIEW;
+    const bool covered = (cov >> j) & 1u;
+    // (4a) common case, uniform over the CTA: whole tile inside the output,
+    // box covered by the footprint and staged -- taps straight from the window
+    if (covered && use_win && full_tile) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (c < C) {
-          const uint32_t sel = 0x3004u + c;
-          o[c] = (uint8_t)blend(__uint_as_float(__byte_perm(K, w00, sel)),
-                                __uint_as_float(__byte_perm(K, w01, sel)),
-                                __uint_as_float(__byte_perm(K, w10, sel)),
-                                __uint_as_float(__byte_perm(K, w11, sel)), ax[k], ay[k]);
+      for (int k = 0; k < K4_PPT; ++k) {
+        WV_ASSERT(y0[k] - yl >= 0 && y0[k] + 1 - yl < rows && x0[k] - wx0 >= 0 &&
+                  x0[k] + 1 - wx0 < P);
+        const uint32_t* p = wj + (y0[k] - yl) * P + (x0[k] - wx0);
+        const uint32_t w00 = p[0], w01 = p[1], w10 = p[P], w11 = p[P + 1];
+        uint8_t* o = oj + (threadIdx.y + 8 * k) * OST_PITCH + threadIdx.x * C;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < C) {
+            const uint32_t sel = 0x3004u + c;
+            o[c] = (uint8_t)blend(__uint_as_float(__byte_perm(K, w00, sel)),
+                                  __uint_as_float(__byte_perm(K, w01, sel)),
+                                  __uint_as_float(__byte_perm(K, w10, sel)),
+                                  __uint_as_float(__byte_perm(K, w11, sel)), ax[k], ay[k]);
+          }
         }
       }
+    } else {
+      // (4b) general case: per-pixel coverage (only when the box test failed),
+      // longitude wrap / pole clamp, partial tiles
+      unsigned n_unc = 0;
+#pragma unroll
+      for (int k = 0; k < K4_PPT; ++k) {
+        const int y = ybase + 8 * k;
+        const bool live = x < out_w && y < out_h;
+        bool uncovered = false;
+        if (live) {
+          int tx0 = x0[k], ty0 = y0[k];
+          float tax = ax[k], tay = ay[k];
+          if (!covered) {
+            const uint32_t* F = vp[j].F;
+            const int wpr0 = vc.wpr0;
+            const int cl = tax < kNear ? tx0 - 1 : tx0, ch = tax > 1.0f - kNear ? tx0 + 2 : tx0 + 1;
+            const int rl = tay < kNear ? ty0 - 1 : ty0, rh = tay > 1.0f - kNear ? ty0 + 2 : ty0 + 1;
+            const int len = ch - cl + 1;
+            const uint32_t full = (1u << len) - 1u;
+            bool ok = true;
+            for (int yy = rl; yy <= rh; ++yy)
+              ok = ok && fp_bits(F + (uint32_t)min(max(yy, 0), m - 1) * wpr0, cl, len, n) == full;
+            if (!ok) {
+              const Taps t = taps_f64(v, x, y);
+              tx0 = t.x0;
+              ty0 = t.y0;
+              tax = t.ax;
+              tay = t.ay;
+              const uint32_t* r0 = F + (uint32_t)min(max(ty0, 0), m - 1) * wpr0;
+              const uint32_t* r1 = F + (uint32_t)min(max(ty0 + 1, 0), m - 1) * wpr0;
+              uncovered = (fp_bits(r0, tx0, 2, n) & fp_bits(r1, tx0, 2, n)) != 3u;
+            }
+          }
+          uint32_t w00, w01, w10, w11;
+          if (use_win) {
+            WV_ASSERT(ty0 - yl >= 0 && ty0 + 1 - yl < rows && tx0 - wx0 >= 0 && tx0 + 1 - wx0 < P);
+            const uint32_t* p = wj + (ty0 - yl) * P + (tx0 - wx0);
+            w00 = p[0];
+            w01 = p[1];
+            w10 = p[P];
+            w11 = p[P + 1];
+          } else {
+            // longitude wrap / pole clamp (projection.py:146-149)
+            const int xa = wrapx(tx0, n), xb = wrapx(tx0 + 1, n);
+            const int ya = min(max(ty0, 0), m - 1), yb = min(max(ty0 + 1, 0), m - 1);
+            const uint32_t o00 = (uint32_t)ya * n + xa, o01 = (uint32_t)ya * n + xb;
+            const uint32_t o10 = (uint32_t)yb * n + xa, o11 = (uint32_t)yb * n + xb;
+            w00 = w01 = w10 = w11 = 0u;
+            const uint8_t* pc = vp[j].img;
+            for (int c = 0; c < C; ++c, pc += vc.plane) {
+              w00 |= (uint32_t)__ldg(pc + o00) << (8 * c);
+              w01 |= (uint32_t)__ldg(pc + o01) << (8 * c);
+              w10 |= (uint32_t)__ldg(pc + o10) << (8 * c);
+              w11 |= (uint32_t)__ldg(pc + o11) << (8 * c);
+            }
+          }
+          uint8_t* o = oj + (threadIdx.y + 8 * k) * OST_PITCH + threadIdx.x * C;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (c < C) {
+              // 2^23 + byte c of each tap (selector: byte c of the tap, zeros, 0x4B)
+              const uint32_t sel = 0x3004u + c;
+              const float b00 = __uint_as_float(__byte_perm(K, w00, sel));
+              const float b01 = __uint_as_float(__byte_perm(K, w01, sel));
+              const float b10 = __uint_as_float(__byte_perm(K, w10, sel));
+              const float b11 = __uint_as_float(__byte_perm(K, w11, sel));
+              o[c] = (uint8_t)blend(b00, b01, b10, b11, tax, tay);
+            }
+          }
+        }
+        n_unc += __popc(__ballot_sync(0xFFFFFFFFu, uncovered));
+      }
+      if (threadIdx.x == 0 && n_unc) atomicAdd(vp[j].uncovered, n_unc);
     }
-  } else {
-  // (4b) general case: per-pixel coverage (only when the box test failed),
-  // longitude wrap / pole clamp, partial tiles
-  unsigned n_unc = 0;
-#pragma unroll
-  for (int k = 0; k < K4_PPT; ++k) {
-    const int y = ybase + 8 * k;
-    const bool live = x < out_w && y < out_h;
-    bool uncovered = false;
-    if (live) {
-      int tx0 = x0[k], ty0 = y0[k];
-      float tax = ax[k], tay = ay[k];
-      if (!covered) {
-        const uint32_t* F = vp.F;
-        const int wpr0 = vc.wpr0;
-        const int cl = tax < kNear ? tx0 - 1 : tx0, ch = tax > 1.0f - kNear ? tx0 + 2 : tx0 + 1;
-        const int rl = tay < kNear ? ty0 - 1 : ty0, rh = tay > 1.0f - kNear ? ty0 + 2 : ty0 + 1;
-        const int len = ch - cl + 1;
-        const uint32_t full = (1u << len) - 1u;
-        bool ok = true;
-        for (int yy = rl; yy <= rh; ++yy)
-          ok = ok && fp_bits(F + (uint32_t)min(max(yy, 0), m - 1) * wpr0, cl, len, n) == full;
-        if (!ok) {
-          const Taps t = taps_f64(v, x, y);
-          tx0 = t.x0;
-          ty0 = t.y0;
-          tax = t.ax;
-          tay = t.ay;
-          const uint32_t* r0 = F + (uint32_t)min(max(ty0, 0), m - 1) * wpr0;
-          const uint32_t* r1 = F + (uint32_t)min(max(ty0 + 1, 0), m - 1) * wpr0;
-          uncovered = (fp_bits(r0, tx0, 2, n) & fp_bits(r1, tx0, 2, n)) != 3u;
-        }
-      }
-      uint32_t w00, w01, w10, w11;
-      if (use_win) {
-        WV_ASSERT(ty0 - yl >= 0 && ty0 + 1 - yl < WIN_H && tx0 - wx0 >= 0 &&
-                  tx0 + 1 - wx0 < WIN_W);
-        const uint32_t* p = win + (ty0 - yl) * WIN_W + (tx0 - wx0);
-        w00 = p[0];
-        w01 = p[1];
-        w10 = p[WIN_W];
-        w11 = p[WIN_W + 1];
-      } else {
-        // longitude wrap / pole clamp (projection.py:146-149)
-        const int xa = wrapx(tx0, n), xb = wrapx(tx0 + 1, n);
-        const int ya = min(max(ty0, 0), m - 1), yb = min(max(ty0 + 1, 0), m - 1);
-        const uint32_t o00 = (uint32_t)ya * n + xa, o01 = (uint32_t)ya * n + xb;
-        const uint32_t o10 = (uint32_t)yb * n + xa, o11 = (uint32_t)yb * n + xb;
-        w00 = w01 = w10 = w11 = 0u;
-        const uint8_t* pc = vp.img;
-        for (int c = 0; c < C; ++c, pc += vc.plane) {
-          w00 |= (uint32_t)__ldg(pc + o00) << (8 * c);
-          w01 |= (uint32_t)__ldg(pc + o01) << (8 * c);
-          w10 |= (uint32_t)__ldg(pc + o10) << (8 * c);
-          w11 |= (uint32_t)__ldg(pc + o11) << (8 * c);
-        }
-      }
-      uint8_t* o = ost + (threadIdx.y + 8 * k) * OST_PITCH + threadIdx.x * C;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (c < C) {
-          // 2^23 + byte c of each tap (selector: byte c of the tap, zeros, 0x4B)
-          const uint32_t sel = 0x3004u + c;
-          const float b00 = __uint_as_float(__byte_perm(K, w00, sel));
-          const float b01 = __uint_as_float(__byte_perm(K, w01, sel));
-          const float b10 = __uint_as_float(__byte_perm(K, w10, sel));
-          const float b11 = __uint_as_float(__byte_perm(K, w11, sel));
-          o[c] = (uint8_t)blend(b00, b01, b10, b11, tax, tay);
-        }
-      }
-    }
-    n_unc += __popc(__ballot_sync(0xFFFFFFFFu, uncovered));
-  }
-  if (threadIdx.x == 0 && n_unc) atomicAdd(vp.uncovered, n_unc);
   }
   __syncthreads();
   // (5) tile rows -> (out_h, out_w, C) with 16-byte stores where aligned
   const int nx = min(K4_TX, out_w - (int)blockIdx.x * K4_TX);
   const int ny = min(K4_TY, out_h - (int)blockIdx.y * K4_TY);
   const int rowb = nx * C;
-  uint8_t* gbase = vp.out + ((uint64_t)blockIdx.y * K4_TY * out_w + blockIdx.x * K4_TX) * C;
   const uint64_t gpitch = (uint64_t)out_w * C;
-  if (((reinterpret_cast<uintptr_t>(gbase) | gpitch | rowb) & 15) == 0) {
-    const int nv = rowb >> 4;
-    for (int idx = tid; idx < ny * nv; idx += 256) {
-      // nv = 6 (RGB, full tile): constant divisor, no division instructions
-      const int r = nv == 6 ? idx / 6 : idx / nv, q = idx - r * nv;
-      __stcs(reinterpret_cast<uint4*>(gbase + r * gpitch) + q,
-             *reinterpret_cast<const uint4*>(ost + r * OST_PITCH + 16 * q));
-    }
-  } else {
-    for (int idx = tid; idx < ny * rowb; idx += 256) {
-      const int r = idx / rowb, b = idx - (idx / rowb) * rowb;
-      gbase[r * gpitch + b] = ost[r * OST_PITCH + b];
+  const uint64_t gofs = ((uint64_t)blockIdx.y * K4_TY * out_w + blockIdx.x * K4_TX) * C;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    uint8_t* gbase = vp[j].out + gofs;
+    const uint8_t* oj = ost + j * OST_VIEW;
+    if (((reinterpret_cast<uintptr_t>(gbase) | gpitch | rowb) & 15) == 0) {
+      const int nv = rowb >> 4;
+      for (int idx = tid; idx < ny * nv; idx += 256) {
+        // nv = 6 (RGB, full tile): constant divisor, no division instructions
+        const int r = nv == 6 ? idx / 6 : idx / nv, q = idx - r * nv;
+        __stcs(reinterpret_cast<uint4*>(gbase + r * gpitch) + q,
+               *reinterpret_cast<const uint4*>(oj + r * OST_PITCH + 16 * q));
+      }
+    } else {
+      for (int idx = tid; idx < ny * rowb; idx += 256) {
+        const int r = idx / rowb, b = idx - (idx / rowb) * rowb;
+        gbase[r * gpitch + b] = oj[r * OST_PITCH + b];
+      }
     }
   }
+}
+
+template <int NV>
+__device__ __forceinline__ void finish_c(const ViewConst& vc, const wv_view_args& v,
+                                         const ViewPtrs (&vp)[NV], uint32_t* win, uint8_t* ost,
+                                         uint32_t* s_ok, const int (&x0)[K4_PPT],
+                                         const int (&y0)[K4_PPT], const float (&ax)[K4_PPT],
+                                         const float (&ay)[K4_PPT], int x, int ybase, int xl,
+                                         int xh, int yl, int yh, int wx0, int ww, bool box_ok,
+                                         bool use_win, int tid) {
+  if (vc.C == 3)
+    finish<3, NV>(vc, v, vp, win, ost, s_ok, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
+                  box_ok, use_win, tid);
+  else
+    finish<0, NV>(vc, v, vp, win, ost, s_ok, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
+                  box_ok, use_win, tid);
 }
 
 // shared_n == 0: CTA (x, y, z) renders view z.  shared_n > 0: the views
@@ -358,8 +408,9 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
                                                      int shared_n) {
   pdl_sync();
   __shared__ ViewConst vc;
-  __shared__ __align__(16) uint32_t win[WIN_H * WIN_W];
-  __shared__ __align__(16) uint8_t ost[K4_TY * OST_PITCH];
+  __shared__ __align__(16) uint32_t win[WIN_WORDS];
+  __shared__ __align__(16) uint8_t ost[2 * OST_VIEW];
+  __shared__ __align__(16) uint32_t s_ok[8];
   const int vz = shared_n > 0 ? 0 : blockIdx.z;
   const wv_view_args& v = DEV ? d_views[vz] : views.v[vz];
   const int tid = threadIdx.y * 32 + threadIdx.x;
@@ -442,20 +493,28 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
   const bool inside = xl >= 0 && xh < n && yl >= 0 && yh < m && xl <= xh;
   const int wx0 = xl & ~3;
   const int ww = ((xh | 3) - wx0 + 1) >> 2;   // 4-pixel words per window row
-  const bool box_ok = inside && (xh - xl) < WIN_W;
-  const bool use_win = inside && (n & 3) == 0 && 4 * ww <= WIN_W && (yh - yl + 1) <= WIN_H;
+  const int vwords = inside ? (yh - yl + 1) * 4 * ww : 0x7FFFFFFF;
+  const bool box_ok = inside && (xh - xl) < BOX_MAX_W;
+  const bool stage = inside && (n & 3) == 0;
   const int nv = shared_n > 0 ? shared_n : 1;
-  for (int vi = 0; vi < nv; ++vi) {
+  auto ptrs = [&](int vi) {
     // phases of consecutive views are separated by finish's own barriers
     const wv_view_args& vv = shared_n > 0 ? (DEV ? d_views[vi] : views.v[vi]) : v;
-    const ViewPtrs vp{vv.d_footprint + (uint64_t)vv.row0 * vc.wpr0,
-                      vv.d_canvas + (uint64_t)vv.row0 * vv.width, vv.d_out, vv.d_uncovered};
-    if (vc.C == 3)
-      finish<3>(vc, vv, vp, win, ost, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww, box_ok,
-                use_win, tid);
-    else
-      finish<0>(vc, vv, vp, win, ost, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww, box_ok,
-                use_win, tid);
+    return ViewPtrs{vv.d_footprint + (uint64_t)vv.row0 * vc.wpr0,
+                    vv.d_canvas + (uint64_t)vv.row0 * vv.width, vv.d_out, vv.d_uncovered};
+  };
+  for (int vi = 0; vi < nv;) {
+    if (vi + 1 < nv && stage && 2 * vwords <= WIN_WORDS) {
+      const ViewPtrs vp[2] = {ptrs(vi), ptrs(vi + 1)};
+      finish_c<2>(vc, v, vp, win, ost, s_ok, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
+                  box_ok, true, tid);
+      vi += 2;
+    } else {
+      const ViewPtrs vp[1] = {ptrs(vi)};
+      finish_c<1>(vc, v, vp, win, ost, s_ok, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
+                  box_ok, stage && vwords <= WIN_WORDS, tid);
+      vi += 1;
+    }
   }
 }
 
