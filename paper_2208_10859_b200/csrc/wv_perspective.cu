@@ -176,18 +176,139 @@ __device__ __forceinline__ SmallDiv small_div(int t, int d, float inv_d) {
   return SmallDiv{q, t - q * d};
 }
 
-struct ViewPtrs {
-  const uint32_t* F;     // footprint rows of the view's region
-  const uint8_t* img;    // canvas plane 0, first row of the region
-  uint8_t* out;
-  uint32_t* uncovered;
+// region pointers of a view, derived where they are used (keeping them live
+// across the phases costs registers)
+__device__ __forceinline__ const uint32_t* view_fp(const wv_view_args& w, int wpr0) {
+  return w.d_footprint + (uint64_t)w.row0 * wpr0;
+}
+__device__ __forceinline__ const uint8_t* view_img(const wv_view_args& w) {
+  return w.d_canvas + (uint64_t)w.row0 * w.width;
+}
+
+// float32 geometry of output pixel (x, y): the column part (camera ray x
+// component through the rotation) and the per-pixel rest.  The general path
+// re-evaluates it with the same code, so both see identical taps.
+struct ColGeo {
+  float cx, cy, cz;
 };
+__device__ __forceinline__ ColGeo col_geo(const ViewConst& vc, int x) {
+  const float u = ((float)x + 0.5f) * vc.inv_w - 1.0f;
+  const float rx = u * vc.tan_h;
+  return ColGeo{rx * vc.r[0] + vc.r[2], rx * vc.r[3] + vc.r[5], rx * vc.r[6] + vc.r[8]};
+}
+__device__ __forceinline__ void pix_geo(const ViewConst& vc, const ColGeo& cg, int y, int& x0,
+                                        int& y0, float& ax, float& ay) {
+  const float w = 1.0f - ((float)y + 0.5f) * vc.inv_h;
+  const float ry = w * vc.tan_v;
+  const float wx = fmaf(ry, vc.r[1], cg.cx), wy = fmaf(ry, vc.r[4], cg.cy),
+              wz = fmaf(ry, vc.r[7], cg.cz);
+  // lon = atan2(x, z); lat = asin(y/|w|) = atan2(y, hypot(x, z))
+  const float lon = fast_atan2(wx, wz) * 57.29577951308232f;
+  const float hz = wx * wx + wz * wz;
+  // (at the poles hz = 0 and fast_atan2(wy, 0) = +-pi/2)
+  const float lat = fast_atan2(wy, sqrt_approx(hz)) * 57.29577951308232f;
+  const float fx = (lon + 180.0f) * vc.sx - 0.5f;
+  const float fy = (90.0f - lat) * vc.sy - 0.5f;
+  const float flx = floorf(fx), fly = floorf(fy);
+  x0 = (int)flx;
+  y0 = (int)fly;
+  ax = fx - flx;
+  ay = fy - fly;
+}
+
+// Phase 4 for one view when the CTA-uniform fast path does not apply:
+// per-pixel coverage (only when the box test failed; a pixel whose float32
+// candidate taps are not all covered takes the reference's float64 taps),
+// longitude wrap / pole clamp, partial tiles.  Re-evaluates the pixel
+// geometry instead of receiving it, so the caller keeps nothing live across
+// the call.
+template <int CT>
+__device__ __noinline__ void general_view(const ViewConst& vc, const wv_view_args& v,
+                                          const wv_view_args& w, const uint32_t* wj, uint8_t* oj,
+                                          int P, int rows, int yl, int wx0, bool use_win,
+                                          bool covered, int x, int ybase) {
+  const int C = CT ? CT : vc.C;
+  const int m = vc.m, n = vc.n, out_w = vc.out_w, out_h = vc.out_h;
+  const uint32_t K = 0x4B000000u;
+  const ColGeo cg = col_geo(vc, x);
+  unsigned n_unc = 0;
+#pragma unroll
+  for (int k = 0; k < K4_PPT; ++k) {
+    const int y = ybase + 8 * k;
+    const bool live = x < out_w && y < out_h;
+    bool uncovered = false;
+    if (live) {
+      int tx0, ty0;
+      float tax, tay;
+      pix_geo(vc, cg, y, tx0, ty0, tax, tay);
+      if (!covered) {
+        const uint32_t* F = view_fp(w, vc.wpr0);
+        const int wpr0 = vc.wpr0;
+        const int cl = tax < kNear ? tx0 - 1 : tx0, ch = tax > 1.0f - kNear ? tx0 + 2 : tx0 + 1;
+        const int rl = tay < kNear ? ty0 - 1 : ty0, rh = tay > 1.0f - kNear ? ty0 + 2 : ty0 + 1;
+        const int len = ch - cl + 1;
+        const uint32_t full = (1u << len) - 1u;
+        bool ok = true;
+        for (int yy = rl; yy <= rh; ++yy)
+          ok = ok && fp_bits(F + (uint32_t)min(max(yy, 0), m - 1) * wpr0, cl, len, n) == full;
+        if (!ok) {
+          const Taps t = taps_f64(v, x, y);
+          tx0 = t.x0;
+          ty0 = t.y0;
+          tax = t.ax;
+          tay = t.ay;
+          const uint32_t* r0 = F + (uint32_t)min(max(ty0, 0), m - 1) * wpr0;
+          const uint32_t* r1 = F + (uint32_t)min(max(ty0 + 1, 0), m - 1) * wpr0;
+          uncovered = (fp_bits(r0, tx0, 2, n) & fp_bits(r1, tx0, 2, n)) != 3u;
+        }
+      }
+      uint32_t w00, w01, w10, w11;
+      if (use_win) {
+        WV_ASSERT(ty0 - yl >= 0 && ty0 + 1 - yl < rows && tx0 - wx0 >= 0 && tx0 + 1 - wx0 < P);
+        const uint32_t* p = wj + (ty0 - yl) * P + (tx0 - wx0);
+        w00 = p[0];
+        w01 = p[1];
+        w10 = p[P];
+        w11 = p[P + 1];
+      } else {
+        // longitude wrap / pole clamp (projection.py:146-149)
+        const int xa = wrapx(tx0, n), xb = wrapx(tx0 + 1, n);
+        const int ya = min(max(ty0, 0), m - 1), yb = min(max(ty0 + 1, 0), m - 1);
+        const uint32_t o00 = (uint32_t)ya * n + xa, o01 = (uint32_t)ya * n + xb;
+        const uint32_t o10 = (uint32_t)yb * n + xa, o11 = (uint32_t)yb * n + xb;
+        w00 = w01 = w10 = w11 = 0u;
+        const uint8_t* pc = view_img(w);
+        for (int c = 0; c < C; ++c, pc += vc.plane) {
+          w00 |= (uint32_t)__ldg(pc + o00) << (8 * c);
+          w01 |= (uint32_t)__ldg(pc + o01) << (8 * c);
+          w10 |= (uint32_t)__ldg(pc + o10) << (8 * c);
+          w11 |= (uint32_t)__ldg(pc + o11) << (8 * c);
+        }
+      }
+      uint8_t* o = oj + (threadIdx.y + 8 * k) * OST_PITCH + threadIdx.x * C;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < C) {
+          // 2^23 + byte c of each tap (selector: byte c of the tap, zeros, 0x4B)
+          const uint32_t sel = 0x3004u + c;
+          const float b00 = __uint_as_float(__byte_perm(K, w00, sel));
+          const float b01 = __uint_as_float(__byte_perm(K, w01, sel));
+          const float b10 = __uint_as_float(__byte_perm(K, w10, sel));
+          const float b11 = __uint_as_float(__byte_perm(K, w11, sel));
+          o[c] = (uint8_t)blend(b00, b01, b10, b11, tax, tay);
+        }
+      }
+    }
+    n_unc += __popc(__ballot_sync(0xFFFFFFFFu, uncovered));
+  }
+  if (threadIdx.x == 0 && n_unc) atomicAdd(w.d_uncovered, n_unc);
+}
 
 // Phases 2-5 for NV views sharing the geometry (NV = 2: a stereo pair staged
 // together), CT channels (CT = 0: any C in 1..4, read at run time).
 template <int CT, int NV>
 __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& v,
-                                       const ViewPtrs (&vp)[NV], uint32_t* win, uint8_t* ost,
+                                       const wv_view_args* const (&vp)[NV], uint32_t* win, uint8_t* ost,
                                        uint32_t* s_ok, const int (&x0)[K4_PPT],
                                        const int (&y0)[K4_PPT], const float (&ax)[K4_PPT],
                                        const float (&ay)[K4_PPT], int x, int ybase, int xl,
@@ -213,7 +334,7 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
       for (int r = dq.q; r < rows; r += rstep) {
 #pragma unroll
         for (int j = 0; j < NV; ++j)
-          if ((__ldg(vp[j].F + o + (uint32_t)r * vc.wpr0) | mk) != 0xFFFFFFFFu) okb &= ~(1u << j);
+          if ((__ldg(view_fp(*vp[j], vc.wpr0) + o + (uint32_t)r * vc.wpr0) | mk) != 0xFFFFFFFFu) okb &= ~(1u << j);
       }
   }
   if (use_win) {
@@ -226,7 +347,7 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
       for (int r = dq.q; r < rows; r += rstep) {
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-          const uint8_t* src = vp[j].img + so + (uint32_t)r * n;
+          const uint8_t* src = view_img(*vp[j]) + so + (uint32_t)r * n;
           const uint32_t R = __ldg(reinterpret_cast<const uint32_t*>(src));
           const uint32_t G = C > 1 ? __ldg(reinterpret_cast<const uint32_t*>(src + plane)) : 0u;
           const uint32_t B = C > 2 ? __ldg(reinterpret_cast<const uint32_t*>(src + 2 * plane)) : 0u;
@@ -281,78 +402,8 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
         }
       }
     } else {
-      // (4b) general case: per-pixel coverage (only when the box test failed),
-      // longitude wrap / pole clamp, partial tiles
-      unsigned n_unc = 0;
-#pragma unroll
-      for (int k = 0; k < K4_PPT; ++k) {
-        const int y = ybase + 8 * k;
-        const bool live = x < out_w && y < out_h;
-        bool uncovered = false;
-        if (live) {
-          int tx0 = x0[k], ty0 = y0[k];
-          float tax = ax[k], tay = ay[k];
-          if (!covered) {
-            const uint32_t* F = vp[j].F;
-            const int wpr0 = vc.wpr0;
-            const int cl = tax < kNear ? tx0 - 1 : tx0, ch = tax > 1.0f - kNear ? tx0 + 2 : tx0 + 1;
-            const int rl = tay < kNear ? ty0 - 1 : ty0, rh = tay > 1.0f - kNear ? ty0 + 2 : ty0 + 1;
-            const int len = ch - cl + 1;
-            const uint32_t full = (1u << len) - 1u;
-            bool ok = true;
-            for (int yy = rl; yy <= rh; ++yy)
-              ok = ok && fp_bits(F + (uint32_t)min(max(yy, 0), m - 1) * wpr0, cl, len, n) == full;
-            if (!ok) {
-              const Taps t = taps_f64(v, x, y);
-              tx0 = t.x0;
-              ty0 = t.y0;
-              tax = t.ax;
-              tay = t.ay;
-              const uint32_t* r0 = F + (uint32_t)min(max(ty0, 0), m - 1) * wpr0;
-              const uint32_t* r1 = F + (uint32_t)min(max(ty0 + 1, 0), m - 1) * wpr0;
-              uncovered = (fp_bits(r0, tx0, 2, n) & fp_bits(r1, tx0, 2, n)) != 3u;
-            }
-          }
-          uint32_t w00, w01, w10, w11;
-          if (use_win) {
-            WV_ASSERT(ty0 - yl >= 0 && ty0 + 1 - yl < rows && tx0 - wx0 >= 0 && tx0 + 1 - wx0 < P);
-            const uint32_t* p = wj + (ty0 - yl) * P + (tx0 - wx0);
-            w00 = p[0];
-            w01 = p[1];
-            w10 = p[P];
-            w11 = p[P + 1];
-          } else {
-            // longitude wrap / pole clamp (projection.py:146-149)
-            const int xa = wrapx(tx0, n), xb = wrapx(tx0 + 1, n);
-            const int ya = min(max(ty0, 0), m - 1), yb = min(max(ty0 + 1, 0), m - 1);
-            const uint32_t o00 = (uint32_t)ya * n + xa, o01 = (uint32_t)ya * n + xb;
-            const uint32_t o10 = (uint32_t)yb * n + xa, o11 = (uint32_t)yb * n + xb;
-            w00 = w01 = w10 = w11 = 0u;
-            const uint8_t* pc = vp[j].img;
-            for (int c = 0; c < C; ++c, pc += vc.plane) {
-              w00 |= (uint32_t)__ldg(pc + o00) << (8 * c);
-              w01 |= (uint32_t)__ldg(pc + o01) << (8 * c);
-              w10 |= (uint32_t)__ldg(pc + o10) << (8 * c);
-              w11 |= (uint32_t)__ldg(pc + o11) << (8 * c);
-            }
-          }
-          uint8_t* o = oj + (threadIdx.y + 8 * k) * OST_PITCH + threadIdx.x * C;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            if (c < C) {
-              // 2^23 + byte c of each tap (selector: byte c of the tap, zeros, 0x4B)
-              const uint32_t sel = 0x3004u + c;
-              const float b00 = __uint_as_float(__byte_perm(K, w00, sel));
-              const float b01 = __uint_as_float(__byte_perm(K, w01, sel));
-              const float b10 = __uint_as_float(__byte_perm(K, w10, sel));
-              const float b11 = __uint_as_float(__byte_perm(K, w11, sel));
-              o[c] = (uint8_t)blend(b00, b01, b10, b11, tax, tay);
-            }
-          }
-        }
-        n_unc += __popc(__ballot_sync(0xFFFFFFFFu, uncovered));
-      }
-      if (threadIdx.x == 0 && n_unc) atomicAdd(vp[j].uncovered, n_unc);
+      // (4b) general case, out of line (its registers stay out of the fast path)
+      general_view<CT>(vc, v, *vp[j], wj, oj, P, rows, yl, wx0, use_win, covered, x, ybase);
     }
   }
   __syncthreads();
@@ -364,7 +415,7 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
   const uint64_t gofs = ((uint64_t)blockIdx.y * K4_TY * out_w + blockIdx.x * K4_TX) * C;
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
-    uint8_t* gbase = vp[j].out + gofs;
+    uint8_t* gbase = vp[j]->d_out + gofs;
     const uint8_t* oj = ost + j * OST_VIEW;
     if (((reinterpret_cast<uintptr_t>(gbase) | gpitch | rowb) & 15) == 0) {
       const int nv = rowb >> 4;
@@ -385,7 +436,7 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
 
 template <int NV>
 __device__ __forceinline__ void finish_c(const ViewConst& vc, const wv_view_args& v,
-                                         const ViewPtrs (&vp)[NV], uint32_t* win, uint8_t* ost,
+                                         const wv_view_args* const (&vp)[NV], uint32_t* win, uint8_t* ost,
                                          uint32_t* s_ok, const int (&x0)[K4_PPT],
                                          const int (&y0)[K4_PPT], const float (&ax)[K4_PPT],
                                          const float (&ay)[K4_PPT], int x, int ybase, int xl,
@@ -444,29 +495,11 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
   float ax[K4_PPT], ay[K4_PPT];
   int bx0 = 0x7FFFFFFF, bx1 = -0x7FFFFFFF, by0 = 0x7FFFFFFF, by1 = -0x7FFFFFFF;
   {
-    const float u = ((float)x + 0.5f) * vc.inv_w - 1.0f;
-    const float rx = u * vc.tan_h;
-    const float cx = rx * vc.r[0] + vc.r[2], cy = rx * vc.r[3] + vc.r[5], cz = rx * vc.r[6] + vc.r[8];
-    const float r1 = vc.r[1], r4 = vc.r[4], r7 = vc.r[7], tv = vc.tan_v, ih = vc.inv_h;
-    const float sx = vc.sx, sy = vc.sy;
+    const ColGeo cg = col_geo(vc, x);
 #pragma unroll
     for (int k = 0; k < K4_PPT; ++k) {
       const int y = ybase + 8 * k;
-      const float w = 1.0f - ((float)y + 0.5f) * ih;
-      const float ry = w * tv;
-      const float wx = fmaf(ry, r1, cx), wy = fmaf(ry, r4, cy), wz = fmaf(ry, r7, cz);
-      // lon = atan2(x, z); lat = asin(y/|w|) = atan2(y, hypot(x, z))
-      const float lon = fast_atan2(wx, wz) * 57.29577951308232f;
-      const float hz = wx * wx + wz * wz;
-      // (at the poles hz = 0 and fast_atan2(wy, 0) = +-pi/2)
-      const float lat = fast_atan2(wy, sqrt_approx(hz)) * 57.29577951308232f;
-      const float fx = (lon + 180.0f) * sx - 0.5f;
-      const float fy = (90.0f - lat) * sy - 0.5f;
-      const float flx = floorf(fx), fly = floorf(fy);
-      x0[k] = (int)flx;
-      y0[k] = (int)fly;
-      ax[k] = fx - flx;
-      ay[k] = fy - fly;
+      pix_geo(vc, cg, y, x0[k], y0[k], ax[k], ay[k]);
       if (x < out_w && y < out_h) {
         bx0 = min(bx0, x0[k] - 1);
         bx1 = max(bx1, x0[k] + 2);
@@ -497,20 +530,17 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
   const bool box_ok = inside && (xh - xl) < BOX_MAX_W;
   const bool stage = inside && (n & 3) == 0;
   const int nv = shared_n > 0 ? shared_n : 1;
-  auto ptrs = [&](int vi) {
-    // phases of consecutive views are separated by finish's own barriers
-    const wv_view_args& vv = shared_n > 0 ? (DEV ? d_views[vi] : views.v[vi]) : v;
-    return ViewPtrs{vv.d_footprint + (uint64_t)vv.row0 * vc.wpr0,
-                    vv.d_canvas + (uint64_t)vv.row0 * vv.width, vv.d_out, vv.d_uncovered};
+  auto vargs = [&](int vi) -> const wv_view_args* {
+    return shared_n > 0 ? (DEV ? d_views + vi : &views.v[vi]) : &v;
   };
   for (int vi = 0; vi < nv;) {
     if (vi + 1 < nv && stage && 2 * vwords <= WIN_WORDS) {
-      const ViewPtrs vp[2] = {ptrs(vi), ptrs(vi + 1)};
+      const wv_view_args* const vp[2] = {vargs(vi), vargs(vi + 1)};
       finish_c<2>(vc, v, vp, win, ost, s_ok, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
                   box_ok, true, tid);
       vi += 2;
     } else {
-      const ViewPtrs vp[1] = {ptrs(vi)};
+      const wv_view_args* const vp[1] = {vargs(vi)};
       finish_c<1>(vc, v, vp, win, ost, s_ok, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
                   box_ok, stage && vwords <= WIN_WORDS, tid);
       vi += 1;
