@@ -165,6 +165,25 @@ __device__ __forceinline__ uint32_t blend(float b00, float b01, float b10, float
   return __float_as_uint(fmaf(ay, bot - top, top) + 8388608.0f) & 0xFFu;
 }
 
+// blend() of channels 0 and 1 at once with paired FP32 operations (each lane
+// rounds exactly like the scalar code); returns byte 0 | byte 1 << 8.
+__device__ __forceinline__ uint32_t blend2(uint32_t w00, uint32_t w01, uint32_t w10, uint32_t w11,
+                                           float ax, float ay) {
+  const uint32_t K = 0x4B000000u;
+  auto biased = [&](uint32_t w) {   // 2^23 + byte 0, 2^23 + byte 1
+    return make_float2(__uint_as_float(__byte_perm(K, w, 0x3004u)),
+                       __uint_as_float(__byte_perm(K, w, 0x3005u)));
+  };
+  const float2 b00 = biased(w00), b01 = biased(w01), b10 = biased(w10), b11 = biased(w11);
+  const float2 nk = make_float2(-8388608.0f, -8388608.0f);
+  const float2 A = make_float2(ax, ax), B = make_float2(ay, ay);
+  auto neg = [](float2 v) { return make_float2(-v.x, -v.y); };
+  const float2 top = __ffma2_rn(A, __fadd2_rn(b01, neg(b00)), __fadd2_rn(b00, nk));
+  const float2 bot = __ffma2_rn(A, __fadd2_rn(b11, neg(b10)), __fadd2_rn(b10, nk));
+  const float2 v = __fadd2_rn(__ffma2_rn(B, __fadd2_rn(bot, neg(top)), top), neg(nk));
+  return __byte_perm(__float_as_uint(v.x), __float_as_uint(v.y), 0x0040u);
+}
+
 // t / d and t % d for 0 <= t <= 256 and 1 <= d <= 64 without an integer
 // division: (t + 0.5) / d is at least 1/128 away from an integer, far beyond
 // the float error, so the truncation is exact.
@@ -309,8 +328,8 @@ __device__ __noinline__ void general_view(const ViewConst& vc, const wv_view_arg
 template <int CT, int NV>
 __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& v,
                                        const wv_view_args* const (&vp)[NV], uint32_t* win, uint8_t* ost,
-                                       uint32_t* s_ok, const int (&x0)[K4_PPT],
-                                       const int (&y0)[K4_PPT], const float (&ax)[K4_PPT],
+                                       uint32_t* s_ok, const int (&off)[K4_PPT],
+                                       const float (&ax)[K4_PPT],
                                        const float (&ay)[K4_PPT], int x, int ybase, int xl,
                                        int xh, int yl, int yh, int wx0, int ww, bool box_ok,
                                        bool use_win, int tid) {
@@ -385,19 +404,30 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
     if (covered && use_win && full_tile) {
 #pragma unroll
       for (int k = 0; k < K4_PPT; ++k) {
-        WV_ASSERT(y0[k] - yl >= 0 && y0[k] + 1 - yl < rows && x0[k] - wx0 >= 0 &&
-                  x0[k] + 1 - wx0 < P);
-        const uint32_t* p = wj + (y0[k] - yl) * P + (x0[k] - wx0);
+        WV_ASSERT(off[k] >= 0 && off[k] + P + 1 < rows * P);
+        const uint32_t* p = wj + off[k];
         const uint32_t w00 = p[0], w01 = p[1], w10 = p[P], w11 = p[P + 1];
         uint8_t* o = oj + (threadIdx.y + 8 * k) * OST_PITCH + threadIdx.x * C;
+        if (CT == 3) {
+          // channels 0 and 1 as one paired-FP32 stream (same per-lane rounding
+          // as blend()), channel 2 scalar
+          const uint32_t rg = blend2(w00, w01, w10, w11, ax[k], ay[k]);
+          o[0] = (uint8_t)rg;
+          o[1] = (uint8_t)(rg >> 8);
+          o[2] = (uint8_t)blend(__uint_as_float(__byte_perm(K, w00, 0x3006u)),
+                                __uint_as_float(__byte_perm(K, w01, 0x3006u)),
+                                __uint_as_float(__byte_perm(K, w10, 0x3006u)),
+                                __uint_as_float(__byte_perm(K, w11, 0x3006u)), ax[k], ay[k]);
+        } else {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c < C) {
-            const uint32_t sel = 0x3004u + c;
-            o[c] = (uint8_t)blend(__uint_as_float(__byte_perm(K, w00, sel)),
-                                  __uint_as_float(__byte_perm(K, w01, sel)),
-                                  __uint_as_float(__byte_perm(K, w10, sel)),
-                                  __uint_as_float(__byte_perm(K, w11, sel)), ax[k], ay[k]);
+          for (int c = 0; c < 4; ++c) {
+            if (c < C) {
+              const uint32_t sel = 0x3004u + c;
+              o[c] = (uint8_t)blend(__uint_as_float(__byte_perm(K, w00, sel)),
+                                    __uint_as_float(__byte_perm(K, w01, sel)),
+                                    __uint_as_float(__byte_perm(K, w10, sel)),
+                                    __uint_as_float(__byte_perm(K, w11, sel)), ax[k], ay[k]);
+            }
           }
         }
       }
@@ -437,16 +467,16 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
 template <int NV>
 __device__ __forceinline__ void finish_c(const ViewConst& vc, const wv_view_args& v,
                                          const wv_view_args* const (&vp)[NV], uint32_t* win, uint8_t* ost,
-                                         uint32_t* s_ok, const int (&x0)[K4_PPT],
-                                         const int (&y0)[K4_PPT], const float (&ax)[K4_PPT],
+                                         uint32_t* s_ok, const int (&off)[K4_PPT],
+                                         const float (&ax)[K4_PPT],
                                          const float (&ay)[K4_PPT], int x, int ybase, int xl,
                                          int xh, int yl, int yh, int wx0, int ww, bool box_ok,
                                          bool use_win, int tid) {
   if (vc.C == 3)
-    finish<3, NV>(vc, v, vp, win, ost, s_ok, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
+    finish<3, NV>(vc, v, vp, win, ost, s_ok, off, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
                   box_ok, use_win, tid);
   else
-    finish<0, NV>(vc, v, vp, win, ost, s_ok, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
+    finish<0, NV>(vc, v, vp, win, ost, s_ok, off, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
                   box_ok, use_win, tid);
 }
 
@@ -528,6 +558,11 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
   const int ww = ((xh | 3) - wx0 + 1) >> 2;   // 4-pixel words per window row
   const int vwords = inside ? (yh - yl + 1) * 4 * ww : 0x7FFFFFFF;
   const bool box_ok = inside && (xh - xl) < BOX_MAX_W;
+  // window offset of each pixel's (x0, y0) tap (used only when staged; the
+  // general path re-evaluates its geometry)
+  int off[K4_PPT];
+#pragma unroll
+  for (int k = 0; k < K4_PPT; ++k) off[k] = (y0[k] - yl) * (4 * ww) + (x0[k] - wx0);
   const bool stage = inside && (n & 3) == 0;
   const int nv = shared_n > 0 ? shared_n : 1;
   auto vargs = [&](int vi) -> const wv_view_args* {
@@ -536,12 +571,12 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
   for (int vi = 0; vi < nv;) {
     if (vi + 1 < nv && stage && 2 * vwords <= WIN_WORDS) {
       const wv_view_args* const vp[2] = {vargs(vi), vargs(vi + 1)};
-      finish_c<2>(vc, v, vp, win, ost, s_ok, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
+      finish_c<2>(vc, v, vp, win, ost, s_ok, off, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
                   box_ok, true, tid);
       vi += 2;
     } else {
       const wv_view_args* const vp[1] = {vargs(vi)};
-      finish_c<1>(vc, v, vp, win, ost, s_ok, x0, y0, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
+      finish_c<1>(vc, v, vp, win, ost, s_ok, off, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
                   box_ok, stage && vwords <= WIN_WORDS, tid);
       vi += 1;
     }
