@@ -204,8 +204,21 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// n / d by multiply-high with m = ceil(2^32 / d) (exact for n * d < 2^32,
+// far above any item or tile index here); d = 1 is the identity.
+struct FastDiv {
+  uint32_t d, m;
+};
+__host__ __device__ inline FastDiv fast_div(uint32_t d) {
+  return FastDiv{d, d > 1 ? (uint32_t)((0x100000000ull + d - 1) / d) : 0u};
+}
+__device__ __forceinline__ uint32_t operator/(uint32_t n, FastDiv f) {
+  return f.d > 1 ? __umulhi(n, f.m) : n;
+}
+
 struct LevelArgs {
   int k, bh, bw, C, ntx;
+  FastDiv divC, divN;  // by C and by ntx
   const uint32_t* list;
   const uint32_t* count;
   float* out;          // non-final: Y_{k-1} planar C x 2bh x out_pitch
@@ -262,12 +275,13 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   // issue the four box loads of an item (elected thread)
   auto issue = [&](uint32_t it) {
     if (tid != 0) return;
-    const uint32_t tile = a.list[it / C] & ~ZERO_FLAG;
-    const int ty = tile / a.ntx, tx = tile - (tile / a.ntx) * a.ntx;
+    const uint32_t itile = it / a.divC;
+    const uint32_t tile = a.list[itile] & ~ZERO_FLAG;
+    const int ty = (int)(tile / a.divN), tx = (int)tile - ty * a.ntx;
     // TMA faults on unaligned/negative innermost box coordinates (observed on
     // B200, driver 580): x starts at ax-4 clamped to 0
     const int oy = max(ty * TY - HALO, 0), ox = max(tx * TX - XPAD, 0);
-    const int c = (int)(it % C);
+    const int c = (int)(it - itile * C);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&bar, 4u * BOX_FLOATS * 4u);
     tma_load_3d(box, &tm_ll, ox, oy, c, &bar);
@@ -278,10 +292,11 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
 
   bool issued = false;   // the current item's boxes are already in flight
   for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const uint32_t entry = a.list[item / C];
-    const int c = (int)(item % C);
+    const uint32_t itile = item / a.divC;
+    const uint32_t entry = a.list[itile];
+    const int c = (int)(item - itile * C);
     const uint32_t tile = entry & ~ZERO_FLAG;
-    const int ty = tile / a.ntx, tx = tile % a.ntx;
+    const int ty = (int)(tile / a.divN), tx = (int)tile - ty * a.ntx;
     const int ay = ty * TY, ax = tx * TX;
     const int by = min(ay + TY, a.bh), bx = min(ax + TX, a.bw);
     const int ny = 2 * (by - ay), nx = 2 * (bx - ax);
@@ -316,7 +331,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
           }
         }
       }
-      if (tid == 0 && a.use_tma && nxt < nitems) nxt_entry = a.list[nxt / C];
+      if (tid == 0 && a.use_tma && nxt < nitems) nxt_entry = a.list[nxt / a.divC];
     }
     if (a.use_tma) {
       if (!issued) issue(item);
@@ -562,6 +577,8 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
     }
     LevelArgs la{};
     la.k = k; la.bh = lo.H >> k; la.bw = lo.W >> k; la.C = C; la.ntx = lo.ntx[k];
+    la.divC = fast_div((uint32_t)C);
+    la.divN = fast_div((uint32_t)lo.ntx[k]);
     la.use_tma = (la.bw % 4) == 0;
     la.ll_ptr = k < L ? (const float*)(ws + lo.ybuf[k]) : plane;
     la.ll_pitch = k < L ? lo.ypitch[k] : lo.W;
