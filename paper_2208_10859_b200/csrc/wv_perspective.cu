@@ -204,9 +204,8 @@ __device__ __forceinline__ const uint8_t* view_img(const wv_view_args& w) {
   return w.d_canvas + (uint64_t)w.row0 * w.width;
 }
 
-// float32 geometry of output pixel (x, y): the column part (camera ray x
-// component through the rotation) and the per-pixel rest.  The general path
-// re-evaluates it with the same code, so both see identical taps.
+// float32 geometry of output column x: the camera ray's x component through
+// the rotation.
 struct ColGeo {
   float cx, cy, cz;
 };
@@ -215,24 +214,94 @@ __device__ __forceinline__ ColGeo col_geo(const ViewConst& vc, int x) {
   const float rx = u * vc.tan_h;
   return ColGeo{rx * vc.r[0] + vc.r[2], rx * vc.r[3] + vc.r[5], rx * vc.r[6] + vc.r[8]};
 }
-__device__ __forceinline__ void pix_geo(const ViewConst& vc, const ColGeo& cg, int y, int& x0,
-                                        int& y0, float& ax, float& ay) {
-  const float w = 1.0f - ((float)y + 0.5f) * vc.inv_h;
-  const float ry = w * vc.tan_v;
-  const float wx = fmaf(ry, vc.r[1], cg.cx), wy = fmaf(ry, vc.r[4], cg.cy),
-              wz = fmaf(ry, vc.r[7], cg.cz);
-  // lon = atan2(x, z); lat = asin(y/|w|) = atan2(y, hypot(x, z))
-  const float lon = fast_atan2(wx, wz) * 57.29577951308232f;
-  const float hz = wx * wx + wz * wz;
-  // (at the poles hz = 0 and fast_atan2(wy, 0) = +-pi/2)
-  const float lat = fast_atan2(wy, sqrt_approx(hz)) * 57.29577951308232f;
-  const float fx = (lon + 180.0f) * vc.sx - 0.5f;
-  const float fy = (90.0f - lat) * vc.sy - 0.5f;
-  const float flx = floorf(fx), fly = floorf(fy);
-  x0 = (int)flx;
-  y0 = (int)fly;
-  ax = fx - flx;
-  ay = fy - fly;
+__device__ __forceinline__ float2 f2v(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 neg2(float2 v) { return make_float2(-v.x, -v.y); }
+__device__ __forceinline__ float sel(bool c, float a, float b) { return c ? a : b; }
+
+// fast_atan2 of two lanes, the arithmetic as paired FP32 operations (the
+// per-lane selects, min/max and reciprocals stay scalar)
+__device__ __forceinline__ float2 fast_atan2_x2(float2 y, float2 x) {
+  const float2 ax = make_float2(fabsf(x.x), fabsf(x.y)), ay = make_float2(fabsf(y.x), fabsf(y.y));
+  const float2 mx = make_float2(fmaxf(ax.x, ay.x), fmaxf(ax.y, ay.y));
+  const float2 mn = make_float2(fminf(ax.x, ay.x), fminf(ax.y, ay.y));
+  float2 a = __fmul2_rn(mn, make_float2(rcp_approx(mx.x), rcp_approx(mx.y)));
+  a = make_float2(sel(mx.x > 1e-30f, a.x, 0.0f), sel(mx.y > 1e-30f, a.y, 0.0f));   // atan2(0, 0) = 0
+  const float2 s = __fmul2_rn(a, a);
+  float2 p = f2v(-0.004054488614201546f);
+  p = __ffma2_rn(p, s, f2v(0.021862687543034554f));
+  p = __ffma2_rn(p, s, f2v(-0.05591195821762085f));
+  p = __ffma2_rn(p, s, f2v(0.09642171859741211f));
+  p = __ffma2_rn(p, s, f2v(-0.13908620178699493f));
+  p = __ffma2_rn(p, s, f2v(0.19946563243865967f));
+  p = __ffma2_rn(p, s, f2v(-0.33329859375953674f));
+  p = __ffma2_rn(p, s, f2v(0.9999993443489075f));
+  float2 r = __fmul2_rn(a, p);
+  const float2 rc = __fadd2_rn(f2v(1.5707963267948966f), neg2(r));
+  r = make_float2(sel(ay.x > ax.x, rc.x, r.x), sel(ay.y > ax.y, rc.y, r.y));
+  const float2 rp = __fadd2_rn(f2v(3.141592653589793f), neg2(r));
+  r = make_float2(sel(x.x < 0.0f, rp.x, r.x), sel(x.y < 0.0f, rp.y, r.y));
+  return make_float2(copysignf(r.x, y.x), copysignf(r.y, y.y));
+}
+
+// float32 tap geometry of the thread's K4_PPT pixels (column x, rows
+// ybase + 8k) (WV_K4_GEO2: two rows per paired-FP32 stream).  The fast path and the
+// general path both use this function, so they see identical taps.
+__device__ __forceinline__ void geo_all(const ViewConst& vc, int x, int ybase, int (&x0)[K4_PPT],
+                                        int (&y0)[K4_PPT], float (&ax)[K4_PPT],
+                                        float (&ay)[K4_PPT]) {
+  const ColGeo cg = col_geo(vc, x);
+  const float kdeg = 57.29577951308232f;
+#if !WV_K4_GEO2
+#pragma unroll
+  for (int k = 0; k < K4_PPT; ++k) {
+    const float w = 1.0f - ((float)(ybase + 8 * k) + 0.5f) * vc.inv_h;
+    const float ry = w * vc.tan_v;
+    const float wx = fmaf(ry, vc.r[1], cg.cx), wy = fmaf(ry, vc.r[4], cg.cy),
+                wz = fmaf(ry, vc.r[7], cg.cz);
+    // lon = atan2(x, z); lat = asin(y/|w|) = atan2(y, hypot(x, z))
+    const float lon = fast_atan2(wx, wz) * kdeg;
+    const float hz = wx * wx + wz * wz;
+    // (at the poles hz = 0 and fast_atan2(wy, 0) = +-pi/2)
+    const float lat = fast_atan2(wy, sqrt_approx(hz)) * kdeg;
+    const float fx = (lon + 180.0f) * vc.sx - 0.5f;
+    const float fy = (90.0f - lat) * vc.sy - 0.5f;
+    const float flx = floorf(fx), fly = floorf(fy);
+    x0[k] = (int)flx;
+    y0[k] = (int)fly;
+    ax[k] = fx - flx;
+    ay[k] = fy - fly;
+  }
+#else
+#pragma unroll
+  for (int k = 0; k < K4_PPT; k += 2) {
+    const float2 yc = __fadd2_rn(make_float2((float)(ybase + 8 * k), (float)(ybase + 8 * k + 8)),
+                                 f2v(0.5f));
+    const float2 w = __ffma2_rn(neg2(yc), f2v(vc.inv_h), f2v(1.0f));
+    const float2 ry = __fmul2_rn(w, f2v(vc.tan_v));
+    const float2 wx = __ffma2_rn(ry, f2v(vc.r[1]), f2v(cg.cx));
+    const float2 wy = __ffma2_rn(ry, f2v(vc.r[4]), f2v(cg.cy));
+    const float2 wz = __ffma2_rn(ry, f2v(vc.r[7]), f2v(cg.cz));
+    // lon = atan2(x, z); lat = asin(y/|w|) = atan2(y, hypot(x, z))
+    const float2 lon = __fmul2_rn(fast_atan2_x2(wx, wz), f2v(kdeg));
+    const float2 hz = __ffma2_rn(wx, wx, __fmul2_rn(wz, wz));
+    // (at the poles hz = 0 and fast_atan2(wy, 0) = +-pi/2)
+    const float2 lat = __fmul2_rn(
+        fast_atan2_x2(wy, make_float2(sqrt_approx(hz.x), sqrt_approx(hz.y))), f2v(kdeg));
+    const float2 fx = __ffma2_rn(__fadd2_rn(lon, f2v(180.0f)), f2v(vc.sx), f2v(-0.5f));
+    const float2 fy = __ffma2_rn(__fadd2_rn(f2v(90.0f), neg2(lat)), f2v(vc.sy), f2v(-0.5f));
+    const float2 fl = make_float2(floorf(fx.x), floorf(fx.y));
+    const float2 gl = make_float2(floorf(fy.x), floorf(fy.y));
+    const float2 fa = __fadd2_rn(fx, neg2(fl)), ga = __fadd2_rn(fy, neg2(gl));
+    x0[k] = (int)fl.x;
+    x0[k + 1] = (int)fl.y;
+    y0[k] = (int)gl.x;
+    y0[k + 1] = (int)gl.y;
+    ax[k] = fa.x;
+    ax[k + 1] = fa.y;
+    ay[k] = ga.x;
+    ay[k + 1] = ga.y;
+  }
+#endif
 }
 
 // Phase 4 for one view when the CTA-uniform fast path does not apply:
@@ -249,7 +318,9 @@ __device__ __noinline__ void general_view(const ViewConst& vc, const wv_view_arg
   const int C = CT ? CT : vc.C;
   const int m = vc.m, n = vc.n, out_w = vc.out_w, out_h = vc.out_h;
   const uint32_t K = 0x4B000000u;
-  const ColGeo cg = col_geo(vc, x);
+  int gx0[K4_PPT], gy0[K4_PPT];
+  float gax[K4_PPT], gay[K4_PPT];
+  geo_all(vc, x, ybase, gx0, gy0, gax, gay);
   unsigned n_unc = 0;
 #pragma unroll
   for (int k = 0; k < K4_PPT; ++k) {
@@ -257,9 +328,8 @@ __device__ __noinline__ void general_view(const ViewConst& vc, const wv_view_arg
     const bool live = x < out_w && y < out_h;
     bool uncovered = false;
     if (live) {
-      int tx0, ty0;
-      float tax, tay;
-      pix_geo(vc, cg, y, tx0, ty0, tax, tay);
+      int tx0 = gx0[k], ty0 = gy0[k];
+      float tax = gax[k], tay = gay[k];
       if (!covered) {
         const uint32_t* F = view_fp(w, vc.wpr0);
         const int wpr0 = vc.wpr0;
@@ -344,7 +414,7 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
   uint32_t okb = box_ok ? (1u << NV) - 1u : 0u;   // bit j: view j's box covered so far
   if (box_ok) {
     const int w0 = xl >> 5, nw = (xh >> 5) - w0 + 1;
-    const float inv = __frcp_rn((float)nw);
+    const float inv = rcp_approx((float)nw);
     const SmallDiv dq = small_div(tid, nw, inv);
     const int q = dq.r, rstep = small_div(256, nw, inv).q, wd = w0 + q;
     const uint32_t mk = ~range_bits(xl, xh + 1, wd);
@@ -358,7 +428,7 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
   }
   if (use_win) {
     const uint32_t plane = vc.plane;
-    const float inv = __frcp_rn((float)ww);
+    const float inv = rcp_approx((float)ww);
     const SmallDiv dq = small_div(tid, ww, inv);
     const int q = dq.r, rstep = small_div(256, ww, inv).q;
     const uint32_t so = (uint32_t)yl * n + wx0 + 4 * q;
@@ -524,12 +594,11 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
   int x0[K4_PPT], y0[K4_PPT];
   float ax[K4_PPT], ay[K4_PPT];
   int bx0 = 0x7FFFFFFF, bx1 = -0x7FFFFFFF, by0 = 0x7FFFFFFF, by1 = -0x7FFFFFFF;
+  geo_all(vc, x, ybase, x0, y0, ax, ay);
   {
-    const ColGeo cg = col_geo(vc, x);
 #pragma unroll
     for (int k = 0; k < K4_PPT; ++k) {
       const int y = ybase + 8 * k;
-      pix_geo(vc, cg, y, x0[k], y0[k], ax[k], ay[k]);
       if (x < out_w && y < out_h) {
         bx0 = min(bx0, x0[k] - 1);
         bx1 = max(bx1, x0[k] + 2);
