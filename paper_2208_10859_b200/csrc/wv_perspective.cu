@@ -12,6 +12,10 @@
 namespace wv {
 namespace {
 
+#ifndef WV_K4_GEO2
+#define WV_K4_GEO2 1     // tap geometry two rows per paired-FP32 stream (0: scalar, ~1% slower)
+#endif
+
 constexpr double kRad2Deg = 57.29577951308232;  // numpy.degrees factor 180/pi
 
 constexpr int kMaxViews = 4;
