@@ -22,6 +22,7 @@
  *                        + u8 conversion                   decoding.py:301
  *   wv_decode_frame      DecodeSession._decode (all of the above)
  *   wv_render_perspective render_perspective               projection.py:111-172
+ *   wv_encode_set        encode_video, one set (mirror path) encoding.py:377-425
  *
  * Conventions: plain pointers and sizes only.  Every pointer named d_* or
  * documented as "device" is CUDA device memory owned by the caller; the
@@ -40,7 +41,7 @@
 extern "C" {
 #endif
 
-#define WV_ABI_VERSION 2
+#define WV_ABI_VERSION 3
 #define WV_MAX_LEVELS 12
 
 enum wv_status {
@@ -211,6 +212,43 @@ int wv_file_set_read(const char* path, int set_index, wv_set_info* set, float* e
  * (>= payload_length bytes; pinned host memory serves both a whole-set
  * upload and WV_FLAG_FETCH's h_payload). */
 int wv_file_payload_read(const char* path, int set_index, void* buf, uint64_t buf_bytes);
+
+/* ---- Encoder: one inter-frame set ----
+ * Replaces the per-set body of the reference encoder, encode_video
+ * (encoding.py:377-425): analyze_2d (wavelets.py:128-149), sparsify
+ * (encoding.py:118-135), haar_time_forward (:153-169), temporal_threshold
+ * (:198-236), compute_extrema (:239-254), quantize (:296-332) and the record
+ * order / BlockEnd counts (fileio.py:142-165).  Output bytes equal the
+ * reference's (the golden sha256 manifest).  Thresholds are passed as the
+ * float32 values the reference compares against:
+ *   level_threshold[k-1] = float32(threshold_value(alpha, k-1, levels)), k = 1..levels
+ *   row_factor[y]        = float32 equirect H(y) (encoding.py:359-362), or 0 (no mapping)
+ *   temporal_threshold[t] = float32(threshold_value(inter_threshold,
+ *                             temporal_level_of(t, n) - 1, log2 n)), t = 1..n-1 */
+#define WV_ENC_MAX_N 64
+typedef struct wv_encode_params {
+  int32_t width, height, channels;  /* frame size (width, height divisible by 2^levels and block_size) */
+  int32_t levels;                   /* spatial DWT levels, 1..WV_MAX_LEVELS */
+  int32_t inter_size;               /* n frames per set: power of two, <= WV_ENC_MAX_N */
+  int32_t block_size;               /* power of two dividing width and height, <= 32 */
+  int32_t quantize;                 /* 1: u8 records, 0: float32 records (FLAG_FLOAT) */
+  int32_t reserved;
+  float level_threshold[WV_MAX_LEVELS];
+  float temporal_threshold[WV_ENC_MAX_N];
+} wv_encode_params;
+
+/* Device workspace bytes for wv_encode_set, and the payload capacity that
+ * can never overflow (every coefficient a record). */
+int wv_encode_workspace_bytes(const wv_encode_params* p, uint64_t* bytes);
+int wv_encode_payload_capacity(const wv_encode_params* p, uint64_t* bytes);
+/* d_frames: n x H x W x C u8 (device), d_row_factor: H float32 (device).
+ * Outputs (device): d_extrema (n, C, 4) float32, d_counts (n, NB) u32
+ * records per (temporal index, block), d_payload packed records in
+ * (t, block, layer, offset) order, d_num_records (1 x u64). */
+int wv_encode_set(const wv_encode_params* p, const uint8_t* d_frames, const float* d_row_factor,
+                  void* d_workspace, uint64_t workspace_bytes, float* d_extrema,
+                  uint32_t* d_counts, uint8_t* d_payload, uint64_t payload_capacity,
+                  uint64_t* d_num_records, void* stream);
 
 /* Views into the workspace for parity tests (no launches). */
 int wv_plane_view(const wv_geometry* g, void* d_workspace, float** d_plane);

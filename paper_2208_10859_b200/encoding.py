@@ -318,11 +318,74 @@ def _encode_set(frames: torch.Tensor, p: EncodeParams, levels: int,
     return EncodedSet(records=rec, extrema=ext.cpu().numpy())
 
 
+def _encode_set_native(chunk: torch.Tensor, p: EncodeParams, levels: int, hfac: np.ndarray,
+                       keep_arrays: bool) -> EncodedSet:
+    """One set through the CUDA encoder (wv_encode_set, csrc/wv_encode.cu):
+    (n, H, W, C) u8 on the device -> packed records, counts, extrema."""
+    import ctypes as C
+    from . import _native as nat
+    lib = nat.load()
+    n, h, w, c = chunk.shape
+    dev = chunk.device
+    ep = nat.EncodeParams()
+    ep.width, ep.height, ep.channels, ep.levels = w, h, c, levels
+    ep.inter_size, ep.block_size, ep.quantize = n, p.block_size, int(p.quantize)
+    if n > nat.WV_ENC_MAX_N or levels > nat.WV_MAX_LEVELS:
+        raise EncodeError("set geometry outside the CUDA encoder's limits")
+    for k in range(1, levels + 1):
+        ep.level_threshold[k - 1] = float(np.float32(threshold_value(p.alpha, k - 1, levels)))
+    if n > 1:
+        big = int(math.log2(n))
+        for ti in range(1, n):
+            ep.temporal_threshold[ti] = float(np.float32(threshold_value(
+                p.inter_threshold, temporal_level_of(ti, n) - 1, big)))
+    ws_bytes, cap = C.c_uint64(), C.c_uint64()
+    nat.check(lib.wv_encode_workspace_bytes(C.byref(ep), C.byref(ws_bytes)), "wv_encode_workspace_bytes")
+    nat.check(lib.wv_encode_payload_capacity(C.byref(ep), C.byref(cap)), "wv_encode_payload_capacity")
+    frames = chunk.contiguous()
+    rowf = torch.as_tensor(np.asarray(hfac, np.float32), device=dev).contiguous()
+    ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=dev)
+    nb = (w // p.block_size) * (h // p.block_size)
+    ext = torch.empty((n, c, 4), dtype=_F, device=dev)
+    counts = torch.empty((n, nb), dtype=torch.int32, device=dev)
+    payload = torch.empty(cap.value, dtype=torch.uint8, device=dev)
+    nrec = torch.zeros(1, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    nat.check(lib.wv_encode_set(C.byref(ep), C.c_void_p(frames.data_ptr()),
+                                C.c_void_p(rowf.data_ptr()), C.c_void_p(ws.data_ptr()),
+                                C.c_uint64(ws_bytes.value), C.c_void_p(ext.data_ptr()),
+                                C.c_void_p(counts.data_ptr()), C.c_void_p(payload.data_ptr()),
+                                C.c_uint64(cap.value), C.c_void_p(nrec.data_ptr()),
+                                C.c_void_p(stream)), "wv_encode_set")
+    r = int(nrec.item())
+    rs = 2 + c if p.quantize else 2 + 4 * c
+    packed = payload[:r * rs].cpu().numpy().tobytes()
+    del ws, payload
+    rec = SparseCoefficients(
+        temporal=np.zeros(0, np.uint8), block=np.zeros(0, np.uint32),
+        offset=np.zeros(r, np.uint16),
+        values=np.zeros((0, c), np.float32 if not p.quantize else np.uint8),
+        packed=packed, counts=counts.cpu().numpy().astype(np.int64))
+    if keep_arrays:
+        arr = np.frombuffer(packed, np.dtype([("o", "<u2"), ("v", "<f4" if not p.quantize else "u1", (c,))]))
+        cnt = rec.counts.reshape(-1)
+        keys = np.repeat(np.arange(n * nb, dtype=np.int64), cnt)
+        rec.temporal = (keys // nb).astype(np.uint8)
+        rec.block = (keys % nb).astype(np.uint32)
+        rec.offset = arr["o"].copy()
+        rec.values = arr["v"].copy()
+    return EncodedSet(records=rec, extrema=ext.cpu().numpy())
+
+
 def encode_video(frames, params: EncodeParams, device=None,
-                 keep_arrays: bool = True) -> EncodedVideo:
+                 keep_arrays: bool = True, backend: str = "native") -> EncodedVideo:
     """Encode (F, H, W[, C]) uint8 frames into sparse sets
     (encoding.py:377-425).  ``frames`` may be a numpy array or a torch
-    tensor (already on ``device``)."""
+    tensor (already on ``device``).  On a CUDA device the sets go through the
+    CUDA encoder (``backend="native"``, csrc/wv_encode.cu); ``backend="torch"``
+    (and every CPU encode) runs the torch restatement below."""
+    if backend not in ("native", "torch"):
+        raise EncodeError(f"unknown backend {backend!r}")
     if isinstance(frames, np.ndarray):
         x = torch.from_numpy(np.ascontiguousarray(frames))
     else:
@@ -343,6 +406,10 @@ def encode_video(frames, params: EncodeParams, device=None,
     for s0 in range(0, count + pad, n):
         idx = [min(i, count - 1) for i in range(s0, s0 + n)]
         chunk = x[idx].to(dev)                                   # (n, H, W, C) u8
+        if dev.type == "cuda" and backend == "native":
+            sets.append(_encode_set_native(chunk, params, levels, hfac, keep_arrays))
+            del chunk
+            continue
         if k255 is None:
             k255 = torch.tensor(255.0, dtype=_F, device=dev)
         f = (chunk.to(_F) / k255).permute(0, 3, 1, 2).contiguous()
