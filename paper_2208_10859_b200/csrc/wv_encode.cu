@@ -11,15 +11,15 @@
 // uses explicit _rn intrinsics), so the payload bytes equal the reference's.
 //
 // Kernels (one set, n frames, C channels, H x W):
-//   E1 k_load      u8 (n, H, W, C) -> float32 planes (n, C, H, W), x / 255
-//   E2 k_rows /    per level: CDF 9/7 analysis along rows (planes -> tmp),
+//   E2 k_rows /    per level: CDF 9/7 analysis along rows (planes -> tmp;
+//      k_rows_u8   level 1 reads the u8 frames directly, x / 255),
 //      k_cols      then along columns (tmp -> planes); each thread lifts a
 //                  16-pair segment from a 2-pair halo (analysis support)
-//   E3 k_point     per position: spatial threshold of each frame (channel
-//                  max magnitude vs level threshold + H(y)), temporal Haar
-//                  forward in Mallat order, temporal threshold
-//   E4 k_extrema   per (t, c): approximation / detail min and max
-//   E5 k_count     per (t, block): nonzero positions -> counts
+//   E3 k_point     per 32x32 block, per position: spatial threshold of each
+//                  frame (channel max magnitude vs level threshold + H(y)),
+//                  temporal Haar forward in Mallat order, temporal
+//                  threshold; emits nonzero bits, (t, block) record counts
+//                  and the per-(t, c) approximation / detail extrema
 //   E6 k_scan*     exclusive scan of the counts -> first record of each block
 //   E7 k_emit      per (t, block): rank by (layer, offset), quantise, write
 #include <cuda_runtime.h>
@@ -45,7 +45,7 @@ constexpr int SEG = 16;         // output pairs per lifting segment
 constexpr int LOC = SEG + 4;    // local pairs: 2-pair halo left, 2 right
 
 struct EncLayout {
-  size_t planes, tmp, starts, ext_bits, partials, total;
+  size_t planes, tmp, starts, ext_bits, partials, nzbits, total;
 };
 
 __host__ __device__ inline int nb_x(const wv_encode_params& p) { return p.width / p.block_size; }
@@ -68,23 +68,9 @@ EncLayout enc_layout(const wv_encode_params& p) {
   L.starts = take(nblk * 8);
   L.ext_bits = take((size_t)p.inter_size * p.channels * 4 * 4);
   L.partials = take(((nblk + 1023) / 1024 + 1) * 8);
+  L.nzbits = take(nblk * ((size_t)(p.block_size * p.block_size + 31) / 32) * 4);
   L.total = off;
   return L;
-}
-
-// ---------------------------------------------------------------- E1
-
-__global__ void k_load(const uint8_t* __restrict__ in, float* __restrict__ out, int n, int C,
-                       int H, int W) {
-  const size_t plane = (size_t)H * W;
-  const size_t total = plane * n;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const size_t t = i / plane, pix = i - t * plane;
-    const uint8_t* src = in + i * C;
-    for (int c = 0; c < C; ++c)
-      out[(t * C + c) * plane + pix] = __fdiv_rn((float)src[c], 255.0f);   // chunk / 255
-  }
 }
 
 // ---------------------------------------------------------------- E2
@@ -132,30 +118,139 @@ __device__ __forceinline__ void analyze_segment(int M, int a, Load load, Store s
     if (lo + j < M) store(lo + j, __fmul_rn(s[j], kIK), __fmul_rn(d[j], kK));
 }
 
-// Row pass of one level: every row of the h x w region of every plane;
-// thread = (row, segment).  src / dst planes have pitch W.
-__global__ void k_rows(const float* __restrict__ src, float* __restrict__ dst, int planes, int H,
-                       int W, int h, int w) {
-  const int M = w / 2, nseg = (M + SEG - 1) / SEG;
-  const size_t total = (size_t)planes * h * nseg;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const int sg = (int)(i % nseg);
-    const size_t row = i / nseg;
+// Row pass of one level: every row of the h x w region of every plane.  A
+// warp takes a chunk of RCH pairs of one row: it stages the chunk plus its
+// 2-pair halos in shared memory with coalesced loads, each lane lifts one
+// 16-pair segment from there, and the s / d halves go back through shared
+// memory to coalesced stores.  Shared pair index p is padded to p + p / 16
+// (conflict-free 8-byte accesses per half-warp).
+constexpr int RCH = 32 * SEG;                       // pairs per warp chunk
+constexpr int RSM = RCH + 4 + (RCH + 4) / 16 + 1;   // padded float2 slots
+__device__ __forceinline__ int rpad(int p) { return p + (p >> 4); }
+
+__global__ void __launch_bounds__(256) k_rows(const float* __restrict__ src, float* __restrict__ dst,
+                                              int planes, int H, int W, int h, int w) {
+  __shared__ float2 sm[8][RSM];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  float2* buf = sm[wp];
+  float* outs = reinterpret_cast<float*>(buf);            // reused for the outputs
+  const int M = w / 2, nch = (M + RCH - 1) / RCH;
+  const size_t total = (size_t)planes * h * nch;
+  for (size_t it = (size_t)blockIdx.x * 8 + wp; it < total; it += (size_t)gridDim.x * 8) {
+    const int ch = (int)(it % nch);
+    const size_t row = it / nch;
     const size_t pl = row / h, y = row - pl * h;
-    const float* in = src + (pl * H + y) * W;
+    const float2* in = reinterpret_cast<const float2*>(src + (pl * H + y) * W);
     float* out = dst + (pl * H + y) * W;
-    analyze_segment(
-        M, sg * SEG,
-        [&](int g, float& s, float& d) {
-          const float2 v = *reinterpret_cast<const float2*>(in + 2 * g);
-          s = v.x;
-          d = v.y;
-        },
-        [&](int g, float s, float d) {
-          out[g] = s;
-          out[M + g] = d;
-        });
+    const int c0 = ch * RCH;                 // first pair of the chunk
+    // stage pairs [c0 - 2, c0 + RCH + 2) (in range only)
+    for (int q = lane; q < RCH + 4; q += 32) {
+      const int g = c0 - 2 + q;
+      if (g >= 0 && g < M) buf[rpad(q)] = in[g];
+    }
+    __syncwarp();
+    float sv[SEG], dv[SEG];
+    const int a = c0 + lane * SEG;
+    if (a < M) {
+      analyze_segment(
+          M, a,
+          [&](int g, float& s, float& d) {
+            const float2 v = buf[rpad(g - (c0 - 2))];
+            s = v.x;
+            d = v.y;
+          },
+          [&](int g, float s, float d) {
+            sv[g - a] = s;
+            dv[g - a] = d;
+          });
+    }
+    __syncwarp();
+    // outputs: s at pair slots [0, RCH), d at [RCH, 2 RCH) of the float view
+    if (a < M) {
+#pragma unroll
+      for (int j = 0; j < SEG; ++j) {
+        if (a + j < M) {
+          outs[rpad(lane * SEG + j)] = sv[j];
+          outs[RSM + rpad(lane * SEG + j)] = dv[j];
+        }
+      }
+    }
+    __syncwarp();
+    const int cnt = min(RCH, M - c0);
+    for (int q = lane; q < cnt; q += 32) {
+      out[c0 + q] = outs[rpad(q)];
+      out[M + c0 + q] = outs[RSM + rpad(q)];
+    }
+    __syncwarp();
+  }
+}
+
+// Level-1 row pass fused with the u8 load (E1): a warp takes a chunk of one
+// frame row, stages its bytes (all C channels interleaved, as stored) once,
+// and lifts every channel from them; x / 255 comes from a 256-entry table of
+// the IEEE quotients (chunk / 255, encoding.py:413).  4 warps per CTA.
+constexpr int UCH = RCH;                               // pairs per warp chunk
+__global__ void __launch_bounds__(128) k_rows_u8(const uint8_t* __restrict__ frames,
+                                                 float* __restrict__ dst, int n, int C, int H,
+                                                 int W) {
+  __shared__ float s_q[256];
+  __shared__ __align__(16) uint8_t sb[4][(UCH + 4) * 2 * 4 + 16];
+  __shared__ float so[4][2 * RSM];
+  for (int i = threadIdx.x; i < 256; i += 128) s_q[i] = __fdiv_rn((float)i, 255.0f);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  uint8_t* bb = sb[wp];
+  float* outs = so[wp];
+  const int M = W / 2, nch = (M + UCH - 1) / UCH;
+  const size_t plane = (size_t)H * W;
+  const size_t total = (size_t)n * H * nch;
+  for (size_t it = (size_t)blockIdx.x * 4 + wp; it < total; it += (size_t)gridDim.x * 4) {
+    const int ch = (int)(it % nch);
+    const size_t row = it / nch;               // t * H + y
+    const size_t t = row / H, y = row - t * H;
+    const int c0 = ch * UCH;
+    const int g0 = c0 - 2 < 0 ? 0 : c0 - 2;                 // first staged pair
+    const int g1 = c0 + UCH + 2 > M ? M : c0 + UCH + 2;     // one past the last
+    const uint8_t* src = frames + ((t * H + y) * W + 2 * (size_t)g0) * C;
+    const int nbytes = (g1 - g0) * 2 * C;
+    // 4-byte words from the aligned-down start; byte b of the chunk is bb[mis + b]
+    const int mis = (int)(reinterpret_cast<uintptr_t>(src) & 3u);
+    const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(src - mis);
+    const int nw = (mis + nbytes + 3) >> 2;
+    for (int q = lane; q < nw; q += 32) reinterpret_cast<uint32_t*>(bb)[q] = wsrc[q];
+    __syncwarp();
+    const int a = c0 + lane * SEG;
+    for (int c = 0; c < C; ++c) {
+      float sv[SEG], dv[SEG];
+      if (a < M) {
+        analyze_segment(
+            M, a,
+            [&](int g, float& sx, float& dx) {
+              const int b = mis + (g - g0) * 2 * C + c;
+              sx = s_q[bb[b]];
+              dx = s_q[bb[b + C]];
+            },
+            [&](int g, float sx, float dx) {
+              sv[g - a] = sx;
+              dv[g - a] = dx;
+            });
+#pragma unroll
+        for (int j = 0; j < SEG; ++j) {
+          if (a + j < M) {
+            outs[rpad(lane * SEG + j)] = sv[j];
+            outs[RSM + rpad(lane * SEG + j)] = dv[j];
+          }
+        }
+      }
+      __syncwarp();
+      float* out = dst + (t * C + c) * plane + y * W;
+      const int cnt = min(UCH, M - c0);
+      for (int q = lane; q < cnt; q += 32) {
+        out[c0 + q] = outs[rpad(q)];
+        out[M + c0 + q] = outs[RSM + rpad(q)];
+      }
+      __syncwarp();
+    }
   }
 }
 
@@ -206,65 +301,6 @@ __device__ __forceinline__ int position_level(int y, int x, int H, int W, int L,
   return 0;
 }
 
-// Per (y, x): sparsify each frame (encoding.py:118-135: keep iff the channel
-// max magnitude exceeds level threshold + H(y); the approximation is kept),
-// temporal Haar forward in Mallat order (:153-169: a = (x0 + x1) * 0.5,
-// d = (x0 - x1) * 0.5, details of the finest temporal level last), then
-// zero temporal details whose channel max magnitude is <= their threshold
-// (:198-236; the approximation band is exempt).
-__global__ void k_point(float* __restrict__ planes, const float* __restrict__ row_factor,
-                        wv_encode_params p) {
-  const int H = p.height, W = p.width, C = p.channels, n = p.inter_size, L = p.levels;
-  const size_t plane = (size_t)H * W;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < plane;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const int y = (int)(i / W), x = (int)(i - (size_t)y * W);
-    int yy;
-    const int k = position_level(y, x, H, W, L, yy);
-    float v[WV_ENC_MAX_N][4];
-    for (int t = 0; t < n; ++t) {
-      float m = 0.0f;
-      for (int c = 0; c < C; ++c) {
-        v[t][c] = planes[(size_t)(t * C + c) * plane + i];
-        m = fmaxf(m, fabsf(v[t][c]));
-      }
-      if (k > 0) {
-        const int ry = min(yy << k, H - 1);
-        const float thr = __fadd_rn(p.level_threshold[k - 1], row_factor[ry]);
-        if (!(m > thr))
-          for (int c = 0; c < C; ++c) v[t][c] = 0.0f;
-      }
-    }
-    // temporal Haar forward (in place over a scratch copy)
-    float out[WV_ENC_MAX_N][4];
-    int cur = n, end = n;
-    while (cur > 1) {
-      const int half = cur / 2;
-      for (int q = 0; q < half; ++q)
-        for (int c = 0; c < C; ++c) {
-          const float a0 = v[2 * q][c], a1 = v[2 * q + 1][c];
-          out[end - half + q][c] = __fmul_rn(__fsub_rn(a0, a1), 0.5f);
-          v[q][c] = __fmul_rn(__fadd_rn(a0, a1), 0.5f);
-        }
-      end -= half;
-      cur = half;
-    }
-    for (int c = 0; c < C; ++c) out[0][c] = v[0][c];
-    const bool approx = k == 0;
-    for (int t = 0; t < n; ++t) {
-      bool kill = false;
-      if (t >= 1 && !approx) {
-        float m = 0.0f;
-        for (int c = 0; c < C; ++c) m = fmaxf(m, fabsf(out[t][c]));
-        kill = m <= p.temporal_threshold[t];
-      }
-      for (int c = 0; c < C; ++c) planes[(size_t)(t * C + c) * plane + i] = kill ? 0.0f : out[t][c];
-    }
-  }
-}
-
-// ---------------------------------------------------------------- E4
-
 // float -> unsigned key with the float order (for atomicMin / atomicMax)
 __device__ __forceinline__ uint32_t fkey(float f) {
   const uint32_t b = __float_as_uint(f);
@@ -280,46 +316,178 @@ __global__ void k_ext_init(uint32_t* keys, int count) {
   if (i < count) keys[i] = (i & 1) ? 0u : 0xFFFFFFFFu;
 }
 
-__global__ void k_extrema(const float* __restrict__ planes, uint32_t* keys, int H, int W, int L) {
-  const int pl = blockIdx.y;   // t * C + c
-  const size_t plane = (size_t)H * W;
-  const float* src = planes + pl * plane;
-  const int ah = H >> L, aw = W >> L;
-  float amin = INFINITY, amax = -INFINITY, dmin = INFINITY, dmax = -INFINITY;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < plane;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const int y = (int)(i / W), x = (int)(i - (size_t)y * W);
-    const float v = src[i];
-    if (y < ah && x < aw) {
-      amin = fminf(amin, v);
-      amax = fmaxf(amax, v);
-    } else {
-      dmin = fminf(dmin, v);
-      dmax = fmaxf(dmax, v);
-    }
-  }
-  for (int o = 16; o; o >>= 1) {
-    amin = fminf(amin, __shfl_xor_sync(0xFFFFFFFFu, amin, o));
-    amax = fmaxf(amax, __shfl_xor_sync(0xFFFFFFFFu, amax, o));
-    dmin = fminf(dmin, __shfl_xor_sync(0xFFFFFFFFu, dmin, o));
-    dmax = fmaxf(dmax, __shfl_xor_sync(0xFFFFFFFFu, dmax, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
-    uint32_t* k = keys + pl * 4;
-    if (amin <= amax) {
-      atomicMin(k + 0, fkey(amin));
-      atomicMax(k + 1, fkey(amax));
-    }
-    if (dmin <= dmax) {
-      atomicMin(k + 2, fkey(dmin));
-      atomicMax(k + 3, fkey(dmax));
-    }
-  }
-}
-
 __global__ void k_ext_final(const uint32_t* keys, float* ext, int count) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) ext[i] = unkey(keys[i]);
+}
+
+// E3-E5, one CTA per 32x32 (bs x bs) block at a time (grid-stride), 256
+// threads, position o = r * 256 + tid of the block.  Per position: sparsify
+// each frame (encoding.py:118-135: keep iff the channel max magnitude
+// exceeds level threshold + H(y); the approximation is kept), temporal Haar
+// forward in Mallat order (:153-169: a = (x0 + x1) * 0.5, d = (x0 - x1) *
+// 0.5, the finest temporal level's details last), then zero temporal
+// details whose channel max magnitude is <= their threshold (:198-236; the
+// approximation band is exempt).  The final values go back to the planes;
+// their nonzero flags (any channel != 0, encoding.py:306) become one bit per
+// (t, position) and the (t, block) record counts (warp atomics: the warps
+// of a CTA never wait for each other); the per-(t, c) extrema
+// (:239-254) are reduced on the way (detail in registers, the rare
+// approximation positions through shared-memory atomics).
+// NT = n, CT = C at compile time (register arrays), or 0 = run time
+template <int NT, int CT>
+__global__ void __launch_bounds__(256) k_point(float* __restrict__ planes,
+                                               const float* __restrict__ row_factor,
+                                               uint32_t* __restrict__ nzbits,
+                                               uint32_t* __restrict__ counts,
+                                               uint32_t* __restrict__ keys, wv_encode_params p) {
+  constexpr int NA = NT ? NT : WV_ENC_MAX_N;
+  constexpr int CA = CT ? CT : 4;
+  const int H = p.height, W = p.width, C = CT ? CT : p.channels, n = NT ? NT : p.inter_size;
+  const int L = p.levels;
+  const int bs = p.block_size, nbx = W / bs, NB = nbx * (H / bs);
+  const int npos = bs * bs, nwords = (npos + 31) / 32;
+  const size_t plane = (size_t)H * W;
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  __shared__ uint32_t s_keys[WV_ENC_MAX_N * 4 * 4];
+  for (int k = tid; k < n * C * 4; k += 256) s_keys[k] = (k & 1) ? 0u : 0xFFFFFFFFu;
+  float dmin[NA][CA], dmax[NA][CA];
+#pragma unroll
+  for (int t = 0; t < NA; ++t)
+#pragma unroll
+    for (int c = 0; c < CA; ++c) {
+      dmin[t][c] = INFINITY;
+      dmax[t][c] = -INFINITY;
+    }
+  __syncthreads();
+  for (int b = blockIdx.x; b < NB; b += gridDim.x) {
+    const int by = b / nbx, bx = b - by * nbx;
+    uint32_t cnt[NA];
+#pragma unroll
+    for (int t = 0; t < NA; ++t) cnt[t] = 0;
+    for (int o0 = 0; o0 < npos; o0 += 256) {
+      const int o = o0 + tid;
+      const bool live = o < npos;
+      const int y = by * bs + (live ? o / bs : 0), x = bx * bs + (live ? o % bs : 0);
+      const size_t i = (size_t)y * W + x;
+      int yy;
+      const int k = position_level(y, x, H, W, L, yy);
+      float v[NA][CA];
+#pragma unroll
+      for (int t = 0; t < NA; ++t) {
+        if (t >= n) break;
+        float m = 0.0f;
+#pragma unroll
+        for (int c = 0; c < CA; ++c) {
+          v[t][c] = 0.0f;
+          if (c < C && live) {
+            v[t][c] = planes[(size_t)(t * C + c) * plane + i];
+            m = fmaxf(m, fabsf(v[t][c]));
+          }
+        }
+        if (k > 0) {
+          const int ry = min(yy << k, H - 1);
+          const float thr = __fadd_rn(p.level_threshold[k - 1], row_factor[ry]);
+          if (!(m > thr)) {
+#pragma unroll
+            for (int c = 0; c < CA; ++c) v[t][c] = 0.0f;
+          }
+        }
+      }
+      float out[NA][CA];
+      int end = n;
+#pragma unroll
+      for (int cur = NA; cur > 1; cur >>= 1) {
+        if (cur > n) continue;
+        const int half = cur >> 1;
+#pragma unroll
+        for (int q = 0; q < NA / 2; ++q) {
+          if (q >= half) break;
+#pragma unroll
+          for (int c = 0; c < CA; ++c) {
+            const float a0 = v[2 * q][c], a1 = v[2 * q + 1][c];
+            out[end - half + q][c] = __fmul_rn(__fsub_rn(a0, a1), 0.5f);
+            v[q][c] = __fmul_rn(__fadd_rn(a0, a1), 0.5f);
+          }
+        }
+        end -= half;
+      }
+#pragma unroll
+      for (int c = 0; c < CA; ++c) out[0][c] = v[0][c];
+      const bool approx = k == 0;
+#pragma unroll
+      for (int t = 0; t < NA; ++t) {
+        if (t >= n) break;
+        bool kill = false;
+        if (t >= 1 && !approx) {
+          float m = 0.0f;
+#pragma unroll
+          for (int c = 0; c < CA; ++c)
+            if (c < C) m = fmaxf(m, fabsf(out[t][c]));
+          kill = m <= p.temporal_threshold[t];
+        }
+        bool nz = false;
+#pragma unroll
+        for (int c = 0; c < CA; ++c)
+          if (c < C && live) nz |= !kill && out[t][c] != 0.0f;
+#pragma unroll
+        for (int c = 0; c < CA; ++c) {
+          if (c < C && live) {
+            const float r = kill ? 0.0f : out[t][c];
+            // only positions with a record are read again (k_emit, via nzbits)
+            if (nz) planes[(size_t)(t * C + c) * plane + i] = r;
+            if (approx) {
+              atomicMin(&s_keys[(t * C + c) * 4 + 0], fkey(r));
+              atomicMax(&s_keys[(t * C + c) * 4 + 1], fkey(r));
+            } else {
+              dmin[t][c] = fminf(dmin[t][c], r);
+              dmax[t][c] = fmaxf(dmax[t][c], r);
+            }
+          }
+        }
+        const uint32_t bits = __ballot_sync(0xFFFFFFFFu, nz);
+        if (lane == 0 && (o0 >> 5) + wp < nwords) {
+          // positions o0 + 32 wp .. +31 of the block (masked to the block for bs < 8)
+          const uint32_t mk = npos - (o0 + 32 * wp) >= 32 ? 0xFFFFFFFFu
+                                                           : ((1u << (npos - (o0 + 32 * wp))) - 1u);
+          nzbits[((size_t)t * NB + b) * nwords + (o0 >> 5) + wp] = bits & mk;
+          cnt[t] += __popc(bits & mk);
+        }
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int t = 0; t < NA; ++t)
+        if (t < n && cnt[t]) atomicAdd(&counts[(size_t)t * NB + b], cnt[t]);
+    }
+  }
+  // detail extrema: warp reduce, shared atomics, then one global atomic per key
+#pragma unroll
+  for (int t = 0; t < NA; ++t) {
+    if (t >= n) break;
+#pragma unroll
+    for (int c = 0; c < CA; ++c) {
+      if (c >= C) break;
+      float mn = dmin[t][c], mx = dmax[t][c];
+      for (int o = 16; o; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+      }
+      if (lane == 0 && mn <= mx) {
+        atomicMin(&s_keys[(t * C + c) * 4 + 2], fkey(mn));
+        atomicMax(&s_keys[(t * C + c) * 4 + 3], fkey(mx));
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = tid; k < n * C * 4; k += 256) {
+    const uint32_t v = s_keys[k];
+    if (k & 1) {
+      if (v != 0u) atomicMax(&keys[k], v);
+    } else if (v != 0xFFFFFFFFu) {
+      atomicMin(&keys[k], v);
+    }
+  }
 }
 
 // ---------------------------------------------------------------- E5 / E7
@@ -330,36 +498,6 @@ __device__ __forceinline__ int position_layer(int y, int x, int H, int W, int L)
   int yy;
   const int k = position_level(y, x, H, W, L, yy);
   return k == 0 ? 0 : L - k + 1;
-}
-
-// One CTA (256 threads) per (t, block); bs*bs <= 1024 positions, 4 per thread
-// (position = offset = (y % bs) * bs + x % bs, ascending with the thread).
-__device__ __forceinline__ bool nonzero_at(const float* planes, size_t plane, int t, int C,
-                                           size_t pix) {
-  bool nz = false;
-  for (int c = 0; c < C; ++c) nz |= planes[(size_t)(t * C + c) * plane + pix] != 0.0f;
-  return nz;
-}
-
-__global__ void k_count(const float* __restrict__ planes, uint32_t* counts, wv_encode_params p) {
-  const int bs = p.block_size, nbx = nb_x(p), NB = nb_all(p);
-  const int t = blockIdx.x / NB, b = blockIdx.x - t * NB;
-  const int by = b / nbx, bx = b - by * nbx;
-  const size_t plane = (size_t)p.height * p.width;
-  int cnt = 0;
-  for (int o = threadIdx.x; o < bs * bs; o += blockDim.x) {
-    const int y = by * bs + o / bs, x = bx * bs + o % bs;
-    cnt += nonzero_at(planes, plane, t, p.channels, (size_t)y * p.width + x);
-  }
-  cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
-  __shared__ int ws[8];
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = cnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int s = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += ws[w];
-    counts[blockIdx.x] = (uint32_t)s;
-  }
 }
 
 // Exclusive scan of the (n * NB) counts in 1024-element tiles: tile sums,
@@ -425,8 +563,8 @@ __global__ void k_scan_apply(const uint32_t* counts, const uint64_t* partials, u
 // u16 offset, then C quantised bytes (cmin/cmax of the position's band:
 // floor((v - lo) / span * 255 + 0.5), 0 when span == 0) or C float32.
 __global__ void k_emit(const float* __restrict__ planes, const float* __restrict__ ext,
-                       const uint64_t* __restrict__ starts, uint8_t* __restrict__ payload,
-                       wv_encode_params p) {
+                       const uint64_t* __restrict__ starts, const uint32_t* __restrict__ nzbits,
+                       uint8_t* __restrict__ payload, wv_encode_params p) {
   const int bs = p.block_size, nbx = nb_x(p), NB = nb_all(p);
   const int H = p.height, W = p.width, C = p.channels, L = p.levels;
   const int t = blockIdx.x / NB, b = blockIdx.x - t * NB;
@@ -436,6 +574,10 @@ __global__ void k_emit(const float* __restrict__ planes, const float* __restrict
   const int rs = p.quantize ? 2 + C : 2 + 4 * C;
   __shared__ int s_layer_count[WV_MAX_LEVELS + 1];
   __shared__ int s_warp[8];
+  if (starts[blockIdx.x + 1 < (unsigned)(p.inter_size * NB) ? blockIdx.x + 1 : blockIdx.x] ==
+          starts[blockIdx.x] &&
+      blockIdx.x + 1 < (unsigned)(p.inter_size * NB))
+    return;   // no records in this (t, block)
   if (threadIdx.x <= WV_MAX_LEVELS) s_layer_count[threadIdx.x] = 0;
   __syncthreads();
   // 4 consecutive offsets per thread (npos <= 1024)
@@ -446,10 +588,12 @@ __global__ void k_emit(const float* __restrict__ planes, const float* __restrict
     nz[k] = false;
     lay[k] = 0;
     if (o < npos) {
-      const int y = by * bs + o / bs, x = bx * bs + o % bs;
-      nz[k] = nonzero_at(planes, plane, t, C, (size_t)y * W + x);
-      lay[k] = position_layer(y, x, H, W, L);
-      if (nz[k]) atomicAdd(&s_layer_count[lay[k]], 1);
+      nz[k] = (nzbits[(size_t)blockIdx.x * ((npos + 31) / 32) + (o >> 5)] >> (o & 31)) & 1u;
+      if (nz[k]) {
+        const int y = by * bs + o / bs, x = bx * bs + o % bs;
+        lay[k] = position_layer(y, x, H, W, L);
+        atomicAdd(&s_layer_count[lay[k]], 1);
+      }
     }
   }
   __syncthreads();
@@ -559,34 +703,49 @@ extern "C" int wv_encode_set(const wv_encode_params* p, const uint8_t* d_frames,
   uint64_t* starts = (uint64_t*)(ws + lo.starts);
   uint32_t* keys = (uint32_t*)(ws + lo.ext_bits);
   uint64_t* partials = (uint64_t*)(ws + lo.partials);
+  uint32_t* nzbits = (uint32_t*)(ws + lo.nzbits);
   const int H = p->height, W = p->width, C = p->channels, n = p->inter_size;
   const int planes_n = n * C;
   const size_t plane = (size_t)H * W;
   constexpr int T = 256;
 
-  k_load<<<grid_for(plane * n, T), T, 0, s>>>(d_frames, planes, n, C, H, W);
   int h = H, w = W;
   for (int k = 0; k < p->levels; ++k) {
-    const size_t rows_work = (size_t)planes_n * h * ((w / 2 + SEG - 1) / SEG);
-    k_rows<<<grid_for(rows_work, T), T, 0, s>>>(planes, tmp, planes_n, H, W, h, w);
+    if (k == 0) {
+      const size_t work = (size_t)n * H * ((W / 2 + UCH - 1) / UCH);   // warps
+      k_rows_u8<<<grid_for(work * 32, 128), 128, 0, s>>>(d_frames, tmp, n, C, H, W);
+    } else {
+      const size_t rows_work = (size_t)planes_n * h * ((w / 2 + RCH - 1) / RCH);   // warps
+      k_rows<<<grid_for(rows_work * 32, T), T, 0, s>>>(planes, tmp, planes_n, H, W, h, w);
+    }
     const size_t cols_work = (size_t)planes_n * ((h / 2 + SEG - 1) / SEG) * w;
     k_cols<<<grid_for(cols_work, T), T, 0, s>>>(tmp, planes, planes_n, H, W, h, w);
     h /= 2;
     w /= 2;
   }
-  k_point<<<grid_for(plane, T), T, 0, s>>>(planes, d_row_factor, *p);
   const int nkeys = planes_n * 4;
-  k_ext_init<<<(nkeys + T - 1) / T, T, 0, s>>>(keys, nkeys);
-  k_extrema<<<dim3(grid_for(plane, T) / 8 + 1, planes_n), T, 0, s>>>(planes, keys, H, W,
-                                                                       p->levels);
-  k_ext_final<<<(nkeys + T - 1) / T, T, 0, s>>>(keys, d_extrema, nkeys);
   const int nblk = n * nb_all(*p);
-  k_count<<<nblk, T, 0, s>>>(planes, d_counts, *p);
+  k_ext_init<<<(nkeys + T - 1) / T, T, 0, s>>>(keys, nkeys);
+  WV_CUDA(cudaMemsetAsync(d_counts, 0, (size_t)nblk * 4, s));
+  {
+    const int g = nb_all(*p) < 148 * 8 ? nb_all(*p) : 148 * 8;
+#define WV_POINT(NTV, CTV) \
+  k_point<NTV, CTV><<<g, T, 0, s>>>(planes, d_row_factor, nzbits, d_counts, keys, *p)
+    if (n == 4 && C == 3) WV_POINT(4, 3);
+    else if (n == 4 && C == 1) WV_POINT(4, 1);
+    else if (n == 1) WV_POINT(1, 0);
+    else if (n == 2) WV_POINT(2, 0);
+    else if (n == 4) WV_POINT(4, 0);
+    else if (n == 8) WV_POINT(8, 0);
+    else WV_POINT(0, 0);
+#undef WV_POINT
+  }
+  k_ext_final<<<(nkeys + T - 1) / T, T, 0, s>>>(keys, d_extrema, nkeys);
   const int ntiles = (nblk + 1023) / 1024;
   k_scan_tiles<<<ntiles, 256, 0, s>>>(d_counts, partials, nblk);
   k_scan_partials<<<1, 32, 0, s>>>(partials, ntiles, d_num_records);
   k_scan_apply<<<ntiles, 256, 0, s>>>(d_counts, partials, starts, nblk);
-  k_emit<<<nblk, T, 0, s>>>(planes, d_extrema, starts, d_payload, *p);
+  k_emit<<<nblk, T, 0, s>>>(planes, d_extrema, starts, nzbits, d_payload, *p);
   WV_CUDA(cudaGetLastError());
   return WV_OK;
 }
