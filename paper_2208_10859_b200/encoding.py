@@ -405,7 +405,10 @@ def encode_video(frames, params: EncodeParams, device=None,
     k255 = None
     for s0 in range(0, count + pad, n):
         idx = [min(i, count - 1) for i in range(s0, s0 + n)]
-        chunk = x[idx].to(dev)                                   # (n, H, W, C) u8
+        if idx[-1] == s0 + n - 1:   # whole set present: a view (pinned sources copy async)
+            chunk = x[s0:s0 + n].to(dev, non_blocking=True)      # (n, H, W, C) u8
+        else:
+            chunk = x[idx].to(dev)
         if dev.type == "cuda" and backend == "native":
             sets.append(_encode_set_native(chunk, params, levels, hfac, keep_arrays))
             del chunk
