@@ -1,12 +1,13 @@
-"""Encoder (input generation for the decode path), torch, CPU or CUDA.
+"""Encoder: the reference's encode_video (pkg/src/wavevid/encoding.py:36-425).
 
-Restates the reference encoder (pkg/src/wavevid/encoding.py:36-425) op for
-op in float32 with float32-rounded constants and no fused multiply-adds, so
-on CPU it reproduces the reference's files byte for byte (the three
-golden.json digests are checked in tests/test_encoder.py).  On a B200 the
-same code encodes an 8K stereo set in seconds instead of the reference's
-~143 s, which is what makes the 8K benchmark inputs practical.  This is the
-mirror path of the product, not the decode hot path.
+On a CUDA device each inter-frame set goes through the CUDA encoder
+(``wv_encode_set``, csrc/wv_encode.cu).  The torch restatement below runs
+the reference op for op in float32 with float32-rounded constants and no
+fused multiply-adds; it is the CPU path (and ``backend="torch"``).  Both
+reproduce the reference's files byte for byte: the golden sha256 digests
+are checked in tests/test_host.py (CPU) and tests/test_gpu_encoder.py
+(CUDA).  This is the mirror path of the product, not
+the decode hot path.
 """
 from __future__ import annotations
 
