@@ -244,7 +244,11 @@ struct LevelArgs {
 // this item's row pass runs (43 KB of shared memory: 5 CTAs per SM).
 constexpr int BOXSET = 4 * BOX_SLOT;
 constexpr int COL_BYTES = 2 * TY * CB_PITCH * 8;
-constexpr int SMEM_MID = BOXSET + COL_BYTES;
+#ifndef WV_K3_MIDPF
+#define WV_K3_MIDPF 0   // mid levels: own output tile + next-item TMA prefetch (61 KB/CTA)
+#endif
+constexpr int OUTB_BYTES = TY * OB_PITCH * 8;
+constexpr int SMEM_MID = BOXSET + COL_BYTES + (WV_K3_MIDPF ? OUTB_BYTES : 0);
 constexpr int SMEM_FIN = BOXSET + COL_BYTES;   // the u8 tile goes from registers to HBM
 
 template <bool FINAL>
@@ -261,7 +265,9 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   const float* bHH = box + 3 * BOX_SLOT / 4;
   float2* colL = reinterpret_cast<float2*>(smem + BOXSET);  // [TY][CB_PITCH]
   float2* colH = colL + TY * CB_PITCH;
-  float2* outb = reinterpret_cast<float2*>(smem);                     // mid: aliases the boxes
+  // mid levels: the f32 output tile aliases the boxes (or, with prefetch, has its own region)
+  float2* outb = reinterpret_cast<float2*>(smem + (WV_K3_MIDPF ? BOXSET + COL_BYTES : 0));
+  constexpr bool PF = FINAL || WV_K3_MIDPF;   // next item's boxes issued after the column pass
   __shared__ uint64_t bar;
 
   const int tid = threadIdx.x;
@@ -331,8 +337,8 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
           }
         }
       }
-      if (tid == 0 && a.use_tma && nxt < nitems) nxt_entry = a.list[nxt / a.divC];
     }
+    if (PF && tid == 0 && a.use_tma && nxt < nitems) nxt_entry = a.list[nxt / a.divC];
     if (a.use_tma) {
       if (!issued) issue(item);
       mbar_wait(&bar, phase);
@@ -397,7 +403,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       }
     }
     __syncthreads();
-    if (FINAL && a.use_tma) {
+    if (PF && a.use_tma) {
       // the boxes are consumed: start the next item's loads now (only the
       // elected thread read nxt_entry and issues)
       issued = !(nxt_entry & ZERO_FLAG);   // meaningful for the elected thread only
