@@ -529,6 +529,240 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   }
 }
 
+#ifndef WV_K3_WS
+#define WV_K3_WS 0
+#endif
+// Finest level, warp-specialised (WV_K3_WS): warps 0-4 (the column group,
+// 160 threads) lift item k + 1's columns into column buffer (k + 1) & 1
+// while warps 5-8 (the row group, 128 threads) lift item k's rows from
+// buffer k & 1 and store its u8 pixels.  Hand-off by named barriers:
+// FULL[b] (ids 2, 3: the column group arrives, the row group waits) and
+// EMPTY[b] (ids 4, 5: the row group arrives, the column group waits before
+// rewriting b); id 1 syncs the column group alone.  The boxes are single
+// buffered: the next item's TMA loads go out as soon as the column group has
+// consumed the current ones.  Items with ZERO_FLAG pass through the same
+// protocol with an empty column phase.  Same arithmetic as k_level<true>.
+constexpr int WS_COL = COL_SEGS * BOX_W;              // 160 column threads
+constexpr int WS_ROW = (TX / SEGLEN_RF) * TY;         // 128 row threads
+constexpr int WS_THREADS = WS_COL + WS_ROW;
+constexpr int SMEM_WS = BOXSET + 2 * COL_BYTES;
+static_assert(WS_COL % 32 == 0 && WS_ROW % 32 == 0, "whole warps per group");
+
+__device__ __forceinline__ void nbar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(WS_THREADS) k_final_ws(const __grid_constant__ CUtensorMap tm_ll,
+                                                         const __grid_constant__ CUtensorMap tm_det,
+                                                         LevelArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* canvas = a.fa->d_canvas;
+  float* box = reinterpret_cast<float*>(smem);
+  const float* bLL = box;
+  const float* bHL = box + BOX_SLOT / 4;
+  const float* bLH = box + 2 * BOX_SLOT / 4;
+  const float* bHH = box + 3 * BOX_SLOT / 4;
+  __shared__ uint64_t bar;
+  const int tid = threadIdx.x;
+  if (tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  const int C = a.C;
+  const uint32_t nitems = *a.count * (uint32_t)C;
+  const int H = 2 * a.bh, W = 2 * a.bw;
+  auto geom = [&](uint32_t it, uint32_t& entry, int& c, int& ay, int& ax) {
+    const uint32_t itile = it / a.divC;
+    entry = a.list[itile];
+    c = (int)(it - itile * C);
+    const uint32_t tile = entry & ~ZERO_FLAG;
+    const int ty = (int)(tile / a.divN), tx = (int)tile - ty * a.ntx;
+    ay = ty * TY;
+    ax = tx * TX;
+  };
+
+  if (tid < WS_COL) {
+    // ------------------------------------------------ column group
+    uint32_t phase = 0u;
+    auto issue = [&](uint32_t it) {
+      uint32_t entry;
+      int c, ay, ax;
+      geom(it, entry, c, ay, ax);
+      const int oy = max(ay - HALO, 0), ox = max(ax - XPAD, 0);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bar, 4u * BOX_FLOATS * 4u);
+      tma_load_3d(box, &tm_ll, ox, oy, c, &bar);
+      tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar);
+      tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar);
+      tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar);
+    };
+    bool issued = false;
+    uint32_t k = 0;
+    for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x, ++k) {
+      const int b = (int)(k & 1u);
+      uint32_t entry;
+      int c, ay, ax;
+      geom(item, entry, c, ay, ax);
+      const uint32_t nxt = item + gridDim.x;
+      uint32_t nxt_entry = ZERO_FLAG;
+      if (tid == 0 && nxt < nitems) nxt_entry = a.list[nxt / a.divC];
+      if (k >= 2) nbar_sync(4 + b, WS_THREADS);   // the row group is done with buffer b
+      if (!(entry & ZERO_FLAG)) {
+        if (tid == 0 && !issued) issue(item);
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        float2* colL = reinterpret_cast<float2*>(smem + BOXSET + b * COL_BYTES);
+        float2* colH = colL + TY * CB_PITCH;
+        const int by = min(ay + TY, a.bh), bx = min(ax + TX, a.bw);
+        const int oy = max(ay - HALO, 0), ox = max(ax - XPAD, 0);
+        const int lc = tid % BOX_W, sg = tid / BOX_W;
+        const int cg = ox + lc;
+        const int pa = ay + sg * SEGLEN_C, pb = min(pa + SEGLEN_C, by);
+        if (pa < pb && cg >= max(ax - HALO, 0) && cg < min(bx + HALO, a.bw)) {
+          if (pa >= HALO && pb + HALO <= a.bh && pb - pa == SEGLEN_C) {
+            const int rb = pa - HALO - oy;
+            const int qb = pa - HALO - ay;
+            lift_interior<SEGLEN_C>(
+                [&](int j, float2& sv, float2& dv) {
+                  const int o = (rb + j) * BOX_W + lc;
+                  sv = make_float2(bLL[o], bHL[o]);
+                  dv = make_float2(bLH[o], bHH[o]);
+                },
+                [&](int pp, float2 s3, float2 d3) {
+                  colL[(qb + pp) * CB_PITCH + lc] = make_float2(s3.x, d3.x);
+                  colH[(qb + pp) * CB_PITCH + lc] = make_float2(s3.y, d3.y);
+                });
+          } else {
+            lift_line(
+                max(pa - HALO, 0), min(pb + HALO, a.bh), a.bh, pa, pb,
+                [&](int j, float2& sv, float2& dv) {
+                  const int o = (j - oy) * BOX_W + lc;
+                  sv = make_float2(bLL[o], bHL[o]);
+                  dv = make_float2(bLH[o], bHH[o]);
+                },
+                [&](int pp, float2 s3, float2 d3) {
+                  const int q = pp - ay;
+                  colL[q * CB_PITCH + lc] = make_float2(s3.x, d3.x);
+                  colH[q * CB_PITCH + lc] = make_float2(s3.y, d3.y);
+                });
+          }
+        }
+        nbar_sync(1, WS_COL);   // boxes consumed by every column thread
+      }
+      issued = false;
+      if (tid == 0 && !(nxt_entry & ZERO_FLAG)) {
+        issue(nxt);
+        issued = true;
+      }
+      nbar_arrive(2 + b, WS_THREADS);   // buffer b holds item k's columns
+    }
+    // complete the last EMPTY generations (no barrier left pending)
+    if (k >= 2) nbar_sync(4 + (int)(k & 1u), WS_THREADS);
+    if (k >= 1) nbar_sync(4 + (int)((k + 1) & 1u), WS_THREADS);
+  } else {
+    // ------------------------------------------------ row group
+    const int rt = tid - WS_COL;
+    const int i = rt % TY, sg = rt / TY;
+    constexpr int SR = SEGLEN_RF;
+    uint32_t k = 0;
+    for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x, ++k) {
+      const int b = (int)(k & 1u);
+      uint32_t entry;
+      int c, ay, ax;
+      geom(item, entry, c, ay, ax);
+      const int by = min(ay + TY, a.bh), bx = min(ax + TX, a.bw);
+      const int ox = max(ax - XPAD, 0);
+      const int pa = ax + sg * SR, pb = min(pa + SR, bx);
+      uint32_t rq[2][SR / 8];
+      const bool act = i < by - ay && pa < pb;
+      if (!(entry & ZERO_FLAG) && act) {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const uint32_t* req = a.R + (uint64_t)a.rowmap[2 * ay + 2 * i + rr] * a.wpr0;
+#pragma unroll
+          for (int q = 0; q < SR / 8; ++q) {
+            const int px = 2 * pa + 16 * q;
+            rq[rr][q] = px < W ? req[px >> 5] : 0u;
+          }
+        }
+      }
+      nbar_sync(2 + b, WS_THREADS);   // item k's columns are in buffer b
+      if (entry & ZERO_FLAG) {
+        const int ny = 2 * (by - ay), nx = 2 * (bx - ax), qw = nx >> 2;
+        for (int idx = rt; idx < ny * qw; idx += WS_ROW) {
+          const int r = idx / qw, q = idx % qw;
+          *reinterpret_cast<uint32_t*>(canvas + ((uint64_t)c * H + 2 * ay + r) * W + 2 * ax +
+                                       4 * q) = 0u;
+        }
+      } else if (act) {
+        const float2* colL = reinterpret_cast<const float2*>(smem + BOXSET + b * COL_BYTES);
+        const float2* colH = colL + TY * CB_PITCH;
+        auto cv = [](float v) { return min(__float2uint_rn(__fmul_rn(v, 255.0f)), 255u); };
+        uint8_t* crow = canvas + ((uint64_t)c * H + 2 * ay + 2 * i) * W;
+        if (pa >= HALO && pb + HALO <= a.bw && pb - pa == SR) {
+          uint32_t w0[SR / 2] = {}, w1[SR / 2] = {};
+          const int cb = pa - HALO - ox;
+          lift_interior<SR>(
+              [&](int j, float2& sv, float2& dv) {
+                sv = colL[i * CB_PITCH + cb + j];
+                dv = colH[i * CB_PITCH + cb + j];
+              },
+              [&](int pp, float2 s3, float2 d3) {
+                const int lq = pp - HALO;
+                w0[lq >> 1] |= (cv(s3.x) | (cv(d3.x) << 8)) << (16 * (lq & 1));
+                w1[lq >> 1] |= (cv(s3.y) | (cv(d3.y) << 8)) << (16 * (lq & 1));
+              });
+          auto bm = [](uint32_t b4) { return ((b4 * 0x00204081u) & 0x01010101u) * 0xFFu; };
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            const uint32_t* wr = rr ? w1 : w0;
+#pragma unroll
+            for (int q = 0; q < SR / 8; ++q) {
+              const int px = 2 * pa + 16 * q;
+              const uint32_t bits = (rq[rr][q] >> (px & 31)) & 0xFFFFu;
+              const uint4 v = make_uint4(wr[4 * q] & bm(bits & 0xFu),
+                                         wr[4 * q + 1] & bm((bits >> 4) & 0xFu),
+                                         wr[4 * q + 2] & bm((bits >> 8) & 0xFu),
+                                         wr[4 * q + 3] & bm(bits >> 12));
+              uint8_t* dst = crow + (uint64_t)rr * W + px;
+              if ((W & 15) == 0) {
+                *reinterpret_cast<uint4*>(dst) = v;
+              } else {
+                uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+                d4[0] = v.x;
+                d4[1] = v.y;
+                d4[2] = v.z;
+                d4[3] = v.w;
+              }
+            }
+          }
+        } else {
+          lift_line(
+              max(pa - HALO, 0), min(pb + HALO, a.bw), a.bw, pa, pb,
+              [&](int j, float2& sv, float2& dv) {
+                sv = colL[i * CB_PITCH + (j - ox)];
+                dv = colH[i * CB_PITCH + (j - ox)];
+              },
+              [&](int pp, float2 s3, float2 d3) {
+                const int px = 2 * pp;
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr) {
+                  const int y = 2 * ay + 2 * i + rr;
+                  const uint32_t bits =
+                      (a.R[(uint64_t)a.rowmap[y] * a.wpr0 + (px >> 5)] >> (px & 31)) & 3u;
+                  const uint32_t lo = rr ? cv(s3.y) : cv(s3.x), hi = rr ? cv(d3.y) : cv(d3.x);
+                  *reinterpret_cast<uint16_t*>(crow + (uint64_t)rr * W + px) =
+                      (uint16_t)(((bits & 1u) ? lo : 0u) | (((bits >> 1) & 1u) ? hi << 8 : 0u));
+                }
+              });
+        }
+      }
+      nbar_arrive(4 + b, WS_THREADS);   // buffer b may be rewritten
+    }
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -603,8 +837,18 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
       la.R = (const uint32_t*)(ws + lo.mrows);
       la.rowmap = (const uint32_t*)(ws + lo.rowmap);
       la.wpr0 = lo.wpr_[0];
-      int grid = max(1, min(ntiles * C, sms * occ_fin));
-      WV_CUDA(launch_k(k_level<true>, dim3(grid), dim3(NTHREADS), smem_fin, s, tm_ll, tm_plane, la));
+      if (WV_K3_WS && la.use_tma) {
+        WV_CUDA(cudaFuncSetAttribute(k_final_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SMEM_WS));
+        int occ_ws = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ws, k_final_ws, WS_THREADS, SMEM_WS);
+        int grid = max(1, min(ntiles * C, sms * occ_ws));
+        WV_CUDA(launch_k(k_final_ws, dim3(grid), dim3(WS_THREADS), (size_t)SMEM_WS, s, tm_ll,
+                         tm_plane, la));
+      } else {
+        int grid = max(1, min(ntiles * C, sms * occ_fin));
+        WV_CUDA(launch_k(k_level<true>, dim3(grid), dim3(NTHREADS), smem_fin, s, tm_ll, tm_plane, la));
+      }
     }
     WV_CUDA(cudaGetLastError());
     if (getenv("WV_DEBUG_SYNC")) {
