@@ -120,7 +120,47 @@ struct CascadeArgs {
   int fov;                         // foveated: batch j also ANDs with batch 0
   uint32_t* pooled;                // one word per tile: bit w = any bit in (32 rows x word w)
   int pool_wpr;                    // tiles per row of the level
+  const uint32_t* src_pooled;      // viewport, j > 1: level j-1's pooled occupancy (else null)
+  int src_pool_wpr;
+  int mh, mw;                      // j == 1: low-res mask size (fa->d_mask)
 };
+
+// Can the tile (rows r0.., words w0.. of level j, with its dilation apron)
+// receive any set bit?  j == 1: the low-res mask cells under it; j > 1
+// (viewport): level j-1's pooled occupancy.  A zero answer is exact: the
+// cascade of an all-zero source region is zero (foveated windows are
+// subsets of the request, so the test holds for every batch at j == 1).
+__device__ bool cascade_tile_live(const CascadeArgs& a, int r0, int w0) {
+  bool hit = false;
+  if (a.j == 1) {
+    const int py0 = max(0, 2 * (r0 - DIL)), py1 = min(a.prow_n, 2 * (r0 + CT_R + DIL));
+    const int px0 = max(0, 64 * (w0 - 1)), px1 = min(a.pcols, 64 * (w0 + CT_W + 1));
+    if (py0 < py1 && px0 < px1) {
+      const int m0 = (int)(((uint32_t)py0 * (uint32_t)a.mh) / (uint32_t)a.prow_n);
+      const int m1 = (int)(((uint32_t)(py1 - 1) * (uint32_t)a.mh) / (uint32_t)a.prow_n);
+      const int c0 = (int)(((uint32_t)px0 * (uint32_t)a.mw) / (uint32_t)a.pcols);
+      const int c1 = (int)(((uint32_t)(px1 - 1) * (uint32_t)a.mw) / (uint32_t)a.pcols);
+      const int nc = c1 - c0 + 1, cells = (m1 - m0 + 1) * nc;
+      const uint8_t* mask = a.fa->d_mask;
+      for (int e = threadIdx.x; e < cells; e += blockDim.x)
+        hit |= mask[(uint64_t)(m0 + e / nc) * a.mw + c0 + e % nc] != 0;
+    }
+  } else {
+    const int sr0 = max(0, 2 * (r0 - DIL)), sr1 = min(a.prow_n, 2 * (r0 + CT_R + DIL));
+    const int sw0 = max(0, 2 * (w0 - 1)), sw1 = min(a.pwpr, 2 * (w0 + CT_W + 1));
+    if (sr0 < sr1 && sw0 < sw1) {
+      const int t0 = sr0 / CT_R, t1 = (sr1 - 1) / CT_R, q0 = sw0 / CT_W, q1 = (sw1 - 1) / CT_W;
+      const int nq = q1 - q0 + 1;
+      for (int e = threadIdx.x; e < (t1 - t0 + 1) * nq; e += blockDim.x) {
+        const int tr = t0 + e / nq, tq = q0 + e % nq;
+        const int lo = max(sw0 - tq * CT_W, 0), hi = min(sw1 - tq * CT_W, 32);
+        const uint32_t m = (hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & (0xFFFFFFFFu << lo);
+        hit |= (a.src_pooled[(uint64_t)tr * a.src_pool_wpr + tq] & m) != 0u;
+      }
+    }
+  }
+  return __syncthreads_or(hit) != 0;
+}
 
 __device__ __forceinline__ uint32_t cas_src(const CascadeArgs& a, const int4& rect, int b,
                                             int rr, int ww) {
@@ -160,6 +200,16 @@ __global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
     rect = make_int4(f[0], f[1], f[2], f[3]);
   }
   const int4 none = make_int4(0, 0, 0, 0);
+  if ((a.j == 1 || a.src_pooled) && !cascade_tile_live(a, r0, w0)) {
+    // nothing can reach this tile: zero words, zero pooled cell
+    for (int e = threadIdx.x; e < CT_R * CT_W; e += blockDim.x) {
+      const int r = r0 + e / CT_W, w = w0 + e % CT_W;
+      if (r < a.rows && w < a.wpr) a.dst[(uint64_t)b * a.dst_stride + (uint64_t)r * a.wpr + w] = 0u;
+    }
+    if (final_mask && a.pooled && threadIdx.x == 0)
+      a.pooled[(uint64_t)blockIdx.z * a.pool_wpr + blockIdx.x] = 0u;
+    return;
+  }
   if (threadIdx.x < CT_W) pool[threadIdx.x] = 0;
   for (int e = threadIdx.x; e < (CT_R + 2 * DIL) * (CT_W + 2); e += blockDim.x) {
     const int lr = e / (CT_W + 2), lw = e % (CT_W + 2);
@@ -688,6 +738,12 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
       for (int k = j; k <= L; ++k) c.batch[c.nbatch++] = k;
     c.pooled = lo.bs == 32 ? (uint32_t*)(ws + lo.pooled[j]) : nullptr;
     c.pool_wpr = cdiv(c.wpr, CT_W);
+    // zero-tile skipping: j == 1 from the low-res mask; j > 1 from level
+    // j-1's pooled occupancy (viewport only: a foveated D_{j-1} is not an
+    // upper bound of the request cascade)
+    c.src_pooled = (j > 1 && !fov && lo.bs == 32) ? (const uint32_t*)(ws + lo.pooled[j - 1]) : nullptr;
+    c.src_pool_wpr = cdiv(lo.wpr_[j - 1], CT_W);
+    c.mh = lo.mh; c.mw = lo.mw;
     dim3 grid(cdiv(c.wpr, CT_W), c.nbatch, cdiv(c.rows, CT_R));
     WV_CUDA(launch_k(k_cascade, dim3(grid), dim3(256), 0, s, c));
   }
