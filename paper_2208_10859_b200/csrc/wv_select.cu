@@ -275,6 +275,8 @@ struct FootArgs {
   const uint32_t* R;          // finest step: requested rows
   const uint32_t* rowmap;
   const wv_frame_args* fa;
+  const uint32_t* dpool;      // pooled occupancy of D_j (bs == 32), else null
+  int dpool_wpr;
 };
 
 constexpr int FP_SR = CT_R / 2 + DIL + 1;  // source rows staged per tile (21)
@@ -285,6 +287,30 @@ __global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
   __shared__ uint32_t sv[FP_SR][FP_SW];
   const int r0 = blockIdx.z * CT_R, w0 = blockIdx.x * CT_W;
   const int sr0 = (r0 - DIL) >> 1, sw0 = (w0 >> 1) - 1;
+  if (a.dpool) {
+    // every output bit ANDs its own (in-range) source bit of V_j & D_j: a
+    // tile whose in-range sources see no D_j bit is zero
+    const int q0 = max(sr0, 0), q1 = min(sr0 + FP_SR, a.srows);
+    const int u0 = max(sw0, 0), u1 = min(sw0 + FP_SW, a.swpr);
+    bool hit = false;
+    if (q0 < q1 && u0 < u1) {
+      const int t0 = q0 / CT_R, t1 = (q1 - 1) / CT_R, c0 = u0 / CT_W, c1 = (u1 - 1) / CT_W;
+      const int nc = c1 - c0 + 1;
+      for (int e = threadIdx.x; e < (t1 - t0 + 1) * nc; e += blockDim.x) {
+        const int tr = t0 + e / nc, tc = c0 + e % nc;
+        const int lo = max(u0 - tc * CT_W, 0), hi = min(u1 - tc * CT_W, 32);
+        const uint32_t m = (hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & (0xFFFFFFFFu << lo);
+        hit |= (a.dpool[(uint64_t)tr * a.dpool_wpr + tc] & m) != 0u;
+      }
+    }
+    if (!__syncthreads_or(hit)) {
+      for (int e = threadIdx.x; e < CT_R * CT_W; e += blockDim.x) {
+        const int r = r0 + e / CT_W, w = w0 + e % CT_W;
+        if (r < a.rows && w < a.wpr) a.out[(uint64_t)r * a.wpr + w] = 0u;
+      }
+      return;
+    }
+  }
   for (int e = threadIdx.x; e < FP_SR * FP_SW; e += blockDim.x) {
     const int lr = e / FP_SW, lw = e % FP_SW;
     const int sr = sr0 + lr, sw = sw0 + lw;
@@ -763,6 +789,8 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     f.D = Dptr(j);
     f.out = (uint32_t*)(ws + lo.fp[j - 1]);
     f.R = R; f.rowmap = rowmap; f.fa = fa;
+    f.dpool = lo.bs == 32 ? (const uint32_t*)(ws + lo.pooled[j]) : nullptr;
+    f.dpool_wpr = cdiv(lo.wpr_[j], CT_W);
     dim3 grid(cdiv(f.wpr, CT_W), 1, cdiv(f.rows, CT_R));
     WV_CUDA(launch_k(k_footprint, dim3(grid), dim3(256), 0, s, f));
   }
