@@ -39,6 +39,9 @@ constexpr int CB_PITCH = BOX_W + 1;   // float2 units, odd -> conflict-free row 
 constexpr int OB_PITCH = OUT_W + 1;   // float2 units (row pairs), odd
 // line segments: every column (row) lifting stream covers SEGLEN_C
 // (SEGLEN_R) output pairs plus its own 2-pair halo on each side
+#ifndef WV_K3_CVT_U8
+#define WV_K3_CVT_U8 1
+#endif
 #ifndef WV_SEGLEN_C
 #define WV_SEGLEN_C 8
 #endif
@@ -61,6 +64,17 @@ static_assert(NTHREADS >= NTHREADS_MIN, "every segment needs a thread");
 static_assert(TY * OB_PITCH * 8 <= 4 * BOX_SLOT, "output tile must fit in the box region");
 
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+// clip(rint(x), 0, 255) (decoding.py:301; rint is round-half-even): one
+// saturating convert (F2IP.U8) instead of F2I + min
+__device__ __forceinline__ uint32_t u8_rint(float x) {
+#if WV_K3_CVT_U8
+  uint32_t u;
+  asm("cvt.rni.sat.u8.f32 %0, %1;" : "=r"(u) : "f"(x));
+  return u;   // zero-extended to 32 bits
+#else
+  return min(__float2uint_rn(x), 255u);
+#endif
+}
 // d * (1/K) feeds the packed add (d[i-1] + d[i]) of the next lifting step; a
 // packed multiply there would be contracted into FFMA2 by ptxas, so the
 // scale is two scalar round-to-nearest multiplies (never contracted).
@@ -418,7 +432,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         // round-half-even like __float2uint_rn, which also saturates below 0)
         // of the segment's 2 x 16 output pixels, kept in registers and
         // written to the canvas with the request mask applied
-        auto cv = [](float v) { return min(__float2uint_rn(__fmul_rn(v, 255.0f)), 255u); };
+        auto cv = [](float v) { return u8_rint(__fmul_rn(v, 255.0f)); };
         uint32_t w0[SR / 2] = {}, w1[SR / 2] = {};   // rows 2i, 2i+1
         uint8_t* crow = FINAL ? canvas + ((uint64_t)c * H + 2 * ay + 2 * i) * W : nullptr;
         // mid levels: f32 pairs into outb
@@ -698,7 +712,7 @@ __global__ void __launch_bounds__(WS_THREADS) k_final_ws(const __grid_constant__
       } else if (act) {
         const float2* colL = reinterpret_cast<const float2*>(smem + BOXSET + b * COL_BYTES);
         const float2* colH = colL + TY * CB_PITCH;
-        auto cv = [](float v) { return min(__float2uint_rn(__fmul_rn(v, 255.0f)), 255u); };
+        auto cv = [](float v) { return u8_rint(__fmul_rn(v, 255.0f)); };
         uint8_t* crow = canvas + ((uint64_t)c * H + 2 * ay + 2 * i) * W;
         if (pa >= HALO && pb + HALO <= a.bw && pb - pa == SR) {
           uint32_t w0[SR / 2] = {}, w1[SR / 2] = {};
