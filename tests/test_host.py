@@ -53,6 +53,30 @@ def test_abi_host_functions(lib):
     assert lib.wv_decode_frame(C.byref(g), C.byref(a), None, None) == N.WV_ERR_ARG
 
 
+def test_encode_abi_host_checks(lib):
+    """wv_encode_*: sizing and argument validation (no GPU needed)."""
+    from paper_2208_10859_b200 import _native as N
+    ep = N.EncodeParams()
+    ep.width = ep.height = 8192
+    ep.channels, ep.levels, ep.inter_size, ep.block_size, ep.quantize = 3, 6, 4, 32, 1
+    ws, cap = C.c_uint64(), C.c_uint64()
+    assert lib.wv_encode_workspace_bytes(C.byref(ep), C.byref(ws)) == 0
+    assert lib.wv_encode_payload_capacity(C.byref(ep), C.byref(cap)) == 0
+    samples = 4 * 8192 * 8192 * 3
+    assert 8 * samples <= ws.value < 8 * samples * 1.05     # two f32 pyramids + tables
+    assert cap.value == 4 * 8192 * 8192 * (2 + 3)           # every coefficient a record
+    for field, value in (("inter_size", 3), ("block_size", 48), ("levels", 0), ("channels", 5)):
+        badp = N.EncodeParams.from_buffer_copy(ep)
+        setattr(badp, field, value)
+        assert lib.wv_encode_workspace_bytes(C.byref(badp), C.byref(ws)) == N.WV_ERR_ARG
+    odd = N.EncodeParams.from_buffer_copy(ep)
+    odd.width = 8192 + 32                                     # not divisible by 2^6
+    assert lib.wv_encode_payload_capacity(C.byref(odd), C.byref(cap)) == N.WV_ERR_ARG
+    # missing device pointers are rejected before any launch
+    assert lib.wv_encode_set(C.byref(ep), None, None, None, C.c_uint64(0), None, None, None,
+                             C.c_uint64(0), None, None) == N.WV_ERR_ARG
+
+
 def test_struct_layouts_match_header():
     from paper_2208_10859_b200 import _native as N
     assert C.sizeof(N.Geometry) == 36
@@ -60,6 +84,7 @@ def test_struct_layouts_match_header():
     assert N.FrameArgs.h_payload.offset == N.FrameArgs.d_result.offset + 8
     assert N.FrameArgs.d_mask.offset == 16
     assert N.FrameArgs.d_payload.offset == 16 + 8 + 12 * 4 * 4
+    assert C.sizeof(N.EncodeParams) == 8 * 4 + 4 * N.WV_MAX_LEVELS + 4 * N.WV_ENC_MAX_N
 
 
 @pytest.mark.parametrize("name", ["golden_quantized.wvv", "golden_float.wvv",
