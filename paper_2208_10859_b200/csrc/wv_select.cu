@@ -103,6 +103,9 @@ __global__ void k_mask_rows(const wv_frame_args* __restrict__ fa, uint32_t* __re
 // pools it into one bit per 32x32 cell (used by the block selection when
 // block_size is 32).
 constexpr int CT_R = 32, CT_W = 32, CT_TW = 8;   // tile rows, tile words, threads per row
+#ifndef WV_K1_FOV_RECT
+#define WV_K1_FOV_RECT 1   // skip gaze-window cascade tiles outside the window's level-j bound
+#endif   // tile rows, tile words, threads per row
 
 struct CascadeArgs {
   int j, L, H;
@@ -200,7 +203,18 @@ __global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
     rect = make_int4(f[0], f[1], f[2], f[3]);
   }
   const int4 none = make_int4(0, 0, 0, 0);
-  if ((a.j == 1 || a.src_pooled) && !cascade_tile_live(a, r0, w0)) {
+  // a gaze-window batch (b > 0) lives inside its pixel window scaled to level
+  // j and grown by the dilations: rows [r0 / 2^j - 8, r1 / 2^j + 8) (each
+  // level halves, then dilates by DIL = 4; 9 with rounding), columns alike
+  bool outside = false;
+  if (WV_K1_FOV_RECT && b > 0) {
+    const int32_t* f = a.fa->fovea[b - 1];
+    const int s = a.j, up = (1 << a.j) - 1;
+    const int lr0 = (f[0] >> s) - 9, lr1 = ((f[1] + up) >> s) + 9;
+    const int lc0 = (f[2] >> s) - 9, lc1 = ((f[3] + up) >> s) + 9;
+    outside = r0 >= lr1 || r0 + CT_R <= lr0 || 32 * w0 >= lc1 || 32 * (w0 + CT_W) <= lc0;
+  }
+  if (outside || ((a.j == 1 || a.src_pooled) && !cascade_tile_live(a, r0, w0))) {
     // nothing can reach this tile: zero words, zero pooled cell
     for (int e = threadIdx.x; e < CT_R * CT_W; e += blockDim.x) {
       const int r = r0 + e / CT_W, w = w0 + e % CT_W;
