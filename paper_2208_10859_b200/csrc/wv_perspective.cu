@@ -130,7 +130,6 @@ struct ViewConst {
   float tan_h, tan_v, inv_w, inv_h, sx, sy;
   int out_w, out_h, m, n, C, wpr0;
   uint32_t plane;
-  int xmin, xmax, ymin, ymax;   // candidate-tap bounding box of the CTA
 };
 
 // One CTA renders a K4_TY x K4_TX output tile (256 threads, K4_PPT pixels per
@@ -467,7 +466,8 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
     cov = a.x & a.y & a.z & a.w & b.x & b.y & b.z & b.w;
   }
   const uint32_t K = 0x4B000000u;
-  const bool full_tile = ((int)blockIdx.x + 1) * K4_TX <= out_w && ((int)blockIdx.y + 1) * K4_TY <= out_h;
+  const int tx0 = x - (int)threadIdx.x, ty0 = ybase - (int)threadIdx.y;   // tile origin
+  const bool full_tile = tx0 + K4_TX <= out_w && ty0 + K4_TY <= out_h;
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const uint32_t* wj = win + j * VW;
@@ -512,11 +512,11 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
   }
   __syncthreads();
   // (5) tile rows -> (out_h, out_w, C) with 16-byte stores where aligned
-  const int nx = min(K4_TX, out_w - (int)blockIdx.x * K4_TX);
-  const int ny = min(K4_TY, out_h - (int)blockIdx.y * K4_TY);
+  const int nx = min(K4_TX, out_w - tx0);
+  const int ny = min(K4_TY, out_h - ty0);
   const int rowb = nx * C;
   const uint64_t gpitch = (uint64_t)out_w * C;
-  const uint64_t gofs = ((uint64_t)blockIdx.y * K4_TY * out_w + blockIdx.x * K4_TX) * C;
+  const uint64_t gofs = ((uint64_t)ty0 * out_w + tx0) * C;
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     uint8_t* gbase = vp[j]->d_out + gofs;
@@ -566,6 +566,7 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
   __shared__ __align__(16) uint32_t win[WIN_WORDS];
   __shared__ __align__(16) uint8_t ost[2 * OST_VIEW];
   __shared__ __align__(16) uint32_t s_ok[8];
+  __shared__ int s_box[2][4];   // candidate-tap box: xmin, xmax, ymin, ymax
   const int vz = shared_n > 0 ? 0 : blockIdx.z;
   const wv_view_args& v = DEV ? d_views[vz] : views.v[vz];
   const int tid = threadIdx.y * 32 + threadIdx.x;
@@ -584,22 +585,28 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
     vc.C = v.channels;
     vc.wpr0 = (v.width + 31) >> 5;
     vc.plane = (uint32_t)v.canvas_h * (uint32_t)v.width;
-    vc.xmin = vc.ymin = 0x7FFFFFFF;
-    vc.xmax = vc.ymax = -0x7FFFFFFF;
+    s_box[0][0] = s_box[0][2] = 0x7FFFFFFF;
+    s_box[0][1] = s_box[0][3] = -0x7FFFFFFF;
   }
   __syncthreads();
   const int out_w = vc.out_w, out_h = vc.out_h;
-  if ((int)blockIdx.x * K4_TX >= out_w || (int)blockIdx.y * K4_TY >= out_h) return;  // smaller view
   const int m = vc.m, n = vc.n;
-  const int x = blockIdx.x * K4_TX + threadIdx.x;
-  const int ybase = blockIdx.y * K4_TY + threadIdx.y;
+  const int ntx = (out_w + K4_TX - 1) / K4_TX, ntiles = ntx * ((out_h + K4_TY - 1) / K4_TY);
+  // persistent CTAs: the view constants are set up once, tiles round-robin;
+  // the candidate-tap box alternates between two shared slots, so the next
+  // tile's slot is reset while the current one is in use (no extra barrier)
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    int* box = s_box[it & 1];
+    const int tby = tile / ntx, tbx = tile - tby * ntx;
+    const int x = tbx * K4_TX + threadIdx.x;
+    const int ybase = tby * K4_TY + threadIdx.y;
 
-  // (1) geometry
-  int x0[K4_PPT], y0[K4_PPT];
-  float ax[K4_PPT], ay[K4_PPT];
-  int bx0 = 0x7FFFFFFF, bx1 = -0x7FFFFFFF, by0 = 0x7FFFFFFF, by1 = -0x7FFFFFFF;
-  geo_all(vc, x, ybase, x0, y0, ax, ay);
-  {
+    // (1) geometry
+    int x0[K4_PPT], y0[K4_PPT];
+    float ax[K4_PPT], ay[K4_PPT];
+    int bx0 = 0x7FFFFFFF, bx1 = -0x7FFFFFFF, by0 = 0x7FFFFFFF, by1 = -0x7FFFFFFF;
+    geo_all(vc, x, ybase, x0, y0, ax, ay);
 #pragma unroll
     for (int k = 0; k < K4_PPT; ++k) {
       const int y = ybase + 8 * k;
@@ -610,53 +617,66 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
         by1 = max(by1, y0[k] + 2);
       }
     }
-  }
-  {
-    // candidate-tap box of the CTA (both tap choices near integer boundaries)
+    // candidate-tap box of the tile (both tap choices near integer boundaries)
     bx0 = __reduce_min_sync(0xFFFFFFFFu, bx0);
     bx1 = __reduce_max_sync(0xFFFFFFFFu, bx1);
     by0 = __reduce_min_sync(0xFFFFFFFFu, by0);
     by1 = __reduce_max_sync(0xFFFFFFFFu, by1);
     if (threadIdx.x == 0) {
-      atomicMin(&vc.xmin, bx0);
-      atomicMax(&vc.xmax, bx1);
-      atomicMin(&vc.ymin, by0);
-      atomicMax(&vc.ymax, by1);
+      atomicMin(&box[0], bx0);
+      atomicMax(&box[1], bx1);
+      atomicMin(&box[2], by0);
+      atomicMax(&box[3], by1);
     }
-  }
-  __syncthreads();
-  const int xl = vc.xmin, xh = vc.xmax, yl = vc.ymin, yh = vc.ymax;
-  const bool inside = xl >= 0 && xh < n && yl >= 0 && yh < m && xl <= xh;
-  const int wx0 = xl & ~3;
-  const int ww = ((xh | 3) - wx0 + 1) >> 2;   // 4-pixel words per window row
-  const int vwords = inside ? (yh - yl + 1) * 4 * ww : 0x7FFFFFFF;
-  const bool box_ok = inside && (xh - xl) < BOX_MAX_W;
-  // window offset of each pixel's (x0, y0) tap (used only when staged; the
-  // general path re-evaluates its geometry)
-  int off[K4_PPT];
+    if (tid == 0) {   // the other slot: last read before the previous tile's barriers
+      int* nb = s_box[(it + 1) & 1];
+      nb[0] = nb[2] = 0x7FFFFFFF;
+      nb[1] = nb[3] = -0x7FFFFFFF;
+    }
+    __syncthreads();
+    const int xl = box[0], xh = box[1], yl = box[2], yh = box[3];
+    const bool inside = xl >= 0 && xh < n && yl >= 0 && yh < m && xl <= xh;
+    const int wx0 = xl & ~3;
+    const int ww = ((xh | 3) - wx0 + 1) >> 2;   // 4-pixel words per window row
+    const int vwords = inside ? (yh - yl + 1) * 4 * ww : 0x7FFFFFFF;
+    const bool box_ok = inside && (xh - xl) < BOX_MAX_W;
+    // window offset of each pixel's (x0, y0) tap (used only when staged; the
+    // general path re-evaluates its geometry)
+    int off[K4_PPT];
 #pragma unroll
-  for (int k = 0; k < K4_PPT; ++k) off[k] = (y0[k] - yl) * (4 * ww) + (x0[k] - wx0);
-  const bool stage = inside && (n & 3) == 0;
-  const int nv = shared_n > 0 ? shared_n : 1;
-  auto vargs = [&](int vi) -> const wv_view_args* {
-    return shared_n > 0 ? (DEV ? d_views + vi : &views.v[vi]) : &v;
-  };
-  for (int vi = 0; vi < nv;) {
-    if (vi + 1 < nv && stage && 2 * vwords <= WIN_WORDS) {
-      const wv_view_args* const vp[2] = {vargs(vi), vargs(vi + 1)};
-      finish_c<2>(vc, v, vp, win, ost, s_ok, off, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
-                  box_ok, true, tid);
-      vi += 2;
-    } else {
-      const wv_view_args* const vp[1] = {vargs(vi)};
-      finish_c<1>(vc, v, vp, win, ost, s_ok, off, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
-                  box_ok, stage && vwords <= WIN_WORDS, tid);
-      vi += 1;
+    for (int k = 0; k < K4_PPT; ++k) off[k] = (y0[k] - yl) * (4 * ww) + (x0[k] - wx0);
+    const bool stage = inside && (n & 3) == 0;
+    const int nv = shared_n > 0 ? shared_n : 1;
+    auto vargs = [&](int vi) -> const wv_view_args* {
+      return shared_n > 0 ? (DEV ? d_views + vi : &views.v[vi]) : &v;
+    };
+    for (int vi = 0; vi < nv;) {
+      if (vi + 1 < nv && stage && 2 * vwords <= WIN_WORDS) {
+        const wv_view_args* const vp[2] = {vargs(vi), vargs(vi + 1)};
+        finish_c<2>(vc, v, vp, win, ost, s_ok, off, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
+                    box_ok, true, tid);
+        vi += 2;
+      } else {
+        const wv_view_args* const vp[1] = {vargs(vi)};
+        finish_c<1>(vc, v, vp, win, ost, s_ok, off, ax, ay, x, ybase, xl, xh, yl, yh, wx0, ww,
+                    box_ok, stage && vwords <= WIN_WORDS, tid);
+        vi += 1;
+      }
     }
   }
 }
 
 }  // namespace
+
+// resident CTAs for the persistent K4 grid (at most one per tile)
+template <class K>
+int persistent_grid(K kernel, int ntiles) {
+  int dev = 0, sms = 148, occ = K4_MIN_BLOCKS;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, 0);
+  return max(1, min(ntiles, sms * max(occ, 1)));
+}
 
 int launch_perspective(const wv_view_args* views, int n, cudaStream_t s) {
   if (n < 1 || n > kMaxViews) return WV_ERR_ARG;
@@ -682,7 +702,8 @@ int launch_perspective(const wv_view_args* views, int n, cudaStream_t s) {
     for (int k = 0; k < 9 && shared; ++k) shared = a.rot[k] == b.rot[k];
   }
   dim3 block(32, 8);
-  dim3 grid(cdiv(mw, K4_TX), cdiv(mh, K4_TY), shared ? 1 : n);
+  dim3 grid(persistent_grid(k_perspective<false>, cdiv(mw, K4_TX) * cdiv(mh, K4_TY)), 1,
+            shared ? 1 : n);
   WV_CUDA(launch_k(k_perspective<false>, dim3(grid), dim3(block), 0, s, pv, nullptr, shared ? n : 0));
   WV_CUDA(cudaGetLastError());
   return WV_OK;
@@ -694,7 +715,8 @@ int launch_perspective_dev(const wv_view_args* d_views, int n, int max_w, int ma
   Views none{};
   const bool shared = shared_geometry && n > 1;
   dim3 block(32, 8);
-  dim3 grid(cdiv(max_w, K4_TX), cdiv(max_h, K4_TY), shared ? 1 : n);
+  dim3 grid(persistent_grid(k_perspective<true>, cdiv(max_w, K4_TX) * cdiv(max_h, K4_TY)), 1,
+            shared ? 1 : n);
   WV_CUDA(launch_k(k_perspective<true>, dim3(grid), dim3(block), 0, s, none, d_views, shared ? n : 0));
   WV_CUDA(cudaGetLastError());
   return WV_OK;
