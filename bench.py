@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--size", type=int, default=8192, help="frame width = height")
-    ap.add_argument("--sets", type=int, default=0, help="inter-frame sets (default max(2, N))")
+    ap.add_argument("--sets", type=int, default=0,
+                    help="inter-frame sets (default: max(2, N); --mode full: 4 per GPU, config 5's "
+                         "long clip)")
     ap.add_argument("--mode", choices=["viewport", "foveated", "full"], default="viewport")
     ap.add_argument("--cache-dir", default="/tmp/wvb200_bench")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -60,6 +62,15 @@ def parse():
 
 
 # ------------------------------------------------------------------ inputs
+
+def default_sets(args, world: int) -> int:
+    """Sets in the input clip: config 5 (full-frame decode of a long clip
+    sharded by group of frames) cycles 4 distinct sets per GPU; the viewport
+    configs use max(2, N)."""
+    if args.sets:
+        return args.sets
+    return max(4, 4 * world) if args.mode == "full" else max(2, world)
+
 
 def input_path(args, n_sets: int) -> str:
     return os.path.join(args.cache_dir, f"c3_{args.size}_s{n_sets}_v1.wvv")
@@ -221,7 +232,7 @@ def run_ours(args):
         build.build()
     if world > 1:
         dist.barrier()
-    n_sets = args.sets or max(2, world)
+    n_sets = default_sets(args, world)
     path = input_path(args, n_sets)
     if rank == 0 and not os.path.exists(path):
         make_input(path, args.size, n_sets, dev)
@@ -543,7 +554,7 @@ def run_reference(args):
         return
     import multiprocessing as mp
     import numpy as np
-    n_sets = args.sets or max(2, world)
+    n_sets = default_sets(args, world)
     path = input_path(args, n_sets)
     if not os.path.exists(path):
         import torch
@@ -579,9 +590,11 @@ def run_reference(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(wall * 1000.0 / n_timed, 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"C3 {h.width}x{h.height} stereo 360 {args.mode} decode + per-eye "
-                               f"{OUT_W}x{OUT_H} perspective writeout (CPU oracle port)",
-                   "frames": h.frame_count},
+        "config": {"workload": (f"C3 {h.width}x{h.height} stereo 360 {args.mode} decode + per-eye "
+                                f"{OUT_W}x{OUT_H} perspective writeout (CPU oracle port)"
+                                if args.mode != "full" else
+                                f"{h.width}x{h.height} full-frame decode (CPU oracle port)"),
+                   "frames": h.frame_count, "sets": h.num_sets},
         "cpu_baseline": {"value": round(fps, 4), "unit": "frames/s", "cores": procs,
                          "kind": "port",
                          "sample": f"{n_timed} display frames (of the {args.steps} requested; "
