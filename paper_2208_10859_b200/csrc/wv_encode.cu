@@ -10,18 +10,22 @@
 // IEEE op in the reference's order (this TU is built with --fmad=false and
 // uses explicit _rn intrinsics), so the payload bytes equal the reference's.
 //
-// Kernels (one set, n frames, C channels, H x W):
-//   E2 k_rows /    per level: CDF 9/7 analysis along rows (planes -> tmp;
-//      k_rows_u8   level 1 reads the u8 frames directly, x / 255),
-//      k_cols      then along columns (tmp -> planes); each thread lifts a
-//                  16-pair segment from a 2-pair halo (analysis support)
+// Kernels (one set, n frames, C channels, H x W; 2L + 7 launches):
+//   E1 k_rows_u8   level-1 row lifting straight from the u8 frames (x / 255
+//                  from a table of the IEEE quotients), warp chunks staged in
+//                  shared memory for coalesced loads and stores
+//   E2 k_rows /    levels 2..L rows (planes -> tmp, same warp chunks) and
+//      k_cols      every level's columns (tmp -> planes, adjacent threads on
+//                  adjacent columns); each lane lifts a 16-pair segment from
+//                  a 2-pair halo (the analysis support)
 //   E3 k_point     per 32x32 block, per position: spatial threshold of each
 //                  frame (channel max magnitude vs level threshold + H(y)),
 //                  temporal Haar forward in Mallat order, temporal
 //                  threshold; emits nonzero bits, (t, block) record counts
 //                  and the per-(t, c) approximation / detail extrema
-//   E6 k_scan*     exclusive scan of the counts -> first record of each block
-//   E7 k_emit      per (t, block): rank by (layer, offset), quantise, write
+//   E4 k_scan*     exclusive scan of the counts -> first record of each block
+//   E5 k_emit      per (t, block) with records: rank by (layer, offset),
+//                  quantise, write
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -73,7 +77,7 @@ EncLayout enc_layout(const wv_encode_params& p) {
   return L;
 }
 
-// ---------------------------------------------------------------- E2
+// ---------------------------------------------------------------- E1 / E2
 
 // CDF 9/7 analysis (wavelets.py:44-65) of pairs [a, a + SEG) of a line of M
 // pairs: d += A(s + s[i+1]); s += B(d[i-1] + d); d += G(s + s[i+1]);
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(256) k_point(float* __restrict__ planes,
   }
 }
 
-// ---------------------------------------------------------------- E5 / E7
+// ---------------------------------------------------------------- E4 / E5
 
 // Storage layer of a position (wavelets.py:202-211): 0 approx, L - k + 1 for
 // level-k detail.
