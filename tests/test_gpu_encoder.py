@@ -75,3 +75,24 @@ def test_cuda_encoder_8k_set_matches_torch():
         del v
         torch.cuda.empty_cache()
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("shape,n,quant,mapping", [
+    ((4, 64, 64, 4), 4, True, "EQUIRECTANGULAR"),     # 4 channels (generic point kernel)
+    ((6, 128, 64, 2), 2, False, "NONE"),              # float records, n = 2, padded last set
+    ((16, 64, 128, 1), 16, True, "EQUIRECTANGULAR"),  # n = 16 (run-time temporal depth)
+])
+def test_cuda_encoder_matches_restatement_other_shapes(shape, n, quant, mapping, tmp_path):
+    """Shapes outside the golden fixtures: CUDA encoder bytes == the torch
+    restatement's on CPU (itself pinned to the reference bytes)."""
+    from paper_2208_10859_b200.encoding import EncodeParams, MappingKind, encode_video
+    from paper_2208_10859_b200.fileio import write_video
+    clip = np.random.default_rng(21).integers(0, 256, shape, dtype=np.uint8)
+    p = EncodeParams(levels=3, inter_size=n, quantize=quant, mapping=MappingKind[mapping],
+                     alpha=0.05, inter_threshold=0.002)
+    outs = []
+    for dev in ("cuda", "cpu"):
+        f = tmp_path / f"{dev}.wvv"
+        write_video(encode_video(clip, p, device=dev), f)
+        outs.append(f.read_bytes())
+    assert outs[0] == outs[1]
