@@ -52,6 +52,7 @@ struct Layout {
   uint64_t plane;                        // C x H x W f32
   uint64_t ybuf[WV_MAX_LEVELS + 1];      // level k (1..L-1): C x (H>>k) x pitch[k] f32
   int ypitch[WV_MAX_LEVELS + 1];
+  uint64_t mbits;                        // low-res mask as bit rows: mh x ceil(mw/32) u32
   uint64_t total;
 };
 
@@ -109,6 +110,7 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
     o->ypitch[k] = (cols + 3) & ~3;
     o->ybuf[k] = take(uint64_t(C) * (H >> k) * o->ypitch[k] * 4);
   }
+  o->mbits = take(uint64_t(g->mask_h) * ((g->mask_w + 31) / 32) * 4);
   o->total = off;
   return WV_OK;
 }

@@ -73,13 +73,24 @@ __device__ __forceinline__ uint32_t shrink(uint32_t p, uint32_t c, uint32_t n) {
 // row map rowmap[y] = (y*mh)/H (fileio.py:434).
 __global__ void k_mask_rows(const wv_frame_args* __restrict__ fa, uint32_t* __restrict__ R,
                             uint32_t* __restrict__ rowmap, uint32_t* __restrict__ counters, int mh,
-                            int mw, int W, int H, int wpr0, int full) {
+                            int mw, int W, int H, int wpr0, int full, uint32_t* __restrict__ mbits) {
   pdl_sync();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const uint8_t* __restrict__ mask = fa->d_mask;
   if (idx == 0) *fa->d_result = wv_frame_result{};
   if (idx < 64) counters[idx] = 0u;   // work-list counters of this call
   if (idx < H) rowmap[idx] = ((uint32_t)idx * (uint32_t)mh) / (uint32_t)H;
+  {
+    // the low-res mask as bit rows (direct cascade source)
+    const int mwpr = (mw + 31) >> 5;
+    if (!full && idx < mh * mwpr) {
+      const int my = idx / mwpr, k = idx - (idx / mwpr) * mwpr;
+      uint32_t b = 0;
+      for (int i = 0; i < 32 && 32 * k + i < mw; ++i)
+        b |= (mask[(uint64_t)my * mw + 32 * k + i] ? 1u : 0u) << i;
+      mbits[idx] = b;
+    }
+  }
   if (idx >= mh * wpr0) return;
   const int my = idx / wpr0, w = idx % wpr0;
   // the word's pixels map to a few runs of mask columns: pixel x -> floor(x*mw/W)
@@ -103,6 +114,9 @@ __global__ void k_mask_rows(const wv_frame_args* __restrict__ fa, uint32_t* __re
 // pools it into one bit per 32x32 cell (used by the block selection when
 // block_size is 32).
 constexpr int CT_R = 32, CT_W = 32, CT_TW = 8;   // tile rows, tile words, threads per row
+#ifndef WV_K1_DIRECT
+#define WV_K1_DIRECT 1     // all cascade levels in one launch as box ORs of the low-res mask
+#endif
 #ifndef WV_K1_FOV_RECT
 #define WV_K1_FOV_RECT 1   // skip gaze-window cascade tiles outside the window's level-j bound
 #endif   // tile rows, tile words, threads per row
@@ -271,6 +285,130 @@ __global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
       const uint32_t bits = __ballot_sync(0xFFFFFFFFu, threadIdx.x < CT_W && pool[threadIdx.x]);
       if (threadIdx.x == 0) a.pooled[(uint64_t)blockIdx.z * a.pool_wpr + blockIdx.x] = bits;
     }
+  }
+}
+
+// ------------------------------------------------- direct cascade (one launch)
+// C_j = dilate4(downmap2(C_{j-1})) with C_0 the upscaled pixel mask is an OR
+// over a box: downmap2 ORs pixel pairs and dilate4 ORs a 9 x 9 box, both
+// separable, so C_j(y, x) = OR of C_0 over rows [2^j y - A_j, 2^j y + B_j]
+// and the same columns, A_j = 8 (2^j - 1), B_j = 9 (2^j - 1), clipped to the
+// frame (out-of-range cells contribute nothing at every level, exactly as in
+// the step-by-step cascade).  A gaze-window batch b > 0 starts from C_0 ∩
+// its pixel window, i.e. the box is clipped to the window too.  C_0 is the
+// nearest upscale of the low-res mask (fileio.py:430-436), so a box reduces
+// to an OR of low-res bit rows and, per set cell, an interval of output
+// bits.  One CTA per (level, batch, 32-row band), 8 warps x 4 rows; the
+// final masks are also pooled per 32 x 32 cell as the step kernel does.
+struct DirectArgs {
+  int L, H, W, mh, mw, mwpr, fov;
+  const uint32_t* mbits;
+  const wv_frame_args* fa;
+  int nitems;                       // entries used in the tables below
+  int first_cta[WV_MAX_LEVELS * (WV_MAX_LEVELS + 1) + 1];
+  uint8_t lev[WV_MAX_LEVELS * (WV_MAX_LEVELS + 1)], bat[WV_MAX_LEVELS * (WV_MAX_LEVELS + 1)];
+  uint32_t* dst[WV_MAX_LEVELS + 1];
+  uint64_t dst_stride[WV_MAX_LEVELS + 1];   // words per batch mask
+  int wpr[WV_MAX_LEVELS + 1];
+  uint32_t* pooled[WV_MAX_LEVELS + 1];      // null: not pooled
+  int pool_wpr[WV_MAX_LEVELS + 1];
+};
+
+// Row y of C_j for batch window win = (r0, r1, c0, c1) (pixels, half open;
+// the whole frame for the request): srow gets the OR of the low-res bit rows
+// under the box; returns whether any of them is set (warp-uniform).
+__device__ __forceinline__ bool direct_prep(const DirectArgs& a, int j, int y, int4 win,
+                                            uint32_t* srow, int lane) {
+  const int A = 8 * ((1 << j) - 1), B = 9 * ((1 << j) - 1);
+  const int p0 = max(max((y << j) - A, 0), win.x), p1 = min(min((y << j) + B, a.H - 1), win.y - 1);
+  uint32_t rowor = 0;
+  if (p0 <= p1 && lane < a.mwpr) {
+    const int m0 = (int)(((uint32_t)p0 * (uint32_t)a.mh) / (uint32_t)a.H);
+    const int m1 = (int)(((uint32_t)p1 * (uint32_t)a.mh) / (uint32_t)a.H);
+    for (int m = m0; m <= m1; ++m) rowor |= a.mbits[(uint64_t)m * a.mwpr + lane];
+  }
+  if (lane < a.mwpr) srow[lane] = rowor;
+  return __any_sync(0xFFFFFFFFu, rowor != 0u);
+}
+
+// word w of that row: each set low-res cell under the box sets the output
+// bits whose box [x 2^j - A, x 2^j + B] meets the cell's pixels (clipped to
+// the window)
+__device__ __forceinline__ uint32_t direct_word(const DirectArgs& a, int j, int4 win,
+                                                const uint32_t* srow, const int* cell_x0, int w) {
+  const int A = 8 * ((1 << j) - 1), B = 9 * ((1 << j) - 1);
+  const int ncols = a.W >> j;
+  const int x0 = 32 * w, x1 = min(32 * w + 31, ncols - 1);
+  const int q0 = max(max((x0 << j) - A, 0), win.z), q1 = min(min((x1 << j) + B, a.W - 1), win.w - 1);
+  if (q0 > q1) return 0u;
+  const int cA = (int)(((uint32_t)q0 * (uint32_t)a.mw) / (uint32_t)a.W);
+  const int cB = (int)(((uint32_t)q1 * (uint32_t)a.mw) / (uint32_t)a.W);
+  uint32_t v = 0;
+  // set cells of srow in [cA, cB], word by word (find-first-set)
+  for (int cw = cA >> 5; cw <= (cB >> 5); ++cw) {
+   uint32_t bits = srow[cw] & range_mask(cA, cB + 1, cw);
+   while (bits) {
+    const int c = 32 * cw + __ffs(bits) - 1;
+    bits &= bits - 1u;
+    // pixels x of cell c: floor(x mw / W) == c (table of cell starts)
+    int s0 = cell_x0[c];
+    int s1 = cell_x0[c + 1] - 1;
+    s0 = max(s0, win.z);
+    s1 = min(s1, win.w - 1);
+    if (s0 > s1) continue;
+    const int lo = max((s0 - B + (1 << j) - 1) >> j, 0);   // ceil((s0 - B) / 2^j), s0 - B >= -B
+    const int hi = min((s1 + A) >> j, ncols - 1);
+    v |= range_mask(lo, hi + 1, w);
+   }
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_cascade_direct(DirectArgs a) {
+  pdl_sync();
+  __shared__ uint32_t srow[8][2][32];
+  __shared__ uint32_t s_pool[64];
+  // which (level, batch) item this CTA serves
+  int it = 0;
+  while (it + 1 < a.nitems && (int)blockIdx.x >= a.first_cta[it + 1]) ++it;
+  const int j = a.lev[it], b = a.bat[it];
+  const int band = blockIdx.x - a.first_cta[it];
+  const int rows = a.H >> j, wpr = a.wpr[j];
+  const bool final_mask = a.fov ? (b == j) : (b == 0);
+  uint32_t* pooled = final_mask ? a.pooled[j] : nullptr;
+  const int npw = (wpr + 31) >> 5;   // pooled words of this band
+  for (int k = threadIdx.x; k < npw; k += blockDim.x) s_pool[k] = 0u;
+  __shared__ int cell_x0[1025];   // first pixel of low-res column c: ceil(c W / mw)
+  for (int c = threadIdx.x; c <= a.mw; c += blockDim.x)
+    cell_x0[c] = (int)(((uint32_t)c * (uint32_t)a.W + a.mw - 1) / (uint32_t)a.mw);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int4 full = make_int4(0, a.H, 0, a.W);
+  int4 win = full;
+  if (b > 0) {
+    const int32_t* f = a.fa->fovea[b - 1];
+    win = make_int4(f[0], f[1], f[2], f[3]);
+  }
+  const bool both = a.fov && b == j;   // D_j = C_j(window j) & C_j(request)
+  for (int r = 0; r < 4; ++r) {
+    const int y = band * 32 + wp * 4 + r;
+    if (y >= rows) break;
+    const bool anyA = direct_prep(a, j, y, win, srow[wp][0], lane);
+    const bool anyB = both ? direct_prep(a, j, y, full, srow[wp][1], lane) : true;
+    __syncwarp();
+    uint32_t* out = a.dst[j] + (uint64_t)b * a.dst_stride[j] + (uint64_t)y * wpr;
+    for (int w = lane; w < wpr; w += 32) {
+      uint32_t v = anyA ? direct_word(a, j, win, srow[wp][0], cell_x0, w) : 0u;
+      if (both && v) v &= anyB ? direct_word(a, j, full, srow[wp][1], cell_x0, w) : 0u;
+      out[w] = v;
+      if (pooled && v) atomicOr(&s_pool[w >> 5], 1u << (w & 31));
+    }
+    __syncwarp();
+  }
+  if (pooled) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < npw; k += blockDim.x)
+      pooled[(uint64_t)band * a.pool_wpr[j] + k] = s_pool[k];
   }
 }
 
@@ -756,11 +894,40 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
   if (st_rows) {
     const int n = max(lo.mh * lo.wpr_[0], H);
     WV_CUDA(launch_k(k_mask_rows, dim3(cdiv(n, 256)), dim3(256), 0, s, fa, R, rowmap, counters,
-                     lo.mh, lo.mw, W, H, lo.wpr_[0], (int)full));
+                     lo.mh, lo.mw, W, H, lo.wpr_[0], (int)full, (uint32_t*)(ws + lo.mbits)));
   }
   // level cascades (batch 0: request closure; batches k>=j: gaze windows);
   // a full-frame decode needs none of them
-  for (int j = 1; j <= L && !full && st_cas; ++j) {
+  const bool direct = WV_K1_DIRECT && lo.mw <= 1024 && !full && st_cas;
+  if (direct) {
+    DirectArgs d{};
+    d.L = L; d.H = H; d.W = W; d.mh = lo.mh; d.mw = lo.mw; d.mwpr = (lo.mw + 31) / 32;
+    d.fov = fov;
+    d.mbits = (const uint32_t*)(ws + lo.mbits);
+    d.fa = fa;
+    int ctas = 0;
+    for (int j = 1; j <= L; ++j) {
+      d.dst[j] = (uint32_t*)(ws + lo.stack[j]);
+      d.dst_stride[j] = lo.stack_stride[j] / 4;
+      d.wpr[j] = lo.wpr_[j];
+      d.pooled[j] = lo.bs == 32 ? (uint32_t*)(ws + lo.pooled[j]) : nullptr;
+      d.pool_wpr[j] = cdiv(lo.wpr_[j], CT_W);
+      const int bands = cdiv(H >> j, 32);
+      auto add = [&](int bb) {
+        d.lev[d.nitems] = (uint8_t)j;
+        d.bat[d.nitems] = (uint8_t)bb;
+        d.first_cta[d.nitems] = ctas;
+        ++d.nitems;
+        ctas += bands;
+      };
+      add(0);
+      if (fov)
+        for (int k = j; k <= L; ++k) add(k);
+    }
+    d.first_cta[d.nitems] = ctas;
+    WV_CUDA(launch_k(k_cascade_direct, dim3(ctas), dim3(256), 0, s, d));
+  }
+  for (int j = 1; j <= L && !full && st_cas && !direct; ++j) {
     CascadeArgs c{};
     c.j = j; c.L = L; c.H = H;
     c.rows = H >> j; c.cols = W >> j; c.wpr = lo.wpr_[j];
