@@ -117,6 +117,9 @@ constexpr int CT_R = 32, CT_W = 32, CT_TW = 8;   // tile rows, tile words, threa
 #ifndef WV_K1_DIRECT
 #define WV_K1_DIRECT 1     // all cascade levels in one launch as box ORs of the low-res mask
 #endif
+#ifndef WV_K1_DIRECT_RPW_WARPS
+#define WV_K1_DIRECT_RPW_WARPS 32   // warps per 32-row band of the direct cascade (one row each)
+#endif
 #ifndef WV_K1_FOV_RECT
 #define WV_K1_FOV_RECT 1   // skip gaze-window cascade tiles outside the window's level-j bound
 #endif   // tile rows, tile words, threads per row
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(256) k_cascade(CascadeArgs a) {
 // its pixel window, i.e. the box is clipped to the window too.  C_0 is the
 // nearest upscale of the low-res mask (fileio.py:430-436), so a box reduces
 // to an OR of low-res bit rows and, per set cell, an interval of output
-// bits.  One CTA per (level, batch, 32-row band), 8 warps x 4 rows; the
+// bits.  One CTA per (level, batch, 32-row band), one warp per row; the
 // final masks are also pooled per 32 x 32 cell as the step kernel does.
 struct DirectArgs {
   int L, H, W, mh, mw, mwpr, fov;
@@ -364,9 +367,34 @@ __device__ __forceinline__ uint32_t direct_word(const DirectArgs& a, int j, int4
   return v;
 }
 
-__global__ void __launch_bounds__(256) k_cascade_direct(DirectArgs a) {
+// direct_word with the candidate cells split over the warp's lanes (coarse
+// levels: a word's box spans tens of cells); every lane gets the word
+__device__ __forceinline__ uint32_t direct_word_warp(const DirectArgs& a, int j, int4 win,
+                                                     const uint32_t* srow, const int* cell_x0,
+                                                     int w, int lane) {
+  const int A = 8 * ((1 << j) - 1), B = 9 * ((1 << j) - 1);
+  const int ncols = a.W >> j;
+  const int x0 = 32 * w, x1 = min(32 * w + 31, ncols - 1);
+  const int q0 = max(max((x0 << j) - A, 0), win.z), q1 = min(min((x1 << j) + B, a.W - 1), win.w - 1);
+  uint32_t v = 0;
+  if (q0 <= q1) {
+    const int cA = (int)(((uint32_t)q0 * (uint32_t)a.mw) / (uint32_t)a.W);
+    const int cB = (int)(((uint32_t)q1 * (uint32_t)a.mw) / (uint32_t)a.W);
+    for (int c = cA + lane; c <= cB; c += 32) {
+      if (!((srow[c >> 5] >> (c & 31)) & 1u)) continue;
+      const int s0 = max(cell_x0[c], win.z), s1 = min(cell_x0[c + 1] - 1, win.w - 1);
+      if (s0 > s1) continue;
+      const int lo = max((s0 - B + (1 << j) - 1) >> j, 0);
+      const int hi = min((s1 + A) >> j, ncols - 1);
+      v |= range_mask(lo, hi + 1, w);
+    }
+  }
+  return __reduce_or_sync(0xFFFFFFFFu, v);
+}
+
+__global__ void __launch_bounds__(32 * WV_K1_DIRECT_RPW_WARPS) k_cascade_direct(DirectArgs a) {
   pdl_sync();
-  __shared__ uint32_t srow[8][2][32];
+  __shared__ uint32_t srow[WV_K1_DIRECT_RPW_WARPS][2][32];
   __shared__ uint32_t s_pool[64];
   // which (level, batch) item this CTA serves
   int it = 0;
@@ -390,18 +418,32 @@ __global__ void __launch_bounds__(256) k_cascade_direct(DirectArgs a) {
     win = make_int4(f[0], f[1], f[2], f[3]);
   }
   const bool both = a.fov && b == j;   // D_j = C_j(window j) & C_j(request)
-  for (int r = 0; r < 4; ++r) {
-    const int y = band * 32 + wp * 4 + r;
+  constexpr int RPW = 32 / WV_K1_DIRECT_RPW_WARPS;   // rows per warp of the 32-row band
+  for (int r = 0; r < RPW; ++r) {
+    const int y = band * 32 + wp * RPW + r;
     if (y >= rows) break;
     const bool anyA = direct_prep(a, j, y, win, srow[wp][0], lane);
     const bool anyB = both ? direct_prep(a, j, y, full, srow[wp][1], lane) : true;
     __syncwarp();
     uint32_t* out = a.dst[j] + (uint64_t)b * a.dst_stride[j] + (uint64_t)y * wpr;
-    for (int w = lane; w < wpr; w += 32) {
-      uint32_t v = anyA ? direct_word(a, j, win, srow[wp][0], cell_x0, w) : 0u;
-      if (both && v) v &= anyB ? direct_word(a, j, full, srow[wp][1], cell_x0, w) : 0u;
-      out[w] = v;
-      if (pooled && v) atomicOr(&s_pool[w >> 5], 1u << (w & 31));
+    if (wpr > 8) {
+      // enough words for the lanes: one word per lane
+      for (int w = lane; w < wpr; w += 32) {
+        uint32_t v = anyA ? direct_word(a, j, win, srow[wp][0], cell_x0, w) : 0u;
+        if (both && v) v &= anyB ? direct_word(a, j, full, srow[wp][1], cell_x0, w) : 0u;
+        out[w] = v;
+        if (pooled && v) atomicOr(&s_pool[w >> 5], 1u << (w & 31));
+      }
+    } else {
+      // coarsest levels: few words, tens of cells each, split over the lanes
+      for (int w = 0; w < wpr; ++w) {
+        uint32_t v = anyA ? direct_word_warp(a, j, win, srow[wp][0], cell_x0, w, lane) : 0u;
+        if (both && v) v &= anyB ? direct_word_warp(a, j, full, srow[wp][1], cell_x0, w, lane) : 0u;
+        if (lane == 0) {
+          out[w] = v;
+          if (pooled && v) atomicOr(&s_pool[w >> 5], 1u << (w & 31));
+        }
+      }
     }
     __syncwarp();
   }
@@ -925,7 +967,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
         for (int k = j; k <= L; ++k) add(k);
     }
     d.first_cta[d.nitems] = ctas;
-    WV_CUDA(launch_k(k_cascade_direct, dim3(ctas), dim3(256), 0, s, d));
+    WV_CUDA(launch_k(k_cascade_direct, dim3(ctas), dim3(32 * WV_K1_DIRECT_RPW_WARPS), 0, s, d));
   }
   for (int j = 1; j <= L && !full && st_cas && !direct; ++j) {
     CascadeArgs c{};

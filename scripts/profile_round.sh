@@ -18,7 +18,7 @@ cap k3_final k_level 11 ""
 cap k3_level2 k_level 10 ""
 cap k2 k_temporal 1 ""
 cap k4 persp 1 ""
-cap k1_cascade1 k_cascade 6 ""
+cap k1_cascade k_cascade 0 ""
 cap k3_final_full k_level 11 "--mode full"
 cap k2_full k_temporal 1 "--mode full"
 ls -la $out
