@@ -184,16 +184,16 @@ def peaks():
 
 
 def launches_per_frame(L: int, mode: str, residency: str) -> int:
-    """Kernels of one frame's graph (csrc launch sequence): K1 rows, one
-    direct cascade (all levels; masks up to 1024 cells wide), L-1 footprint
-    steps, blocks, tile lists (2), finest footprint; K2; K3 L levels; K4 --
-    full frame: rows, footprint fill, blocks, tile lists, K2, K3 (no
-    cascades, footprint chain or writeout)."""
+    """Kernels of one frame's graph (csrc launch sequence): K1 rows, L
+    cascade steps (the default build; WV_K1_DIRECT=1 makes them one launch),
+    L-1 footprint steps, blocks, tile lists (2), finest footprint; K2; K3 L
+    levels; K4 -- full frame: rows, footprint fill, blocks, tile lists, K2,
+    K3 (no cascades, footprint chain or writeout)."""
     tiles = 1 + (1 if L >= 2 else 0)
     if mode == "full":
         n = 1 + 1 + 1 + tiles + 1 + L
     else:
-        n = 1 + 1 + (L - 1) + 1 + tiles + 1 + 1 + L + 1
+        n = 1 + L + (L - 1) + 1 + tiles + 1 + 1 + L + 1
     return n + (1 if residency == "spans" else 0)
 
 

@@ -115,7 +115,7 @@ __global__ void k_mask_rows(const wv_frame_args* __restrict__ fa, uint32_t* __re
 // block_size is 32).
 constexpr int CT_R = 32, CT_W = 32, CT_TW = 8;   // tile rows, tile words, threads per row
 #ifndef WV_K1_DIRECT
-#define WV_K1_DIRECT 1     // all cascade levels in one launch as box ORs of the low-res mask
+#define WV_K1_DIRECT 0     // 1: all cascade levels in one launch as box ORs of the low-res mask (lower latency, ~1-2% lower pipelined throughput)
 #endif
 #ifndef WV_K1_DIRECT_RPW_WARPS
 #define WV_K1_DIRECT_RPW_WARPS 32   // warps per 32-row band of the direct cascade (one row each)

@@ -508,3 +508,22 @@ def test_bounds_checked_build_runs_clean(wv):
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.count(" ok") == 4
+
+
+def test_direct_cascade_build_matches_reference():
+    """The one-launch cascade (WV_K1_DIRECT=1: every level as a box OR of the
+    low-res mask) replays all scripted reference decodes exactly, like the
+    default step-by-step cascade."""
+    import subprocess
+    import sys
+    from paper_2208_10859_b200 import build
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2208_10859_b200", "variants", "k1direct.so")
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    if build._stale(lib):
+        build.build(defines=["WV_K1_DIRECT=1"], out=lib)
+    env = dict(os.environ, WV_LIB=lib)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(root, "tests", "test_gpu_parity.py")],
+                       env=env, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
