@@ -384,6 +384,8 @@ def run_ours(args):
     k3f = mean([e[3].elapsed_time(e[4]) for e in ks])
     k4 = mean([e[5].elapsed_time(e[6]) for e in ks]) if args.mode != "full" else 0.0
     k2_items = int(len(sess.block_work()))   # last frame's K2 work list
+    lvl_tiles = sess.tile_counts()             # last frame's synthesis tiles per level
+    records = mean([fo.result().records for fo in frames_out])
     tiles = mean([fo.result().n_tiles for fo in frames_out])
     sel_blocks = mean([fo.result().n_selected for fo in frames_out])
     C = h.channels
@@ -392,6 +394,16 @@ def run_ours(args):
     alg = tiles * (4 * 32 * 32 * 4 * C + 64 * 64 * C)
     peak, peak_kind = peaks()
     achieved = alg / (k3f * 1e-3) / 1e9
+    # whole display frame, SURVEY §8(d) byte model over the work actually done:
+    # K2 = BlockEnd spans (8 B x n) + records (2 + C B, u8) + dense f32 block
+    # write; K3 level k >= 2 = 4 subband tiles read + 64x64 f32 written per
+    # tile-channel; K3 level 1 = `alg`; K4 = C B canvas read + C B written
+    # per output pixel.  K1's bit masks (~3 MB) are left out.
+    out_px_frame = views * OUT_W * OUT_H if args.mode != "full" else 0
+    frame_bytes = (k2_items * (8 * h.inter_size + 4 * C * h.block_size ** 2)
+                   + records * (2 + C)
+                   + sum(lvl_tiles[1:]) * (4 * 32 * 32 * 4 + 64 * 64 * 4) * C
+                   + alg + 2 * C * out_px_frame)
     traffic, _ = ncu_traffic(args.mode)
 
     # end-to-end through the public API with host buffers: every step copies
@@ -484,6 +496,13 @@ def run_ours(args):
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "algorithmic_bytes_per_launch": int(alg),
                          "launch_ms": round(k3f, 4)},
+            "frame_roofline": {"bytes_per_frame": int(frame_bytes),
+                               "fps_at_peak": round(peak * 1e9 / frame_bytes, 1),
+                               "frac": round(fps * frame_bytes / (peak * 1e9), 4),
+                               "tiles_per_level": lvl_tiles,
+                               "model": "SURVEY 8(d) bytes over the work done (K2 spans+records+"
+                                        "dense blocks, K3 tiles per level, K4 canvas read + "
+                                        "output write; K1 masks excluded), whole job rate"},
             "stage_ms": {"k1_select": round(k1, 4), "k2_dequant_temporal": round(k2, 4),
                          "k3_levels_L_to_2": round(k3m, 4), "k3_level1_final": round(k3f, 4),
                          "k4_perspective": round(k4, 4)},

@@ -688,6 +688,18 @@ class DecodeSession:
         off = lst.value - base
         return self._ws[off: off + 4 * n].view(torch.int32).cpu().numpy().view(np.uint32)
 
+    def tile_counts(self) -> list:
+        """Synthesis tiles listed per level [k = 1..L] by the last decode
+        (level 1 includes the tiles only cleared because they left the
+        request), after the stream has finished."""
+        lst, cnt = C.c_void_p(), C.c_void_p()
+        N.check(self._lib.wv_block_list_view(C.byref(self._geom), C.c_void_p(self._ws.data_ptr()),
+                                             C.byref(lst), C.byref(cnt)), "wv_block_list_view")
+        self.stream.synchronize()
+        off = cnt.value - self._ws.data_ptr()   # counters[CNT_BLOCKS]; tiles at [1 + k]
+        ctr = self._ws[off: off + 4 * 64].view(torch.int32).cpu().numpy()
+        return [int(ctr[1 + k]) for k in range(1, self.header.levels + 1)]
+
     # -- prefetch (decoding.py:335-354) -------------------------------------------
 
     def advance(self, current_frame: int, next_mask: np.ndarray) -> None:
