@@ -453,6 +453,28 @@ def run_ours(args):
         e2e = {"value": round(world * args.steps / (float(te.item()) / 1000.0), 2),
                "unit": "frames/s",
                "h2d_bytes_per_step": bi // args.steps, "d2h_bytes_per_step": bo // args.steps}
+        # the link the e2e rate is bound by: plain device->pinned-host copies of
+        # the same output buffers, same streams, no decode
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        nrep = min(args.steps, 64)
+        torch.cuda.synchronize()
+        r0.record(stream)
+        for ss in sessions[1:]:
+            ss.stream.wait_event(r0)
+        for i in range(nrep):
+            p_ = i % P
+            with torch.cuda.stream(sessions[p_].stream):
+                host_outs[p_].copy_(outs[p_], non_blocking=True)
+        for ss in sessions[1:]:
+            e = torch.cuda.Event()
+            e.record(ss.stream)
+            stream.wait_event(e)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        d2h_gbs = nrep * host_outs[0].numel() / (r0.elapsed_time(r1) * 1e-3) / 1e9
+        e2e["d2h_link_gbs"] = round(d2h_gbs, 1)
+        e2e["d2h_link_frac"] = round(e2e["value"] * (bo / args.steps) / (d2h_gbs * 1e9), 4)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
