@@ -261,6 +261,10 @@ constexpr int COL_BYTES = 2 * TY * CB_PITCH * 8;
 #ifndef WV_K3_MIDPF
 #define WV_K3_MIDPF 0   // mid levels: own output tile + next-item TMA prefetch (61 KB/CTA)
 #endif
+#ifndef WV_K3_MIDREG
+#define WV_K3_MIDREG 0  // mid levels: row-pass results stored from registers (no output tile),
+                        // next item's boxes prefetched like the finest level
+#endif
 constexpr int OUTB_BYTES = TY * OB_PITCH * 8;
 constexpr int SMEM_MID = BOXSET + COL_BYTES + (WV_K3_MIDPF ? OUTB_BYTES : 0);
 constexpr int SMEM_FIN = BOXSET + COL_BYTES;   // the u8 tile goes from registers to HBM
@@ -281,7 +285,8 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   float2* colH = colL + TY * CB_PITCH;
   // mid levels: the f32 output tile aliases the boxes (or, with prefetch, has its own region)
   float2* outb = reinterpret_cast<float2*>(smem + (WV_K3_MIDPF ? BOXSET + COL_BYTES : 0));
-  constexpr bool PF = FINAL || WV_K3_MIDPF;   // next item's boxes issued after the column pass
+  constexpr bool PF = FINAL || WV_K3_MIDPF || WV_K3_MIDREG;   // next item's boxes issued after the column pass
+  constexpr bool MIDREG = !FINAL && WV_K3_MIDREG;
   __shared__ uint64_t bar;
 
   const int tid = threadIdx.x;
@@ -435,6 +440,8 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         auto cv = [](float v) { return u8_rint(__fmul_rn(v, 255.0f)); };
         uint32_t w0[SR / 2] = {}, w1[SR / 2] = {};   // rows 2i, 2i+1
         uint8_t* crow = FINAL ? canvas + ((uint64_t)c * H + 2 * ay + 2 * i) * W : nullptr;
+        float* mrow = MIDREG ? a.out + ((uint64_t)c * H + 2 * ay + 2 * i) * a.out_pitch : nullptr;
+        float2 m0 = make_float2(0.f, 0.f), m1 = m0;   // MIDREG: the row pair's previous pair
         // mid levels: f32 pairs into outb
         auto emit_mid = [&](int q, float2 s3, float2 d3) {
           WV_ASSERT(q >= 0 && q < TX && i < TY);
@@ -450,7 +457,19 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
                 d = colH[i * CB_PITCH + cb + j];
               },
               [&](int p, float2 s3, float2 d3) {
-                if (!FINAL) {
+                if (MIDREG) {
+                  // pairs 2m, 2m+1 of each row -> one float4 store
+                  const int lq = p - HALO;
+                  if ((lq & 1) == 0) {
+                    m0 = make_float2(s3.x, d3.x);
+                    m1 = make_float2(s3.y, d3.y);
+                  } else {
+                    float* r0 = mrow + 2 * (pa + lq - 1);
+                    *reinterpret_cast<float4*>(r0) = make_float4(m0.x, m0.y, s3.x, d3.x);
+                    *reinterpret_cast<float4*>(r0 + a.out_pitch) =
+                        make_float4(m1.x, m1.y, s3.y, d3.y);
+                  }
+                } else if (!FINAL) {
                   emit_mid(qb + p, s3, d3);
                 } else {
                   // p - HALO is the segment-local pair: compile-time after unrolling
@@ -495,7 +514,11 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
                 d = colH[i * CB_PITCH + (j - ox)];
               },
               [&](int p, float2 s3, float2 d3) {
-                if (!FINAL) {
+                if (MIDREG) {
+                  float* r0 = mrow + 2 * p;
+                  *reinterpret_cast<float2*>(r0) = make_float2(s3.x, d3.x);
+                  *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(s3.y, d3.y);
+                } else if (!FINAL) {
                   emit_mid(p - ax, s3, d3);
                 } else {
                   // level borders: two pixels per row straight to the canvas
@@ -515,7 +538,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       }
     }
     __syncthreads();   // mid: outb complete; final: colL / colH free for the next item
-    if (!FINAL) {
+    if (!FINAL && !MIDREG) {
       float* base = a.out + ((uint64_t)c * H + 2 * ay) * a.out_pitch + 2 * ax;
       if (nx == OUT_W && ny == OUT_H) {
         // full tile: 32 row pairs x 32 float2 columns, shifts only
