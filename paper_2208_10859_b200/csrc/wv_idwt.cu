@@ -265,6 +265,22 @@ constexpr int COL_BYTES = 2 * TY * CB_PITCH * 8;
 #define WV_K3_MIDREG 0  // mid levels: row-pass results stored from registers (no output tile),
                         // next item's boxes prefetched like the finest level
 #endif
+#ifndef WV_K3_PAIRSEG
+#define WV_K3_PAIRSEG 1  // finest row pass: a warp = 16 row pairs x 2 adjacent segments, so
+                         // each 16-B store pair fills whole 32-B sectors
+#endif
+// row-pass thread -> (row pair i, segment sg)
+template <bool FINAL>
+__device__ __forceinline__ void row_map(int tid, int& i, int& sg) {
+  if (FINAL && WV_K3_PAIRSEG && TY == 32) {
+    const int w = tid >> 5, l = tid & 31;
+    i = 16 * (w & 1) + (l & 15);
+    sg = 2 * (w >> 1) + (l >> 4);
+  } else {
+    i = tid % TY;
+    sg = tid / TY;
+  }
+}
 constexpr int OUTB_BYTES = TY * OB_PITCH * 8;
 constexpr int SMEM_MID = BOXSET + COL_BYTES + (WV_K3_MIDPF ? OUTB_BYTES : 0);
 constexpr int SMEM_FIN = BOXSET + COL_BYTES;   // the u8 tile goes from registers to HBM
@@ -344,7 +360,9 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     uint32_t nxt_entry = ZERO_FLAG;
     const uint32_t nxt = item + gridDim.x;
     if (FINAL) {
-      const int i = tid % TY, pa = ax + (tid / TY) * SR;
+      int i, sg;
+      row_map<FINAL>(tid, i, sg);
+      const int pa = ax + sg * SR;
       if (tid < (TX / SR) * TY && i < by - ay && pa < bx) {
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
@@ -430,7 +448,8 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     }
     // row pass: (segment, output row pair) per thread, two rows packed
     if (tid < (TX / SR) * TY) {
-      const int i = tid % TY, sg = tid / TY;
+      int i, sg;
+      row_map<FINAL>(tid, i, sg);
       const int pa = ax + sg * SR, pb = min(pa + SR, bx);
       if (i < by - ay && pa < pb) {
         // finest level: clip(rint(x*255)) (decoding.py:301; rint is
