@@ -281,7 +281,13 @@ __device__ __forceinline__ void row_map(int tid, int& i, int& sg) {
     sg = tid / TY;
   }
 }
-constexpr int OUTB_BYTES = TY * OB_PITCH * 8;
+#ifndef WV_K3_OUT4
+#define WV_K3_OUT4 1   // mid-level output tile as float4 (s3.x, d3.x, s3.y, d3.y) per pair:
+                       // one conflict-free 16-B shared store / load instead of two 8-B ones
+#endif
+constexpr int OB4_PITCH = TX + 1;     // float4 units, odd
+static_assert(TY * OB4_PITCH * 16 <= 4 * BOX_SLOT, "float4 output tile must fit in the box region");
+constexpr int OUTB_BYTES = WV_K3_OUT4 ? TY * OB4_PITCH * 16 : TY * OB_PITCH * 8;
 constexpr int SMEM_MID = BOXSET + COL_BYTES + (WV_K3_MIDPF ? OUTB_BYTES : 0);
 constexpr int SMEM_FIN = BOXSET + COL_BYTES;   // the u8 tile goes from registers to HBM
 
@@ -464,8 +470,12 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         // mid levels: f32 pairs into outb
         auto emit_mid = [&](int q, float2 s3, float2 d3) {
           WV_ASSERT(q >= 0 && q < TX && i < TY);
-          outb[i * OB_PITCH + 2 * q] = s3;
-          outb[i * OB_PITCH + 2 * q + 1] = d3;
+          if (WV_K3_OUT4) {
+            reinterpret_cast<float4*>(outb)[i * OB4_PITCH + q] = make_float4(s3.x, d3.x, s3.y, d3.y);
+          } else {
+            outb[i * OB_PITCH + 2 * q] = s3;
+            outb[i * OB_PITCH + 2 * q + 1] = d3;
+          }
         };
         if (pa >= HALO && pb + HALO <= a.bw && pb - pa == SR) {
           const int cb = pa - HALO - ox, qb = pa - HALO - ax;
@@ -563,21 +573,33 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         // full tile: 32 row pairs x 32 float2 columns, shifts only
         for (int idx = tid; idx < TY * TX; idx += NTHREADS) {
           const int i = idx / TX, x2 = idx % TX;
-          const float2 u = outb[i * OB_PITCH + 2 * x2];
-          const float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
           float* r0 = base + (uint64_t)(2 * i) * a.out_pitch + 2 * x2;
-          *reinterpret_cast<float2*>(r0) = make_float2(u.x, v.x);
-          *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
+          if (WV_K3_OUT4) {
+            const float4 t = reinterpret_cast<const float4*>(outb)[i * OB4_PITCH + x2];
+            *reinterpret_cast<float2*>(r0) = make_float2(t.x, t.y);
+            *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(t.z, t.w);
+          } else {
+            const float2 u = outb[i * OB_PITCH + 2 * x2];
+            const float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
+            *reinterpret_cast<float2*>(r0) = make_float2(u.x, v.x);
+            *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
+          }
         }
       } else {
         const int half = nx >> 1;   // float2 columns per row
         for (int idx = tid; idx < (ny >> 1) * half; idx += NTHREADS) {
           const int i = idx / half, x2 = idx % half;
-          const float2 u = outb[i * OB_PITCH + 2 * x2];
-          const float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
           float* r0 = base + (uint64_t)(2 * i) * a.out_pitch + 2 * x2;
-          *reinterpret_cast<float2*>(r0) = make_float2(u.x, v.x);
-          *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
+          if (WV_K3_OUT4) {
+            const float4 t = reinterpret_cast<const float4*>(outb)[i * OB4_PITCH + x2];
+            *reinterpret_cast<float2*>(r0) = make_float2(t.x, t.y);
+            *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(t.z, t.w);
+          } else {
+            const float2 u = outb[i * OB_PITCH + 2 * x2];
+            const float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
+            *reinterpret_cast<float2*>(r0) = make_float2(u.x, v.x);
+            *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
+          }
         }
       }
       __syncthreads();
