@@ -2,16 +2,22 @@
 """Headline benchmark: 8192x8192 stereo 360-degree viewport decode on B200.
 
 Workload (BASELINE.json configs[2]): a synthetic
-8192x8192x3 top-bottom stereo clip (make_synthetic_clip restated for HxW),
-encoded with the reference encoder's algorithm (package torch encoder,
-alpha 0.1, beta 0.005, n 4, 32-px blocks, 6 levels, 256x256 mask grid,
-120 fps header).  One step = one display frame: stereo viewport mask of the
-circle-trajectory pose (90x90 FOV) -> K1 select -> K2 dequant+temporal ->
-K3 6-level synthesis into the u8 canvas -> K4 per-eye perspective
-writeout to 2000x2000.  Inputs are resident in HBM; L2 is flushed (256 MiB
-write) before every timed step.
+8192x8192x3 top-bottom stereo clip of 4 inter-frame sets / 16 frames
+(make_synthetic_clip restated for HxW, encoded with the reference
+encoder's algorithm: alpha 0.1, beta 0.005, n 4, 32-px blocks, 6 levels,
+256x256 mask grid, 120 fps header; committed as
+tests/golden/bench_c3_8k.wvv.xz, set 0 pinned against the reference
+encoder and 9 decodes pinned against the reference decoder in
+tests/golden/bench_8k.json).  One step = one display frame: step i shows
+frame i mod 16 under the head pose of the circle trajectory at time
+i / 120 s (a new pose every step) -> stereo viewport mask (90x90 FOV) ->
+K1 select -> K2 dequant+temporal -> K3 6-level synthesis into the u8
+canvas -> K4 per-eye perspective writeout to 2000x2000.  Inputs are
+resident in HBM for ``value``; ``e2e`` adds the host->device set payload
+and the device->host result every step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--config c3|c2] [--mode viewport|foveated|full]
 
 N>1 runs under torchrun: sets are sharded round-robin over ranks (weak
 scaling), and every step gathers each rank's two eye images to rank 0 over
@@ -42,11 +48,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--size", type=int, default=8192, help="frame width = height")
-    ap.add_argument("--sets", type=int, default=0,
-                    help="inter-frame sets (default: max(2, N); --mode full: 4 per GPU, config 5's "
-                         "long clip)")
-    ap.add_argument("--mode", choices=["viewport", "foveated", "full"], default="viewport")
+    ap.add_argument("--config", choices=["c3", "c2"], default="c3",
+                    help="c3: 8192x8192 stereo (configs 3-5); c2: 4096x2048 mono (config 2)")
+    ap.add_argument("--mode", choices=["viewport", "foveated", "full"], default=None,
+                    help="default: viewport for c3, full for c2")
+    ap.add_argument("--clip", default=None, help="decode this .wvv instead of the config's clip")
     ap.add_argument("--cache-dir", default="/tmp/wvb200_bench")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -63,60 +69,42 @@ def parse():
 
 # ------------------------------------------------------------------ inputs
 
-def default_sets(args, world: int) -> int:
-    """Sets in the input clip: config 5 (full-frame decode of a long clip
-    sharded by group of frames) cycles 4 distinct sets per GPU; the viewport
-    configs use max(2, N)."""
-    if args.sets:
-        return args.sets
-    return max(4, 4 * world) if args.mode == "full" else max(2, world)
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+import make_bench_input as mbi  # noqa: E402  (stdlib-only at import)
 
 
-def input_path(args, n_sets: int) -> str:
-    return os.path.join(args.cache_dir, f"c3_{args.size}_s{n_sets}_v1.wvv")
+def clip_for(args) -> str:
+    """The committed benchmark clip (decompressed once into the cache dir),
+    or --clip."""
+    return args.clip or mbi.ensure_clip(args.config, args.cache_dir)
 
 
-def make_input(path: str, size: int, n_sets: int, device) -> None:
-    """Encode the synthetic stereo clip once (not timed)."""
-    import torch
-    from paper_2208_10859_b200.encoding import EncodeParams, MappingKind, encode_video
-    from paper_2208_10859_b200.fileio import write_video
-    from paper_2208_10859_b200.synthetic import make_synthetic_clip_torch
-    os.makedirs(os.path.dirname(path), exist_ok=True)
-    frames = 4 * n_sets
-    params = EncodeParams(alpha=0.1, inter_threshold=0.005, inter_size=4, block_size=32,
-                          mapping=MappingKind.EQUIRECTANGULAR, stereo=True, fps=FPS,
-                          mask_w=256, mask_h=256)
-    sets = []
-    video = None
-    for si in range(n_sets):
-        clip = make_synthetic_clip_torch(4, size, size, 3, seed=7, device=device,
-                                         first_frame=4 * si, total_frames=frames)
-        v = encode_video(clip, params, device=device, keep_arrays=False)
-        sets.extend(v.sets)
-        video = v
-        del clip
-        if torch.cuda.is_available():
-            torch.cuda.empty_cache()
-    video.sets = sets
-    video.frame_count = frames
-    video.pad_frames = 0
-    tmp = path + f".tmp{os.getpid()}"
-    write_video(video, tmp)
-    os.replace(tmp, path)
+class Schedule:
+    """Display step -> (frame, pose, mask, gaze): frames cycle through
+    ``frames`` while the head walks the circle trajectory at 120 Hz
+    (scripts/make_bench_input.display_step), so consecutive steps -- and
+    the sessions they land on -- never repeat an input.  ``api`` supplies
+    CameraPose / stereo_mask / viewport_to_mask (ours, or the reference's
+    in the reference arm)."""
 
+    def __init__(self, header, frames, CameraPose, stereo_mask, viewport_to_mask, traj):
+        self.h, self.frames, self.traj = header, list(frames), traj
+        self.CameraPose, self.stereo_mask, self.viewport_to_mask = (CameraPose, stereo_mask,
+                                                                    viewport_to_mask)
+        self._masks = {}
 
-def poses_and_masks(header, frames):
-    from paper_2208_10859_b200.projection import CameraPose, stereo_mask
-    from paper_2208_10859_b200.synthetic import circle_trajectory
-    traj = circle_trajectory()
-    out = {}
-    for f in frames:
-        _, yaw, pitch, roll, gu, gv = traj.sample_at(f * 1000.0 / header.fps)
-        pose = CameraPose(yaw=float(yaw), pitch=float(pitch), roll=float(roll), fov_h=90, fov_v=90)
-        mask = (stereo_mask(pose, (header.mask_w, header.mask_h)) if header.stereo else None)
-        out[f] = (pose, mask, (float(gu), float(gv)))
-    return out
+    def __call__(self, step: int):
+        h = self.h
+        _, yaw, pitch, roll, gu, gv = mbi.display_step(step, 1, h.fps or FPS, self.traj)
+        frame = self.frames[step % len(self.frames)]
+        pose = self.CameraPose(yaw=yaw, pitch=pitch, roll=roll, fov_h=90, fov_v=90)
+        key = (yaw, pitch, roll)
+        mask = self._masks.get(key)
+        if mask is None:
+            dims = (h.mask_w, h.mask_h)
+            mask = self.stereo_mask(pose, dims) if h.stereo else self.viewport_to_mask(pose, dims)
+            self._masks[key] = mask
+        return frame, pose, mask, (gu, gv)
 
 
 # ------------------------------------------------------------------ clocks
@@ -220,7 +208,9 @@ def run_ours(args):
     import paper_2208_10859_b200 as wv
     from paper_2208_10859_b200 import build
     from paper_2208_10859_b200.decoding import FoveationSchedule
+    from paper_2208_10859_b200.projection import CameraPose, stereo_mask, viewport_to_mask
     from paper_2208_10859_b200.sharding import frames_for_sets, gather_views, sets_for_rank
+    from paper_2208_10859_b200.replay import circle_trajectory
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -231,17 +221,15 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if rank == 0:
         build.build()
+        path = clip_for(args)
     if world > 1:
         dist.barrier()
-    n_sets = default_sets(args, world)
-    path = input_path(args, n_sets)
-    if rank == 0 and not os.path.exists(path):
-        make_input(path, args.size, n_sets, dev)
-    if world > 1:
-        dist.barrier()
+    if rank != 0:
+        path = clip_for(args)
+    mode = args.mode
 
     P = max(1, args.pipeline)
-    sessions = [wv.DecodeSession(path, device=dev, max_resident_sets=n_sets + 1,
+    sessions = [wv.DecodeSession(path, device=dev, max_resident_sets=8,
                                  residency=args.residency) for _ in range(P)]
     for s_ in sessions:
         s_.time_stages = False
@@ -249,50 +237,56 @@ def run_ours(args):
     h = sess.header
     my_sets = sets_for_rank(h.num_sets, rank, world)
     frames = frames_for_sets(my_sets, h.inter_size, h.frame_count)
-    pm = poses_and_masks(h, frames)
+    sched = Schedule(h, frames, CameraPose, stereo_mask, viewport_to_mask,
+                     circle_trajectory(mbi.TRAJ_MS, mbi.TRAJ_STEPS))
+    # every step's inputs are prepared before timing (host pose -> mask work
+    # is the caller's, as in bench.replay)
+    plan = []
+    for i in range(args.warmup + args.steps):
+        f, pose, mask, gaze = sched(i)
+        sc = FoveationSchedule.default(h.levels, *gaze) if mode == "foveated" else None
+        plan.append((f, pose, mask, sc))
     views = 2 if h.stereo else 1
     outs = [torch.empty((views, OUT_H, OUT_W, h.channels), dtype=torch.uint8, device=dev)
             for _ in range(P)]
     out = outs[0]
-    gather_buf = ([torch.empty_like(out) for _ in range(world)] if (world > 1 and rank == 0)
-                  else None)
+    # the step's result: the eye images, or the whole decoded canvas in full mode
+    results = [s_._canvas if mode == "full" else o for s_, o in zip(sessions, outs)]
+    gather_buf = ([torch.empty_like(results[0]) for _ in range(world)]
+                  if (world > 1 and rank == 0) else None)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = sess.stream
 
-    def step(i, ss=None, ob=None):
-        ss = ss or sess
-        ob = out if ob is None else ob
-        f = frames[i % len(frames)]
-        pose, mask, gaze = pm[f]
-        if args.mode == "full":
+    def step(i, p_=0):
+        ss = sessions[p_]
+        f, pose, mask, sc = plan[i]
+        if mode == "full":
             ss.decode_full_device(f)
         else:
-            sc = FoveationSchedule.default(h.levels, *gaze) if args.mode == "foveated" else None
-            ss.decode_render_device(f, args.mode, mask, pose, (OUT_W, OUT_H), ob, schedule=sc)
+            ss.decode_render_device(f, mode, mask, pose, (OUT_W, OUT_H), outs[p_], schedule=sc)
 
-    def gather(ss=None, ob=None):
+    def gather(p_=0):
         if world > 1:
-            with torch.cuda.stream((ss or sess).stream):
-                gather_views(out if ob is None else ob, rank, world, 0, gather_buf)
+            with torch.cuda.stream(sessions[p_].stream):
+                gather_views(results[p_], rank, world, 0, gather_buf)
 
     # make every set resident and warm up
     for ss in sessions:
         for s in my_sets:
             ss._make_resident(s)
     for i in range(args.warmup):
-        for p_, ss in enumerate(sessions):
-            step(i, ss, outs[p_])
-            gather(ss, outs[p_])
+        for p_ in range(P):
+            step(i, p_)
+            gather(p_)
     torch.cuda.synchronize()
     for ss in sessions:
         ss._settle_until(None)
     if args.profile_only:
         return
 
-    # headline: P sessions (streams), frames round-robin, whole-job time from
+    # headline: P sessions (streams), steps round-robin, whole-job time from
     # one start event to the join of all streams (per-frame working set
     # ~300 MB of plane/level/canvas traffic > 126 MB L2; no flush needed)
-    t_host = time.perf_counter()
     start_ev = torch.cuda.Event(enable_timing=True)
     end_ev = torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -305,8 +299,8 @@ def run_ours(args):
         t_host = time.perf_counter()
         for i in range(args.steps):
             p_ = i % P
-            step(args.warmup + i, sessions[p_], outs[p_])
-            gather(sessions[p_], outs[p_])
+            step(args.warmup + i, p_)
+            gather(p_)
         t_host = (time.perf_counter() - t_host) * 1000.0 / args.steps
         for ss in sessions[1:]:
             e = torch.cuda.Event()
@@ -348,31 +342,30 @@ def run_ours(args):
     # a GPU-side sleep before each timed stage keeps the stream busy while the
     # host enqueues the stage, so the event intervals hold kernel time only
     busy = int(4e5)   # clock cycles (~0.2 ms)
-    if args.mode != "full":
+    if mode != "full":
         # first use of the by-value K4 launch path loads its kernel (lazy module
         # loading): keep that out of the timed frames
-        sess.render_views(pm[frames[0]][0], (OUT_W, OUT_H), out=out, check=False,
-                          all_covered=args.mode == "foveated")
+        sess.render_views(plan[0][1], (OUT_W, OUT_H), out=out, check=False,
+                          all_covered=mode == "foveated")
         torch.cuda.synchronize()
     for i in range(R):
         with torch.cuda.stream(stream):
             flush.zero_()
             torch.cuda._sleep(busy)
-        f = frames[i % len(frames)]
-        pose, mask, gaze = pm[f]
-        if args.mode == "full":
+        f, pose, mask, sc = plan[i % len(plan)]
+        if mode == "full":
             frames_out.append(sess.decode_full_device(f))
-        elif args.mode == "foveated":
-            frames_out.append(sess.decode_foveated_device(f, mask, FoveationSchedule.default(h.levels, *gaze)))
+        elif mode == "foveated":
+            frames_out.append(sess.decode_foveated_device(f, mask, sc))
         else:
             frames_out.append(sess.decode_viewport_device(f, mask))
-        if args.mode != "full":
+        if mode != "full":
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(stream):
                 torch.cuda._sleep(busy)
             sess.render_views(pose, (OUT_W, OUT_H), out=out, check=False,
-                              all_covered=args.mode == "foveated", events=(e0, e1))
+                              all_covered=mode == "foveated", events=(e0, e1))
             sess.kernel_events[-1].extend([e0, e1])
     torch.cuda.synchronize()
     sess.kernel_timing = False
@@ -382,7 +375,7 @@ def run_ours(args):
     k2 = mean([e[1].elapsed_time(e[2]) for e in ks])
     k3m = mean([e[2].elapsed_time(e[3]) for e in ks])
     k3f = mean([e[3].elapsed_time(e[4]) for e in ks])
-    k4 = mean([e[5].elapsed_time(e[6]) for e in ks]) if args.mode != "full" else 0.0
+    k4 = mean([e[5].elapsed_time(e[6]) for e in ks]) if mode != "full" else 0.0
     k2_items = int(len(sess.block_work()))   # last frame's K2 work list
     lvl_tiles = sess.tile_counts()             # last frame's synthesis tiles per level
     records = mean([fo.result().records for fo in frames_out])
@@ -399,20 +392,22 @@ def run_ours(args):
     # write; K3 level k >= 2 = 4 subband tiles read + 64x64 f32 written per
     # tile-channel; K3 level 1 = `alg`; K4 = C B canvas read + C B written
     # per output pixel.  K1's bit masks (~3 MB) are left out.
-    out_px_frame = views * OUT_W * OUT_H if args.mode != "full" else 0
+    out_px_frame = views * OUT_W * OUT_H if mode != "full" else 0
     frame_bytes = (k2_items * (8 * h.inter_size + 4 * C * h.block_size ** 2)
                    + records * (2 + C)
                    + sum(lvl_tiles[1:]) * (4 * 32 * 32 * 4 + 64 * 64 * 4) * C
                    + alg + 2 * C * out_px_frame)
-    traffic, _ = ncu_traffic(args.mode)
+    traffic, _ = ncu_traffic(mode)
 
     # end-to-end through the public API with host buffers: every step copies
-    # its set payload + mask from pinned host memory and reads the two eye
-    # images back into pinned host memory (same pipelining as the headline)
+    # its set payload + mask from pinned host memory and reads the step's
+    # result (the two eye images; in full mode the decoded u8 canvas, as
+    # decode_full returns it, decoding.py:328-331) back into pinned host
+    # memory, with the same pipelining as the headline
     e2e = None
     if not args.no_e2e:
         pinned = {s: sess.pinned_payload(s) for s in my_sets}
-        host_outs = [torch.empty(out.shape, dtype=torch.uint8).pin_memory() for _ in range(P)]
+        host_outs = [torch.empty(r.shape, dtype=torch.uint8).pin_memory() for r in results]
         bi = bo = 0
         if world > 1:
             dist.barrier()
@@ -426,17 +421,16 @@ def run_ours(args):
         for i in range(args.steps):
             p_ = i % P
             ss = sessions[p_]
-            f = frames[i % len(frames)]
-            s = f // h.inter_size
+            s = plan[args.warmup + i][0] // h.inter_size
             # whole payload ("set") or BlockEnd table + spans fetched by the
             # decode ("spans", counted after the run)
             ss.upload_set(s, pinned[s])
-            step(i, ss, outs[p_])
-            gather(ss, outs[p_])
+            step(args.warmup + i, p_)
+            gather(p_)
             with torch.cuda.stream(ss.stream):
-                host_outs[p_].copy_(outs[p_], non_blocking=True)
+                host_outs[p_].copy_(results[p_], non_blocking=True)
             bi += (pinned[s].numel() if args.residency == "set" else h.table_bytes)
-            bi += h.mask_w * h.mask_h
+            bi += h.mask_w * h.mask_h if mode != "full" else 0
             bo += host_outs[p_].numel()
         for ss in sessions[1:]:
             e = torch.cuda.Event()
@@ -452,12 +446,14 @@ def run_ours(args):
         bi += sum(ss.bytes_fetched for ss in sessions) - fetched0
         e2e = {"value": round(world * args.steps / (float(te.item()) / 1000.0), 2),
                "unit": "frames/s",
-               "h2d_bytes_per_step": bi // args.steps, "d2h_bytes_per_step": bo // args.steps}
+               "h2d_bytes_per_step": bi // args.steps, "d2h_bytes_per_step": bo // args.steps,
+               "result": "decoded u8 canvas (C, H, W)" if mode == "full"
+                         else "per-eye perspective images"}
         # the link the e2e rate is bound by: plain device->pinned-host copies of
-        # the same output buffers, same streams, no decode
+        # the same result buffers, same streams, no decode
         r0 = torch.cuda.Event(enable_timing=True)
         r1 = torch.cuda.Event(enable_timing=True)
-        nrep = min(args.steps, 64)
+        nrep = min(args.steps, 64 if mode != "full" else 16)
         torch.cuda.synchronize()
         r0.record(stream)
         for ss in sessions[1:]:
@@ -465,7 +461,7 @@ def run_ours(args):
         for i in range(nrep):
             p_ = i % P
             with torch.cuda.stream(sessions[p_].stream):
-                host_outs[p_].copy_(outs[p_], non_blocking=True)
+                host_outs[p_].copy_(results[p_], non_blocking=True)
         for ss in sessions[1:]:
             e = torch.cuda.Event()
             e.record(ss.stream)
@@ -478,13 +474,21 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(path, frames[0], pm[frames[0]], args.mode)
+        cpu = cpu_baseline_sample(path, [plan[args.warmup + i] for i in range(3)], mode)
 
     if rank == 0:
         fps = world * args.steps / (max_ms / 1000.0)
-        out_px = views * OUT_W * OUT_H if args.mode != "full" else h.width * h.height
+        out_px = views * OUT_W * OUT_H if mode != "full" else h.width * h.height
+        stereo = "stereo" if h.stereo else "mono"
+        workload = (f"{args.config.upper()} {h.width}x{h.height} {stereo} 360 {mode} decode + "
+                    f"per-eye {OUT_W}x{OUT_H} perspective writeout, 90x90 FOV, circle trajectory"
+                    if mode != "full" else
+                    f"{args.config.upper()} {h.width}x{h.height} {stereo} full-frame decode"
+                    + (" (config 5 per GPU)" if args.config == "c3" else ""))
+        metric = (METRIC if (args.config, mode) == ("c3", "viewport")
+                  else f"decoded frames/s (Mpixel/s) for {workload}")
         line = {
-            "metric": METRIC,
+            "metric": metric,
             "value": round(fps, 2),
             "unit": "frames/s",
             "n_gpus": world,
@@ -495,22 +499,26 @@ def run_ours(args):
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f32",
-            "data": "synthetic (make_synthetic_clip HxW, encoded by the package encoder = reference algorithm)",
+            "data": ("synthetic: make_synthetic_clip restated for HxW, encoded with the reference "
+                     "encoder's algorithm (committed clip; set 0 byte-identical to the reference "
+                     "encoder, decodes pinned to the reference, tests/golden/bench_8k.json)"),
             "serial_ms_per_frame": round(serial_ms, 4),
             "host_ms_per_step": round(t_host, 4),
             "config": {
-                "workload": (f"C3 {h.width}x{h.height} stereo 360 {args.mode} decode + per-eye "
-                             f"{OUT_W}x{OUT_H} perspective writeout, 90x90 FOV, circle trajectory"
-                             if args.mode != "full" else f"{h.width}x{h.height} full-frame decode"),
+                "workload": workload,
                 "levels": h.levels, "inter_size": h.inter_size, "block_size": h.block_size,
                 "mask": f"{h.mask_w}x{h.mask_h}", "alpha": 0.1, "inter_threshold": 0.005,
                 "sets": h.num_sets, "frames": h.frame_count, "sets_per_rank": len(my_sets),
+                "schedule": ("step i: frame i mod frames, head pose of circle_trajectory(2000 ms, "
+                             "240 samples) at i/120 s"),
                 "l2": ("headline: per-frame working set (~300 MB plane/level/canvas traffic) "
                        "exceeds the 126 MB L2; serial_ms_per_frame: L2 flushed (256 MiB write) "
                        "before every step"),
-                "pipeline": f"{P} decode sessions (CUDA streams) per GPU, frames round-robin",
+                "pipeline": f"{P} decode sessions (CUDA streams) per GPU, steps round-robin",
                 "residency": args.residency,
-                "parallelism": f"sets round-robin over {world} GPU(s), eye images gathered to rank 0",
+                "parallelism": (f"sets round-robin over {world} GPU(s), "
+                                + ("decoded canvas" if mode == "full" else "eye images")
+                                + " gathered to rank 0"),
             },
             "mpix_per_s": round(fps * out_px / 1e6, 1),
             "roofline": {"bound": "hbm", "kernel": "k_level<FINAL> (K3 finest level + u8 writeout)",
@@ -533,9 +541,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
-            # per frame: K1 2L+4 (mask rows, L cascades, L footprint, blocks,
-            # tiles, finalize) + K2 1 + K3 L + K4 1 (not in full mode)
-            "gpu_launches": args.steps * launches_per_frame(h.levels, args.mode, args.residency),
+            "gpu_launches": args.steps * launches_per_frame(h.levels, mode, args.residency),
         }
         print(json.dumps(line), flush=True)
     for ss in sessions:
@@ -544,22 +550,34 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-# --------------------------------------------------------- CPU (oracle) legs
+# ----------------------------------------------- CPU legs (no CUDA, no .so)
 
-def _oracle_frame(path, frame, pose_t, mask, mode):
+_W = {}
+
+
+def _oracle_init(path):
+    from oracle import wavevid_oracle as wo
+    _W["wo"] = wo
+    _W["path"] = path
+
+
+def _oracle_frame(job):
     """One display frame through the CPU oracle (decode + per-eye render)."""
     import numpy as np
-    from oracle import wavevid_oracle as wo
-    sess = wo.OracleSession(path)
+    wo = _W["wo"]
+    frame, ypr, mask, fractions, gaze, mode = job
+    sess = wo.OracleSession(_W["path"])
     h = sess.header
     t0 = time.perf_counter()
-    kind = {"viewport": "viewport", "foveated": "foveated", "full": "full"}[mode]
-    pix, fp, _ = sess.decode(frame, kind, None if mode == "full" else mask)
+    if mode == "full":
+        pix, fp, _ = sess.decode(frame, "full")
+    elif mode == "foveated":
+        pix, fp, _ = sess.decode(frame, "foveated", mask, fractions, gaze)
+        fp = np.ones_like(fp)   # the reference's foveated callers (cli.py:177)
+    else:
+        pix, fp, _ = sess.decode(frame, "viewport", mask)
     if mode != "full":
-        if mode == "foveated":   # the reference's foveated callers check coverage
-            fp = np.ones_like(fp)   # against an all-ones footprint (cli.py:177)
-        yaw, pitch, roll = pose_t
-        rot = wo.pose_rotation(yaw, pitch, roll)
+        rot = wo.pose_rotation(*ypr)
         half = h.height // 2 if h.stereo else h.height
         for e in range(2 if h.stereo else 1):
             wo.perspective(pix[e * half:(e + 1) * half], fp[e * half:(e + 1) * half], rot,
@@ -567,90 +585,170 @@ def _oracle_frame(path, frame, pose_t, mask, mode):
     return time.perf_counter() - t0
 
 
-def cpu_baseline_sample(path, frame, pm_entry, mode):
-    pose, mask, _ = pm_entry
-    el = _oracle_frame(path, frame, (pose.yaw, pose.pitch, pose.roll), mask, mode)
-    return {"value": round(1.0 / el, 4), "unit": "frames/s", "cores": 1, "kind": "port",
-            "sample": (f"1 display frame ({mode} decode of frame {frame} + "
-                       f"{'2 eye' if mode != 'full' else 'no'} {OUT_W}x{OUT_H} renders), "
-                       f"numpy oracle, single process, {el:.1f} s")}
+def cpu_baseline_sample(path, plan_rows, mode):
+    """The oracle port on the host cores: one worker process per sample,
+    each warmed by one frame, then the samples timed in parallel."""
+    import multiprocessing as mp
+    jobs = []
+    for f, pose, mask, sc in plan_rows:
+        jobs.append((f, (pose.yaw, pose.pitch, pose.roll), mask,
+                     sc.fractions if sc is not None else None,
+                     (sc.gaze_u, sc.gaze_v) if sc is not None else None, mode))
+    n = len(jobs)
+    with mp.get_context("spawn").Pool(n, initializer=_oracle_init, initargs=(path,)) as pool:
+        pool.map(_oracle_frame, jobs, chunksize=1)
+        t0 = time.perf_counter()
+        per = pool.map(_oracle_frame, jobs, chunksize=1)
+        wall = time.perf_counter() - t0
+    return {"value": round(n / wall, 4), "unit": "frames/s", "cores": n, "kind": "port",
+            "sample": (f"{n} display frames ({mode} decode"
+                       + ("" if mode == "full" else f" + per-eye {OUT_W}x{OUT_H} renders")
+                       + f") of the timed schedule, numpy oracle, {n} processes in parallel "
+                         f"after one warm-up frame each; per-frame s "
+                       + ", ".join(f"{x:.1f}" for x in per))}
 
 
-def _init_worker():
-    import numpy  # noqa: F401
-    from oracle import wavevid_oracle  # noqa: F401
+def _ref_path():
+    return os.path.join(ROOT, "baseline", "_ref")
 
 
-def _worker(a):
-    path, frame, pose_t, mask, mode = a
-    return _oracle_frame(path, frame, pose_t, mask, mode)
+def _ref_init(path):
+    sys.path.insert(0, _ref_path())
+    import wavevid
+    _W["wv"] = wavevid
+    _W["sess"] = wavevid.DecodeSession(path)
+
+
+def _ref_frame(job):
+    """One display frame through the UNMODIFIED reference package
+    (baseline/_ref): DecodeSession.decode_* then render_perspective per eye,
+    timed with perf_counter as bench.replay does (bench.py:178-185)."""
+    import numpy as np
+    wv = _W["wv"]
+    sess = _W["sess"]
+    frame, ypr, mask, fractions, gaze, mode = job
+    h = sess.header
+    pose = wv.CameraPose(yaw=ypr[0], pitch=ypr[1], roll=ypr[2], fov_h=90, fov_v=90)
+    t0 = time.perf_counter()
+    if mode == "full":
+        pix, fp, _ = sess.decode_full(frame)
+    elif mode == "foveated":
+        pix, fp, _ = sess.decode_foveated(frame, mask,
+                                          wv.FoveationSchedule(tuple(fractions), *gaze))
+        fp = np.ones_like(fp)   # cli.py:177, service.py:135
+    else:
+        pix, fp, _ = sess.decode_viewport(frame, mask)
+    uncovered = 0
+    if mode != "full":
+        half = h.height // 2 if h.stereo else h.height
+        for e in range(2 if h.stereo else 1):
+            sl = slice(e * half, (e + 1) * half)
+            try:
+                wv.render_perspective(pix[sl], fp[sl], pose, (OUT_W, OUT_H))
+            except wv.CoverageError:   # cli.py:242-245 reports it; count it here
+                uncovered += 1
+    return time.perf_counter() - t0, _native_of_ours(), uncovered
+
+
+def _native_of_ours():
+    """Shared objects of this repo's package mapped into this process."""
+    try:
+        with open("/proc/self/maps") as fh:
+            return sorted({l.split()[-1] for l in fh
+                           if "paper_2208_10859_b200" in l and ".so" in l})
+    except OSError:
+        return []
 
 
 def run_reference(args):
-    """--impl reference: the reference CPU algorithm (oracle port; the
-    reference package is Python and cannot be compiled) on the host cores,
-    frames decoded in parallel worker processes."""
+    """--impl reference: the reference package itself (baseline/_ref, pure
+    Python/numpy, unmodified) on the host cores, one DecodeSession per
+    worker process, display frames of the same schedule in parallel.  No
+    torch, no CUDA and nothing of paper_2208_10859_b200 is imported."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     import multiprocessing as mp
-    import numpy as np
-    n_sets = default_sets(args, world)
-    path = input_path(args, n_sets)
-    if not os.path.exists(path):
-        import torch
-        make_input(path, args.size, n_sets,
-                   torch.device("cuda", 0) if torch.cuda.is_available() else "cpu")
-    from paper_2208_10859_b200.fileio import read_header
-    h, _ = read_header(path)
-    frames = list(range(h.frame_count))
-    pm = poses_and_masks(h, frames)
+    path = clip_for(args)
+    mode = args.mode
+    if not os.path.isdir(os.path.join(_ref_path(), "wavevid")):
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "baseline/_ref missing (pip install --target "
+                                         "baseline/_ref of /root/reference/pkg not done)"}))
+        return
+    sys.path.insert(0, _ref_path())
+    import wavevid as rw
+    with rw.VideoReader(path) as r:
+        h = r.header
+    sched = Schedule(h, range(h.frame_count), rw.CameraPose, _ref_stereo_mask(rw),
+                     rw.viewport_to_mask, rw.circle_trajectory(mbi.TRAJ_MS, mbi.TRAJ_STEPS))
     cores = len(os.sched_getaffinity(0))
     try:
         avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
     except (ValueError, OSError):
         avail = 16 << 30
-    per = 7 << 30 if args.size >= 8192 else max(1 << 28, (args.size * args.size * 100))
+    per = (7 << 30) if h.width * h.height >= (1 << 26) else (2 << 30)
     procs = max(1, min(cores, int(avail // per), args.steps))
-    # bounded sample: at most two frames per worker (~15 s of wall time)
+    # bounded sample: at most two timed frames per worker (~30 s at 8K)
     n_timed = max(1, min(args.steps, 2 * procs))
-    jobs = [(path, f, (pm[f][0].yaw, pm[f][0].pitch, pm[f][0].roll), pm[f][1], args.mode)
-            for f in frames]
+
+    def job(i):
+        f, pose, mask, gaze = sched(i)
+        fr = None
+        if mode == "foveated":
+            fr = tuple(rw.FoveationSchedule.default(h.levels, *gaze).fractions)
+        return (f, (pose.yaw, pose.pitch, pose.roll), mask, fr, gaze, mode)
+
     ctx = mp.get_context("spawn")
-    with ctx.Pool(procs, initializer=_init_worker) as pool:
-        # warm every worker (imports, first-touch allocations) before timing
-        wj = [jobs[i % len(jobs)] for i in range(procs)]
-        pool.map(_worker, wj, chunksize=1)
-        tj = [jobs[i % len(jobs)] for i in range(n_timed)]
+    with ctx.Pool(procs, initializer=_ref_init, initargs=(path,)) as pool:
+        # warm every worker (imports, first set load, first-touch allocations)
+        pool.map(_ref_frame, [job(i) for i in range(procs)], chunksize=1)
         t0 = time.perf_counter()
-        pool.map(_worker, tj, chunksize=1)
+        res = pool.map(_ref_frame, [job(args.warmup + i) for i in range(n_timed)], chunksize=1)
         wall = time.perf_counter() - t0
     fps = n_timed / wall
+    ours_loaded = sorted(set(_native_of_ours()).union(*[set(r[1]) for r in res]))
+    stereo = "stereo" if h.stereo else "mono"
+    workload = (f"{args.config.upper()} {h.width}x{h.height} {stereo} 360 {mode} decode + per-eye "
+                f"{OUT_W}x{OUT_H} perspective writeout, 90x90 FOV, circle trajectory"
+                if mode != "full" else f"{args.config.upper()} {h.width}x{h.height} {stereo} "
+                                       f"full-frame decode")
+    metric = (METRIC if (args.config, mode) == ("c3", "viewport")
+              else f"decoded frames/s (Mpixel/s) for {workload}")
+    sample = (f"{n_timed} display frames (steps {args.warmup}..{args.warmup + n_timed - 1} of the "
+              f"schedule; bounded sample of the {args.steps} requested) over {procs} worker "
+              f"processes, each with its own reference DecodeSession (wavevid "
+              f"{getattr(rw, '__version__', '?')} from baseline/_ref, decode_{mode} + "
+              f"render_perspective per eye), after one warm-up frame per worker; per-frame s "
+              f"median {statistics.median(r[0] for r in res):.2f}")
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(fps, 4), "unit": "frames/s",
+        "impl": "reference", "metric": metric, "value": round(fps, 4), "unit": "frames/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(wall * 1000.0 / n_timed, 2), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": (f"C3 {h.width}x{h.height} stereo 360 {args.mode} decode + per-eye "
-                                f"{OUT_W}x{OUT_H} perspective writeout (CPU oracle port)"
-                                if args.mode != "full" else
-                                f"{h.width}x{h.height} full-frame decode (CPU oracle port)"),
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (the same committed clip as the GPU arm)",
+        "config": {"workload": workload + " (reference CPU decoder)",
                    "frames": h.frame_count, "sets": h.num_sets},
         "cpu_baseline": {"value": round(fps, 4), "unit": "frames/s", "cores": procs,
-                         "kind": "port",
-                         "sample": f"{n_timed} display frames (of the {args.steps} requested; "
-                                   f"bounded sample) over {procs} worker processes (numpy "
-                                   f"oracle of the reference decode + render), after {procs} "
-                                   f"warm-up frames"},
+                         "kind": "reference", "sample": sample},
         "e2e": {"value": round(fps, 4), "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "repo_native_loaded": ours_loaded,
+        "coverage_errors": sum(r[2] for r in res),
     }
     print(json.dumps(line), flush=True)
 
 
+def _ref_stereo_mask(rw):
+    from wavevid.projection import stereo_mask
+    return stereo_mask
+
+
 def main():
     args = parse()
+    if args.mode is None:
+        args.mode = "full" if args.config == "c2" else "viewport"
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -85,7 +85,8 @@ int walk_meta(File& fh, const wv_file_info& info, int upto, wv_set_info* want, f
       return WV_ERR_IO;
     }
     if (i && m.payload_offset != prev.payload_offset + prev.payload_length) return WV_ERR_FORMAT;
-    if (m.record_count * rs > m.payload_length) return WV_ERR_FORMAT;
+    // record_count * rs > payload_length, without the u64 wrap-around
+    if (m.record_count > m.payload_length / (uint64_t)rs) return WV_ERR_FORMAT;
     if (m.payload_length < info.table_bytes) return WV_ERR_FORMAT;
     prev = m;
   }

@@ -258,13 +258,6 @@ struct LevelArgs {
 // this item's row pass runs (43 KB of shared memory: 5 CTAs per SM).
 constexpr int BOXSET = 4 * BOX_SLOT;
 constexpr int COL_BYTES = 2 * TY * CB_PITCH * 8;
-#ifndef WV_K3_MIDPF
-#define WV_K3_MIDPF 0   // mid levels: own output tile + next-item TMA prefetch (61 KB/CTA)
-#endif
-#ifndef WV_K3_MIDREG
-#define WV_K3_MIDREG 0  // mid levels: row-pass results stored from registers (no output tile),
-                        // next item's boxes prefetched like the finest level
-#endif
 #ifndef WV_K3_PAIRSEG
 #define WV_K3_PAIRSEG 1  // finest row pass: a warp = 16 row pairs x 2 adjacent segments, so
                          // each 16-B store pair fills whole 32-B sectors
@@ -288,7 +281,7 @@ __device__ __forceinline__ void row_map(int tid, int& i, int& sg) {
 constexpr int OB4_PITCH = TX + 1;     // float4 units, odd
 static_assert(TY * OB4_PITCH * 16 <= 4 * BOX_SLOT, "float4 output tile must fit in the box region");
 constexpr int OUTB_BYTES = WV_K3_OUT4 ? TY * OB4_PITCH * 16 : TY * OB_PITCH * 8;
-constexpr int SMEM_MID = BOXSET + COL_BYTES + (WV_K3_MIDPF ? OUTB_BYTES : 0);
+constexpr int SMEM_MID = BOXSET + COL_BYTES;
 constexpr int SMEM_FIN = BOXSET + COL_BYTES;   // the u8 tile goes from registers to HBM
 
 template <bool FINAL>
@@ -305,10 +298,9 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   const float* bHH = box + 3 * BOX_SLOT / 4;
   float2* colL = reinterpret_cast<float2*>(smem + BOXSET);  // [TY][CB_PITCH]
   float2* colH = colL + TY * CB_PITCH;
-  // mid levels: the f32 output tile aliases the boxes (or, with prefetch, has its own region)
-  float2* outb = reinterpret_cast<float2*>(smem + (WV_K3_MIDPF ? BOXSET + COL_BYTES : 0));
-  constexpr bool PF = FINAL || WV_K3_MIDPF || WV_K3_MIDREG;   // next item's boxes issued after the column pass
-  constexpr bool MIDREG = !FINAL && WV_K3_MIDREG;
+  // mid levels: the f32 output tile aliases the boxes
+  float2* outb = reinterpret_cast<float2*>(smem);
+  constexpr bool PF = FINAL;   // next item's boxes issued after the column pass
   __shared__ uint64_t bar;
 
   const int tid = threadIdx.x;
@@ -465,8 +457,6 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         auto cv = [](float v) { return u8_rint(__fmul_rn(v, 255.0f)); };
         uint32_t w0[SR / 2] = {}, w1[SR / 2] = {};   // rows 2i, 2i+1
         uint8_t* crow = FINAL ? canvas + ((uint64_t)c * H + 2 * ay + 2 * i) * W : nullptr;
-        float* mrow = MIDREG ? a.out + ((uint64_t)c * H + 2 * ay + 2 * i) * a.out_pitch : nullptr;
-        float2 m0 = make_float2(0.f, 0.f), m1 = m0;   // MIDREG: the row pair's previous pair
         // mid levels: f32 pairs into outb
         auto emit_mid = [&](int q, float2 s3, float2 d3) {
           WV_ASSERT(q >= 0 && q < TX && i < TY);
@@ -486,19 +476,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
                 d = colH[i * CB_PITCH + cb + j];
               },
               [&](int p, float2 s3, float2 d3) {
-                if (MIDREG) {
-                  // pairs 2m, 2m+1 of each row -> one float4 store
-                  const int lq = p - HALO;
-                  if ((lq & 1) == 0) {
-                    m0 = make_float2(s3.x, d3.x);
-                    m1 = make_float2(s3.y, d3.y);
-                  } else {
-                    float* r0 = mrow + 2 * (pa + lq - 1);
-                    *reinterpret_cast<float4*>(r0) = make_float4(m0.x, m0.y, s3.x, d3.x);
-                    *reinterpret_cast<float4*>(r0 + a.out_pitch) =
-                        make_float4(m1.x, m1.y, s3.y, d3.y);
-                  }
-                } else if (!FINAL) {
+                if (!FINAL) {
                   emit_mid(qb + p, s3, d3);
                 } else {
                   // p - HALO is the segment-local pair: compile-time after unrolling
@@ -543,11 +521,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
                 d = colH[i * CB_PITCH + (j - ox)];
               },
               [&](int p, float2 s3, float2 d3) {
-                if (MIDREG) {
-                  float* r0 = mrow + 2 * p;
-                  *reinterpret_cast<float2*>(r0) = make_float2(s3.x, d3.x);
-                  *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(s3.y, d3.y);
-                } else if (!FINAL) {
+                if (!FINAL) {
                   emit_mid(p - ax, s3, d3);
                 } else {
                   // level borders: two pixels per row straight to the canvas
@@ -567,7 +541,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       }
     }
     __syncthreads();   // mid: outb complete; final: colL / colH free for the next item
-    if (!FINAL && !MIDREG) {
+    if (!FINAL) {
       float* base = a.out + ((uint64_t)c * H + 2 * ay) * a.out_pitch + 2 * ax;
       if (nx == OUT_W && ny == OUT_H) {
         // full tile: 32 row pairs x 32 float2 columns, shifts only
@@ -607,237 +581,292 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   }
 }
 
-#ifndef WV_K3_WS
-#define WV_K3_WS 0
+// ------------------------------------------------------------- K3 strips
+// Strip-streaming synthesis (default).  Work item = (unit, channel): a unit
+// is UNIT_T = 4 horizontally adjacent tiles of one tile row, i.e. 32
+// coefficient rows x 128 coefficient columns of each subband (256 x 64
+// outputs).  Column pass: one thread per coefficient column (the unit's 128
+// plus 2 halo columns per side) streams DOWN the 32 rows, the lifting state
+// carried in registers from row to row, so rows are read once (no vertical
+// halo re-reads except the 2+2 rows at the unit's top and bottom) and the
+// loads are warp-coalesced 128-B rows of each subband, batched 8 rows at a
+// time (32 independent loads in flight per thread).  Every 8 output row
+// pairs (one stage) the column results go to a double-buffered shared
+// column buffer and the row pass lifts them along x (8-pair segments, their
+// 2-column halos read from the neighbouring segments' entries), then writes
+// f32 (mid levels) or request-masked u8 (level 1) with 16-byte stores.
+// Same arithmetic as k_level (lift_interior / lift_line, paired RN f32 ops,
+// no FMA), so results are bit-identical.
+constexpr int UW = UNIT_T * TX;              // 128 coefficient columns per unit
+constexpr int CS = UW + 2 * HALO;            // 132 column streams
+constexpr int SP = 8;                        // output row pairs per stage
+constexpr int NSTAGE = TY / SP;              // 4
+#ifndef WV_K3S_SEGR
+#define WV_K3S_SEGR 8
 #endif
-// Finest level, warp-specialised (WV_K3_WS): warps 0-4 (the column group,
-// 160 threads) lift item k + 1's columns into column buffer (k + 1) & 1
-// while warps 5-8 (the row group, 128 threads) lift item k's rows from
-// buffer k & 1 and store its u8 pixels.  Hand-off by named barriers:
-// FULL[b] (ids 2, 3: the column group arrives, the row group waits) and
-// EMPTY[b] (ids 4, 5: the row group arrives, the column group waits before
-// rewriting b); id 1 syncs the column group alone.  The boxes are single
-// buffered: the next item's TMA loads go out as soon as the column group has
-// consumed the current ones.  Items with ZERO_FLAG pass through the same
-// protocol with an empty column phase.  Same arithmetic as k_level<true>.
-constexpr int WS_COL = COL_SEGS * BOX_W;              // 160 column threads
-constexpr int WS_ROW = (TX / SEGLEN_RF) * TY;         // 128 row threads
-constexpr int WS_THREADS = WS_COL + WS_ROW;
-constexpr int SMEM_WS = BOXSET + 2 * COL_BYTES;
-static_assert(WS_COL % 32 == 0 && WS_ROW % 32 == 0, "whole warps per group");
+constexpr int SEGR = WV_K3S_SEGR;            // row-pass segment (output pairs)
+constexpr int RSEGS = UW / SEGR;
+constexpr int ROW_THREADS = SP * RSEGS;
+constexpr int S_THREADS = 160;
+static_assert(S_THREADS >= CS && S_THREADS >= ROW_THREADS, "one thread per stream");
+static_assert(SEGR % 8 == 0 && TX % SEGR == 0, "segments store 16-pixel chunks inside one tile");
+// column-buffer row: local column c (0..CS-1, c = x - ux0 + 2) sits at c + c/8
+// (one float2 of padding per 8 columns: the row pass's 16 segment streams of
+// a half-warp then hit 16 distinct bank pairs)
+constexpr int CBP = CS + CS / 8 + 1;
+__device__ __forceinline__ int cphys(int c) { return c + (c >> 3); }
+constexpr int SLOT_F2 = 2 * SP * CBP;        // float2 per slot: L half then H half
+constexpr int SMEM_S = 2 * SLOT_F2 * 8;      // two slots
 
-__device__ __forceinline__ void nbar_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void nbar_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
+struct StripArgs {
+  int k, bh, bw, C, ngx;
+  FastDiv divC, divG;
+  const uint32_t* list;
+  const uint32_t* count;
+  const float* ll;     // LL band: C x ll_rows x ll_pitch (the plane for k = L)
+  int ll_pitch, ll_rows;
+  const float* plane;  // detail bands: planar C x H x W
+  int W, H;
+  float* out;          // mid levels: C x 2bh x out_pitch
+  int out_pitch;
+  const wv_frame_args* fa;  // level 1: fa->d_canvas, planar C x H x W u8
+  const uint32_t* R;
+  const uint32_t* rowmap;
+  int wpr0;
+};
 
-__global__ void __launch_bounds__(WS_THREADS) k_final_ws(const __grid_constant__ CUtensorMap tm_ll,
-                                                         const __grid_constant__ CUtensorMap tm_det,
-                                                         LevelArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* canvas = a.fa->d_canvas;
-  float* box = reinterpret_cast<float*>(smem);
-  const float* bLL = box;
-  const float* bHL = box + BOX_SLOT / 4;
-  const float* bLH = box + 2 * BOX_SLOT / 4;
-  const float* bHH = box + 3 * BOX_SLOT / 4;
-  __shared__ uint64_t bar;
+template <bool FINAL>
+__global__ void __launch_bounds__(S_THREADS) k_strip(const StripArgs a) {
+  pdl_sync();
+  extern __shared__ __align__(16) float2 sbuf[];
   const int tid = threadIdx.x;
-  if (tid == 0) mbar_init(&bar, 1);
-  __syncthreads();
   const int C = a.C;
   const uint32_t nitems = *a.count * (uint32_t)C;
-  const int H = 2 * a.bh, W = 2 * a.bw;
-  auto geom = [&](uint32_t it, uint32_t& entry, int& c, int& ay, int& ax) {
-    const uint32_t itile = it / a.divC;
-    entry = a.list[itile];
-    c = (int)(it - itile * C);
-    const uint32_t tile = entry & ~ZERO_FLAG;
-    const int ty = (int)(tile / a.divN), tx = (int)tile - ty * a.ntx;
-    ay = ty * TY;
-    ax = tx * TX;
-  };
+  const int bh = a.bh, bw = a.bw;
+  const int OH = 2 * bh, OW = 2 * bw;   // output (level k-1) dims
+  uint8_t* canvas = FINAL ? a.fa->d_canvas : nullptr;
+  // this thread's column stream: tid < UW -> unit column tid; UW..UW+3 -> halo
+  const int cl = tid < UW ? tid + HALO : (tid - UW < HALO ? tid - UW : tid - UW + UW);
+  // row-pass role
+  const int sg = tid % RSEGS, ri = tid / RSEGS;
 
-  if (tid < WS_COL) {
-    // ------------------------------------------------ column group
-    uint32_t phase = 0u;
-    auto issue = [&](uint32_t it) {
-      uint32_t entry;
-      int c, ay, ax;
-      geom(it, entry, c, ay, ax);
-      const int oy = max(ay - HALO, 0), ox = max(ax - XPAD, 0);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&bar, 4u * BOX_FLOATS * 4u);
-      tma_load_3d(box, &tm_ll, ox, oy, c, &bar);
-      tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar);
-      tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar);
-      tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar);
-    };
-    bool issued = false;
-    uint32_t k = 0;
-    for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x, ++k) {
-      const int b = (int)(k & 1u);
-      uint32_t entry;
-      int c, ay, ax;
-      geom(item, entry, c, ay, ax);
-      const uint32_t nxt = item + gridDim.x;
-      uint32_t nxt_entry = ZERO_FLAG;
-      if (tid == 0 && nxt < nitems) nxt_entry = a.list[nxt / a.divC];
-      if (k >= 2) nbar_sync(4 + b, WS_THREADS);   // the row group is done with buffer b
-      if (!(entry & ZERO_FLAG)) {
-        if (tid == 0 && !issued) issue(item);
-        mbar_wait(&bar, phase);
-        phase ^= 1u;
-        float2* colL = reinterpret_cast<float2*>(smem + BOXSET + b * COL_BYTES);
-        float2* colH = colL + TY * CB_PITCH;
-        const int by = min(ay + TY, a.bh), bx = min(ax + TX, a.bw);
-        const int oy = max(ay - HALO, 0), ox = max(ax - XPAD, 0);
-        const int lc = tid % BOX_W, sg = tid / BOX_W;
-        const int cg = ox + lc;
-        const int pa = ay + sg * SEGLEN_C, pb = min(pa + SEGLEN_C, by);
-        if (pa < pb && cg >= max(ax - HALO, 0) && cg < min(bx + HALO, a.bw)) {
-          if (pa >= HALO && pb + HALO <= a.bh && pb - pa == SEGLEN_C) {
-            const int rb = pa - HALO - oy;
-            const int qb = pa - HALO - ay;
-            lift_interior<SEGLEN_C>(
-                [&](int j, float2& sv, float2& dv) {
-                  const int o = (rb + j) * BOX_W + lc;
-                  sv = make_float2(bLL[o], bHL[o]);
-                  dv = make_float2(bLH[o], bHH[o]);
-                },
-                [&](int pp, float2 s3, float2 d3) {
-                  colL[(qb + pp) * CB_PITCH + lc] = make_float2(s3.x, d3.x);
-                  colH[(qb + pp) * CB_PITCH + lc] = make_float2(s3.y, d3.y);
-                });
-          } else {
-            lift_line(
-                max(pa - HALO, 0), min(pb + HALO, a.bh), a.bh, pa, pb,
-                [&](int j, float2& sv, float2& dv) {
-                  const int o = (j - oy) * BOX_W + lc;
-                  sv = make_float2(bLL[o], bHL[o]);
-                  dv = make_float2(bLH[o], bHH[o]);
-                },
-                [&](int pp, float2 s3, float2 d3) {
-                  const int q = pp - ay;
-                  colL[q * CB_PITCH + lc] = make_float2(s3.x, d3.x);
-                  colH[q * CB_PITCH + lc] = make_float2(s3.y, d3.y);
-                });
-          }
-        }
-        nbar_sync(1, WS_COL);   // boxes consumed by every column thread
-      }
-      issued = false;
-      if (tid == 0 && !(nxt_entry & ZERO_FLAG)) {
-        issue(nxt);
-        issued = true;
-      }
-      nbar_arrive(2 + b, WS_THREADS);   // buffer b holds item k's columns
-    }
-    // complete the last EMPTY generations (no barrier left pending)
-    if (k >= 2) nbar_sync(4 + (int)(k & 1u), WS_THREADS);
-    if (k >= 1) nbar_sync(4 + (int)((k + 1) & 1u), WS_THREADS);
-  } else {
-    // ------------------------------------------------ row group
-    const int rt = tid - WS_COL;
-    const int i = rt % TY, sg = rt / TY;
-    constexpr int SR = SEGLEN_RF;
-    uint32_t k = 0;
-    for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x, ++k) {
-      const int b = (int)(k & 1u);
-      uint32_t entry;
-      int c, ay, ax;
-      geom(item, entry, c, ay, ax);
-      const int by = min(ay + TY, a.bh), bx = min(ax + TX, a.bw);
-      const int ox = max(ax - XPAD, 0);
-      const int pa = ax + sg * SR, pb = min(pa + SR, bx);
-      uint32_t rq[2][SR / 8];
-      const bool act = i < by - ay && pa < pb;
-      if (!(entry & ZERO_FLAG) && act) {
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const uint32_t* req = a.R + (uint64_t)a.rowmap[2 * ay + 2 * i + rr] * a.wpr0;
-#pragma unroll
-          for (int q = 0; q < SR / 8; ++q) {
-            const int px = 2 * pa + 16 * q;
-            rq[rr][q] = px < W ? req[px >> 5] : 0u;
-          }
-        }
-      }
-      nbar_sync(2 + b, WS_THREADS);   // item k's columns are in buffer b
-      if (entry & ZERO_FLAG) {
-        const int ny = 2 * (by - ay), nx = 2 * (bx - ax), qw = nx >> 2;
-        for (int idx = rt; idx < ny * qw; idx += WS_ROW) {
-          const int r = idx / qw, q = idx % qw;
-          *reinterpret_cast<uint32_t*>(canvas + ((uint64_t)c * H + 2 * ay + r) * W + 2 * ax +
+  for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const uint32_t iu = item / a.divC;
+    const int c = (int)(item - iu * C);
+    const uint32_t entry = a.list[iu];
+    const uint32_t unit = entry & UNIT_IDX;
+    const uint32_t need = (entry >> 24) & 0xFu, clr = entry >> 28;
+    const int uy = (int)(unit / a.divG), ug = (int)unit - uy * a.ngx;
+    const int ay = uy * TY, ux0 = ug * UW;
+    const int by = min(ay + TY, bh), ux1 = min(ux0 + UW, bw);
+    if (FINAL && clr) {
+      // tiles that left the request: clear what an earlier frame wrote there
+      for (int t = 0; t < UNIT_T; ++t) {
+        if (!((clr >> t) & 1u)) continue;
+        const int tx0 = ux0 + t * TX;
+        if (tx0 >= bw) break;
+        const int nx = 2 * (min(tx0 + TX, bw) - tx0), ny = 2 * (by - ay), qw = nx >> 2;
+        for (int idx = tid; idx < ny * qw; idx += S_THREADS) {
+          const int r = idx / qw, q = idx - (idx / qw) * qw;
+          *reinterpret_cast<uint32_t*>(canvas + ((uint64_t)c * OH + 2 * ay + r) * OW + 2 * tx0 +
                                        4 * q) = 0u;
         }
-      } else if (act) {
-        const float2* colL = reinterpret_cast<const float2*>(smem + BOXSET + b * COL_BYTES);
-        const float2* colH = colL + TY * CB_PITCH;
-        auto cv = [](float v) { return u8_rint(__fmul_rn(v, 255.0f)); };
-        uint8_t* crow = canvas + ((uint64_t)c * H + 2 * ay + 2 * i) * W;
-        if (pa >= HALO && pb + HALO <= a.bw && pb - pa == SR) {
-          uint32_t w0[SR / 2] = {}, w1[SR / 2] = {};
-          const int cb = pa - HALO - ox;
-          lift_interior<SR>(
-              [&](int j, float2& sv, float2& dv) {
-                sv = colL[i * CB_PITCH + cb + j];
-                dv = colH[i * CB_PITCH + cb + j];
-              },
-              [&](int pp, float2 s3, float2 d3) {
-                const int lq = pp - HALO;
-                w0[lq >> 1] |= (cv(s3.x) | (cv(d3.x) << 8)) << (16 * (lq & 1));
-                w1[lq >> 1] |= (cv(s3.y) | (cv(d3.y) << 8)) << (16 * (lq & 1));
+      }
+    }
+    if (!need) continue;   // uniform across the CTA
+    const int nst = (by - ay + SP - 1) / SP;
+    const bool interior = ay >= HALO && ay + TY + HALO <= bh;
+    // column stream
+    const int xcol = ux0 - HALO + cl;
+    const bool cact = tid < CS && xcol >= max(ux0 - HALO, 0) && xcol < min(ux1 + HALO, bw);
+    const float* pLL = a.ll + ((uint64_t)c * a.ll_rows) * a.ll_pitch + xcol;
+    const float* pLH = a.plane + ((uint64_t)c * a.H + bh) * a.W + xcol;
+    const float* pHL = a.plane + ((uint64_t)c * a.H) * a.W + bw + xcol;
+    const float* pHH = pLH + bw;
+    const size_t lp = a.ll_pitch, pp = a.W;
+    auto ldrow = [&](int r, float2& s, float2& d) {
+      s = make_float2(__ldg(pLL + r * lp), __ldg(pHL + r * pp));
+      d = make_float2(__ldg(pLH + r * pp), __ldg(pHH + r * pp));
+    };
+    const float2 KS = f2(__uint_as_float(0x3f9d7658u));
+    const float2 IK = f2(__uint_as_float(0x3f5019c3u));
+    const float2 ND = f2(-__uint_as_float(0x3ee31355u));
+    const float2 NG = f2(-__uint_as_float(0x3f620676u));
+    const float2 NB = f2(-__uint_as_float(0xbd5901aeu));
+    const float2 NA = f2(-__uint_as_float(0xbfcb0673u));
+    float2 d1m, s2m, d2mm, s3mm;
+    if (interior && cact) {
+      // warm-up: rows ay-2 .. ay+1 (lift_interior inputs 0..3, nothing emitted)
+      float2 s[4], d[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ldrow(ay - HALO + q, s[q], d[q]);
+      d1m = dscale(d[0], IK);
+      s2m = __fmul2_rn(s[0], KS);
+      float2 d1 = dscale(d[1], IK);
+      float2 s2 = lstep(__fmul2_rn(s[1], KS), ND, d1m, d1);
+      d2mm = lstep(d1m, NG, s2m, s2);
+      s3mm = s2;
+      d1m = d1;
+      s2m = s2;
+#pragma unroll
+      for (int q = 2; q < 4; ++q) {
+        d1 = dscale(d[q], IK);
+        s2 = lstep(__fmul2_rn(s[q], KS), ND, d1m, d1);
+        const float2 d2 = lstep(d1m, NG, s2m, s2);
+        const float2 s3 = lstep(s2m, NB, d2mm, d2);
+        d2mm = d2;
+        s3mm = s3;
+        d1m = d1;
+        s2m = s2;
+      }
+    }
+    for (int st = 0; st < nst; ++st) {
+      float2* colL = sbuf + (st & 1) * SLOT_F2;
+      float2* colH = colL + SP * CBP;
+      const int pa = ay + SP * st, pb = min(pa + SP, by);
+      // level 1: this thread's request-mask words of the stage (two dependent
+      // loads), issued before the column work so their latency hides there
+      const int xa = ux0 + sg * SEGR, xb = min(xa + SEGR, ux1);
+      const int rp = pa + ri;   // coefficient row pair of this row-pass thread
+      const bool ract = tid < ROW_THREADS && rp < pb && xa < xb &&
+                        ((need >> ((sg * SEGR) / TX)) & 1u);
+      uint32_t rq[2] = {0u, 0u};
+      if (FINAL && ract) {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr)
+          rq[rr] = a.R[(uint64_t)a.rowmap[2 * rp + rr] * a.wpr0 + ((2 * xa) >> 5)];
+      }
+      if (cact) {
+        const int lc = cphys(cl);
+        if (interior) {
+          // rows pa+2 .. pa+9 -> pairs pa .. pa+7 (lift_interior inputs 4+8st ..)
+          float2 s[SP], d[SP];
+#pragma unroll
+          for (int q = 0; q < SP; ++q) ldrow(pa + HALO + q, s[q], d[q]);
+#pragma unroll
+          for (int q = 0; q < SP; ++q) {
+            const float2 d1 = dscale(d[q], IK);
+            const float2 s2 = lstep(__fmul2_rn(s[q], KS), ND, d1m, d1);
+            const float2 d2 = lstep(d1m, NG, s2m, s2);
+            const float2 s3 = lstep(s2m, NB, d2mm, d2);
+            const float2 d3 = lstep(d2mm, NA, s3mm, s3);
+            colL[q * CBP + lc] = make_float2(s3mm.x, d3.x);
+            colH[q * CBP + lc] = make_float2(s3mm.y, d3.y);
+            d2mm = d2;
+            s3mm = s3;
+            d1m = d1;
+            s2m = s2;
+          }
+        } else {
+          // level border (symmetric extension) or short level: the stage's
+          // pairs from their own 2-row halo
+          lift_line(
+              max(pa - HALO, 0), min(pb + HALO, bh), bh, pa, pb,
+              [&](int j, float2& s, float2& d) { ldrow(j, s, d); },
+              [&](int p, float2 s3, float2 d3) {
+                colL[(p - pa) * CBP + lc] = make_float2(s3.x, d3.x);
+                colH[(p - pa) * CBP + lc] = make_float2(s3.y, d3.y);
               });
-          auto bm = [](uint32_t b4) { return ((b4 * 0x00204081u) & 0x01010101u) * 0xFFu; };
+        }
+      }
+      __syncthreads();
+      // row pass: row pair rp, pairs [xa, xb) along x
+      if (ract) {
+        const float2* rowL = colL + ri * CBP;
+        const float2* rowH = colH + ri * CBP;
+        const int y0 = 2 * rp;
+        if (xa >= HALO && xb + HALO <= bw && xb - xa == SEGR) {
+          const int cb = xa - ux0;   // local column of lift input 0 (x = xa - 2)
+          if (FINAL) {
+            auto cv = [](float v) { return u8_rint(__fmul_rn(v, 255.0f)); };
+            uint32_t w0[SEGR / 2] = {}, w1[SEGR / 2] = {};
+            lift_interior<SEGR>(
+                [&](int j, float2& s, float2& d) {
+                  s = rowL[cphys(cb + j)];
+                  d = rowH[cphys(cb + j)];
+                },
+                [&](int p, float2 s3, float2 d3) {
+                  const int lq = p - HALO;
+                  w0[lq >> 1] |= (cv(s3.x) | (cv(d3.x) << 8)) << (16 * (lq & 1));
+                  w1[lq >> 1] |= (cv(s3.y) | (cv(d3.y) << 8)) << (16 * (lq & 1));
+                });
+            auto bm = [](uint32_t b4) { return ((b4 * 0x00204081u) & 0x01010101u) * 0xFFu; };
 #pragma unroll
-          for (int rr = 0; rr < 2; ++rr) {
-            const uint32_t* wr = rr ? w1 : w0;
+            for (int rr = 0; rr < 2; ++rr) {
+              const uint32_t* wr = rr ? w1 : w0;
+              uint8_t* crow = canvas + ((uint64_t)c * OH + y0 + rr) * OW;
 #pragma unroll
-            for (int q = 0; q < SR / 8; ++q) {
-              const int px = 2 * pa + 16 * q;
-              const uint32_t bits = (rq[rr][q] >> (px & 31)) & 0xFFFFu;
-              const uint4 v = make_uint4(wr[4 * q] & bm(bits & 0xFu),
-                                         wr[4 * q + 1] & bm((bits >> 4) & 0xFu),
-                                         wr[4 * q + 2] & bm((bits >> 8) & 0xFu),
-                                         wr[4 * q + 3] & bm(bits >> 12));
-              uint8_t* dst = crow + (uint64_t)rr * W + px;
-              if ((W & 15) == 0) {
-                *reinterpret_cast<uint4*>(dst) = v;
-              } else {
-                uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
-                d4[0] = v.x;
-                d4[1] = v.y;
-                d4[2] = v.z;
-                d4[3] = v.w;
+              for (int k = 0; k < SEGR / 8; ++k) {
+                const int px = 2 * xa + 16 * k;
+                const uint32_t bits = (rq[rr] >> (px & 31)) & 0xFFFFu;
+                const uint4 v = make_uint4(wr[4 * k] & bm(bits & 0xFu),
+                                           wr[4 * k + 1] & bm((bits >> 4) & 0xFu),
+                                           wr[4 * k + 2] & bm((bits >> 8) & 0xFu),
+                                           wr[4 * k + 3] & bm(bits >> 12));
+                if ((OW & 15) == 0) {
+                  *reinterpret_cast<uint4*>(crow + px) = v;
+                } else {
+                  uint32_t* d4 = reinterpret_cast<uint32_t*>(crow + px);
+                  d4[0] = v.x;
+                  d4[1] = v.y;
+                  d4[2] = v.z;
+                  d4[3] = v.w;
+                }
               }
+            }
+          } else {
+            float r0[2 * SEGR], r1[2 * SEGR];
+            lift_interior<SEGR>(
+                [&](int j, float2& s, float2& d) {
+                  s = rowL[cphys(cb + j)];
+                  d = rowH[cphys(cb + j)];
+                },
+                [&](int p, float2 s3, float2 d3) {
+                  const int lq = p - HALO;
+                  r0[2 * lq] = s3.x;
+                  r0[2 * lq + 1] = d3.x;
+                  r1[2 * lq] = s3.y;
+                  r1[2 * lq + 1] = d3.y;
+                });
+            float* o0 = a.out + ((uint64_t)c * OH + y0) * a.out_pitch + 2 * xa;
+#pragma unroll
+            for (int q = 0; q < SEGR / 2; ++q) {
+              *reinterpret_cast<float4*>(o0 + 4 * q) =
+                  make_float4(r0[4 * q], r0[4 * q + 1], r0[4 * q + 2], r0[4 * q + 3]);
+              *reinterpret_cast<float4*>(o0 + a.out_pitch + 4 * q) =
+                  make_float4(r1[4 * q], r1[4 * q + 1], r1[4 * q + 2], r1[4 * q + 3]);
             }
           }
         } else {
           lift_line(
-              max(pa - HALO, 0), min(pb + HALO, a.bw), a.bw, pa, pb,
-              [&](int j, float2& sv, float2& dv) {
-                sv = colL[i * CB_PITCH + (j - ox)];
-                dv = colH[i * CB_PITCH + (j - ox)];
+              max(xa - HALO, 0), min(xb + HALO, bw), bw, xa, xb,
+              [&](int j, float2& s, float2& d) {
+                s = rowL[cphys(j - ux0 + HALO)];
+                d = rowH[cphys(j - ux0 + HALO)];
               },
-              [&](int pp, float2 s3, float2 d3) {
-                const int px = 2 * pp;
+              [&](int p, float2 s3, float2 d3) {
+                if (FINAL) {
+                  auto cv = [](float v) { return u8_rint(__fmul_rn(v, 255.0f)); };
+                  const int px = 2 * p;
 #pragma unroll
-                for (int rr = 0; rr < 2; ++rr) {
-                  const int y = 2 * ay + 2 * i + rr;
-                  const uint32_t bits =
-                      (a.R[(uint64_t)a.rowmap[y] * a.wpr0 + (px >> 5)] >> (px & 31)) & 3u;
-                  const uint32_t lo = rr ? cv(s3.y) : cv(s3.x), hi = rr ? cv(d3.y) : cv(d3.x);
-                  *reinterpret_cast<uint16_t*>(crow + (uint64_t)rr * W + px) =
-                      (uint16_t)(((bits & 1u) ? lo : 0u) | (((bits >> 1) & 1u) ? hi << 8 : 0u));
+                  for (int rr = 0; rr < 2; ++rr) {
+                    const uint32_t bits = (rq[rr] >> (px & 31)) & 3u;
+                    const uint32_t lo = rr ? cv(s3.y) : cv(s3.x), hi = rr ? cv(d3.y) : cv(d3.x);
+                    *reinterpret_cast<uint16_t*>(canvas + ((uint64_t)c * OH + y0 + rr) * OW + px) =
+                        (uint16_t)(((bits & 1u) ? lo : 0u) | (((bits >> 1) & 1u) ? hi << 8 : 0u));
+                  }
+                } else {
+                  float* o0 = a.out + ((uint64_t)c * OH + y0) * a.out_pitch + 2 * p;
+                  *reinterpret_cast<float2*>(o0) = make_float2(s3.x, d3.x);
+                  *reinterpret_cast<float2*>(o0 + a.out_pitch) = make_float2(s3.y, d3.y);
                 }
               });
         }
       }
-      nbar_arrive(4 + b, WS_THREADS);   // buffer b may be rewritten
     }
+    // the next item's first stage writes slot 0: with an odd stage count this
+    // item's last row pass may still be reading it
+    if (nst & 1) __syncthreads();
   }
 }
 
@@ -863,17 +892,68 @@ int make_map(CUtensorMap* m, const float* base, int cols, int rows, int pitch, i
   return r == CUDA_SUCCESS ? WV_OK : WV_ERR_CUDA;
 }
 
+#ifndef WV_K3_STRIP
+#define WV_K3_STRIP 1   // strip-streaming synthesis (k_strip); 0: per-tile TMA boxes (k_level)
+#endif
+
+int launch_strips(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStream_t s,
+                  int only_level, int sms) {
+  const int L = lo.L, C = lo.C;
+  float* plane = (float*)(ws + lo.plane);
+  const uint32_t* counters = (const uint32_t*)(ws + lo.counters);
+  static int occ_mid = 0, occ_fin = 0;   // per-process constants of the kernels
+  if (!occ_fin) {
+    WV_CUDA(cudaFuncSetAttribute(k_strip<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_S));
+    WV_CUDA(cudaFuncSetAttribute(k_strip<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_S));
+    int om = 1, of = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_strip<false>, S_THREADS, SMEM_S);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k_strip<true>, S_THREADS, SMEM_S);
+    occ_mid = max(om, 1);
+    occ_fin = max(of, 1);
+  }
+  for (int k = L; k >= 1; --k) {
+    if (only_level && k != only_level) continue;
+    StripArgs a{};
+    a.k = k; a.bh = lo.H >> k; a.bw = lo.W >> k; a.C = C; a.ngx = lo.ngx[k];
+    a.divC = fast_div((uint32_t)C);
+    a.divG = fast_div((uint32_t)lo.ngx[k]);
+    a.list = (const uint32_t*)(ws + lo.ulist[k]);
+    a.count = counters + CNT_UNITS + k;
+    a.ll = k < L ? (const float*)(ws + lo.ybuf[k]) : plane;
+    a.ll_pitch = k < L ? lo.ypitch[k] : lo.W;
+    a.ll_rows = k < L ? (lo.H >> k) : lo.H;
+    a.plane = plane; a.W = lo.W; a.H = lo.H;
+    const int items = lo.nty[k] * lo.ngx[k] * C;
+    if (k > 1) {
+      a.out = (float*)(ws + lo.ybuf[k - 1]);
+      a.out_pitch = lo.ypitch[k - 1];
+      const int grid = max(1, min(items, sms * occ_mid));
+      WV_CUDA(launch_k(k_strip<false>, dim3(grid), dim3(S_THREADS), (size_t)SMEM_S, s, a));
+    } else {
+      a.fa = fa;
+      a.R = (const uint32_t*)(ws + lo.mrows);
+      a.rowmap = (const uint32_t*)(ws + lo.rowmap);
+      a.wpr0 = lo.wpr_[0];
+      const int grid = max(1, min(items, sms * occ_fin));
+      WV_CUDA(launch_k(k_strip<true>, dim3(grid), dim3(S_THREADS), (size_t)SMEM_S, s, a));
+    }
+    WV_CUDA(cudaGetLastError());
+  }
+  return WV_OK;
+}
+
 }  // namespace
 
 int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* fa, uint8_t* ws,
                      cudaStream_t s, int only_level) {
   (void)g;
   const int L = lo.L, C = lo.C;
-  float* plane = (float*)(ws + lo.plane);
-  const uint32_t* counters = (const uint32_t*)(ws + lo.counters);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (WV_K3_STRIP) return launch_strips(lo, fa, ws, s, only_level, sms);
+  float* plane = (float*)(ws + lo.plane);
+  const uint32_t* counters = (const uint32_t*)(ws + lo.counters);
   const size_t smem_mid = SMEM_MID;
   const size_t smem_fin = SMEM_FIN;
   WV_CUDA(cudaFuncSetAttribute(k_level<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -915,18 +995,8 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
       la.R = (const uint32_t*)(ws + lo.mrows);
       la.rowmap = (const uint32_t*)(ws + lo.rowmap);
       la.wpr0 = lo.wpr_[0];
-      if (WV_K3_WS && la.use_tma) {
-        WV_CUDA(cudaFuncSetAttribute(k_final_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     SMEM_WS));
-        int occ_ws = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ws, k_final_ws, WS_THREADS, SMEM_WS);
-        int grid = max(1, min(ntiles * C, sms * occ_ws));
-        WV_CUDA(launch_k(k_final_ws, dim3(grid), dim3(WS_THREADS), (size_t)SMEM_WS, s, tm_ll,
-                         tm_plane, la));
-      } else {
-        int grid = max(1, min(ntiles * C, sms * occ_fin));
-        WV_CUDA(launch_k(k_level<true>, dim3(grid), dim3(NTHREADS), smem_fin, s, tm_ll, tm_plane, la));
-      }
+      int grid = max(1, min(ntiles * C, sms * occ_fin));
+      WV_CUDA(launch_k(k_level<true>, dim3(grid), dim3(NTHREADS), smem_fin, s, tm_ll, tm_plane, la));
     }
     WV_CUDA(cudaGetLastError());
     if (getenv("WV_DEBUG_SYNC")) {

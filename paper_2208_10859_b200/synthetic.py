@@ -11,7 +11,6 @@ changes the synthetic input, never a parity comparison).
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -88,27 +87,6 @@ def make_synthetic_clip_torch(frames: int, height: int, width: int,
                 img = torch.where(inside, torch.tensor(float(col[i, c]), dtype=f64, device=d), img)
             out[j, :, :, c] = torch.round(img).clamp(0, 255).to(torch.uint8)
     return out
-
-
-@dataclass
-class TrajectoryLog:
-    """Head/gaze samples (t_ms, yaw, pitch, roll, gaze_u, gaze_v)
-    (bench.py:73-109)."""
-
-    samples: np.ndarray
-
-    def sample_at(self, t_ms: float) -> np.ndarray:
-        idx = int(np.searchsorted(self.samples[:, 0], t_ms, side="right")) - 1
-        return self.samples[max(idx, 0)]
-
-
-def circle_trajectory(duration_ms: float = 2000.0, steps: int = 20) -> TrajectoryLog:
-    """Yaw sweep -60..60 with mild pitch (bench.py:241-250)."""
-    t = np.linspace(0, duration_ms, steps)
-    rows = np.stack([t, np.linspace(-60, 60, steps),
-                     15 * np.sin(np.linspace(0, np.pi, steps)), np.zeros(steps),
-                     np.full(steps, 0.5), np.full(steps, 0.5)], axis=1)
-    return TrajectoryLog(rows)
 
 
 def psnr(a, b) -> float:
