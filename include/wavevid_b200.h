@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define WV_ABI_VERSION 3
+#define WV_ABI_VERSION 4
 #define WV_MAX_LEVELS 12
 
 enum wv_status {
@@ -180,6 +180,22 @@ enum wv_stage {
 };
 int wv_decode_stages_desc(const wv_geometry* g, int mode, int flags, int stages,
                           void* d_workspace, void* stream);
+
+/* One frame of a captured decode graph in a single call (the per-frame host
+ * path of DecodeSession): copy the frame's descriptor -- wv_frame_args, the
+ * wv_view_args and the request-mask bytes, laid out as in the workspace
+ * descriptor slot -- from pinned host memory to the slot (d_desc, from
+ * wv_desc_view), launch the graph (a cudaGraphExec_t recorded from
+ * wv_decode_stages_desc / wv_render_perspective_desc reading that slot),
+ * copy the frame's wv_frame_result back to pinned host memory and record
+ * `event` (a cudaEvent_t, may be NULL), all on `stream`.  Replaces the
+ * decode call of DecodeSession._decode (decoding.py:260-307) for callers
+ * that pipeline frames. */
+int wv_enqueue_frame(void* d_desc, const void* h_desc, uint64_t desc_bytes, void* graph_exec,
+                     void* stream, const void* d_result, void* h_result, void* event);
+/* Bytes of the descriptor slot: wv_frame_args, 4 wv_view_args, then the
+ * mask bytes (mask_h * mask_w) at wv_desc_mask_offset(). */
+int wv_desc_layout(const wv_geometry* g, uint64_t* mask_offset, uint64_t* slot_bytes);
 
 /* shared_geometry != 0: all views share pose, FOV, region size and output
  * size (a stereo pair rendered with one head pose) -- the ray geometry is

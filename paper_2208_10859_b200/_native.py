@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(HERE, "_wvb200.so")
 WV_OK, WV_ERR_ARG, WV_ERR_CUDA, WV_ERR_UNSUPPORTED, WV_ERR_FORMAT, WV_ERR_IO = 0, 1, 2, 3, 4, 5
 WV_MODE_FULL, WV_MODE_VIEWPORT, WV_MODE_FOVEATED = 0, 1, 2
 WV_FLAG_ACCOUNT_ONLY, WV_FLAG_FETCH = 1, 2
-WV_ABI_VERSION = 3
+WV_ABI_VERSION = 4
 WV_ENC_MAX_N = 64
 (WV_STAGE_ROWS, WV_STAGE_CASCADES, WV_STAGE_FOOTPRINT, WV_STAGE_BLOCKS, WV_STAGE_TILES,
  WV_STAGE_FOOTPRINT_TILES, WV_STAGE_DEQUANT, WV_STAGE_SYNTH) = 1, 2, 4, 8, 16, 32, 64, 128
@@ -28,7 +28,8 @@ EXPORTS = ["wv_abi_version", "wv_status_string", "wv_workspace_bytes", "wv_works
            "wv_block_list_view", "wv_desc_view", "wv_decode_frame_desc",
            "wv_render_perspective_desc", "wv_file_info_read", "wv_file_set_read",
            "wv_file_payload_read", "wv_decode_stages_desc", "wv_encode_workspace_bytes",
-           "wv_encode_payload_capacity", "wv_encode_set"]
+           "wv_encode_payload_capacity", "wv_encode_set", "wv_enqueue_frame",
+           "wv_desc_layout"]
 
 
 class Geometry(C.Structure):

@@ -175,6 +175,27 @@ int wv_render_perspective(const wv_view_args* views, int n_views, void* stream) 
   return launch_perspective(views, n_views, (cudaStream_t)stream);
 }
 
+int wv_enqueue_frame(void* d_desc, const void* h_desc, uint64_t desc_bytes, void* graph_exec,
+                     void* stream, const void* d_result, void* h_result, void* event) {
+  if (!d_desc || !h_desc || !graph_exec || !d_result || !h_result) return WV_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  WV_CUDA(cudaMemcpyAsync(d_desc, h_desc, desc_bytes, cudaMemcpyHostToDevice, s));
+  WV_CUDA(cudaGraphLaunch((cudaGraphExec_t)graph_exec, s));
+  WV_CUDA(cudaMemcpyAsync(h_result, d_result, sizeof(wv_frame_result), cudaMemcpyDeviceToHost, s));
+  if (event) WV_CUDA(cudaEventRecord((cudaEvent_t)event, s));
+  return WV_OK;
+}
+
+int wv_desc_layout(const wv_geometry* g, uint64_t* mask_offset, uint64_t* slot_bytes) {
+  Layout lo;
+  int st = build_layout(g, &lo);
+  if (st != WV_OK) return st;
+  if (!mask_offset || !slot_bytes) return WV_ERR_ARG;
+  *mask_offset = lo.desc_mask;
+  *slot_bytes = lo.desc_bytes;
+  return WV_OK;
+}
+
 int wv_plane_view(const wv_geometry* g, void* ws, float** d_plane) {
   Layout lo;
   int st = build_layout(g, &lo);

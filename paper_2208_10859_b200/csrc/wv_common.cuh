@@ -57,7 +57,8 @@ struct Layout {
   uint64_t ulist[WV_MAX_LEVELS + 1];     // u32 per unit (K3 strip work list)
   uint64_t clear1;                       // level-1 tiles that left the request: bit rows like need[1]
   uint64_t counters;                     // u32[64]
-  uint64_t desc;                         // device wv_frame_args + 4 wv_view_args (per-frame inputs)
+  uint64_t desc;                         // device wv_frame_args + 4 wv_view_args + mask bytes
+  uint64_t desc_mask, desc_bytes;        // mask offset inside the slot, slot size
   uint64_t plane;                        // C x H x W f32
   uint64_t ybuf[WV_MAX_LEVELS + 1];      // level k (1..L-1): C x (H>>k) x pitch[k] f32
   int ypitch[WV_MAX_LEVELS + 1];
@@ -116,7 +117,9 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
   o->clear1 = take(uint64_t(o->nty[1]) * wpr(o->ntx[1]) * 4);
   o->prev_need = take(uint64_t(o->nty[1]) * o->ntx[1]);
   o->counters = take(64 * 4);
-  o->desc = take(sizeof(wv_frame_args) + 4 * sizeof(wv_view_args));
+  o->desc_mask = (sizeof(wv_frame_args) + 4 * sizeof(wv_view_args) + 15) & ~size_t(15);
+  o->desc_bytes = o->desc_mask + (uint64_t(g->mask_h) * g->mask_w + 15) / 16 * 16;
+  o->desc = take(o->desc_bytes);
   o->plane = take(uint64_t(C) * H * W * 4);
   for (int k = 1; k < L; ++k) {
     int cols = W >> k;

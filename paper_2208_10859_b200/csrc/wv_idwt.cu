@@ -600,7 +600,6 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
 constexpr int UW = UNIT_T * TX;              // 128 coefficient columns per unit
 constexpr int CS = UW + 2 * HALO;            // 132 column streams
 constexpr int SP = 8;                        // output row pairs per stage
-constexpr int NSTAGE = TY / SP;              // 4
 #ifndef WV_K3S_SEGR
 #define WV_K3S_SEGR 8
 #endif
@@ -635,8 +634,19 @@ struct StripArgs {
   int wpr0;
 };
 
+#ifndef WV_K3S_MINB
+#define WV_K3S_MINB 0   // > 0: __launch_bounds__ min blocks per SM (register cap)
+#endif
+#if WV_K3S_MINB > 0
+#define K3S_BOUNDS __launch_bounds__(S_THREADS, WV_K3S_MINB)
+#else
+#define K3S_BOUNDS __launch_bounds__(S_THREADS)
+#endif
+#ifndef WV_K3S_PF
+#define WV_K3S_PF 0     // issue stage s+1's row loads before stage s's row pass
+#endif
 template <bool FINAL>
-__global__ void __launch_bounds__(S_THREADS) k_strip(const StripArgs a) {
+__global__ void K3S_BOUNDS k_strip(const StripArgs a) {
   pdl_sync();
   extern __shared__ __align__(16) float2 sbuf[];
   const int tid = threadIdx.x;
@@ -695,11 +705,18 @@ __global__ void __launch_bounds__(S_THREADS) k_strip(const StripArgs a) {
     const float2 NB = f2(-__uint_as_float(0xbd5901aeu));
     const float2 NA = f2(-__uint_as_float(0xbfcb0673u));
     float2 d1m, s2m, d2mm, s3mm;
+#if WV_K3S_PF
+    float2 ps[SP], pd[SP];   // the next stage's rows
+#endif
     if (interior && cact) {
       // warm-up: rows ay-2 .. ay+1 (lift_interior inputs 0..3, nothing emitted)
       float2 s[4], d[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) ldrow(ay - HALO + q, s[q], d[q]);
+#if WV_K3S_PF
+#pragma unroll
+      for (int q = 0; q < SP; ++q) ldrow(ay + HALO + q, ps[q], pd[q]);
+#endif
       d1m = dscale(d[0], IK);
       s2m = __fmul2_rn(s[0], KS);
       float2 d1 = dscale(d[1], IK);
@@ -741,8 +758,20 @@ __global__ void __launch_bounds__(S_THREADS) k_strip(const StripArgs a) {
         if (interior) {
           // rows pa+2 .. pa+9 -> pairs pa .. pa+7 (lift_interior inputs 4+8st ..)
           float2 s[SP], d[SP];
+#if WV_K3S_PF
+#pragma unroll
+          for (int q = 0; q < SP; ++q) {
+            s[q] = ps[q];
+            d[q] = pd[q];
+          }
+          if (st + 1 < nst) {
+#pragma unroll
+            for (int q = 0; q < SP; ++q) ldrow(pa + SP + HALO + q, ps[q], pd[q]);
+          }
+#else
 #pragma unroll
           for (int q = 0; q < SP; ++q) ldrow(pa + HALO + q, s[q], d[q]);
+#endif
 #pragma unroll
           for (int q = 0; q < SP; ++q) {
             const float2 d1 = dscale(d[q], IK);
@@ -892,8 +921,69 @@ int make_map(CUtensorMap* m, const float* base, int cols, int rows, int pitch, i
   return r == CUDA_SUCCESS ? WV_OK : WV_ERR_CUDA;
 }
 
+// one level with the per-tile TMA-box kernel (k_level)
+int launch_tiles(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStream_t s, int k,
+                 int sms) {
+  const int L = lo.L, C = lo.C;
+  float* plane = (float*)(ws + lo.plane);
+  const uint32_t* counters = (const uint32_t*)(ws + lo.counters);
+  static int occ_mid = 0, occ_fin = 0;   // per-process constants of the kernels
+  if (!occ_fin) {
+    WV_CUDA(cudaFuncSetAttribute(k_level<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SMEM_MID));
+    WV_CUDA(cudaFuncSetAttribute(k_level<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SMEM_FIN));
+    int om = 1, of = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_level<false>, NTHREADS, SMEM_MID);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k_level<true>, NTHREADS, SMEM_FIN);
+    occ_mid = max(om, 1);
+    occ_fin = max(of, 1);
+  }
+  CUtensorMap tm_plane;
+  if (make_map(&tm_plane, plane, lo.W, lo.H, lo.W, C) != WV_OK) return WV_ERR_CUDA;
+  CUtensorMap tm_ll = tm_plane;
+  if (k < L) {
+    if (make_map(&tm_ll, (const float*)(ws + lo.ybuf[k]), lo.W >> k, lo.H >> k, lo.ypitch[k], C) !=
+        WV_OK)
+      return WV_ERR_CUDA;
+  }
+  LevelArgs la{};
+  la.k = k; la.bh = lo.H >> k; la.bw = lo.W >> k; la.C = C; la.ntx = lo.ntx[k];
+  la.divC = fast_div((uint32_t)C);
+  la.divN = fast_div((uint32_t)lo.ntx[k]);
+  la.use_tma = (la.bw % 4) == 0;
+  la.ll_ptr = k < L ? (const float*)(ws + lo.ybuf[k]) : plane;
+  la.ll_pitch = k < L ? lo.ypitch[k] : lo.W;
+  la.ll_rows = k < L ? (lo.H >> k) : lo.H;
+  la.plane = plane; la.plane_w = lo.W; la.plane_h = lo.H;
+  la.list = (const uint32_t*)(ws + lo.tlist[k]);
+  la.count = counters + CNT_TILES + k;
+  const int ntiles = lo.nty[k] * lo.ntx[k];
+  if (k > 1) {
+    la.out = (float*)(ws + lo.ybuf[k - 1]);
+    la.out_pitch = lo.ypitch[k - 1];
+    const int grid = max(1, min(ntiles * C, sms * occ_mid));
+    WV_CUDA(launch_k(k_level<false>, dim3(grid), dim3(NTHREADS), (size_t)SMEM_MID, s, tm_ll,
+                     tm_plane, la));
+  } else {
+    la.fa = fa;
+    la.R = (const uint32_t*)(ws + lo.mrows);
+    la.rowmap = (const uint32_t*)(ws + lo.rowmap);
+    la.wpr0 = lo.wpr_[0];
+    const int grid = max(1, min(ntiles * C, sms * occ_fin));
+    WV_CUDA(launch_k(k_level<true>, dim3(grid), dim3(NTHREADS), (size_t)SMEM_FIN, s, tm_ll,
+                     tm_plane, la));
+  }
+  WV_CUDA(cudaGetLastError());
+  return WV_OK;
+}
+
 #ifndef WV_K3_STRIP
-#define WV_K3_STRIP 1   // strip-streaming synthesis (k_strip); 0: per-tile TMA boxes (k_level)
+#define WV_K3_STRIP 1   // strip-streaming synthesis (k_strip) for levels whose subband has at
+                        // least WV_K3_STRIP_MIN coefficients; per-tile TMA boxes (k_level) below
+#endif
+#ifndef WV_K3_STRIP_MIN
+#define WV_K3_STRIP_MIN 0
 #endif
 
 int launch_strips(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStream_t s,
@@ -913,6 +1003,11 @@ int launch_strips(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaSt
   }
   for (int k = L; k >= 1; --k) {
     if (only_level && k != only_level) continue;
+    if ((long)(lo.H >> k) * (lo.W >> k) < (long)WV_K3_STRIP_MIN) {
+      const int st = launch_tiles(lo, fa, ws, s, k, sms);
+      if (st != WV_OK) return st;
+      continue;
+    }
     StripArgs a{};
     a.k = k; a.bh = lo.H >> k; a.bw = lo.W >> k; a.C = C; a.ngx = lo.ngx[k];
     a.divC = fast_div((uint32_t)C);
@@ -947,65 +1042,19 @@ int launch_strips(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaSt
 int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* fa, uint8_t* ws,
                      cudaStream_t s, int only_level) {
   (void)g;
-  const int L = lo.L, C = lo.C;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (WV_K3_STRIP) return launch_strips(lo, fa, ws, s, only_level, sms);
-  float* plane = (float*)(ws + lo.plane);
-  const uint32_t* counters = (const uint32_t*)(ws + lo.counters);
-  const size_t smem_mid = SMEM_MID;
-  const size_t smem_fin = SMEM_FIN;
-  WV_CUDA(cudaFuncSetAttribute(k_level<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem_mid));
-  WV_CUDA(cudaFuncSetAttribute(k_level<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem_fin));
-  int occ_mid = 1, occ_fin = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_mid, k_level<false>, NTHREADS, smem_mid);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fin, k_level<true>, NTHREADS, smem_fin);
-  CUtensorMap tm_plane;
-  if (make_map(&tm_plane, plane, lo.W, lo.H, lo.W, C) != WV_OK) return WV_ERR_CUDA;
-  for (int k = L; k >= 1; --k) {
+#if WV_K3_STRIP
+  return launch_strips(lo, fa, ws, s, only_level, sms);
+#else
+  for (int k = lo.L; k >= 1; --k) {
     if (only_level && k != only_level) continue;
-    CUtensorMap tm_ll = tm_plane;
-    if (k < L) {
-      if (make_map(&tm_ll, (const float*)(ws + lo.ybuf[k]), lo.W >> k, lo.H >> k, lo.ypitch[k],
-                   C) != WV_OK)
-        return WV_ERR_CUDA;
-    }
-    LevelArgs la{};
-    la.k = k; la.bh = lo.H >> k; la.bw = lo.W >> k; la.C = C; la.ntx = lo.ntx[k];
-    la.divC = fast_div((uint32_t)C);
-    la.divN = fast_div((uint32_t)lo.ntx[k]);
-    la.use_tma = (la.bw % 4) == 0;
-    la.ll_ptr = k < L ? (const float*)(ws + lo.ybuf[k]) : plane;
-    la.ll_pitch = k < L ? lo.ypitch[k] : lo.W;
-    la.ll_rows = k < L ? (lo.H >> k) : lo.H;
-    la.plane = plane; la.plane_w = lo.W; la.plane_h = lo.H;
-    la.list = (const uint32_t*)(ws + lo.tlist[k]);
-    la.count = counters + CNT_TILES + k;
-    const int ntiles = lo.nty[k] * lo.ntx[k];
-    if (k > 1) {
-      la.out = (float*)(ws + lo.ybuf[k - 1]);
-      la.out_pitch = lo.ypitch[k - 1];
-      int grid = max(1, min(ntiles * C, sms * occ_mid));
-      WV_CUDA(launch_k(k_level<false>, dim3(grid), dim3(NTHREADS), smem_mid, s, tm_ll, tm_plane, la));
-    } else {
-      la.fa = fa;
-      la.R = (const uint32_t*)(ws + lo.mrows);
-      la.rowmap = (const uint32_t*)(ws + lo.rowmap);
-      la.wpr0 = lo.wpr_[0];
-      int grid = max(1, min(ntiles * C, sms * occ_fin));
-      WV_CUDA(launch_k(k_level<true>, dim3(grid), dim3(NTHREADS), smem_fin, s, tm_ll, tm_plane, la));
-    }
-    WV_CUDA(cudaGetLastError());
-    if (getenv("WV_DEBUG_SYNC")) {
-      cudaError_t e = cudaStreamSynchronize(s);
-      fprintf(stderr, "[wv] level %d (%s): %s\n", k, k > 1 ? "mid" : "final", cudaGetErrorString(e));
-      if (e != cudaSuccess) return WV_ERR_CUDA;
-    }
+    const int st = launch_tiles(lo, fa, ws, s, k, sms);
+    if (st != WV_OK) return st;
   }
   return WV_OK;
+#endif
 }
 
 }  // namespace wv

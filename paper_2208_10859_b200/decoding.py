@@ -220,12 +220,25 @@ class DecodeSession:
                                         device=self.device)
             self._uncovered = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._mask_host = torch.zeros((_RING, h.mask_h * h.mask_w), dtype=torch.uint8).pin_memory()
-        self._desc_host = torch.zeros((_RING, _DESC_BYTES), dtype=torch.uint8).pin_memory()
+        # descriptor slot: wv_frame_args, 4 wv_view_args, mask bytes (wv_desc_layout)
+        moff, sbytes = C.c_uint64(), C.c_uint64()
+        N.check(self._lib.wv_desc_layout(C.byref(self._geom), C.byref(moff), C.byref(sbytes)),
+                "wv_desc_layout")
+        self._desc_mask_off, self._desc_bytes = int(moff.value), int(sbytes.value)
+        self._desc_host = torch.zeros((_RING, self._desc_bytes), dtype=torch.uint8).pin_memory()
         dptr = C.c_void_p()
         N.check(self._lib.wv_desc_view(C.byref(self._geom), C.c_void_p(self._ws.data_ptr()),
                                        C.byref(dptr)), "wv_desc_view")
         doff = dptr.value - self._ws.data_ptr()
-        self._desc_dev = self._ws[doff: doff + _DESC_BYTES]
+        self._desc_dev = self._ws[doff: doff + self._desc_bytes]
+        self._desc_dev_ptr = self._desc_dev.data_ptr()
+        # per ring slot: the frame arguments live directly in the pinned slot;
+        # masks are copied next to them, so one H2D per frame carries both
+        self._slot_args = [N.FrameArgs.from_address(self._desc_host[i].data_ptr())
+                           for i in range(_RING)]
+        self._slot_mask = [self._desc_host[i].numpy()[self._desc_mask_off:
+                                                      self._desc_mask_off + h.mask_h * h.mask_w]
+                           for i in range(_RING)]
         self._graphs: dict = {}
         self.use_graphs = True
         with torch.cuda.stream(self.stream):
@@ -236,6 +249,13 @@ class DecodeSession:
         self._aux_stream = torch.cuda.Stream(self.device)
         self._aux_stream2 = torch.cuda.Stream(self.device)
         self._results_host = torch.zeros((_RING, _RESULT_BYTES), dtype=torch.uint8).pin_memory()
+        # one completion event per ring slot, materialised (recorded once) so
+        # that wv_enqueue_frame can record its handle
+        self._slot_events = []
+        for _ in range(_RING):
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+            self._slot_events.append(ev)
         self._slot = 0
         self._cache: dict[int, _Entry] = {}
         self._resident: OrderedDict = OrderedDict()
@@ -354,16 +374,24 @@ class DecodeSession:
             raise DecodeError(f"mask dims {m.shape} != header ({h.mask_h}, {h.mask_w})")
         return m if m.dtype == np.bool_ else m.astype(bool)
 
-    def _mode_args(self, mode: str, mask, schedule, slot: int):
+    def _mode_args(self, mode: str, mask, schedule, slot: int, in_desc: bool = False):
+        """Frame arguments in ring slot ``slot``.  ``in_desc``: the mask
+        travels inside the descriptor slot (graph path, one H2D per frame);
+        otherwise it is copied to its own device buffer now."""
         h = self.header
-        args = N.FrameArgs()
+        args = self._slot_args[slot]
+        C.memset(C.addressof(args), 0, _FA_BYTES)
         if mode == "full":
             args.mode = N.WV_MODE_FULL
             return args
         m = self._check_mask(mask)
-        np.copyto(self._mask_host[slot].numpy(), m.reshape(-1), casting="unsafe")
-        self._mask_dev[slot].copy_(self._mask_host[slot], non_blocking=True)
-        args.d_mask = self._mask_dev[slot].data_ptr()
+        if in_desc:
+            np.copyto(self._slot_mask[slot], m.reshape(-1), casting="unsafe")
+            args.d_mask = self._desc_dev_ptr + self._desc_mask_off
+        else:
+            np.copyto(self._mask_host[slot].numpy(), m.reshape(-1), casting="unsafe")
+            self._mask_dev[slot].copy_(self._mask_host[slot], non_blocking=True)
+            args.d_mask = self._mask_dev[slot].data_ptr()
         args.mode = N.WV_MODE_VIEWPORT
         if mode == "foveated":
             bbox = mask_bbox(m, h.width, h.height)
@@ -375,21 +403,28 @@ class DecodeSession:
         return args
 
     def _run_fast(self, slot: int, args: N.FrameArgs, mode: str, views=None, out_dims=None,
-                  flags: int = 0):
-        """Per-frame inputs -> the workspace descriptor (one H2D from a pinned
-        ring slot), then the fixed launch sequence of this mode -- replayed
-        from a CUDA graph after its first direct run."""
+                  flags: int = 0) -> bool:
+        """Per-frame inputs (already in pinned ring slot ``slot``: arguments,
+        views, mask) -> the workspace descriptor, then the fixed launch
+        sequence of this mode.  After its first direct run the sequence is a
+        CUDA graph, and a frame is ONE C call (wv_enqueue_frame: descriptor
+        H2D, graph launch, result D2H, completion event); returns True then."""
         host = self._desc_host[slot]
-        C.memmove(host.data_ptr(), C.addressof(args), _FA_BYTES)
+        hptr = host.data_ptr()
         nv = len(views) if views else 0
         for i in range(nv):
-            C.memmove(host.data_ptr() + _FA_BYTES + i * _VA_BYTES, C.addressof(views[i]), _VA_BYTES)
-        self._desc_dev.copy_(host, non_blocking=True)
+            C.memmove(hptr + _FA_BYTES + i * _VA_BYTES, C.addressof(views[i]), _VA_BYTES)
         key = (_MODES[mode], nv, tuple(out_dims) if nv else None, flags)
         g = self._graphs.get(key)
         if g is not None:
-            g.replay()
-            return
+            N.check(self._lib.wv_enqueue_frame(
+                C.c_void_p(self._desc_dev_ptr), C.c_void_p(hptr), C.c_uint64(self._desc_bytes),
+                C.c_void_p(g[1]), C.c_void_p(self.stream.cuda_stream),
+                C.c_void_p(self._results[slot].data_ptr()),
+                C.c_void_p(self._results_host[slot].data_ptr()),
+                C.c_void_p(self._slot_events[slot].cuda_event)), "wv_enqueue_frame")
+            return True
+        self._desc_dev.copy_(host, non_blocking=True)
 
         def run(stages, stream):
             N.check(self._lib.wv_decode_stages_desc(
@@ -439,7 +474,8 @@ class DecodeSession:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=self.stream, capture_error_mode="relaxed"):
                 seq()
-            self._graphs[key] = graph
+            self._graphs[key] = (graph, graph.raw_cuda_graph_exec())
+        return False
 
     def _launch(self, frame: int, mode: str, mask=None, schedule=None,
                 account_only: bool = False, time_stages: bool = False,
@@ -459,7 +495,8 @@ class DecodeSession:
             if ev0 is not None:
                 ev0.record(s)
             dev, ext, keep = self._make_resident(si)
-            args = self._mode_args(mode, mask, schedule, slot)
+            fast = not (account_only or self.kernel_timing or time_stages)
+            args = self._mode_args(mode, mask, schedule, slot, in_desc=fast)
             entry, existed, may_evict = self._entry_for(si)
             args.t = t
             args.flags = N.WV_FLAG_ACCOUNT_ONLY if account_only else 0
@@ -477,6 +514,7 @@ class DecodeSession:
             args.d_result = self._results[slot].data_ptr()
             g, ws, cs = C.byref(self._geom), C.c_void_p(self._ws.data_ptr()), C.c_void_p(s.cuda_stream)
             evs = None
+            done = None
             if account_only:
                 N.check(self._lib.wv_select(g, C.byref(args), ws, cs), "wv_select")
             elif self.kernel_timing:
@@ -505,11 +543,12 @@ class DecodeSession:
                 evs[1].record(s)
                 N.check(self._lib.wv_synthesize(g, C.byref(args), ws, cs), "wv_synthesize")
                 evs[2].record(s)
-            else:
-                self._run_fast(slot, args, mode, views, out_dims, args.flags)
-            self._results_host[slot].copy_(self._results[slot], non_blocking=True)
-            done = torch.cuda.Event()
-            done.record(s)
+            elif self._run_fast(slot, args, mode, views, out_dims, args.flags):
+                done = self._slot_events[slot]   # recorded by wv_enqueue_frame
+            if done is None:
+                self._results_host[slot].copy_(self._results[slot], non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(s)
         p.slot, p.set_index, p.entry, p.existed, p.may_evict = slot, si, entry, existed, may_evict
         p.event, p.ev, p.account_only = done, (ev0, evs), account_only
         self._pending.append(p)

@@ -260,6 +260,30 @@ def test_corrupt_offset_raises(wv, tmp_path):
             s.decode_full(0)
 
 
+@pytest.mark.parametrize("mode", ["full", "viewport"])
+def test_blockend_past_payload_raises(wv, tmp_path, mode):
+    """A BlockEnd entry pointing past the set payload is a corrupt stream:
+    K2 and the span fetch skip the span (no out-of-bounds read) and the
+    decode raises CorruptStreamError; the session stays usable."""
+    src = os.path.join(GOLDEN, "golden_quantized.wvv")
+    dst = tmp_path / "corrupt_table.wvv"
+    shutil.copy(src, dst)
+    raw = bytearray(open(dst, "rb").read())
+    from paper_2208_10859_b200.fileio import read_header
+    h, metas = read_header(src)
+    t0 = metas[0].payload_offset
+    raw[t0 + 8 * 5:t0 + 8 * 6] = (1 << 40).to_bytes(8, "little")   # (t=0, block 5) end
+    open(dst, "wb").write(bytes(raw))
+    mask = np.ones((h.mask_h, h.mask_w), bool)
+    for residency in ("set", "spans"):
+        with wv.DecodeSession(dst, residency=residency) as s:
+            with pytest.raises(wv.CorruptStreamError):
+                s.decode_full(0) if mode == "full" else s.decode_viewport(0, mask)
+            # the context is intact: a good file still decodes afterwards
+        with wv.DecodeSession(src) as s:
+            s.decode_full(1)
+
+
 # ------------------------------------------------------ larger frames
 
 @pytest.mark.parametrize("mode", ["viewport", "foveated", "full"])

@@ -39,7 +39,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_abi_host_functions(lib):
     from paper_2208_10859_b200 import _native as N
-    assert lib.wv_abi_version() == 3
+    assert lib.wv_abi_version() == N.WV_ABI_VERSION == 4
     assert lib.wv_status_string(0) == b"ok"
     g = N.Geometry(8192, 8192, 3, 6, 4, 32, 0, 256, 256)
     b = C.c_uint64()
