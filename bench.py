@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--residency", choices=["set", "spans"], default="set",
                     help="spans: only BlockEnd tables are uploaded; the GPU fetches the record "
                          "spans of selected blocks from pinned host memory (load_blocks)")
+    ap.add_argument("--split", choices=["sets", "eyes"], default="sets",
+                    help="N>1: sets round-robin over ranks (both eyes each), or rank pairs "
+                         "splitting the stereo eyes of each frame (sets round-robin over pairs)")
     ap.add_argument("--profile-only", action="store_true",
                     help="a few decodes for ncu; prints nothing")
     return ap.parse_args()
@@ -209,7 +212,7 @@ def run_ours(args):
     from paper_2208_10859_b200 import build
     from paper_2208_10859_b200.decoding import FoveationSchedule
     from paper_2208_10859_b200.projection import CameraPose, stereo_mask, viewport_to_mask
-    from paper_2208_10859_b200.sharding import frames_for_sets, gather_views, sets_for_rank
+    from paper_2208_10859_b200.sharding import assign, gather_views
     from paper_2208_10859_b200.replay import circle_trajectory
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -235,8 +238,9 @@ def run_ours(args):
         s_.time_stages = False
     sess = sessions[0]
     h = sess.header
-    my_sets = sets_for_rank(h.num_sets, rank, world)
-    frames = frames_for_sets(my_sets, h.inter_size, h.frame_count)
+    share = assign(h.num_sets, h.inter_size, h.frame_count, rank, world,
+                   args.split if mode != "full" else "sets", h.stereo)
+    my_sets, frames, eye = share.sets, share.frames, share.eye
     sched = Schedule(h, frames, CameraPose, stereo_mask, viewport_to_mask,
                      circle_trajectory(mbi.TRAJ_MS, mbi.TRAJ_STEPS))
     # every step's inputs are prepared before timing (host pose -> mask work
@@ -246,7 +250,7 @@ def run_ours(args):
         f, pose, mask, gaze = sched(i)
         sc = FoveationSchedule.default(h.levels, *gaze) if mode == "foveated" else None
         plan.append((f, pose, mask, sc))
-    views = 2 if h.stereo else 1
+    views = (2 if h.stereo else 1) if eye is None else 1
     outs = [torch.empty((views, OUT_H, OUT_W, h.channels), dtype=torch.uint8, device=dev)
             for _ in range(P)]
     out = outs[0]
@@ -263,7 +267,8 @@ def run_ours(args):
         if mode == "full":
             ss.decode_full_device(f)
         else:
-            ss.decode_render_device(f, mode, mask, pose, (OUT_W, OUT_H), outs[p_], schedule=sc)
+            ss.decode_render_device(f, mode, mask, pose, (OUT_W, OUT_H), outs[p_], schedule=sc,
+                                    eye=eye)
 
     def gather(p_=0):
         if world > 1:
@@ -444,7 +449,8 @@ def run_ours(args):
         for ss in sessions:
             ss._settle_until(None)
         bi += sum(ss.bytes_fetched for ss in sessions) - fetched0
-        e2e = {"value": round(world * args.steps / (float(te.item()) / 1000.0), 2),
+        e2e = {"value": round(world * share.frames_per_step * args.steps /
+                              (float(te.item()) / 1000.0), 2),
                "unit": "frames/s",
                "h2d_bytes_per_step": bi // args.steps, "d2h_bytes_per_step": bo // args.steps,
                "result": "decoded u8 canvas (C, H, W)" if mode == "full"
@@ -477,8 +483,9 @@ def run_ours(args):
         cpu = cpu_baseline_sample(path, [plan[args.warmup + i] for i in range(3)], mode)
 
     if rank == 0:
-        fps = world * args.steps / (max_ms / 1000.0)
-        out_px = views * OUT_W * OUT_H if mode != "full" else h.width * h.height
+        fps = world * share.frames_per_step * args.steps / (max_ms / 1000.0)
+        out_px = ((2 if h.stereo else 1) * OUT_W * OUT_H if mode != "full"
+                  else h.width * h.height)
         stereo = "stereo" if h.stereo else "mono"
         workload = (f"{args.config.upper()} {h.width}x{h.height} {stereo} 360 {mode} decode + "
                     f"per-eye {OUT_W}x{OUT_H} perspective writeout, 90x90 FOV, circle trajectory"
@@ -516,7 +523,10 @@ def run_ours(args):
                        "before every step"),
                 "pipeline": f"{P} decode sessions (CUDA streams) per GPU, steps round-robin",
                 "residency": args.residency,
-                "parallelism": (f"sets round-robin over {world} GPU(s), "
+                "parallelism": ((f"sets round-robin over {world} GPU(s), "
+                                 if eye is None else
+                                 f"stereo eyes split over rank pairs, sets round-robin over "
+                                 f"{world // 2} pair(s), ")
                                 + ("decoded canvas" if mode == "full" else "eye images")
                                 + " gathered to rank 0"),
             },

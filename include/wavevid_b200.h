@@ -116,6 +116,12 @@ typedef struct wv_frame_args {
                                      pointer, same layout as d_payload) */
   uint32_t* d_fetched;            /* WV_FLAG_FETCH: NB-bit bitmap, records of block b are in
                                      d_payload; zero it when d_payload is (re)filled */
+  int32_t out_row0, out_row1;     /* output pixel rows this call must produce, half open
+                                     (0, 0 = the whole frame).  A stereo eye split
+                                     ([0, H/2) or [H/2, H)) synthesises only the tiles those
+                                     rows depend on; its pixels and footprint inside the rows
+                                     equal a whole-frame decode's.  Masks, block selection,
+                                     K2 and the stats are unchanged. */
 } wv_frame_args;
 
 /* One perspective view (projection.py:111-172). */

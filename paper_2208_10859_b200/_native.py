@@ -69,7 +69,8 @@ class FrameArgs(C.Structure):
                 ("d_extrema", C.c_void_p), ("d_set_loaded", C.c_void_p),
                 ("d_set_bytes", C.c_void_p), ("d_canvas", C.c_void_p),
                 ("d_footprint", C.c_void_p), ("d_result", C.c_void_p),
-                ("h_payload", C.c_void_p), ("d_fetched", C.c_void_p)]
+                ("h_payload", C.c_void_p), ("d_fetched", C.c_void_p),
+                ("out_row0", C.c_int32), ("out_row1", C.c_int32)]
 
 
 class ViewArgs(C.Structure):

@@ -845,7 +845,11 @@ __global__ void __launch_bounds__(256) k_tiles1(TileArgs a) {
   if (t < nt1) {
     const int ty = t / a.ntx[1], tx = t % a.ntx[1];
     nd = a.full != 0;
-    if (!nd) {
+    const int ro0 = a.fa->out_row0, ro1 = a.fa->out_row1;
+    const bool in_rows = ro1 <= ro0 || (ty * OUT_H < ro1 && min((ty + 1) * OUT_H, a.H) > ro0);
+    if (!in_rows) {
+      nd = false;
+    } else if (!nd) {
       const int y0 = ty * OUT_H, y1 = min(y0 + OUT_H, a.H);
       const int c0 = tx * OUT_W, c1 = min(c0 + OUT_W, a.W);
       const uint32_t m0 = a.rowmap[y0], m1 = a.rowmap[y1 - 1];

@@ -479,7 +479,7 @@ class DecodeSession:
 
     def _launch(self, frame: int, mode: str, mask=None, schedule=None,
                 account_only: bool = False, time_stages: bool = False,
-                views=None, out_dims=None) -> _Pending:
+                views=None, out_dims=None, out_rows=None) -> _Pending:
         self.join_prefetch()
         si, t = self._frame_set(frame)
         if mode != "full":
@@ -500,6 +500,8 @@ class DecodeSession:
             entry, existed, may_evict = self._entry_for(si)
             args.t = t
             args.flags = N.WV_FLAG_ACCOUNT_ONLY if account_only else 0
+            if out_rows is not None:
+                args.out_row0, args.out_row1 = out_rows
             if self.residency == "spans":
                 args.flags |= N.WV_FLAG_FETCH
                 args.h_payload = keep[0].data_ptr()
@@ -634,11 +636,14 @@ class DecodeSession:
                                                      (h.height // 2, h.height // 2)]
 
     def decode_render_device(self, frame: int, mode: str, mask, pose: CameraPose, out_dims,
-                             out: torch.Tensor, schedule: FoveationSchedule | None = None
-                             ) -> DeviceFrame:
+                             out: torch.Tensor, schedule: FoveationSchedule | None = None,
+                             eye: int | None = None) -> DeviceFrame:
         """Decode + per-eye perspective writeout as one graph replay (the
         throughput path of a viewer).  ``out`` is (views, out_h, out_w, C) u8
-        on the device; coverage is counted in ``uncovered()``."""
+        on the device; coverage is counted in ``uncovered()``.  ``eye`` (0 or
+        1, stereo only): synthesise and render that eye alone (its half of
+        the canvas, out[0]) -- the per-GPU share of a stereo eye split; its
+        pixels and footprint equal the whole-frame decode's."""
         h = self.header
         if mode == "foveated" and schedule is None:
             schedule = FoveationSchedule.default(h.levels)
@@ -649,15 +654,23 @@ class DecodeSession:
             if self._ones_fp is None:
                 self._ones_fp = torch.full_like(self._footprint, -1)
             fp = self._ones_fp
-        key = (fp.data_ptr(), out.data_ptr(), tuple(out.shape))
+        eyes = self._eyes()
+        out_rows = None
+        if eye is not None:
+            if not h.stereo or eye not in (0, 1):
+                raise ValueError("eye must be 0 or 1 for a stereo file")
+            eyes = [eyes[eye]]
+            out_rows = (eyes[0][0], eyes[0][0] + eyes[0][1])
+        key = (fp.data_ptr(), out.data_ptr(), tuple(out.shape), eye)
         views = self._view_cache.get(key)
         if views is None:
             views = [view_args(self._canvas, fp, r0, rows, h.width, h.channels, pose,
-                               out[i], self._uncovered) for i, (r0, rows) in enumerate(self._eyes())]
+                               out[i], self._uncovered) for i, (r0, rows) in enumerate(eyes)]
             self._view_cache[key] = views
         else:
             set_view_pose(views, pose)
-        p = self._launch(frame, mode, mask, schedule, views=views, out_dims=tuple(out_dims))
+        p = self._launch(frame, mode, mask, schedule, views=views, out_dims=tuple(out_dims),
+                         out_rows=out_rows)
         return DeviceFrame(self, p, self._canvas, self._footprint)
 
     def uncovered(self, reset: bool = False) -> int:

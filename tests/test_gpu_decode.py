@@ -551,3 +551,45 @@ def test_direct_cascade_build_matches_reference():
                         os.path.join(root, "tests", "test_gpu_parity.py")],
                        env=env, capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+# ------------------------------------------------------ stereo eye split
+
+@pytest.mark.parametrize("clip", ["golden_stereo", "bench_c3"])
+def test_eye_split_equals_whole_frame(wv, clip):
+    """Each eye decoded alone (out_rows = that eye's half; the per-GPU share
+    of a stereo eye split): its canvas rows, footprint rows and rendered eye
+    image equal the whole-frame decode's, bit for bit, for viewport and
+    foveated frames."""
+    import sys
+    import torch
+    sys.path.insert(0, os.path.join(os.path.dirname(GOLDEN), "..", "scripts"))
+    import make_bench_input as mbi
+    path = (os.path.join(GOLDEN, "golden_stereo.wvv") if clip == "golden_stereo"
+            else mbi.ensure_clip("c3", os.environ.get("WV_BENCH_CACHE", "/tmp/wvb200_bench")))
+    whole = wv.DecodeSession(path)
+    eyes = [wv.DecodeSession(path), wv.DecodeSession(path)]
+    h = whole.header
+    half = h.height // 2
+    R = 200 if clip == "golden_stereo" else 1000
+    outw = torch.empty((2, R, R, h.channels), dtype=torch.uint8, device="cuda")
+    oute = [torch.empty((1, R, R, h.channels), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    for i, (yaw, pitch, mode) in enumerate([(30, 10, "viewport"), (-40, -60, "viewport"),
+                                             (100, 75, "foveated"), (0, 0, "foveated")]):
+        frame = i % h.frame_count
+        pose = wv.CameraPose(yaw=yaw, pitch=pitch)
+        mask = wv.stereo_mask(pose, (h.mask_w, h.mask_h))
+        sc = wv.FoveationSchedule.default(h.levels, 0.4, 0.6) if mode == "foveated" else None
+        whole.decode_render_device(frame, mode, mask, pose, (R, R), outw, schedule=sc)
+        torch.cuda.synchronize()
+        cw, fw = whole._canvas.clone(), whole._footprint.clone()
+        for e in range(2):
+            eyes[e].decode_render_device(frame, mode, mask, pose, (R, R), oute[e], schedule=sc,
+                                         eye=e)
+            torch.cuda.synchronize()
+            rows = slice(e * half, (e + 1) * half)
+            assert torch.equal(eyes[e]._canvas[:, rows], cw[:, rows]), (i, e, "canvas")
+            assert torch.equal(eyes[e]._footprint[rows], fw[rows]), (i, e, "footprint")
+            assert torch.equal(oute[e][0], outw[e]), (i, e, "eye image")
+    for s in [whole] + eyes:
+        s.close()
