@@ -272,6 +272,17 @@ int wv_encode_set(const wv_encode_params* p, const uint8_t* d_frames, const floa
                   uint32_t* d_counts, uint8_t* d_payload, uint64_t payload_capacity,
                   uint64_t* d_num_records, void* stream);
 
+/* Full inverse 2-D CDF 9/7 of a float32 Mallat pyramid (synthesize_2d,
+ * wavelets.py:167-182) with the K3 kernels: d_pyramid and d_out are planar
+ * (C, H, W) float32 device buffers (geometry: width, height, channels,
+ * levels; the other fields only size the workspace), d_result a device
+ * wv_frame_result scratch.  Bit-exact with the reference (same lifting,
+ * columns then rows, one rounding per operation).  Uses the workspace's
+ * coefficient plane, so it must not run concurrently with a decode on the
+ * same workspace. */
+int wv_synthesize_2d(const wv_geometry* g, const float* d_pyramid, float* d_out, void* d_workspace,
+                     void* d_result, void* stream);
+
 /* Views into the workspace for parity tests (no launches). */
 int wv_plane_view(const wv_geometry* g, void* d_workspace, float** d_plane);
 int wv_level_mask_view(const wv_geometry* g, void* d_workspace, int level,

@@ -29,7 +29,7 @@ EXPORTS = ["wv_abi_version", "wv_status_string", "wv_workspace_bytes", "wv_works
            "wv_render_perspective_desc", "wv_file_info_read", "wv_file_set_read",
            "wv_file_payload_read", "wv_decode_stages_desc", "wv_encode_workspace_bytes",
            "wv_encode_payload_capacity", "wv_encode_set", "wv_enqueue_frame",
-           "wv_desc_layout"]
+           "wv_desc_layout", "wv_synthesize_2d"]
 
 
 class Geometry(C.Structure):

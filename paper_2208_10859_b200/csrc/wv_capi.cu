@@ -186,6 +186,28 @@ int wv_enqueue_frame(void* d_desc, const void* h_desc, uint64_t desc_bytes, void
   return WV_OK;
 }
 
+int wv_synthesize_2d(const wv_geometry* g, const float* d_pyramid, float* d_out, void* ws,
+                     void* d_result, void* stream) {
+  Layout lo;
+  int st = build_layout(g, &lo);
+  if (st != WV_OK) return st;
+  if (!d_pyramid || !d_out || !ws || !d_result) return WV_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t* w = (uint8_t*)ws;
+  WV_CUDA(cudaMemcpyAsync(w + lo.plane, d_pyramid, (size_t)lo.C * lo.H * lo.W * 4,
+                          cudaMemcpyDeviceToDevice, s));
+  // a full-frame descriptor: every tile of every level (LevelMaskSet.full)
+  wv_frame_args fa{};
+  fa.mode = WV_MODE_FULL;
+  fa.d_result = (wv_frame_result*)d_result;
+  wv_frame_args* d_fa = (wv_frame_args*)(w + lo.desc);
+  WV_CUDA(cudaMemcpyAsync(d_fa, &fa, sizeof(fa), cudaMemcpyHostToDevice, s));
+  if ((st = launch_select(lo, g, WV_MODE_FULL, 0, d_fa, w, s, WV_STAGE_ROWS | WV_STAGE_TILES)) !=
+      WV_OK)
+    return st;
+  return launch_synthesis_f32(lo, d_fa, w, d_out, s);
+}
+
 int wv_desc_layout(const wv_geometry* g, uint64_t* mask_offset, uint64_t* slot_bytes) {
   Layout lo;
   int st = build_layout(g, &lo);

@@ -194,6 +194,8 @@ int launch_temporal(const Layout& lo, const wv_geometry* g, int mode, const wv_f
                     uint8_t* ws, cudaStream_t s);
 int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* d_fa,
                      uint8_t* ws, cudaStream_t s, int only_level = 0);
+int launch_synthesis_f32(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, float* f32_out,
+                         cudaStream_t s);
 int launch_perspective(const wv_view_args* v, int n, cudaStream_t s);
 int launch_perspective_dev(const wv_view_args* d_views, int n, int max_w, int max_h,
                            int shared_geometry, cudaStream_t s);

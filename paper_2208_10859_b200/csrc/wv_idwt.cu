@@ -615,7 +615,19 @@ static_assert(SEGR % 8 == 0 && TX % SEGR == 0, "segments store 16-pixel chunks i
 constexpr int CBP = CS + CS / 8 + 1;
 __device__ __forceinline__ int cphys(int c) { return c + (c >> 3); }
 constexpr int SLOT_F2 = 2 * SP * CBP;        // float2 per slot: L half then H half
-constexpr int SMEM_S = 2 * SLOT_F2 * 8;      // two slots
+#ifndef WV_K3S_TMA
+#define WV_K3S_TMA 0    // interior units: rows arrive by TMA into a shared ring (producer = thread 0)
+#endif
+#ifndef WV_K3S_RING
+#define WV_K3S_RING 2   // TMA ring slots (8-row groups of the four subbands)
+#endif
+constexpr int TBW = UW + 2 * XPAD;            // 136-float TMA box rows (start ux0 - 4: 16-B aligned)
+constexpr int RING_SLOT = 4 * SP * TBW;       // floats per ring slot
+constexpr int NRING = WV_K3S_TMA ? WV_K3S_RING : 0;
+constexpr int SMEM_S = 2 * SLOT_F2 * 8 + NRING * RING_SLOT * 4;   // column buffers + ring
+struct StripMaps {
+  CUtensorMap ll8, ll4, pl8, pl4;   // LL source / plane, 8- and 4-row boxes of TBW floats
+};
 
 struct StripArgs {
   int k, bh, bw, C, ngx;
@@ -646,13 +658,68 @@ struct StripArgs {
 #define WV_K3S_PF 0     // issue stage s+1's row loads before stage s's row pass
 #endif
 template <bool FINAL>
-__global__ void K3S_BOUNDS k_strip(const StripArgs a) {
+__global__ void K3S_BOUNDS k_strip(const StripArgs a, const __grid_constant__ StripMaps maps) {
   pdl_sync();
-  extern __shared__ __align__(16) float2 sbuf[];
+  extern __shared__ __align__(128) float2 sbuf[];
   const int tid = threadIdx.x;
   const int C = a.C;
   const uint32_t nitems = *a.count * (uint32_t)C;
   const int bh = a.bh, bw = a.bw;
+#if WV_K3S_TMA
+  // TMA ring: groups (warm-up 4 rows, then 4 stages of 8 rows) of every
+  // interior item this CTA serves, in item order; thread 0 issues a group
+  // as soon as a slot is free (after the barrier that ends the column pass
+  // which consumed it), so up to NRING groups are in flight ahead of use
+  float* ring = reinterpret_cast<float*>(sbuf + 2 * SLOT_F2);
+  __shared__ uint64_t rbar[NRING > 0 ? NRING : 1];
+  auto tma_item = [&](uint32_t it, int& c_, int& ay_, int& ux0_) -> bool {
+    const uint32_t iu_ = it / a.divC;
+    c_ = (int)(it - iu_ * C);
+    const uint32_t e_ = a.list[iu_];
+    const uint32_t u_ = e_ & UNIT_IDX;
+    const int uy_ = (int)(u_ / a.divG);
+    ay_ = uy_ * TY;
+    ux0_ = ((int)u_ - uy_ * a.ngx) * UW;
+    return ((e_ >> 24) & 0xFu) && ay_ >= HALO && ay_ + TY + HALO <= bh;
+  };
+  uint32_t p_item = blockIdx.x;   // producer (thread 0): next group to issue
+  int p_g = -2;                   // -2: find the next interior item; -1: warm-up; 0..3: stages
+  uint32_t p_seq = 0, c_seq = 0;  // groups issued / consumed
+  auto issue_next = [&]() {       // thread 0 only
+    if (p_g == -2) {
+      int c_, ay_, ux0_;
+      while (p_item < nitems && !tma_item(p_item, c_, ay_, ux0_)) p_item += gridDim.x;
+      if (p_item >= nitems) return;
+      p_g = -1;
+    }
+    int c_, ay_, ux0_;
+    tma_item(p_item, c_, ay_, ux0_);
+    const int slot = (int)(p_seq % NRING);
+    const int x0 = max(ux0_ - XPAD, 0);
+    const int rows = p_g < 0 ? 4 : SP;
+    const int y = p_g < 0 ? ay_ - HALO : ay_ + HALO + SP * p_g;
+    const CUtensorMap* mll = p_g < 0 ? &maps.ll4 : &maps.ll8;
+    const CUtensorMap* mpl = p_g < 0 ? &maps.pl4 : &maps.pl8;
+    float* dst = ring + slot * RING_SLOT;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&rbar[slot], 4u * rows * TBW * 4u);
+    tma_load_3d(dst, mll, x0, y, c_, &rbar[slot]);
+    tma_load_3d(dst + SP * TBW, mpl, bw + x0, y, c_, &rbar[slot]);
+    tma_load_3d(dst + 2 * SP * TBW, mpl, x0, bh + y, c_, &rbar[slot]);
+    tma_load_3d(dst + 3 * SP * TBW, mpl, bw + x0, bh + y, c_, &rbar[slot]);
+    ++p_seq;
+    if (++p_g == 4) {
+      p_g = -2;
+      p_item += gridDim.x;
+    }
+  };
+  if (tid == 0) {
+    for (int i = 0; i < NRING; ++i) mbar_init(&rbar[i], 1);
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int i = 0; i < NRING; ++i) issue_next();
+#endif
   const int OH = 2 * bh, OW = 2 * bw;   // output (level k-1) dims
   uint8_t* canvas = FINAL ? a.fa->d_canvas : nullptr;
   // this thread's column stream: tid < UW -> unit column tid; UW..UW+3 -> halo
@@ -708,11 +775,33 @@ __global__ void K3S_BOUNDS k_strip(const StripArgs a) {
 #if WV_K3S_PF
     float2 ps[SP], pd[SP];   // the next stage's rows
 #endif
+#if WV_K3S_TMA
+    const int tx0 = max(ux0 - XPAD, 0);
+    // column xcol of ring row r of the slot's subband q
+    auto ring_at = [&](const float* slotp, int q, int r) -> float {
+      return slotp[q * SP * TBW + r * TBW + (xcol - tx0)];
+    };
+    const float* wslot = nullptr;
+    if (interior) {
+      const int slot = (int)(c_seq % NRING);
+      mbar_wait(&rbar[slot], (c_seq / NRING) & 1u);
+      wslot = ring + slot * RING_SLOT;
+      ++c_seq;
+    }
+#endif
     if (interior && cact) {
       // warm-up: rows ay-2 .. ay+1 (lift_interior inputs 0..3, nothing emitted)
       float2 s[4], d[4];
+#if WV_K3S_TMA
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        s[q] = make_float2(ring_at(wslot, 0, q), ring_at(wslot, 1, q));
+        d[q] = make_float2(ring_at(wslot, 2, q), ring_at(wslot, 3, q));
+      }
+#else
 #pragma unroll
       for (int q = 0; q < 4; ++q) ldrow(ay - HALO + q, s[q], d[q]);
+#endif
 #if WV_K3S_PF
 #pragma unroll
       for (int q = 0; q < SP; ++q) ldrow(ay + HALO + q, ps[q], pd[q]);
@@ -753,12 +842,27 @@ __global__ void K3S_BOUNDS k_strip(const StripArgs a) {
         for (int rr = 0; rr < 2; ++rr)
           rq[rr] = a.R[(uint64_t)a.rowmap[2 * rp + rr] * a.wpr0 + ((2 * xa) >> 5)];
       }
+#if WV_K3S_TMA
+      const float* sslot = nullptr;   // this stage's ring slot (every thread waits: uniform)
+      if (interior) {
+        const int slot = (int)(c_seq % NRING);
+        mbar_wait(&rbar[slot], (c_seq / NRING) & 1u);
+        sslot = ring + slot * RING_SLOT;
+        ++c_seq;
+      }
+#endif
       if (cact) {
         const int lc = cphys(cl);
         if (interior) {
           // rows pa+2 .. pa+9 -> pairs pa .. pa+7 (lift_interior inputs 4+8st ..)
           float2 s[SP], d[SP];
-#if WV_K3S_PF
+#if WV_K3S_TMA
+#pragma unroll
+          for (int q = 0; q < SP; ++q) {
+            s[q] = make_float2(ring_at(sslot, 0, q), ring_at(sslot, 1, q));
+            d[q] = make_float2(ring_at(sslot, 2, q), ring_at(sslot, 3, q));
+          }
+#elif WV_K3S_PF
 #pragma unroll
           for (int q = 0; q < SP; ++q) {
             s[q] = ps[q];
@@ -799,6 +903,13 @@ __global__ void K3S_BOUNDS k_strip(const StripArgs a) {
         }
       }
       __syncthreads();
+#if WV_K3S_TMA
+      // the slots this column pass consumed (stage 0: the warm-up group too) are free
+      if (interior && tid == 0) {
+        issue_next();
+        if (st == 0) issue_next();
+      }
+#endif
       // row pass: row pair rp, pairs [xa, xb) along x
       if (ract) {
         const float2* rowL = colL + ri * CBP;
@@ -908,12 +1019,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
   return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
 }
 
-int make_map(CUtensorMap* m, const float* base, int cols, int rows, int pitch, int chans) {
+int make_map(CUtensorMap* m, const float* base, int cols, int rows, int pitch, int chans,
+             int box_w = BOX_W, int box_h = BOX_H) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = get_encoder();  // immutable after init
   if (!enc) return WV_ERR_CUDA;
   cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)chans};
   cuuint64_t strides[2] = {(cuuint64_t)pitch * 4, (cuuint64_t)pitch * 4 * rows};
-  cuuint32_t box[3] = {BOX_W, BOX_H, 1};
+  cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -923,7 +1035,7 @@ int make_map(CUtensorMap* m, const float* base, int cols, int rows, int pitch, i
 
 // one level with the per-tile TMA-box kernel (k_level)
 int launch_tiles(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStream_t s, int k,
-                 int sms) {
+                 int sms, float* f32_out = nullptr) {
   const int L = lo.L, C = lo.C;
   float* plane = (float*)(ws + lo.plane);
   const uint32_t* counters = (const uint32_t*)(ws + lo.counters);
@@ -959,9 +1071,11 @@ int launch_tiles(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStr
   la.list = (const uint32_t*)(ws + lo.tlist[k]);
   la.count = counters + CNT_TILES + k;
   const int ntiles = lo.nty[k] * lo.ntx[k];
-  if (k > 1) {
-    la.out = (float*)(ws + lo.ybuf[k - 1]);
-    la.out_pitch = lo.ypitch[k - 1];
+  if (k > 1 || f32_out) {
+    // mid levels into the next level's LL buffer; with f32_out level 1 too
+    // (wv_synthesize_2d: a float32 frame instead of the u8 canvas)
+    la.out = k > 1 ? (float*)(ws + lo.ybuf[k - 1]) : f32_out;
+    la.out_pitch = k > 1 ? lo.ypitch[k - 1] : lo.W;
     const int grid = max(1, min(ntiles * C, sms * occ_mid));
     WV_CUDA(launch_k(k_level<false>, dim3(grid), dim3(NTHREADS), (size_t)SMEM_MID, s, tm_ll,
                      tm_plane, la));
@@ -979,7 +1093,7 @@ int launch_tiles(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStr
 }
 
 #ifndef WV_K3_STRIP
-#define WV_K3_STRIP 1   // strip-streaming synthesis (k_strip) for levels whose subband has at
+#define WV_K3_STRIP 0   // strip-streaming synthesis (k_strip) for levels whose subband has at
                         // least WV_K3_STRIP_MIN coefficients; per-tile TMA boxes (k_level) below
 #endif
 #ifndef WV_K3_STRIP_MIN
@@ -1009,6 +1123,17 @@ int launch_strips(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaSt
       continue;
     }
     StripArgs a{};
+    StripMaps maps{};
+    if (WV_K3S_TMA) {
+      const float* llb = k < L ? (const float*)(ws + lo.ybuf[k]) : plane;
+      const int llc = k < L ? lo.W >> k : lo.W, llr = k < L ? lo.H >> k : lo.H;
+      const int llp = k < L ? lo.ypitch[k] : lo.W;
+      if (make_map(&maps.ll8, llb, llc, llr, llp, C, TBW, SP) != WV_OK ||
+          make_map(&maps.ll4, llb, llc, llr, llp, C, TBW, 4) != WV_OK ||
+          make_map(&maps.pl8, plane, lo.W, lo.H, lo.W, C, TBW, SP) != WV_OK ||
+          make_map(&maps.pl4, plane, lo.W, lo.H, lo.W, C, TBW, 4) != WV_OK)
+        return WV_ERR_CUDA;
+    }
     a.k = k; a.bh = lo.H >> k; a.bw = lo.W >> k; a.C = C; a.ngx = lo.ngx[k];
     a.divC = fast_div((uint32_t)C);
     a.divG = fast_div((uint32_t)lo.ngx[k]);
@@ -1023,14 +1148,14 @@ int launch_strips(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaSt
       a.out = (float*)(ws + lo.ybuf[k - 1]);
       a.out_pitch = lo.ypitch[k - 1];
       const int grid = max(1, min(items, sms * occ_mid));
-      WV_CUDA(launch_k(k_strip<false>, dim3(grid), dim3(S_THREADS), (size_t)SMEM_S, s, a));
+      WV_CUDA(launch_k(k_strip<false>, dim3(grid), dim3(S_THREADS), (size_t)SMEM_S, s, a, maps));
     } else {
       a.fa = fa;
       a.R = (const uint32_t*)(ws + lo.mrows);
       a.rowmap = (const uint32_t*)(ws + lo.rowmap);
       a.wpr0 = lo.wpr_[0];
       const int grid = max(1, min(items, sms * occ_fin));
-      WV_CUDA(launch_k(k_strip<true>, dim3(grid), dim3(S_THREADS), (size_t)SMEM_S, s, a));
+      WV_CUDA(launch_k(k_strip<true>, dim3(grid), dim3(S_THREADS), (size_t)SMEM_S, s, a, maps));
     }
     WV_CUDA(cudaGetLastError());
   }
@@ -1055,6 +1180,20 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
   }
   return WV_OK;
 #endif
+}
+
+// Full-frame float32 synthesis of a Mallat pyramid already in the plane
+// (wv_synthesize_2d): the per-tile kernel for every level, level 1 into f32_out.
+int launch_synthesis_f32(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, float* f32_out,
+                         cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int k = lo.L; k >= 1; --k) {
+    const int st = launch_tiles(lo, fa, ws, s, k, sms, k == 1 ? f32_out : nullptr);
+    if (st != WV_OK) return st;
+  }
+  return WV_OK;
 }
 
 }  // namespace wv

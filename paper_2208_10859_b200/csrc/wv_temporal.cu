@@ -97,7 +97,7 @@ __device__ __forceinline__ int tweight(int ti, int t, int n) {
 #endif
 constexpr int K2_THREADS = WV_K2_THREADS;
 #ifndef WV_K2_STAGED
-#define WV_K2_STAGED 1   // staged K2 (k_temporal_staged) where the geometry allows
+#define WV_K2_STAGED 0   // staged K2 (k_temporal_staged) where the geometry allows
 #endif
 constexpr int K2_MAXN = 32;
 

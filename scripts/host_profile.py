@@ -1,13 +1,16 @@
 """Host-side cost of one decode_render_device call (the bench's headline
-path): cProfile over N frames after warm-up.  Run on the GPU box:
+path), isolated from GPU time: a small stereo file (tests/golden/
+golden_stereo.wvv, so the kernels are short), cProfile over N frames after
+warm-up, plus the unprofiled wall time per frame.  Run on the GPU box:
     python scripts/host_profile.py [N]"""
 import cProfile
+import os
 import pstats
 import sys
 import time
 
-sys.path.insert(0, ".")
-import bench  # noqa: E402
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_2208_10859_b200 as wv  # noqa: E402
@@ -15,29 +18,31 @@ import paper_2208_10859_b200 as wv  # noqa: E402
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 400
-    path = bench.input_path(type("A", (), {"cache_dir": "/tmp/wvb200_bench", "size": 8192})(), 2)
-    import os
-    if not os.path.exists(path):
-        bench.make_input(path, 8192, 2, torch.device("cuda"))
-    s = wv.DecodeSession(path)
+    s = wv.DecodeSession(os.path.join(ROOT, "tests", "golden", "golden_stereo.wvv"))
+    s.time_stages = False
     h = s.header
-    frames = list(range(h.frame_count))
-    pm = bench.poses_and_masks(h, frames)
-    out = torch.empty((2, bench.OUT_H, bench.OUT_W, 3), dtype=torch.uint8, device="cuda")
-    for i in range(20):
-        f = frames[i % len(frames)]
-        s.decode_render_device(f, "viewport", pm[f][1], pm[f][0], (bench.OUT_W, bench.OUT_H), out)
+    poses = [wv.CameraPose(yaw=-60 + 0.5 * i, pitch=10) for i in range(64)]
+    masks = [wv.stereo_mask(p, (h.mask_w, h.mask_h)) for p in poses]
+    out = torch.empty((2, 256, 256, 3), dtype=torch.uint8, device="cuda")
+
+    def run(k):
+        for i in range(k):
+            s.decode_render_device(i % h.frame_count, "viewport", masks[i % 64], poses[i % 64],
+                                   (256, 256), out)
+
+    run(80)
     torch.cuda.synchronize()
     t = time.perf_counter()
+    run(n)
+    host = (time.perf_counter() - t) / n * 1e6
+    torch.cuda.synchronize()
+    print(f"{host:.1f} us/frame host enqueue (unprofiled)")
     pr = cProfile.Profile()
     pr.enable()
-    for i in range(n):
-        f = frames[i % len(frames)]
-        s.decode_render_device(f, "viewport", pm[f][1], pm[f][0], (bench.OUT_W, bench.OUT_H), out)
+    run(n)
     pr.disable()
     torch.cuda.synchronize()
-    print(f"{(time.perf_counter() - t) / n * 1e6:.1f} us/frame wall (profiled)")
-    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+    pstats.Stats(pr).sort_stats("tottime").print_stats(22)
 
 
 if __name__ == "__main__":
