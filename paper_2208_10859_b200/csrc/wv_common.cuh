@@ -23,12 +23,6 @@ constexpr int BOX_H = TY + 2 * HALO;
 constexpr int OUT_H = 2 * TY;
 constexpr int OUT_W = 2 * TX;
 constexpr uint32_t ZERO_FLAG = 0x80000000u;  // work-list entry: zero-fill only
-// K3 strip units: UNIT_T horizontally adjacent synthesis tiles (one tile row
-// high).  Unit-list entry: bits 0-23 unit index (row-major over the level's
-// unit grid), 24-27 tiles of the unit that are needed, 28-31 level-1 tiles
-// that left the request (canvas cleared there).
-constexpr int UNIT_T = 4;
-constexpr uint32_t UNIT_IDX = 0x00FFFFFFu;
 constexpr int DIL = 4;                // WaveletKind.CDF97.half_width (wavelets.py:30-32)
 
 __host__ __device__ inline int wpr(int cols) { return (cols + 31) >> 5; }
@@ -53,9 +47,6 @@ struct Layout {
   uint64_t need[WV_MAX_LEVELS + 1];      // u8 per tile
   uint64_t prev_need;                    // level 1, u8 per tile
   uint64_t tlist[WV_MAX_LEVELS + 1];     // u32 per tile
-  int ngx[WV_MAX_LEVELS + 1];            // K3 units per tile row: ceil(ntx / UNIT_T)
-  uint64_t ulist[WV_MAX_LEVELS + 1];     // u32 per unit (K3 strip work list)
-  uint64_t clear1;                       // level-1 tiles that left the request: bit rows like need[1]
   uint64_t counters;                     // u32[64]
   uint64_t desc;                         // device wv_frame_args + 4 wv_view_args + mask bytes
   uint64_t desc_mask, desc_bytes;        // mask offset inside the slot, slot size
@@ -67,8 +58,7 @@ struct Layout {
 };
 
 // counter slots
-enum { CNT_BLOCKS = 0, CNT_TILES = 1 /* + level */, CNT_UNITS = 16 /* + level */,
-       CNT_FETCH = 40 };
+enum { CNT_BLOCKS = 0, CNT_TILES = 1 /* + level */, CNT_FETCH = 40 };
 
 inline int build_layout(const wv_geometry* g, Layout* o) {
   if (!g || !o) return WV_ERR_ARG;
@@ -111,10 +101,7 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
     // level 1: need bits (rows of tiles); other levels unused
     o->need[k] = take(k == 1 ? uint64_t(o->nty[1]) * wpr(o->ntx[1]) * 4 : 4);
     o->tlist[k] = take(nt * 4 * (k == 1 ? 2 : 1));
-    o->ngx[k] = cdiv(o->ntx[k], UNIT_T);
-    o->ulist[k] = take(uint64_t(o->nty[k]) * o->ngx[k] * 4);
   }
-  o->clear1 = take(uint64_t(o->nty[1]) * wpr(o->ntx[1]) * 4);
   o->prev_need = take(uint64_t(o->nty[1]) * o->ntx[1]);
   o->counters = take(64 * 4);
   o->desc_mask = (sizeof(wv_frame_args) + 4 * sizeof(wv_view_args) + 15) & ~size_t(15);

@@ -581,435 +581,6 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   }
 }
 
-// ------------------------------------------------------------- K3 strips
-// Strip-streaming synthesis (default).  Work item = (unit, channel): a unit
-// is UNIT_T = 4 horizontally adjacent tiles of one tile row, i.e. 32
-// coefficient rows x 128 coefficient columns of each subband (256 x 64
-// outputs).  Column pass: one thread per coefficient column (the unit's 128
-// plus 2 halo columns per side) streams DOWN the 32 rows, the lifting state
-// carried in registers from row to row, so rows are read once (no vertical
-// halo re-reads except the 2+2 rows at the unit's top and bottom) and the
-// loads are warp-coalesced 128-B rows of each subband, batched 8 rows at a
-// time (32 independent loads in flight per thread).  Every 8 output row
-// pairs (one stage) the column results go to a double-buffered shared
-// column buffer and the row pass lifts them along x (8-pair segments, their
-// 2-column halos read from the neighbouring segments' entries), then writes
-// f32 (mid levels) or request-masked u8 (level 1) with 16-byte stores.
-// Same arithmetic as k_level (lift_interior / lift_line, paired RN f32 ops,
-// no FMA), so results are bit-identical.
-constexpr int UW = UNIT_T * TX;              // 128 coefficient columns per unit
-constexpr int CS = UW + 2 * HALO;            // 132 column streams
-constexpr int SP = 8;                        // output row pairs per stage
-#ifndef WV_K3S_SEGR
-#define WV_K3S_SEGR 8
-#endif
-constexpr int SEGR = WV_K3S_SEGR;            // row-pass segment (output pairs)
-constexpr int RSEGS = UW / SEGR;
-constexpr int ROW_THREADS = SP * RSEGS;
-constexpr int S_THREADS = 160;
-static_assert(S_THREADS >= CS && S_THREADS >= ROW_THREADS, "one thread per stream");
-static_assert(SEGR % 8 == 0 && TX % SEGR == 0, "segments store 16-pixel chunks inside one tile");
-// column-buffer row: local column c (0..CS-1, c = x - ux0 + 2) sits at c + c/8
-// (one float2 of padding per 8 columns: the row pass's 16 segment streams of
-// a half-warp then hit 16 distinct bank pairs)
-constexpr int CBP = CS + CS / 8 + 1;
-__device__ __forceinline__ int cphys(int c) { return c + (c >> 3); }
-constexpr int SLOT_F2 = 2 * SP * CBP;        // float2 per slot: L half then H half
-#ifndef WV_K3S_TMA
-#define WV_K3S_TMA 0    // interior units: rows arrive by TMA into a shared ring (producer = thread 0)
-#endif
-#ifndef WV_K3S_RING
-#define WV_K3S_RING 2   // TMA ring slots (8-row groups of the four subbands)
-#endif
-constexpr int TBW = UW + 2 * XPAD;            // 136-float TMA box rows (start ux0 - 4: 16-B aligned)
-constexpr int RING_SLOT = 4 * SP * TBW;       // floats per ring slot
-constexpr int NRING = WV_K3S_TMA ? WV_K3S_RING : 0;
-constexpr int SMEM_S = 2 * SLOT_F2 * 8 + NRING * RING_SLOT * 4;   // column buffers + ring
-struct StripMaps {
-  CUtensorMap ll8, ll4, pl8, pl4;   // LL source / plane, 8- and 4-row boxes of TBW floats
-};
-
-struct StripArgs {
-  int k, bh, bw, C, ngx;
-  FastDiv divC, divG;
-  const uint32_t* list;
-  const uint32_t* count;
-  const float* ll;     // LL band: C x ll_rows x ll_pitch (the plane for k = L)
-  int ll_pitch, ll_rows;
-  const float* plane;  // detail bands: planar C x H x W
-  int W, H;
-  float* out;          // mid levels: C x 2bh x out_pitch
-  int out_pitch;
-  const wv_frame_args* fa;  // level 1: fa->d_canvas, planar C x H x W u8
-  const uint32_t* R;
-  const uint32_t* rowmap;
-  int wpr0;
-};
-
-#ifndef WV_K3S_MINB
-#define WV_K3S_MINB 0   // > 0: __launch_bounds__ min blocks per SM (register cap)
-#endif
-#if WV_K3S_MINB > 0
-#define K3S_BOUNDS __launch_bounds__(S_THREADS, WV_K3S_MINB)
-#else
-#define K3S_BOUNDS __launch_bounds__(S_THREADS)
-#endif
-#ifndef WV_K3S_PF
-#define WV_K3S_PF 0     // issue stage s+1's row loads before stage s's row pass
-#endif
-template <bool FINAL>
-__global__ void K3S_BOUNDS k_strip(const StripArgs a, const __grid_constant__ StripMaps maps) {
-  pdl_sync();
-  extern __shared__ __align__(128) float2 sbuf[];
-  const int tid = threadIdx.x;
-  const int C = a.C;
-  const uint32_t nitems = *a.count * (uint32_t)C;
-  const int bh = a.bh, bw = a.bw;
-#if WV_K3S_TMA
-  // TMA ring: groups (warm-up 4 rows, then 4 stages of 8 rows) of every
-  // interior item this CTA serves, in item order; thread 0 issues a group
-  // as soon as a slot is free (after the barrier that ends the column pass
-  // which consumed it), so up to NRING groups are in flight ahead of use
-  float* ring = reinterpret_cast<float*>(sbuf + 2 * SLOT_F2);
-  __shared__ uint64_t rbar[NRING > 0 ? NRING : 1];
-  auto tma_item = [&](uint32_t it, int& c_, int& ay_, int& ux0_) -> bool {
-    const uint32_t iu_ = it / a.divC;
-    c_ = (int)(it - iu_ * C);
-    const uint32_t e_ = a.list[iu_];
-    const uint32_t u_ = e_ & UNIT_IDX;
-    const int uy_ = (int)(u_ / a.divG);
-    ay_ = uy_ * TY;
-    ux0_ = ((int)u_ - uy_ * a.ngx) * UW;
-    return ((e_ >> 24) & 0xFu) && ay_ >= HALO && ay_ + TY + HALO <= bh;
-  };
-  uint32_t p_item = blockIdx.x;   // producer (thread 0): next group to issue
-  int p_g = -2;                   // -2: find the next interior item; -1: warm-up; 0..3: stages
-  uint32_t p_seq = 0, c_seq = 0;  // groups issued / consumed
-  auto issue_next = [&]() {       // thread 0 only
-    if (p_g == -2) {
-      int c_, ay_, ux0_;
-      while (p_item < nitems && !tma_item(p_item, c_, ay_, ux0_)) p_item += gridDim.x;
-      if (p_item >= nitems) return;
-      p_g = -1;
-    }
-    int c_, ay_, ux0_;
-    tma_item(p_item, c_, ay_, ux0_);
-    const int slot = (int)(p_seq % NRING);
-    const int x0 = max(ux0_ - XPAD, 0);
-    const int rows = p_g < 0 ? 4 : SP;
-    const int y = p_g < 0 ? ay_ - HALO : ay_ + HALO + SP * p_g;
-    const CUtensorMap* mll = p_g < 0 ? &maps.ll4 : &maps.ll8;
-    const CUtensorMap* mpl = p_g < 0 ? &maps.pl4 : &maps.pl8;
-    float* dst = ring + slot * RING_SLOT;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&rbar[slot], 4u * rows * TBW * 4u);
-    tma_load_3d(dst, mll, x0, y, c_, &rbar[slot]);
-    tma_load_3d(dst + SP * TBW, mpl, bw + x0, y, c_, &rbar[slot]);
-    tma_load_3d(dst + 2 * SP * TBW, mpl, x0, bh + y, c_, &rbar[slot]);
-    tma_load_3d(dst + 3 * SP * TBW, mpl, bw + x0, bh + y, c_, &rbar[slot]);
-    ++p_seq;
-    if (++p_g == 4) {
-      p_g = -2;
-      p_item += gridDim.x;
-    }
-  };
-  if (tid == 0) {
-    for (int i = 0; i < NRING; ++i) mbar_init(&rbar[i], 1);
-  }
-  __syncthreads();
-  if (tid == 0)
-    for (int i = 0; i < NRING; ++i) issue_next();
-#endif
-  const int OH = 2 * bh, OW = 2 * bw;   // output (level k-1) dims
-  uint8_t* canvas = FINAL ? a.fa->d_canvas : nullptr;
-  // this thread's column stream: tid < UW -> unit column tid; UW..UW+3 -> halo
-  const int cl = tid < UW ? tid + HALO : (tid - UW < HALO ? tid - UW : tid - UW + UW);
-  // row-pass role
-  const int sg = tid % RSEGS, ri = tid / RSEGS;
-
-  for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const uint32_t iu = item / a.divC;
-    const int c = (int)(item - iu * C);
-    const uint32_t entry = a.list[iu];
-    const uint32_t unit = entry & UNIT_IDX;
-    const uint32_t need = (entry >> 24) & 0xFu, clr = entry >> 28;
-    const int uy = (int)(unit / a.divG), ug = (int)unit - uy * a.ngx;
-    const int ay = uy * TY, ux0 = ug * UW;
-    const int by = min(ay + TY, bh), ux1 = min(ux0 + UW, bw);
-    if (FINAL && clr) {
-      // tiles that left the request: clear what an earlier frame wrote there
-      for (int t = 0; t < UNIT_T; ++t) {
-        if (!((clr >> t) & 1u)) continue;
-        const int tx0 = ux0 + t * TX;
-        if (tx0 >= bw) break;
-        const int nx = 2 * (min(tx0 + TX, bw) - tx0), ny = 2 * (by - ay), qw = nx >> 2;
-        for (int idx = tid; idx < ny * qw; idx += S_THREADS) {
-          const int r = idx / qw, q = idx - (idx / qw) * qw;
-          *reinterpret_cast<uint32_t*>(canvas + ((uint64_t)c * OH + 2 * ay + r) * OW + 2 * tx0 +
-                                       4 * q) = 0u;
-        }
-      }
-    }
-    if (!need) continue;   // uniform across the CTA
-    const int nst = (by - ay + SP - 1) / SP;
-    const bool interior = ay >= HALO && ay + TY + HALO <= bh;
-    // column stream
-    const int xcol = ux0 - HALO + cl;
-    const bool cact = tid < CS && xcol >= max(ux0 - HALO, 0) && xcol < min(ux1 + HALO, bw);
-    const float* pLL = a.ll + ((uint64_t)c * a.ll_rows) * a.ll_pitch + xcol;
-    const float* pLH = a.plane + ((uint64_t)c * a.H + bh) * a.W + xcol;
-    const float* pHL = a.plane + ((uint64_t)c * a.H) * a.W + bw + xcol;
-    const float* pHH = pLH + bw;
-    const size_t lp = a.ll_pitch, pp = a.W;
-    auto ldrow = [&](int r, float2& s, float2& d) {
-      s = make_float2(__ldg(pLL + r * lp), __ldg(pHL + r * pp));
-      d = make_float2(__ldg(pLH + r * pp), __ldg(pHH + r * pp));
-    };
-    const float2 KS = f2(__uint_as_float(0x3f9d7658u));
-    const float2 IK = f2(__uint_as_float(0x3f5019c3u));
-    const float2 ND = f2(-__uint_as_float(0x3ee31355u));
-    const float2 NG = f2(-__uint_as_float(0x3f620676u));
-    const float2 NB = f2(-__uint_as_float(0xbd5901aeu));
-    const float2 NA = f2(-__uint_as_float(0xbfcb0673u));
-    float2 d1m, s2m, d2mm, s3mm;
-#if WV_K3S_PF
-    float2 ps[SP], pd[SP];   // the next stage's rows
-#endif
-#if WV_K3S_TMA
-    const int tx0 = max(ux0 - XPAD, 0);
-    // column xcol of ring row r of the slot's subband q
-    auto ring_at = [&](const float* slotp, int q, int r) -> float {
-      return slotp[q * SP * TBW + r * TBW + (xcol - tx0)];
-    };
-    const float* wslot = nullptr;
-    if (interior) {
-      const int slot = (int)(c_seq % NRING);
-      mbar_wait(&rbar[slot], (c_seq / NRING) & 1u);
-      wslot = ring + slot * RING_SLOT;
-      ++c_seq;
-    }
-#endif
-    if (interior && cact) {
-      // warm-up: rows ay-2 .. ay+1 (lift_interior inputs 0..3, nothing emitted)
-      float2 s[4], d[4];
-#if WV_K3S_TMA
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        s[q] = make_float2(ring_at(wslot, 0, q), ring_at(wslot, 1, q));
-        d[q] = make_float2(ring_at(wslot, 2, q), ring_at(wslot, 3, q));
-      }
-#else
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ldrow(ay - HALO + q, s[q], d[q]);
-#endif
-#if WV_K3S_PF
-#pragma unroll
-      for (int q = 0; q < SP; ++q) ldrow(ay + HALO + q, ps[q], pd[q]);
-#endif
-      d1m = dscale(d[0], IK);
-      s2m = __fmul2_rn(s[0], KS);
-      float2 d1 = dscale(d[1], IK);
-      float2 s2 = lstep(__fmul2_rn(s[1], KS), ND, d1m, d1);
-      d2mm = lstep(d1m, NG, s2m, s2);
-      s3mm = s2;
-      d1m = d1;
-      s2m = s2;
-#pragma unroll
-      for (int q = 2; q < 4; ++q) {
-        d1 = dscale(d[q], IK);
-        s2 = lstep(__fmul2_rn(s[q], KS), ND, d1m, d1);
-        const float2 d2 = lstep(d1m, NG, s2m, s2);
-        const float2 s3 = lstep(s2m, NB, d2mm, d2);
-        d2mm = d2;
-        s3mm = s3;
-        d1m = d1;
-        s2m = s2;
-      }
-    }
-    for (int st = 0; st < nst; ++st) {
-      float2* colL = sbuf + (st & 1) * SLOT_F2;
-      float2* colH = colL + SP * CBP;
-      const int pa = ay + SP * st, pb = min(pa + SP, by);
-      // level 1: this thread's request-mask words of the stage (two dependent
-      // loads), issued before the column work so their latency hides there
-      const int xa = ux0 + sg * SEGR, xb = min(xa + SEGR, ux1);
-      const int rp = pa + ri;   // coefficient row pair of this row-pass thread
-      const bool ract = tid < ROW_THREADS && rp < pb && xa < xb &&
-                        ((need >> ((sg * SEGR) / TX)) & 1u);
-      uint32_t rq[2] = {0u, 0u};
-      if (FINAL && ract) {
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr)
-          rq[rr] = a.R[(uint64_t)a.rowmap[2 * rp + rr] * a.wpr0 + ((2 * xa) >> 5)];
-      }
-#if WV_K3S_TMA
-      const float* sslot = nullptr;   // this stage's ring slot (every thread waits: uniform)
-      if (interior) {
-        const int slot = (int)(c_seq % NRING);
-        mbar_wait(&rbar[slot], (c_seq / NRING) & 1u);
-        sslot = ring + slot * RING_SLOT;
-        ++c_seq;
-      }
-#endif
-      if (cact) {
-        const int lc = cphys(cl);
-        if (interior) {
-          // rows pa+2 .. pa+9 -> pairs pa .. pa+7 (lift_interior inputs 4+8st ..)
-          float2 s[SP], d[SP];
-#if WV_K3S_TMA
-#pragma unroll
-          for (int q = 0; q < SP; ++q) {
-            s[q] = make_float2(ring_at(sslot, 0, q), ring_at(sslot, 1, q));
-            d[q] = make_float2(ring_at(sslot, 2, q), ring_at(sslot, 3, q));
-          }
-#elif WV_K3S_PF
-#pragma unroll
-          for (int q = 0; q < SP; ++q) {
-            s[q] = ps[q];
-            d[q] = pd[q];
-          }
-          if (st + 1 < nst) {
-#pragma unroll
-            for (int q = 0; q < SP; ++q) ldrow(pa + SP + HALO + q, ps[q], pd[q]);
-          }
-#else
-#pragma unroll
-          for (int q = 0; q < SP; ++q) ldrow(pa + HALO + q, s[q], d[q]);
-#endif
-#pragma unroll
-          for (int q = 0; q < SP; ++q) {
-            const float2 d1 = dscale(d[q], IK);
-            const float2 s2 = lstep(__fmul2_rn(s[q], KS), ND, d1m, d1);
-            const float2 d2 = lstep(d1m, NG, s2m, s2);
-            const float2 s3 = lstep(s2m, NB, d2mm, d2);
-            const float2 d3 = lstep(d2mm, NA, s3mm, s3);
-            colL[q * CBP + lc] = make_float2(s3mm.x, d3.x);
-            colH[q * CBP + lc] = make_float2(s3mm.y, d3.y);
-            d2mm = d2;
-            s3mm = s3;
-            d1m = d1;
-            s2m = s2;
-          }
-        } else {
-          // level border (symmetric extension) or short level: the stage's
-          // pairs from their own 2-row halo
-          lift_line(
-              max(pa - HALO, 0), min(pb + HALO, bh), bh, pa, pb,
-              [&](int j, float2& s, float2& d) { ldrow(j, s, d); },
-              [&](int p, float2 s3, float2 d3) {
-                colL[(p - pa) * CBP + lc] = make_float2(s3.x, d3.x);
-                colH[(p - pa) * CBP + lc] = make_float2(s3.y, d3.y);
-              });
-        }
-      }
-      __syncthreads();
-#if WV_K3S_TMA
-      // the slots this column pass consumed (stage 0: the warm-up group too) are free
-      if (interior && tid == 0) {
-        issue_next();
-        if (st == 0) issue_next();
-      }
-#endif
-      // row pass: row pair rp, pairs [xa, xb) along x
-      if (ract) {
-        const float2* rowL = colL + ri * CBP;
-        const float2* rowH = colH + ri * CBP;
-        const int y0 = 2 * rp;
-        if (xa >= HALO && xb + HALO <= bw && xb - xa == SEGR) {
-          const int cb = xa - ux0;   // local column of lift input 0 (x = xa - 2)
-          if (FINAL) {
-            auto cv = [](float v) { return u8_rint(__fmul_rn(v, 255.0f)); };
-            uint32_t w0[SEGR / 2] = {}, w1[SEGR / 2] = {};
-            lift_interior<SEGR>(
-                [&](int j, float2& s, float2& d) {
-                  s = rowL[cphys(cb + j)];
-                  d = rowH[cphys(cb + j)];
-                },
-                [&](int p, float2 s3, float2 d3) {
-                  const int lq = p - HALO;
-                  w0[lq >> 1] |= (cv(s3.x) | (cv(d3.x) << 8)) << (16 * (lq & 1));
-                  w1[lq >> 1] |= (cv(s3.y) | (cv(d3.y) << 8)) << (16 * (lq & 1));
-                });
-            auto bm = [](uint32_t b4) { return ((b4 * 0x00204081u) & 0x01010101u) * 0xFFu; };
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-              const uint32_t* wr = rr ? w1 : w0;
-              uint8_t* crow = canvas + ((uint64_t)c * OH + y0 + rr) * OW;
-#pragma unroll
-              for (int k = 0; k < SEGR / 8; ++k) {
-                const int px = 2 * xa + 16 * k;
-                const uint32_t bits = (rq[rr] >> (px & 31)) & 0xFFFFu;
-                const uint4 v = make_uint4(wr[4 * k] & bm(bits & 0xFu),
-                                           wr[4 * k + 1] & bm((bits >> 4) & 0xFu),
-                                           wr[4 * k + 2] & bm((bits >> 8) & 0xFu),
-                                           wr[4 * k + 3] & bm(bits >> 12));
-                if ((OW & 15) == 0) {
-                  *reinterpret_cast<uint4*>(crow + px) = v;
-                } else {
-                  uint32_t* d4 = reinterpret_cast<uint32_t*>(crow + px);
-                  d4[0] = v.x;
-                  d4[1] = v.y;
-                  d4[2] = v.z;
-                  d4[3] = v.w;
-                }
-              }
-            }
-          } else {
-            float r0[2 * SEGR], r1[2 * SEGR];
-            lift_interior<SEGR>(
-                [&](int j, float2& s, float2& d) {
-                  s = rowL[cphys(cb + j)];
-                  d = rowH[cphys(cb + j)];
-                },
-                [&](int p, float2 s3, float2 d3) {
-                  const int lq = p - HALO;
-                  r0[2 * lq] = s3.x;
-                  r0[2 * lq + 1] = d3.x;
-                  r1[2 * lq] = s3.y;
-                  r1[2 * lq + 1] = d3.y;
-                });
-            float* o0 = a.out + ((uint64_t)c * OH + y0) * a.out_pitch + 2 * xa;
-#pragma unroll
-            for (int q = 0; q < SEGR / 2; ++q) {
-              *reinterpret_cast<float4*>(o0 + 4 * q) =
-                  make_float4(r0[4 * q], r0[4 * q + 1], r0[4 * q + 2], r0[4 * q + 3]);
-              *reinterpret_cast<float4*>(o0 + a.out_pitch + 4 * q) =
-                  make_float4(r1[4 * q], r1[4 * q + 1], r1[4 * q + 2], r1[4 * q + 3]);
-            }
-          }
-        } else {
-          lift_line(
-              max(xa - HALO, 0), min(xb + HALO, bw), bw, xa, xb,
-              [&](int j, float2& s, float2& d) {
-                s = rowL[cphys(j - ux0 + HALO)];
-                d = rowH[cphys(j - ux0 + HALO)];
-              },
-              [&](int p, float2 s3, float2 d3) {
-                if (FINAL) {
-                  auto cv = [](float v) { return u8_rint(__fmul_rn(v, 255.0f)); };
-                  const int px = 2 * p;
-#pragma unroll
-                  for (int rr = 0; rr < 2; ++rr) {
-                    const uint32_t bits = (rq[rr] >> (px & 31)) & 3u;
-                    const uint32_t lo = rr ? cv(s3.y) : cv(s3.x), hi = rr ? cv(d3.y) : cv(d3.x);
-                    *reinterpret_cast<uint16_t*>(canvas + ((uint64_t)c * OH + y0 + rr) * OW + px) =
-                        (uint16_t)(((bits & 1u) ? lo : 0u) | (((bits >> 1) & 1u) ? hi << 8 : 0u));
-                  }
-                } else {
-                  float* o0 = a.out + ((uint64_t)c * OH + y0) * a.out_pitch + 2 * p;
-                  *reinterpret_cast<float2*>(o0) = make_float2(s3.x, d3.x);
-                  *reinterpret_cast<float2*>(o0 + a.out_pitch) = make_float2(s3.y, d3.y);
-                }
-              });
-        }
-      }
-    }
-    // the next item's first stage writes slot 0: with an odd stage count this
-    // item's last row pass may still be reading it
-    if (nst & 1) __syncthreads();
-  }
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -1092,76 +663,6 @@ int launch_tiles(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStr
   return WV_OK;
 }
 
-#ifndef WV_K3_STRIP
-#define WV_K3_STRIP 0   // strip-streaming synthesis (k_strip) for levels whose subband has at
-                        // least WV_K3_STRIP_MIN coefficients; per-tile TMA boxes (k_level) below
-#endif
-#ifndef WV_K3_STRIP_MIN
-#define WV_K3_STRIP_MIN 0
-#endif
-
-int launch_strips(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStream_t s,
-                  int only_level, int sms) {
-  const int L = lo.L, C = lo.C;
-  float* plane = (float*)(ws + lo.plane);
-  const uint32_t* counters = (const uint32_t*)(ws + lo.counters);
-  static int occ_mid = 0, occ_fin = 0;   // per-process constants of the kernels
-  if (!occ_fin) {
-    WV_CUDA(cudaFuncSetAttribute(k_strip<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_S));
-    WV_CUDA(cudaFuncSetAttribute(k_strip<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_S));
-    int om = 1, of = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k_strip<false>, S_THREADS, SMEM_S);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k_strip<true>, S_THREADS, SMEM_S);
-    occ_mid = max(om, 1);
-    occ_fin = max(of, 1);
-  }
-  for (int k = L; k >= 1; --k) {
-    if (only_level && k != only_level) continue;
-    if ((long)(lo.H >> k) * (lo.W >> k) < (long)WV_K3_STRIP_MIN) {
-      const int st = launch_tiles(lo, fa, ws, s, k, sms);
-      if (st != WV_OK) return st;
-      continue;
-    }
-    StripArgs a{};
-    StripMaps maps{};
-    if (WV_K3S_TMA) {
-      const float* llb = k < L ? (const float*)(ws + lo.ybuf[k]) : plane;
-      const int llc = k < L ? lo.W >> k : lo.W, llr = k < L ? lo.H >> k : lo.H;
-      const int llp = k < L ? lo.ypitch[k] : lo.W;
-      if (make_map(&maps.ll8, llb, llc, llr, llp, C, TBW, SP) != WV_OK ||
-          make_map(&maps.ll4, llb, llc, llr, llp, C, TBW, 4) != WV_OK ||
-          make_map(&maps.pl8, plane, lo.W, lo.H, lo.W, C, TBW, SP) != WV_OK ||
-          make_map(&maps.pl4, plane, lo.W, lo.H, lo.W, C, TBW, 4) != WV_OK)
-        return WV_ERR_CUDA;
-    }
-    a.k = k; a.bh = lo.H >> k; a.bw = lo.W >> k; a.C = C; a.ngx = lo.ngx[k];
-    a.divC = fast_div((uint32_t)C);
-    a.divG = fast_div((uint32_t)lo.ngx[k]);
-    a.list = (const uint32_t*)(ws + lo.ulist[k]);
-    a.count = counters + CNT_UNITS + k;
-    a.ll = k < L ? (const float*)(ws + lo.ybuf[k]) : plane;
-    a.ll_pitch = k < L ? lo.ypitch[k] : lo.W;
-    a.ll_rows = k < L ? (lo.H >> k) : lo.H;
-    a.plane = plane; a.W = lo.W; a.H = lo.H;
-    const int items = lo.nty[k] * lo.ngx[k] * C;
-    if (k > 1) {
-      a.out = (float*)(ws + lo.ybuf[k - 1]);
-      a.out_pitch = lo.ypitch[k - 1];
-      const int grid = max(1, min(items, sms * occ_mid));
-      WV_CUDA(launch_k(k_strip<false>, dim3(grid), dim3(S_THREADS), (size_t)SMEM_S, s, a, maps));
-    } else {
-      a.fa = fa;
-      a.R = (const uint32_t*)(ws + lo.mrows);
-      a.rowmap = (const uint32_t*)(ws + lo.rowmap);
-      a.wpr0 = lo.wpr_[0];
-      const int grid = max(1, min(items, sms * occ_fin));
-      WV_CUDA(launch_k(k_strip<true>, dim3(grid), dim3(S_THREADS), (size_t)SMEM_S, s, a, maps));
-    }
-    WV_CUDA(cudaGetLastError());
-  }
-  return WV_OK;
-}
-
 }  // namespace
 
 int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* fa, uint8_t* ws,
@@ -1170,16 +671,12 @@ int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-#if WV_K3_STRIP
-  return launch_strips(lo, fa, ws, s, only_level, sms);
-#else
   for (int k = lo.L; k >= 1; --k) {
     if (only_level && k != only_level) continue;
     const int st = launch_tiles(lo, fa, ws, s, k, sms);
     if (st != WV_OK) return st;
   }
   return WV_OK;
-#endif
 }
 
 // Full-frame float32 synthesis of a Mallat pyramid already in the plane

@@ -830,11 +830,8 @@ struct TileArgs {
   int nwords1;
   uint32_t* list[WV_MAX_LEVELS + 1];
   uint8_t* prev_need;
-  uint32_t* counters;                // CNT_TILES + k, CNT_UNITS + k
+  uint32_t* counters;                // CNT_TILES + k
   const wv_frame_args* fa;
-  uint32_t* clear1;                  // bit rows like need1: tile left the request this frame
-  uint32_t* ulist[WV_MAX_LEVELS + 1];
-  int ngx[WV_MAX_LEVELS + 1];
 };
 
 __global__ void __launch_bounds__(256) k_tiles1(TileArgs a) {
@@ -863,8 +860,6 @@ __global__ void __launch_bounds__(256) k_tiles1(TileArgs a) {
     a.prev_need[t] = nd;
     if (nd) atomicOr(&a.need1[ty * a.nwords1 + (tx >> 5)], 1u << (tx & 31));
     else atomicAnd(&a.need1[ty * a.nwords1 + (tx >> 5)], ~(1u << (tx & 31)));
-    if (pv && !nd) atomicOr(&a.clear1[ty * a.nwords1 + (tx >> 5)], 1u << (tx & 31));
-    else atomicAnd(&a.clear1[ty * a.nwords1 + (tx >> 5)], ~(1u << (tx & 31)));
   }
   const bool emit = nd || pv;
   const uint32_t m = __ballot_sync(0xFFFFFFFFu, emit);
@@ -879,8 +874,6 @@ __global__ void __launch_bounds__(256) k_tiles1(TileArgs a) {
 
 // Coarser levels in one CTA: need maps live as bit rows in shared memory and
 // level k is derived from level k-1 (rows 2u-1..2u+2 x cols 2v-1..2v+2).
-// Every level's K3 strip units (UNIT_T adjacent tiles of one tile row) are
-// then listed with the unit's need bits (and, at level 1, its clear bits).
 __global__ void __launch_bounds__(1024) k_tiles_up(TileArgs a) {
   pdl_sync();
   extern __shared__ uint32_t nbits[];
@@ -891,45 +884,26 @@ __global__ void __launch_bounds__(1024) k_tiles_up(TileArgs a) {
   for (int i = threadIdx.x; i < off[a.L + 1]; i += blockDim.x)
     nbits[i] = i < off[2] ? a.need1[i] : 0u;
   __syncthreads();
-  for (int k = 1; k <= a.L; ++k) {
+  for (int k = 2; k <= a.L; ++k) {
     if (threadIdx.x == 0) cnt = 0;
     __syncthreads();
     const int ntx = a.ntx[k], nt = a.nty[k] * ntx;
-    if (k >= 2) {
-      const int fy = a.nty[k - 1], fx = a.ntx[k - 1], fw = wpr(fx);
-      const uint32_t* prev = nbits + off[k - 1];
-      for (int t = threadIdx.x; t < nt; t += blockDim.x) {
-        const int u = t / ntx, v = t - (t / ntx) * ntx;
-        const int x0 = max(2 * v - 1, 0), x1 = min(2 * v + 2, fx - 1);
-        bool nd = false;
-        for (int ty = max(2 * u - 1, 0); ty <= min(2 * u + 2, fy - 1) && !nd; ++ty)
-          for (int w = x0 >> 5; w <= (x1 >> 5); ++w)
-            if (prev[ty * fw + w] & range_mask(x0, x1 + 1, w)) { nd = true; break; }
-        if (nd) {
-          atomicOr(&nbits[off[k] + u * wpr(ntx) + (v >> 5)], 1u << (v & 31));
-          a.list[k][atomicAdd(&cnt, 1u)] = (uint32_t)t;
-        }
+    const int fy = a.nty[k - 1], fx = a.ntx[k - 1], fw = wpr(fx);
+    const uint32_t* prev = nbits + off[k - 1];
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+      const int u = t / ntx, v = t - (t / ntx) * ntx;
+      const int x0 = max(2 * v - 1, 0), x1 = min(2 * v + 2, fx - 1);
+      bool nd = false;
+      for (int ty = max(2 * u - 1, 0); ty <= min(2 * u + 2, fy - 1) && !nd; ++ty)
+        for (int w = x0 >> 5; w <= (x1 >> 5); ++w)
+          if (prev[ty * fw + w] & range_mask(x0, x1 + 1, w)) { nd = true; break; }
+      if (nd) {
+        atomicOr(&nbits[off[k] + u * wpr(ntx) + (v >> 5)], 1u << (v & 31));
+        a.list[k][atomicAdd(&cnt, 1u)] = (uint32_t)t;
       }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        a.counters[CNT_TILES + k] = cnt;
-        cnt = 0;
-      }
-      __syncthreads();
-    }
-    // strip units of level k (UNIT_T = 4 divides 32: a unit never straddles a word)
-    const int ngx = a.ngx[k], nu = a.nty[k] * ngx, nw = wpr(ntx);
-    const uint32_t* lev = nbits + off[k];
-    for (int uix = threadIdx.x; uix < nu; uix += blockDim.x) {
-      const int u = uix / ngx, g = uix - u * ngx;
-      const int v0 = g * UNIT_T;
-      const uint32_t need = (lev[u * nw + (v0 >> 5)] >> (v0 & 31)) & 0xFu;
-      const uint32_t clr = k == 1 ? (a.clear1[u * nw + (v0 >> 5)] >> (v0 & 31)) & 0xFu : 0u;
-      if (need | clr) a.ulist[k][atomicAdd(&cnt, 1u)] = (uint32_t)uix | (need << 24) | (clr << 28);
     }
     __syncthreads();
-    if (threadIdx.x == 0) a.counters[CNT_UNITS + k] = cnt;
-    __syncthreads();
+    if (threadIdx.x == 0) a.counters[CNT_TILES + k] = cnt;
   }
 }
 
@@ -1089,11 +1063,6 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
     }
     t.need1 = (uint32_t*)(ws + lo.need[1]);
     t.nwords1 = wpr(lo.ntx[1]);
-    t.clear1 = (uint32_t*)(ws + lo.clear1);
-    for (int k = 1; k <= L; ++k) {
-      t.ulist[k] = (uint32_t*)(ws + lo.ulist[k]);
-      t.ngx[k] = lo.ngx[k];
-    }
     t.prev_need = ws + lo.prev_need;
     t.counters = counters;
     t.fa = fa;
@@ -1115,7 +1084,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
                        (const uint32_t*)t.list[1], (const uint32_t*)(counters + CNT_TILES + 1),
                        lo.ntx[1]));
     }
-    if (st_tiles) {
+    if (L >= 2 && st_tiles) {
       size_t words = 0;
       for (int k = 1; k <= L; ++k) words += (size_t)lo.nty[k] * wpr(lo.ntx[k]);
       if (words * 4 > 200 * 1024) return WV_ERR_UNSUPPORTED;

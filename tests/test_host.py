@@ -329,3 +329,14 @@ def test_c_only_consumer_builds_and_reads(lib, tmp_path):
     out = subprocess.run([str(exe), os.path.join(GOLDEN, "smooth_n8.wvv")], capture_output=True,
                          text=True, check=True).stdout
     assert "64x64 C3 L2 n8 bs32 frames 10 sets 2" in out and "set 1:" in out
+
+
+def test_q255_table_matches_numpy():
+    """K2's compiled q/255 table is numpy's float32 division, bit for bit
+    (dequantize_values, encoding.py:270-271)."""
+    src = open(os.path.join(ROOT, "paper_2208_10859_b200", "csrc", "wv_temporal.cu")).read()
+    body = src[src.index("kQ255Bits[256] = {"):]
+    body = body[:body.index("};")]
+    got = np.array([int(x, 16) for x in re.findall(r"0x([0-9a-f]{8})u", body)], np.uint32)
+    want = (np.arange(256, dtype=np.float32) / np.float32(255.0)).view(np.uint32)
+    assert np.array_equal(got, want)
