@@ -175,16 +175,16 @@ def peaks():
 
 
 def launches_per_frame(L: int, mode: str, residency: str) -> int:
-    """Kernels of one frame's graph (csrc launch sequence): K1 rows, L
-    cascade steps (the default build; WV_K1_DIRECT=1 makes them one launch),
-    L-1 footprint steps, blocks, tile lists (2), finest footprint; K2; K3 L
-    levels; K4 -- full frame: rows, footprint fill, blocks, tile lists, K2,
-    K3 (no cascades, footprint chain or writeout)."""
+    """Kernels of one frame's graph (csrc launch sequence): K1 rows, one
+    direct cascade launch (all levels), L-1 footprint steps, blocks, tile
+    lists (2), finest footprint; K2; K3 L levels; K4 -- full frame: rows,
+    footprint fill, blocks, tile lists, K2, K3 (no cascades, footprint chain
+    or writeout)."""
     tiles = 1 + (1 if L >= 2 else 0)
     if mode == "full":
         n = 1 + 1 + 1 + tiles + 1 + L
     else:
-        n = 1 + L + (L - 1) + 1 + tiles + 1 + 1 + L + 1
+        n = 1 + 1 + (L - 1) + 1 + tiles + 1 + 1 + L + 1
     return n + (1 if residency == "spans" else 0)
 
 
@@ -322,6 +322,16 @@ def run_ours(args):
     for ss in sessions:
         ss._settle_until(None)
     unc = sum(ss.uncovered() for ss in sessions)
+    # host cost of one frame's enqueue (the public call), measured where the
+    # GPU cannot push back: an idle GPU, fewer frames than the session ring
+    torch.cuda.synchronize()
+    nh = min(args.steps, 48)
+    th = time.perf_counter()
+    for i in range(nh):
+        step(args.warmup + i, 0)
+    host_enqueue_us = (time.perf_counter() - th) * 1e6 / nh
+    torch.cuda.synchronize()
+    sess._settle_until(None)
 
     # serial latency view: one stream, L2 flushed (256 MiB write) before each
     # step, each step bracketed by events
@@ -511,6 +521,7 @@ def run_ours(args):
                      "encoder, decodes pinned to the reference, tests/golden/bench_8k.json)"),
             "serial_ms_per_frame": round(serial_ms, 4),
             "host_ms_per_step": round(t_host, 4),
+            "host_enqueue_us": round(host_enqueue_us, 1),
             "config": {
                 "workload": workload,
                 "levels": h.levels, "inter_size": h.inter_size, "block_size": h.block_size,

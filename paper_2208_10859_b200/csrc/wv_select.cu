@@ -115,7 +115,7 @@ __global__ void k_mask_rows(const wv_frame_args* __restrict__ fa, uint32_t* __re
 // block_size is 32).
 constexpr int CT_R = 32, CT_W = 32, CT_TW = 8;   // tile rows, tile words, threads per row
 #ifndef WV_K1_DIRECT
-#define WV_K1_DIRECT 0     // 1: all cascade levels in one launch as box ORs of the low-res mask (lower latency, ~1-2% lower pipelined throughput)
+#define WV_K1_DIRECT 1     // all cascade levels in one launch as box ORs of the low-res mask (0: one launch per level)
 #endif
 #ifndef WV_K1_DIRECT_RPW_WARPS
 #define WV_K1_DIRECT_RPW_WARPS 32   // warps per 32-row band of the direct cascade (one row each)
@@ -367,6 +367,62 @@ __device__ __forceinline__ uint32_t direct_word(const DirectArgs& a, int j, int4
   return v;
 }
 
+// The row's output as intervals: every run of consecutive set cells of srow
+// maps to one interval of level-j columns (the per-cell intervals of
+// adjacent cells abut or overlap), clipped to the window and the frame.
+// Lane 0 scans the runs; returns the interval count (warp-uniform), or -1
+// if there are more than kMaxIv (the caller then takes the per-cell path).
+constexpr int kMaxIv = 16;
+__device__ __forceinline__ int direct_intervals(const DirectArgs& a, int j, int4 win,
+                                                const uint32_t* srow, const int* cell_x0,
+                                                int2* iv, int lane) {
+  int n = 0;
+  if (lane == 0) {
+    const int A = 8 * ((1 << j) - 1), B = 9 * ((1 << j) - 1);
+    const int ncols = a.W >> j;
+    int c = 0;
+    while (c < a.mw && n >= 0) {
+      // next set cell at or after c
+      int w = c >> 5;
+      uint32_t bits = srow[w] & (0xFFFFFFFFu << (c & 31));
+      while (!bits && ++w < a.mwpr) bits = srow[w];
+      if (!bits) break;
+      const int c0 = 32 * w + __ffs(bits) - 1;
+      // end of the run: next clear cell after c0
+      int e = c0 + 1;
+      while (e < a.mw) {
+        const uint32_t clr = ~srow[e >> 5] & (0xFFFFFFFFu << (e & 31));
+        if (clr) {
+          e = min(a.mw, 32 * (e >> 5) + __ffs(clr) - 1);
+          break;
+        }
+        e = 32 * ((e >> 5) + 1);
+      }
+      e = min(e, a.mw);
+      const int s0 = max(cell_x0[c0], win.z), s1 = min(cell_x0[e] - 1, win.w - 1);
+      if (s0 <= s1) {
+        const int lo = max((s0 - B + (1 << j) - 1) >> j, 0);
+        const int hi = min((s1 + A) >> j, ncols - 1);
+        if (lo <= hi) {
+          if (n == kMaxIv) {
+            n = -1;
+            break;
+          }
+          iv[n++] = make_int2(lo, hi);
+        }
+      }
+      c = e;
+    }
+  }
+  return __shfl_sync(0xFFFFFFFFu, n, 0);
+}
+
+__device__ __forceinline__ uint32_t intervals_word(const int2* iv, int n, int w) {
+  uint32_t v = 0;
+  for (int i = 0; i < n; ++i) v |= range_mask(iv[i].x, iv[i].y + 1, w);
+  return v;
+}
+
 // direct_word with the candidate cells split over the warp's lanes (coarse
 // levels: a word's box spans tens of cells); every lane gets the word
 __device__ __forceinline__ uint32_t direct_word_warp(const DirectArgs& a, int j, int4 win,
@@ -395,6 +451,7 @@ __device__ __forceinline__ uint32_t direct_word_warp(const DirectArgs& a, int j,
 __global__ void __launch_bounds__(32 * WV_K1_DIRECT_RPW_WARPS) k_cascade_direct(DirectArgs a) {
   pdl_sync();
   __shared__ uint32_t srow[WV_K1_DIRECT_RPW_WARPS][2][32];
+  __shared__ int2 siv[WV_K1_DIRECT_RPW_WARPS][2][kMaxIv];
   __shared__ uint32_t s_pool[64];
   // which (level, batch) item this CTA serves
   int it = 0;
@@ -426,7 +483,20 @@ __global__ void __launch_bounds__(32 * WV_K1_DIRECT_RPW_WARPS) k_cascade_direct(
     const bool anyB = both ? direct_prep(a, j, y, full, srow[wp][1], lane) : true;
     __syncwarp();
     uint32_t* out = a.dst[j] + (uint64_t)b * a.dst_stride[j] + (uint64_t)y * wpr;
-    if (wpr > 8) {
+    const int nA = anyA ? direct_intervals(a, j, win, srow[wp][0], cell_x0, siv[wp][0], lane) : 0;
+    const int nB = (both && anyB) ? direct_intervals(a, j, full, srow[wp][1], cell_x0, siv[wp][1],
+                                                     lane)
+                                  : 0;
+    __syncwarp();
+    if (nA >= 0 && nB >= 0) {
+      // runs of set cells -> at most kMaxIv intervals per row: one word per lane
+      for (int w = lane; w < wpr; w += 32) {
+        uint32_t v = intervals_word(siv[wp][0], nA, w);
+        if (both) v &= intervals_word(siv[wp][1], nB, w);
+        out[w] = v;
+        if (pooled && v) atomicOr(&s_pool[w >> 5], 1u << (w & 31));
+      }
+    } else if (wpr > 8) {
       // enough words for the lanes: one word per lane
       for (int w = lane; w < wpr; w += 32) {
         uint32_t v = anyA ? direct_word(a, j, win, srow[wp][0], cell_x0, w) : 0u;

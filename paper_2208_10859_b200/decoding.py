@@ -18,6 +18,7 @@ raises.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import math
 import os
@@ -173,6 +174,7 @@ _FA_BYTES = C.sizeof(N.FrameArgs)
 _VA_BYTES = C.sizeof(N.ViewArgs)
 _DESC_BYTES = _FA_BYTES + 4 * _VA_BYTES
 _RING = 64
+_NO_CTX = contextlib.nullcontext()
 _MODES = {"full": N.WV_MODE_FULL, "viewport": N.WV_MODE_VIEWPORT, "foveated": N.WV_MODE_FOVEATED}
 
 
@@ -256,6 +258,14 @@ class DecodeSession:
             ev = torch.cuda.Event()
             ev.record(self.stream)
             self._slot_events.append(ev)
+        # wv_enqueue_frame arguments that never change, per ring slot
+        self._enq_desc = C.c_void_p(self._desc_dev_ptr)
+        self._enq_bytes = C.c_uint64(self._desc_bytes)
+        self._enq_stream = C.c_void_p(self.stream.cuda_stream)
+        self._enq_args = [(C.c_void_p(self._desc_host[i].data_ptr()),
+                           C.c_void_p(self._results[i].data_ptr()),
+                           C.c_void_p(self._results_host[i].data_ptr()),
+                           C.c_void_p(self._slot_events[i].cuda_event)) for i in range(_RING)]
         self._slot = 0
         self._cache: dict[int, _Entry] = {}
         self._resident: OrderedDict = OrderedDict()
@@ -355,7 +365,8 @@ class DecodeSession:
             self._settle_until(None)
         entry = self._cache.get(set_index)
         if entry is None:
-            entry = _Entry(set_index, self.header.num_blocks, self.device)
+            with torch.cuda.stream(self.stream):
+                entry = _Entry(set_index, self.header.num_blocks, self.device)
             self._store(entry)
             return entry, False, False
         return entry, True, len(self._cache) > 2
@@ -417,13 +428,17 @@ class DecodeSession:
         key = (_MODES[mode], nv, tuple(out_dims) if nv else None, flags)
         g = self._graphs.get(key)
         if g is not None:
-            N.check(self._lib.wv_enqueue_frame(
-                C.c_void_p(self._desc_dev_ptr), C.c_void_p(hptr), C.c_uint64(self._desc_bytes),
-                C.c_void_p(g[1]), C.c_void_p(self.stream.cuda_stream),
-                C.c_void_p(self._results[slot].data_ptr()),
-                C.c_void_p(self._results_host[slot].data_ptr()),
-                C.c_void_p(self._slot_events[slot].cuda_event)), "wv_enqueue_frame")
+            ea = self._enq_args[slot]
+            st = self._lib.wv_enqueue_frame(self._enq_desc, ea[0], self._enq_bytes, g[1],
+                                            self._enq_stream, ea[1], ea[2], ea[3])
+            if st:
+                N.check(st, "wv_enqueue_frame")
             return True
+        with torch.cuda.stream(self.stream):
+            return self._first_run(host, key, flags, nv, views, out_dims)
+
+    def _first_run(self, host, key, flags, nv, views, out_dims) -> bool:
+        """Direct run of a mode's launch sequence, then its graph capture."""
         self._desc_dev.copy_(host, non_blocking=True)
 
         def run(stages, stream):
@@ -474,7 +489,7 @@ class DecodeSession:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=self.stream, capture_error_mode="relaxed"):
                 seq()
-            self._graphs[key] = (graph, graph.raw_cuda_graph_exec())
+            self._graphs[key] = (graph, C.c_void_p(graph.raw_cuda_graph_exec()))
         return False
 
     def _launch(self, frame: int, mode: str, mask=None, schedule=None,
@@ -490,12 +505,14 @@ class DecodeSession:
             self._settle_until(self._pending[0])
         slot = self._slot
         self._slot = (self._slot + 1) % _RING
-        with torch.cuda.stream(s):
+        fast = not (account_only or self.kernel_timing or time_stages)
+        # the graph fast path enqueues through the C ABI with the stream
+        # passed explicitly; only the other paths issue torch ops here
+        with (_NO_CTX if fast else torch.cuda.stream(s)):
             ev0 = torch.cuda.Event(enable_timing=True) if time_stages else None
             if ev0 is not None:
                 ev0.record(s)
             dev, ext, keep = self._make_resident(si)
-            fast = not (account_only or self.kernel_timing or time_stages)
             args = self._mode_args(mode, mask, schedule, slot, in_desc=fast)
             entry, existed, may_evict = self._entry_for(si)
             args.t = t
@@ -548,7 +565,8 @@ class DecodeSession:
             elif self._run_fast(slot, args, mode, views, out_dims, args.flags):
                 done = self._slot_events[slot]   # recorded by wv_enqueue_frame
             if done is None:
-                self._results_host[slot].copy_(self._results[slot], non_blocking=True)
+                with torch.cuda.stream(s):
+                    self._results_host[slot].copy_(self._results[slot], non_blocking=True)
                 done = torch.cuda.Event()
                 done.record(s)
         p.slot, p.set_index, p.entry, p.existed, p.may_evict = slot, si, entry, existed, may_evict

@@ -8,6 +8,7 @@ the reference signature (projection.py:111) but runs the K4 kernel.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 from dataclasses import dataclass
 
@@ -140,13 +141,20 @@ def view_args(canvas: torch.Tensor, footprint_bits: torch.Tensor, row0: int, row
     return v
 
 
+@functools.lru_cache(maxsize=4096)
+def _pose_consts(yaw, pitch, roll, fov_h, fov_v):
+    """Rotation (row major, the numpy product the reference forms) and FOV
+    tangents of a pose; cached, since a viewer revisits poses."""
+    rot = CameraPose(yaw, pitch, roll, fov_h, fov_v).rotation().reshape(-1).tolist()
+    return rot, math.tan(math.radians(fov_h / 2.0)), math.tan(math.radians(fov_v / 2.0))
+
+
 def set_view_pose(views: list, pose: CameraPose) -> None:
     """Re-point cached K4 arguments at a new pose (one rotation for all views)."""
     if not (pose.fov_h < 180 and pose.fov_v < 180):
         raise ProjectionError("perspective rendering requires FOV < 180 degrees")
-    rot = pose.rotation().reshape(-1).tolist()
-    tan_h = math.tan(math.radians(pose.fov_h / 2.0))
-    tan_v = math.tan(math.radians(pose.fov_v / 2.0))
+    rot, tan_h, tan_v = _pose_consts(float(pose.yaw), float(pose.pitch), float(pose.roll),
+                                     float(pose.fov_h), float(pose.fov_v))
     for v in views:
         v.rot[:] = rot
         v.tan_h, v.tan_v = tan_h, tan_v

@@ -32,11 +32,15 @@ def main():
 
     run(80)
     torch.cuda.synchronize()
+    s._settle_until(None)
+    # fewer frames than the session's result ring, GPU idle at the start:
+    # nothing pushes back on the host, so this is the enqueue cost alone
     t = time.perf_counter()
-    run(n)
-    host = (time.perf_counter() - t) / n * 1e6
+    run(48)
+    host = (time.perf_counter() - t) / 48 * 1e6
     torch.cuda.synchronize()
-    print(f"{host:.1f} us/frame host enqueue (unprofiled)")
+    s._settle_until(None)
+    print(f"{host:.1f} us/frame host enqueue (unprofiled, no back-pressure)")
     pr = cProfile.Profile()
     pr.enable()
     run(n)
