@@ -116,6 +116,11 @@ typedef struct wv_frame_args {
                                      pointer, same layout as d_payload) */
   uint32_t* d_fetched;            /* WV_FLAG_FETCH: NB-bit bitmap, records of block b are in
                                      d_payload; zero it when d_payload is (re)filled */
+  uint32_t* h_fetch_list;         /* WV_FLAG_FETCH, optional: host (pinned) buffers that receive
+                                     this call's fetch list -- the blocks whose records are not yet
+                                     in HBM (NB u32) -- and its length, before the fetch stage
+                                     (span streaming from the file, wv_span_queue_enqueue) */
+  uint32_t* h_fetch_count;
   int32_t out_row0, out_row1;     /* output pixel rows this call must produce, half open
                                      (0, 0 = the whole frame).  A stereo eye split
                                      ([0, H/2) or [H/2, H)) synthesises only the tiles those
@@ -181,8 +186,10 @@ enum wv_stage {
   WV_STAGE_FOOTPRINT_TILES = 32,  /* finest footprint on the level-1 tiles (K1) */
   WV_STAGE_DEQUANT = 64,          /* K2 */
   WV_STAGE_SYNTH = 128,           /* K3, all levels */
+  WV_STAGE_FETCH = 256,           /* WV_FLAG_FETCH: copy the listed blocks' records host -> HBM
+                                     (k_fetch) <- BLOCKS; DEQUANT waits for it */
   WV_STAGE_SELECT = 63,
-  WV_STAGE_ALL = 255
+  WV_STAGE_ALL = 511
 };
 int wv_decode_stages_desc(const wv_geometry* g, int mode, int flags, int stages,
                           void* d_workspace, void* stream);
@@ -234,6 +241,53 @@ int wv_file_set_read(const char* path, int set_index, wv_set_info* set, float* e
  * (>= payload_length bytes; pinned host memory serves both a whole-set
  * upload and WV_FLAG_FETCH's h_payload). */
 int wv_file_payload_read(const char* path, int set_index, void* buf, uint64_t buf_bytes);
+
+/* ---- Span streaming from the file ----
+ * VideoReader.load_blocks (fileio.py:346-390) for a block list made on the
+ * GPU: for every temporal index and every run of consecutive ids, the span
+ * (end of the previous (t, block) entry, end of the run's last block)
+ * (block_range_bytes, fileio.py:168-181) of the record data is read from
+ * `fd` into the same payload offset of `dst` (widened to whole 16-byte
+ * chunks, which the fetch kernel copies); ranges are merged through gaps
+ * <= coalesce_gap (COALESCE_GAP 4096, fileio.py:31, :264-274), one pread
+ * per merged range.  bytes_read: the reference's coalesced read of the
+ * exact spans (VideoReader.io_trace), bytes_spans: bytes of the requested
+ * spans. */
+#define WV_SPAN_QUEUE 64
+typedef struct wv_span_job {
+  int32_t fd;                     /* open .wvv file */
+  int32_t n, nb;                  /* inter_size, blocks per frame */
+  int32_t status;                 /* out: WV_* of the read */
+  uint64_t payload_offset;        /* file offset of the set's payload (its BlockEnd table) */
+  uint64_t payload_bytes;         /* payload length */
+  uint64_t table_bytes;           /* n * nb * 8 */
+  const uint64_t* table;          /* host BlockEnd table of the set, n * nb u64 */
+  uint8_t* dst;                   /* host buffer mirroring the payload (16-byte chunks of
+                                     every requested span are filled from the file) */
+  const uint32_t* ids;            /* host block list (any order) ... */
+  const uint32_t* count;          /* ... and its length */
+  uint64_t coalesce_gap;
+  uint64_t bytes_read, bytes_spans;   /* out */
+  int32_t done, reserved;         /* out: 1 once read */
+} wv_span_job;
+/* FIFO of jobs consumed by stream-ordered reads (caller-owned host memory,
+ * zero-initialised; one producer, the stream's host-function thread as the
+ * consumer). */
+typedef struct wv_span_queue {
+  wv_span_job jobs[WV_SPAN_QUEUE];
+  uint32_t fifo[WV_SPAN_QUEUE];
+  uint32_t head, tail;
+} wv_span_queue;
+int wv_spans_read(const wv_span_job* job, uint64_t* bytes_read, uint64_t* bytes_spans);
+/* Append a copy of *job (stored in jobs[slot]) to the queue. */
+int wv_span_queue_push(wv_span_queue* q, const wv_span_job* job, uint32_t slot);
+/* Enqueue on `stream` a host function that runs the oldest queued job
+ * (cudaLaunchHostFunc; capturable into a CUDA graph, where every replay
+ * consumes the next job). */
+int wv_span_queue_enqueue(wv_span_queue* q, void* stream);
+/* Device views of the fetch list of the last select (k_blocks output). */
+int wv_fetch_list_view(const wv_geometry* g, void* d_workspace, uint32_t** d_list,
+                       uint32_t** d_count);
 
 /* ---- Encoder: one inter-frame set ----
  * Replaces the per-set body of the reference encoder, encode_video

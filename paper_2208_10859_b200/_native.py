@@ -17,7 +17,8 @@ WV_FLAG_ACCOUNT_ONLY, WV_FLAG_FETCH = 1, 2
 WV_ABI_VERSION = 4
 WV_ENC_MAX_N = 64
 (WV_STAGE_ROWS, WV_STAGE_CASCADES, WV_STAGE_FOOTPRINT, WV_STAGE_BLOCKS, WV_STAGE_TILES,
- WV_STAGE_FOOTPRINT_TILES, WV_STAGE_DEQUANT, WV_STAGE_SYNTH) = 1, 2, 4, 8, 16, 32, 64, 128
+ WV_STAGE_FOOTPRINT_TILES, WV_STAGE_DEQUANT, WV_STAGE_SYNTH, WV_STAGE_FETCH) = (
+    1, 2, 4, 8, 16, 32, 64, 128, 256)
 WV_DERR_OFFSET, WV_DERR_TABLE = 1, 2
 WV_MAX_LEVELS = 12
 
@@ -29,7 +30,8 @@ EXPORTS = ["wv_abi_version", "wv_status_string", "wv_workspace_bytes", "wv_works
            "wv_render_perspective_desc", "wv_file_info_read", "wv_file_set_read",
            "wv_file_payload_read", "wv_decode_stages_desc", "wv_encode_workspace_bytes",
            "wv_encode_payload_capacity", "wv_encode_set", "wv_enqueue_frame",
-           "wv_desc_layout", "wv_synthesize_2d"]
+           "wv_desc_layout", "wv_synthesize_2d", "wv_spans_read", "wv_span_queue_push",
+           "wv_span_queue_enqueue", "wv_fetch_list_view"]
 
 
 class Geometry(C.Structure):
@@ -70,7 +72,25 @@ class FrameArgs(C.Structure):
                 ("d_set_bytes", C.c_void_p), ("d_canvas", C.c_void_p),
                 ("d_footprint", C.c_void_p), ("d_result", C.c_void_p),
                 ("h_payload", C.c_void_p), ("d_fetched", C.c_void_p),
+                ("h_fetch_list", C.c_void_p), ("h_fetch_count", C.c_void_p),
                 ("out_row0", C.c_int32), ("out_row1", C.c_int32)]
+
+
+WV_SPAN_QUEUE = 64
+
+
+class SpanJob(C.Structure):
+    _fields_ = [("fd", C.c_int32), ("n", C.c_int32), ("nb", C.c_int32), ("status", C.c_int32),
+                ("payload_offset", C.c_uint64), ("payload_bytes", C.c_uint64),
+                ("table_bytes", C.c_uint64), ("table", C.c_void_p), ("dst", C.c_void_p),
+                ("ids", C.c_void_p), ("count", C.c_void_p),
+                ("coalesce_gap", C.c_uint64), ("bytes_read", C.c_uint64),
+                ("bytes_spans", C.c_uint64), ("done", C.c_int32), ("reserved", C.c_int32)]
+
+
+class SpanQueue(C.Structure):
+    _fields_ = [("jobs", SpanJob * WV_SPAN_QUEUE), ("fifo", C.c_uint32 * WV_SPAN_QUEUE),
+                ("head", C.c_uint32), ("tail", C.c_uint32)]
 
 
 class ViewArgs(C.Structure):
@@ -135,3 +155,7 @@ def check(status: int, what: str) -> None:
     if status != WV_OK:
         msg = load().wv_status_string(status).decode()
         raise NativeError(f"{what} failed: {msg} (status {status})")
+
+
+def status_name(status: int) -> str:
+    return load().wv_status_string(status).decode()

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["wv_select.cu", "wv_temporal.cu", "wv_idwt.cu", "wv_perspective.cu", "wv_capi.cu",
-           "wv_file.cpp", "wv_encode.cu"]
+           "wv_file.cpp", "wv_encode.cu", "wv_spans.cpp"]
 HEADERS = ["wv_common.cuh"]
 LIB = os.path.join(HERE, "_wvb200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

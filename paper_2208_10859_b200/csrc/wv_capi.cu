@@ -75,12 +75,22 @@ static int stage(const wv_geometry* g, const wv_frame_args* a, void* ws, void* s
   return WV_OK;
 }
 
+// the fetch stage right after selection, unless the caller streams the spans
+// from the file in between (h_fetch_list set: it runs WV_STAGE_FETCH itself)
+static int select_and_fetch(const Layout& lo, const wv_geometry* g, const wv_frame_args* a,
+                            const wv_frame_args* d, uint8_t* ws, cudaStream_t s) {
+  int st = launch_select(lo, g, a->mode, a->flags, d, ws, s);
+  if (st != WV_OK) return st;
+  if ((a->flags & WV_FLAG_FETCH) && !a->h_fetch_list) return launch_fetch(lo, d, ws, s);
+  return WV_OK;
+}
+
 int wv_select(const wv_geometry* g, const wv_frame_args* a, void* ws, void* stream) {
   Layout lo;
   wv_frame_args* d;
   int st = stage(g, a, ws, stream, &lo, &d);
   if (st != WV_OK) return st;
-  return launch_select(lo, g, a->mode, a->flags, d, (uint8_t*)ws, (cudaStream_t)stream);
+  return select_and_fetch(lo, g, a, d, (uint8_t*)ws, (cudaStream_t)stream);
 }
 
 int wv_dequant_temporal(const wv_geometry* g, const wv_frame_args* a, void* ws, void* stream) {
@@ -105,7 +115,7 @@ int wv_decode_frame(const wv_geometry* g, const wv_frame_args* a, void* ws, void
   int st = stage(g, a, ws, stream, &lo, &d);
   if (st != WV_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  if ((st = launch_select(lo, g, a->mode, a->flags, d, (uint8_t*)ws, s)) != WV_OK) return st;
+  if ((st = select_and_fetch(lo, g, a, d, (uint8_t*)ws, s)) != WV_OK) return st;
   if (a->flags & WV_FLAG_ACCOUNT_ONLY) return WV_OK;
   if ((st = launch_temporal(lo, g, a->mode, d, (uint8_t*)ws, s)) != WV_OK) return st;
   return launch_synthesis(lo, g, d, (uint8_t*)ws, s);
@@ -138,6 +148,7 @@ int wv_decode_frame_desc(const wv_geometry* g, int mode, int flags, void* ws, vo
   const wv_frame_args* d = (const wv_frame_args*)((uint8_t*)ws + lo.desc);
   cudaStream_t s = (cudaStream_t)stream;
   if ((st = launch_select(lo, g, mode, flags, d, (uint8_t*)ws, s)) != WV_OK) return st;
+  if ((flags & WV_FLAG_FETCH) && (st = launch_fetch(lo, d, (uint8_t*)ws, s)) != WV_OK) return st;
   if (flags & WV_FLAG_ACCOUNT_ONLY) return WV_OK;
   if ((st = launch_temporal(lo, g, mode, d, (uint8_t*)ws, s)) != WV_OK) return st;
   return launch_synthesis(lo, g, d, (uint8_t*)ws, s);
@@ -156,6 +167,9 @@ int wv_decode_stages_desc(const wv_geometry* g, int mode, int flags, int stages,
     if ((st = launch_select(lo, g, mode, flags, d, (uint8_t*)ws, s, stages & WV_STAGE_SELECT)) !=
         WV_OK)
       return st;
+  if ((stages & WV_STAGE_FETCH) && (flags & WV_FLAG_FETCH) &&
+      (st = launch_fetch(lo, d, (uint8_t*)ws, s)) != WV_OK)
+    return st;
   if (flags & WV_FLAG_ACCOUNT_ONLY) return WV_OK;
   if ((stages & WV_STAGE_DEQUANT) &&
       (st = launch_temporal(lo, g, mode, d, (uint8_t*)ws, s)) != WV_OK)
@@ -236,6 +250,16 @@ int wv_level_mask_view(const wv_geometry* g, void* ws, int level, uint32_t** d_b
   // viewport/full masks sit in batch 0 of the level stack; foveated masks in batch `level`
   *d_bits = (uint32_t*)((uint8_t*)ws + lo.stack[level]);
   *words_per_row = lo.wpr_[level];
+  return WV_OK;
+}
+
+int wv_fetch_list_view(const wv_geometry* g, void* ws, uint32_t** d_list, uint32_t** d_count) {
+  Layout lo;
+  int st = build_layout(g, &lo);
+  if (st != WV_OK) return st;
+  if (!ws || !d_list || !d_count) return WV_ERR_ARG;
+  *d_list = (uint32_t*)((uint8_t*)ws + lo.flist);
+  *d_count = (uint32_t*)((uint8_t*)ws + lo.counters) + CNT_FETCH;
   return WV_OK;
 }
 

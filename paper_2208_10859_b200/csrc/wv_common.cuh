@@ -177,6 +177,7 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
                   const wv_frame_args* d_fa, uint8_t* ws, cudaStream_t s,
                   int stages = WV_STAGE_SELECT);
+int launch_fetch(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStream_t s);
 int launch_temporal(const Layout& lo, const wv_geometry* g, int mode, const wv_frame_args* d_fa,
                     uint8_t* ws, cudaStream_t s);
 int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* d_fa,

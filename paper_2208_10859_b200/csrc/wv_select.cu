@@ -849,6 +849,23 @@ __global__ void __launch_bounds__(256) k_blocks(BlockArgs a) {
   }
 }
 
+// The fetch list (and its length) to the caller's pinned host buffers, so a
+// stream-ordered host function can read exactly those spans from the file
+// before k_fetch copies them to HBM (plain stores over PCIe; no-op without
+// h_fetch_list).
+__global__ void __launch_bounds__(256) k_list_to_host(const wv_frame_args* __restrict__ fa,
+                                                      const uint32_t* __restrict__ flist,
+                                                      const uint32_t* __restrict__ fcount) {
+  pdl_sync();
+  uint32_t* hl = fa->h_fetch_list;
+  if (!hl || !fa->h_fetch_count) return;
+  const uint32_t n = *fcount;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    hl[i] = flist[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *fa->h_fetch_count = n;
+  __threadfence_system();
+}
+
 // --------------------------------------------------------------- span fetch
 // VideoReader.load_blocks (fileio.py:346-390) for one decode: copy the record
 // spans of the listed blocks, all temporal indices, from the set payload in
@@ -1114,13 +1131,9 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
       b.pool_wpr[k] = cdiv(lo.wpr_[k], CT_W);
     }
     WV_CUDA(launch_k(k_blocks, dim3(cdiv(lo.NB, 256)), dim3(256), 0, s, b));
-    if (b.fetch) {
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      WV_CUDA(launch_k(k_fetch, dim3(4 * sms), dim3(256), 0, s, fa, (const uint32_t*)b.flist,
-                       (const uint32_t*)b.fcount, lo.n, lo.NB, b.table_bytes));
-    }
+    if (b.fetch)
+      WV_CUDA(launch_k(k_list_to_host, dim3(8), dim3(256), 0, s, fa, (const uint32_t*)b.flist,
+                       (const uint32_t*)b.fcount));
   }
   if (acct && st_blocks) {
     WV_CUDA(launch_k(k_finalize, dim3(1), dim3(1), 0, s, fa));
@@ -1164,6 +1177,18 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
       WV_CUDA(launch_k(k_tiles_up, dim3(1), dim3(1024), words * 4, s, t));
     }
   }
+  WV_CUDA(cudaGetLastError());
+  return WV_OK;
+}
+
+// WV_STAGE_FETCH: the listed blocks' records, all temporal indices, host -> HBM
+int launch_fetch(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t* counters = (const uint32_t*)(ws + lo.counters);
+  WV_CUDA(launch_k(k_fetch, dim3(4 * sms), dim3(256), 0, s, fa, (const uint32_t*)(ws + lo.flist),
+                   counters + CNT_FETCH, lo.n, lo.NB, (unsigned long long)lo.n * lo.NB * 8));
   WV_CUDA(cudaGetLastError());
   return WV_OK;
 }

@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .fileio import VideoReader
+from .fileio import COALESCE_GAP, VideoReader
 from .projection import (CameraPose, CoverageError, launch_views, set_view_pose, unpack_footprint,
                          view_args)
 
@@ -182,10 +182,13 @@ class DecodeSession:
     """Single-owner decode session on one GPU stream with one-slot prefetch."""
 
     def __init__(self, path, device=None, max_resident_sets: int = 4, residency: str = "set"):
-        """``residency``: "set" uploads a set's whole payload to HBM when it is
-        first decoded; "spans" uploads only its BlockEnd table and, per decode,
-        the GPU copies the record spans of newly selected blocks from the set
-        payload in pinned host memory (VideoReader.load_blocks, fileio.py:346-390)."""
+        """``residency``: "set" reads a set's whole payload and uploads it to
+        HBM when it is first decoded; "spans" reads and uploads only its
+        BlockEnd table, and each decode streams the record spans of newly
+        selected blocks from the file (VideoReader.load_blocks,
+        fileio.py:346-390, 4 KiB coalescing) inside the frame's stream order:
+        the GPU lists the blocks, a stream-ordered host function reads their
+        spans into pinned memory, and the fetch kernel copies them to HBM."""
         if residency not in ("set", "spans"):
             raise ValueError(f"residency {residency!r} not in ('set', 'spans')")
         self.residency = residency
@@ -196,6 +199,14 @@ class DecodeSession:
         self.reader = VideoReader(path)
         h = self.reader.header
         self.header = h
+        self._fd = None
+        if residency == "spans":
+            # span streaming: a private descriptor for pread, the job queue of
+            # the stream-ordered reads, and the GPU's fetch list in host memory
+            self._fd = os.open(path, os.O_RDONLY)
+            self._spanq = N.SpanQueue()
+            self._h_flist = torch.zeros(max(1, h.num_blocks), dtype=torch.int32).pin_memory()
+            self._h_fcount = torch.zeros(4, dtype=torch.int32).pin_memory()
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         self._geom = N.Geometry(h.width, h.height, h.channels, h.levels, h.inter_size,
@@ -287,6 +298,9 @@ class DecodeSession:
         if self._pending:
             self._settle_until(None)
         self.reader.close()
+        if self.residency == "spans" and self._fd is not None:
+            os.close(self._fd)
+            self._fd = None
 
     def __enter__(self):
         return self
@@ -303,12 +317,45 @@ class DecodeSession:
 
     def _read_payload(self, set_index: int) -> torch.Tensor:
         """The set payload in pinned host memory, zero-padded to 16 bytes (the
-        span fetch copies 16-byte chunks)."""
+        span fetch copies 16-byte chunks).  Span residency reads only the
+        BlockEnd table here; record spans are read per decode."""
         n = self.reader.payload_length(set_index)
         host = torch.zeros((n + 15) // 16 * 16, dtype=torch.uint8).pin_memory()
         with self._io_lock:
-            self.reader.read_set_payload(set_index, memoryview(host.numpy()[:n]))
+            if self.residency == "spans":
+                self.reader.read_set_table(set_index, memoryview(host.numpy()[:n]))
+            else:
+                self.reader.read_set_payload(set_index, memoryview(host.numpy()[:n]))
         return host
+
+    def _push_span_job(self, set_index: int, host: torch.Tensor, slot: int) -> None:
+        """Queue the file read of this frame's fetch list (consumed in stream
+        order by the host function that wv_span_queue_enqueue placed)."""
+        h = self.header
+        tb = h.table_bytes
+        j = N.SpanJob()
+        j.fd, j.n, j.nb = self._fd, h.inter_size, h.num_blocks
+        j.payload_offset = self.reader.set_meta[set_index].payload_offset
+        j.payload_bytes = self.reader.payload_length(set_index)
+        j.table_bytes = tb
+        j.table = host.data_ptr()
+        j.dst = host.data_ptr()
+        j.ids, j.count = self._h_flist.data_ptr(), self._h_fcount.data_ptr()
+        j.coalesce_gap = COALESCE_GAP
+        N.check(self._lib.wv_span_queue_push(C.byref(self._spanq), C.byref(j), slot),
+                "wv_span_queue_push")
+
+    def _span_read_then_fetch(self, stream) -> None:
+        """Stream-ordered: read the listed spans from the file, then copy
+        them to HBM (the host-argument call paths)."""
+        N.check(self._lib.wv_span_queue_enqueue(C.byref(self._spanq),
+                                                C.c_void_p(stream.cuda_stream)),
+                "wv_span_queue_enqueue")
+        mode = N.WV_MODE_FULL   # the fetch stage ignores the mode
+        N.check(self._lib.wv_decode_stages_desc(
+            C.byref(self._geom), mode, N.WV_FLAG_FETCH, N.WV_STAGE_FETCH,
+            C.c_void_p(self._ws.data_ptr()), C.c_void_p(stream.cuda_stream)),
+            "wv_decode_stages_desc")
 
     def pinned_payload(self, set_index: int) -> torch.Tensor:
         """The set's payload (BlockEnd table + records) read into pinned host
@@ -440,6 +487,7 @@ class DecodeSession:
     def _first_run(self, host, key, flags, nv, views, out_dims) -> bool:
         """Direct run of a mode's launch sequence, then its graph capture."""
         self._desc_dev.copy_(host, non_blocking=True)
+        spans = self.residency == "spans"
 
         def run(stages, stream):
             N.check(self._lib.wv_decode_stages_desc(
@@ -467,11 +515,26 @@ class DecodeSession:
                 run(N.WV_STAGE_FOOTPRINT, aux)
                 ev_f = torch.cuda.Event()
                 ev_f.record(aux)
-                run(N.WV_STAGE_BLOCKS | N.WV_STAGE_DEQUANT, cur)
+                if spans:
+                    # span streaming: the GPU's fetch list -> file reads
+                    # (stream-ordered host function) -> fetch kernel -> K2
+                    run(N.WV_STAGE_BLOCKS, cur)
+                    N.check(self._lib.wv_span_queue_enqueue(
+                        C.byref(self._spanq), C.c_void_p(cur.cuda_stream)),
+                        "wv_span_queue_enqueue")
+                    run(N.WV_STAGE_FETCH | N.WV_STAGE_DEQUANT, cur)
+                else:
+                    run(N.WV_STAGE_BLOCKS | N.WV_STAGE_FETCH | N.WV_STAGE_DEQUANT, cur)
                 cur.wait_event(ev_t)
                 run(N.WV_STAGE_SYNTH, cur)
                 cur.wait_event(ev_f)
                 run(N.WV_STAGE_FOOTPRINT_TILES, cur)
+            elif spans:
+                run(N.WV_STAGE_SELECT, cur)
+                N.check(self._lib.wv_span_queue_enqueue(
+                    C.byref(self._spanq), C.c_void_p(cur.cuda_stream)),
+                    "wv_span_queue_enqueue")
+                run(N.WV_STAGE_FETCH | N.WV_STAGE_DEQUANT | N.WV_STAGE_SYNTH, cur)
             else:
                 N.check(self._lib.wv_decode_frame_desc(
                     C.byref(self._geom), key[0], flags, C.c_void_p(self._ws.data_ptr()),
@@ -519,10 +582,14 @@ class DecodeSession:
             args.flags = N.WV_FLAG_ACCOUNT_ONLY if account_only else 0
             if out_rows is not None:
                 args.out_row0, args.out_row1 = out_rows
-            if self.residency == "spans":
+            spans = self.residency == "spans"
+            if spans:
                 args.flags |= N.WV_FLAG_FETCH
                 args.h_payload = keep[0].data_ptr()
                 args.d_fetched = keep[2].data_ptr()
+                args.h_fetch_list = self._h_flist.data_ptr()
+                args.h_fetch_count = self._h_fcount.data_ptr()
+                self._push_span_job(si, keep[0], slot)
             args.d_payload = dev.data_ptr()
             args.payload_bytes = self.reader.payload_length(si)
             args.d_extrema = ext.data_ptr()
@@ -536,11 +603,15 @@ class DecodeSession:
             done = None
             if account_only:
                 N.check(self._lib.wv_select(g, C.byref(args), ws, cs), "wv_select")
+                if spans:
+                    self._span_read_then_fetch(s)
             elif self.kernel_timing:
                 # per-kernel CUDA events on this stream: K1, K2, K3 levels L..2, K3 level 1
                 e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
                 e[0].record(s)
                 N.check(self._lib.wv_select(g, C.byref(args), ws, cs), "wv_select")
+                if spans:
+                    self._span_read_then_fetch(s)
                 e[1].record(s)
                 N.check(self._lib.wv_dequant_temporal(g, C.byref(args), ws, cs),
                         "wv_dequant_temporal")
@@ -556,6 +627,8 @@ class DecodeSession:
             elif time_stages:
                 evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 N.check(self._lib.wv_select(g, C.byref(args), ws, cs), "wv_select")
+                if spans:
+                    self._span_read_then_fetch(s)
                 evs[0].record(s)
                 N.check(self._lib.wv_dequant_temporal(g, C.byref(args), ws, cs),
                         "wv_dequant_temporal")
@@ -597,6 +670,14 @@ class DecodeSession:
             p.stats = st
             p.raw = r
             self.bytes_fetched += int(r.fetched_bytes)
+            if self.residency == "spans":
+                job = self._spanq.jobs[p.slot]
+                if job.done and job.bytes_read:
+                    self.reader.io_trace.append((p.set_index, int(job.bytes_read)))
+                if job.done and job.status:
+                    raise CorruptStreamError(
+                        f"span read failed ({N.status_name(job.status)}): BlockEnd table "
+                        "inconsistent with the file")
             if not p.account_only:
                 self._stats.bytes_loaded += st.bytes_loaded
                 self._stats.records_processed += st.records_processed

@@ -503,6 +503,16 @@ def test_span_streaming_residency(wv, tmp_path):
         _decode(b, frame, mode, mask, sc)
         assert b.bytes_fetched == again
     assert 0 < b.bytes_fetched <= total_records
+    # the file reads: the BlockEnd table, then the coalesced spans of the
+    # blocks a decode newly needs -- one viewport decode reads far less than
+    # the set's records
+    assert len(b.reader.io_trace) > h.num_sets
+    with wv.DecodeSession(path, residency="spans") as c:
+        pose = wv.CameraPose(yaw=30, pitch=10)
+        c.decode_viewport(1, wv.stereo_mask(pose, (h.mask_w, h.mask_h)))
+        trace = c.reader.io_trace
+        assert trace[0] == (0, h.table_bytes) and len(trace) == 2 and trace[1][0] == 0
+        assert 0 < trace[1][1] < 0.8 * (a.reader.set_meta[0].payload_length - h.table_bytes)
     # device path (graph replay with the fetch step)
     out_a = torch.empty((2, 256, 256, 3), dtype=torch.uint8, device="cuda")
     out_b = torch.empty_like(out_a)

@@ -340,3 +340,64 @@ def test_q255_table_matches_numpy():
     got = np.array([int(x, 16) for x in re.findall(r"0x([0-9a-f]{8})u", body)], np.uint32)
     want = (np.arange(256, dtype=np.float32) / np.float32(255.0)).view(np.uint32)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("name", ["noise_bs16.wvv", "smooth_hq.wvv", "golden_stereo.wvv"])
+def test_spans_read_matches_load_blocks(lib, name):
+    """wv_spans_read (span streaming's file reader, host-only): the records
+    of the listed blocks land at their payload offsets, and the byte counts
+    follow VideoReader.load_blocks (fileio.py:346-390: spans per (t, run),
+    coalesced through 4 KiB gaps)."""
+    from paper_2208_10859_b200 import _native as N
+    from paper_2208_10859_b200.fileio import VideoReader
+    path = os.path.join(GOLDEN, name)
+    rng = np.random.default_rng(len(name))
+    with VideoReader(path) as r:
+        h = r.header
+        for si in range(h.num_sets):
+            m = r.set_meta[si]
+            full = bytes(r.read_set_payload(si))
+            table = np.frombuffer(full[:h.table_bytes], "<u8").reshape(h.inter_size, h.num_blocks)
+            ids = np.unique(rng.integers(0, h.num_blocks, max(1, h.num_blocks // 3))).astype(np.uint32)
+            ids = rng.permutation(ids)                       # any order, as the GPU lists them
+            buf = np.zeros(m.payload_length + 16, np.uint8)
+            buf[:h.table_bytes] = np.frombuffer(full[:h.table_bytes], np.uint8)
+            cnt = np.array([len(ids)], np.uint32)
+            fd = os.open(path, os.O_RDONLY)
+            try:
+                j = N.SpanJob(fd=fd, n=h.inter_size, nb=h.num_blocks,
+                              payload_offset=m.payload_offset, payload_bytes=m.payload_length,
+                              table_bytes=h.table_bytes, table=buf.ctypes.data, dst=buf.ctypes.data,
+                              ids=ids.ctypes.data, count=cnt.ctypes.data, coalesce_gap=4096)
+                br, bs = C.c_uint64(), C.c_uint64()
+                assert lib.wv_spans_read(C.byref(j), C.byref(br), C.byref(bs)) == 0
+            finally:
+                os.close(fd)
+            flat = table.reshape(-1)
+            srt = np.sort(ids)
+            runs, i = [], 0
+            while i < len(srt):
+                e = i
+                while e + 1 < len(srt) and srt[e + 1] == srt[e] + 1:
+                    e += 1
+                runs.append((int(srt[i]), int(srt[e])))
+                i = e + 1
+            spans = []
+            for t in range(h.inter_size):
+                for a, b in runs:
+                    k = t * h.num_blocks + a
+                    st = int(flat[k - 1]) if k else 0
+                    spans.append((st, int(flat[t * h.num_blocks + b])))
+            tb = h.table_bytes
+            for st, en in spans:                             # every record in place
+                assert bytes(buf[tb + st:tb + en]) == full[tb + st:tb + en]
+            merged = []
+            for st, en in sorted(spans):
+                if st >= en:
+                    continue
+                if merged and st - merged[-1][1] <= 4096:
+                    merged[-1][1] = max(merged[-1][1], en)
+                else:
+                    merged.append([st, en])
+            assert bs.value == sum(e - s for s, e in spans)
+            assert br.value == sum(e - s for s, e in merged)
