@@ -11,14 +11,16 @@ cmd="python bench.py --profile-only --warmup 4 --steps 1 --pipeline 1"
 $cmd
 $cmd --mode full
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_${tag}.csv $cmd > /dev/null
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_full_${tag}.csv $cmd --mode full > /dev/null
 cap() {  # name, kernel regex, skip, extra bench args
-  ncu --set full --import-source on --clock-control none -k regex:$2 -s $3 -c 1 -o $out/${tag}_$1 $cmd $4 > $out/${tag}_$1.log 2>&1 || tail -5 $out/${tag}_$1.log
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$2 -s $3 -c 1 -o $out/${tag}_$1 $cmd $4 > $out/${tag}_$1.log 2>&1 || tail -5 $out/${tag}_$1.log
 }
-cap k3_final k_level 11 ""
-cap k3_level2 k_level 10 ""
-cap k2 k_temporal 1 ""
-cap k4 persp 1 ""
-cap k1_cascade k_cascade 0 ""
-cap k3_final_full k_level 11 "--mode full"
-cap k2_full k_temporal 1 "--mode full"
+# per frame: k_level x L (levels L..2 are k_level<false>, level 1 k_level<true>)
+cap k3_final "k_level" 11 ""
+cap k3_level2 "k_level" 10 ""
+cap k2 "k_temporal" 1 ""
+cap k4 "k_perspective" 1 ""
+cap k1_cascade "k_cascade_direct" 1 ""
+cap k3_final_full "k_level" 11 "--mode full"
+cap k2_full "k_temporal" 1 "--mode full"
 ls -la $out
