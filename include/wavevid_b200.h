@@ -101,7 +101,9 @@ typedef struct wv_frame_args {
   const uint8_t* d_mask;          /* (mask_h, mask_w) bytes 0/1; unused for FULL */
   int32_t fovea[WV_MAX_LEVELS][4];/* FOVEATED: detail level k at [k-1]: r0, r1, c0, c1
                                      pixel window, half-open (decoding.py:147-150) */
-  const void* d_payload;          /* set payload: BlockEnd table (n*NB u64) + packed records, 16-B aligned */
+  const void* d_payload;          /* set payload: BlockEnd table (n*NB u64) + packed records, 16-B aligned
+                                     and readable up to the next 16-byte boundary past payload_bytes
+                                     (K2 stages record spans in 16-byte chunks) */
   uint64_t payload_bytes;
   const float* d_extrema;         /* (n, C, 4) float32 (fileio.py:123) */
   uint32_t* d_set_loaded;         /* NB-bit block bitmap of the set's cache entry */
@@ -159,6 +161,9 @@ int wv_decode_frame(const wv_geometry* g, const wv_frame_args* a, void* d_worksp
  * levels must run L..1 after wv_select/wv_dequant_temporal (timing, profiling). */
 int wv_synthesize_level(const wv_geometry* g, const wv_frame_args* a, void* d_workspace,
                         int level, void* stream);
+/* The same level reading the frame arguments already in the workspace
+ * descriptor (no argument copy on the stream: per-kernel timing). */
+int wv_synthesize_level_desc(const wv_geometry* g, void* d_workspace, int level, void* stream);
 
 int wv_render_perspective(const wv_view_args* views, int n_views, void* stream);
 

@@ -131,6 +131,15 @@ int wv_synthesize_level(const wv_geometry* g, const wv_frame_args* a, void* ws, 
   return launch_synthesis(lo, g, d, (uint8_t*)ws, (cudaStream_t)stream, level);
 }
 
+int wv_synthesize_level_desc(const wv_geometry* g, void* ws, int level, void* stream) {
+  Layout lo;
+  int st = build_layout(g, &lo);
+  if (st != WV_OK) return st;
+  if (!ws || level < 1 || level > lo.L) return WV_ERR_ARG;
+  const wv_frame_args* d = (const wv_frame_args*)((uint8_t*)ws + lo.desc);
+  return launch_synthesis(lo, g, d, (uint8_t*)ws, (cudaStream_t)stream, level);
+}
+
 int wv_desc_view(const wv_geometry* g, void* ws, void** d_desc) {
   Layout lo;
   int st = build_layout(g, &lo);

@@ -513,6 +513,10 @@ class DecodeSession:
                 ev_c.record(cur)
                 aux.wait_event(ev_c)
                 run(N.WV_STAGE_FOOTPRINT, aux)
+                # the finest footprint step needs the level-1 tile list, not
+                # K3: it runs beside synthesis and only K4 waits for it
+                aux.wait_event(ev_t)
+                run(N.WV_STAGE_FOOTPRINT_TILES, aux)
                 ev_f = torch.cuda.Event()
                 ev_f.record(aux)
                 if spans:
@@ -528,7 +532,6 @@ class DecodeSession:
                 cur.wait_event(ev_t)
                 run(N.WV_STAGE_SYNTH, cur)
                 cur.wait_event(ev_f)
-                run(N.WV_STAGE_FOOTPRINT_TILES, cur)
             elif spans:
                 run(N.WV_STAGE_SELECT, cur)
                 N.check(self._lib.wv_span_queue_enqueue(
@@ -613,15 +616,18 @@ class DecodeSession:
                 if spans:
                     self._span_read_then_fetch(s)
                 e[1].record(s)
-                N.check(self._lib.wv_dequant_temporal(g, C.byref(args), ws, cs),
-                        "wv_dequant_temporal")
+                N.check(self._lib.wv_decode_stages_desc(g, args.mode, args.flags,
+                                                        N.WV_STAGE_DEQUANT, ws, cs),
+                        "wv_decode_stages_desc")
                 e[2].record(s)
+                # (the arguments are in the descriptor since wv_dequant_temporal:
+                # the level launches are timed without an argument copy)
                 for k in range(self.header.levels, 1, -1):
-                    N.check(self._lib.wv_synthesize_level(g, C.byref(args), ws, k, cs),
-                            "wv_synthesize_level")
+                    N.check(self._lib.wv_synthesize_level_desc(g, ws, k, cs),
+                            "wv_synthesize_level_desc")
                 e[3].record(s)
-                N.check(self._lib.wv_synthesize_level(g, C.byref(args), ws, 1, cs),
-                        "wv_synthesize_level")
+                N.check(self._lib.wv_synthesize_level_desc(g, ws, 1, cs),
+                        "wv_synthesize_level_desc")
                 e[4].record(s)
                 self.kernel_events.append(e)
             elif time_stages:
