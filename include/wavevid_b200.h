@@ -150,6 +150,11 @@ const char* wv_status_string(int status);
 
 /* Bytes of device workspace one decode stream needs for this geometry. */
 int wv_workspace_bytes(const wv_geometry* g, uint64_t* bytes);
+/* Bytes of a selection-only workspace: enough for wv_select with
+ * WV_FLAG_ACCOUNT_ONLY (and WV_STAGE_FETCH through wv_decode_stages_desc) on
+ * a second stream, e.g. prefetching the next set beside the current decodes
+ * (DecodeSession.advance, decoding.py:335-354).  Zero it once. */
+int wv_workspace_bytes_select(const wv_geometry* g, uint64_t* bytes);
 /* Zero the workspace (coefficient plane, dirty maps). Call once after allocation. */
 int wv_workspace_reset(const wv_geometry* g, void* d_workspace, void* stream);
 

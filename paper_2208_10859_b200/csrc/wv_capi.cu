@@ -52,6 +52,15 @@ int wv_workspace_bytes(const wv_geometry* g, uint64_t* bytes) {
   return WV_OK;
 }
 
+int wv_workspace_bytes_select(const wv_geometry* g, uint64_t* bytes) {
+  Layout lo;
+  if (!bytes) return WV_ERR_ARG;
+  int st = build_layout(g, &lo);
+  if (st != WV_OK) return st;
+  *bytes = lo.select_bytes;
+  return WV_OK;
+}
+
 int wv_workspace_reset(const wv_geometry* g, void* ws, void* stream) {
   Layout lo;
   int st = build_layout(g, &lo);

@@ -54,6 +54,7 @@ struct Layout {
   uint64_t ybuf[WV_MAX_LEVELS + 1];      // level k (1..L-1): C x (H>>k) x pitch[k] f32
   int ypitch[WV_MAX_LEVELS + 1];
   uint64_t mbits;                        // low-res mask as bit rows: mh x ceil(mw/32) u32
+  uint64_t select_bytes;                 // prefix holding all selection state (wv_select alone)
   uint64_t total;
 };
 
@@ -107,13 +108,16 @@ inline int build_layout(const wv_geometry* g, Layout* o) {
   o->desc_mask = (sizeof(wv_frame_args) + 4 * sizeof(wv_view_args) + 15) & ~size_t(15);
   o->desc_bytes = o->desc_mask + (uint64_t(g->mask_h) * g->mask_w + 15) / 16 * 16;
   o->desc = take(o->desc_bytes);
+  o->mbits = take(uint64_t(g->mask_h) * ((g->mask_w + 31) / 32) * 4);
+  // everything above is selection state; the synthesis buffers come last, so
+  // a selection-only workspace (prefetch accounting) is a prefix
+  o->select_bytes = off;
   o->plane = take(uint64_t(C) * H * W * 4);
   for (int k = 1; k < L; ++k) {
     int cols = W >> k;
     o->ypitch[k] = (cols + 3) & ~3;
     o->ybuf[k] = take(uint64_t(C) * (H >> k) * o->ypitch[k] * 4);
   }
-  o->mbits = take(uint64_t(g->mask_h) * ((g->mask_w + 31) / 32) * 4);
   o->total = off;
   return WV_OK;
 }

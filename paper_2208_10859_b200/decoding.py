@@ -141,11 +141,36 @@ class _Entry:
 
 class _Pending:
     __slots__ = ("slot", "set_index", "entry", "existed", "may_evict", "event", "ev",
-                 "account_only", "stats", "raw")
+                 "account_only", "stats", "raw", "spanq")
 
     def __init__(self):
         self.stats = None
         self.raw = None
+        self.spanq = None
+
+
+class _Prefetcher:
+    """Span residency's prefetch engine (DecodeSession.advance,
+    decoding.py:335-354): a selection-only workspace, its own descriptor,
+    fetch-list buffers and read queue, all driven on the session's copy
+    stream -- the next set's block selection, file reads and host -> HBM
+    copies overlap the current set's decodes on the session stream."""
+
+    def __init__(self, sess):
+        lib, g = sess._lib, sess._geom
+        nbytes = C.c_uint64()
+        N.check(lib.wv_workspace_bytes_select(C.byref(g), C.byref(nbytes)),
+                "wv_workspace_bytes_select")
+        h = sess.header
+        with torch.cuda.stream(sess._copy_stream):
+            self.ws = torch.zeros(int(nbytes.value), dtype=torch.uint8, device=sess.device)
+            self.mask = torch.zeros(h.mask_h * h.mask_w, dtype=torch.uint8, device=sess.device)
+        self.mask_host = torch.zeros(h.mask_h * h.mask_w, dtype=torch.uint8).pin_memory()
+        self.args_host = torch.zeros(_FA_BYTES, dtype=torch.uint8).pin_memory()
+        self.args = N.FrameArgs.from_address(self.args_host.data_ptr())
+        self.flist = torch.zeros(max(1, h.num_blocks), dtype=torch.int32).pin_memory()
+        self.fcount = torch.zeros(4, dtype=torch.int32).pin_memory()
+        self.spanq = N.SpanQueue()
 
 
 class DeviceFrame:
@@ -287,6 +312,8 @@ class DecodeSession:
         self._stats = SessionStats()
         self._prefetch_thread: threading.Thread | None = None
         self._prefetch_job = None
+        self._prefetcher = None          # spans residency: created by the first advance()
+        self._prefetch_ready: dict = {}  # set -> event of its prefetch on the copy stream
         self.time_stages = True
         self.kernel_timing = False
         self.kernel_events: list = []
@@ -328,9 +355,13 @@ class DecodeSession:
                 self.reader.read_set_payload(set_index, memoryview(host.numpy()[:n]))
         return host
 
-    def _push_span_job(self, set_index: int, host: torch.Tensor, slot: int) -> None:
+    def _push_span_job(self, set_index: int, host: torch.Tensor, slot: int,
+                       q=None, flist=None, fcount=None) -> None:
         """Queue the file read of this frame's fetch list (consumed in stream
         order by the host function that wv_span_queue_enqueue placed)."""
+        q = self._spanq if q is None else q
+        flist = self._h_flist if flist is None else flist
+        fcount = self._h_fcount if fcount is None else fcount
         h = self.header
         tb = h.table_bytes
         j = N.SpanJob()
@@ -340,9 +371,9 @@ class DecodeSession:
         j.table_bytes = tb
         j.table = host.data_ptr()
         j.dst = host.data_ptr()
-        j.ids, j.count = self._h_flist.data_ptr(), self._h_fcount.data_ptr()
+        j.ids, j.count = flist.data_ptr(), fcount.data_ptr()
         j.coalesce_gap = COALESCE_GAP
-        N.check(self._lib.wv_span_queue_push(C.byref(self._spanq), C.byref(j), slot),
+        N.check(self._lib.wv_span_queue_push(C.byref(q), C.byref(j), slot),
                 "wv_span_queue_push")
 
     def _span_read_then_fetch(self, stream) -> None:
@@ -368,7 +399,7 @@ class DecodeSession:
         self._resident.pop(set_index, None)
         self._make_resident(set_index, host)
 
-    def _make_resident(self, set_index: int, host: torch.Tensor | None = None):
+    def _make_resident(self, set_index: int, host: torch.Tensor | None = None, stream=None):
         if set_index in self._resident:
             self._resident.move_to_end(set_index)
             return self._resident[set_index]
@@ -377,7 +408,7 @@ class DecodeSession:
         meta = self.reader.set_meta[set_index]
         ext_host = torch.from_numpy(np.ascontiguousarray(meta.extrema, np.float32)).pin_memory()
         fetched = None
-        with torch.cuda.stream(self.stream):
+        with torch.cuda.stream(stream or self.stream):
             dev = torch.empty(host.numel(), dtype=torch.uint8, device=self.device)
             if self.residency == "set":
                 dev.copy_(host, non_blocking=True)
@@ -574,6 +605,9 @@ class DecodeSession:
         fast = not (account_only or self.kernel_timing or time_stages)
         # the graph fast path enqueues through the C ABI with the stream
         # passed explicitly; only the other paths issue torch ops here
+        ready = self._prefetch_ready.pop(si, None)
+        if ready is not None:   # the set's prefetch (copy stream) precedes its decodes
+            s.wait_event(ready)
         with (_NO_CTX if fast else torch.cuda.stream(s)):
             ev0 = torch.cuda.Event(enable_timing=True) if time_stages else None
             if ev0 is not None:
@@ -677,7 +711,7 @@ class DecodeSession:
             p.raw = r
             self.bytes_fetched += int(r.fetched_bytes)
             if self.residency == "spans":
-                job = self._spanq.jobs[p.slot]
+                job = (p.spanq or self._spanq).jobs[p.slot]
                 if job.done and job.bytes_read:
                     self.reader.io_trace.append((p.set_index, int(job.bytes_read)))
                 if job.done and job.status:
@@ -867,6 +901,9 @@ class DecodeSession:
             return
         mask = self._check_mask(next_mask)
         self.join_prefetch()
+        if self.residency == "spans":
+            self._prefetch_spans(set_index, mask)
+            return
         job = {"set": set_index, "mask": mask, "host": None}
 
         def work():
@@ -876,6 +913,59 @@ class DecodeSession:
         self._prefetch_job = job
         self._prefetch_thread = threading.Thread(target=work, daemon=True)
         self._prefetch_thread.start()
+
+    def _prefetch_spans(self, si: int, mask: np.ndarray) -> None:
+        """Span residency: the next set's BlockEnd table, then -- on the copy
+        stream, with the selection-only workspace -- its block selection for
+        the predicted mask (accounted in the cache as the reference's
+        prefetch does), the file reads of those spans (stream-ordered host
+        function) and their copy to HBM.  The set's decodes wait for it."""
+        pf = self._prefetcher
+        if pf is None:
+            pf = self._prefetcher = _Prefetcher(self)
+        cs = self._copy_stream
+        h = self.header
+        # the previous prefetch's list / queue slot must be consumed first
+        for p in list(self._pending):
+            if p.spanq is pf.spanq:
+                self._settle_until(p)
+        dev, ext, keep = self._make_resident(si, stream=cs)
+        entry, existed, may_evict = self._entry_for(si)
+        if len(self._pending) >= _RING:
+            self._settle_until(self._pending[0])
+        slot = self._slot
+        self._slot = (self._slot + 1) % _RING
+        np.copyto(pf.mask_host.numpy(), mask.reshape(-1), casting="unsafe")
+        a = pf.args
+        C.memset(C.addressof(a), 0, _FA_BYTES)
+        a.mode, a.t = N.WV_MODE_VIEWPORT, 0
+        a.flags = N.WV_FLAG_ACCOUNT_ONLY | N.WV_FLAG_FETCH
+        a.d_mask = pf.mask.data_ptr()
+        a.d_payload, a.payload_bytes = dev.data_ptr(), self.reader.payload_length(si)
+        a.d_extrema = ext.data_ptr()
+        a.d_set_loaded, a.d_set_bytes = entry.loaded.data_ptr(), entry.nbytes.data_ptr()
+        a.d_canvas, a.d_footprint = self._canvas.data_ptr(), self._footprint.data_ptr()
+        a.d_result = self._results[slot].data_ptr()
+        a.h_payload, a.d_fetched = keep[0].data_ptr(), keep[2].data_ptr()
+        a.h_fetch_list, a.h_fetch_count = pf.flist.data_ptr(), pf.fcount.data_ptr()
+        self._push_span_job(si, keep[0], slot, pf.spanq, pf.flist, pf.fcount)
+        g, ws, css = C.byref(self._geom), C.c_void_p(pf.ws.data_ptr()), C.c_void_p(cs.cuda_stream)
+        with torch.cuda.stream(cs):
+            pf.mask.copy_(pf.mask_host, non_blocking=True)
+            N.check(self._lib.wv_select(g, C.byref(a), ws, css), "wv_select")
+            N.check(self._lib.wv_span_queue_enqueue(C.byref(pf.spanq), css),
+                    "wv_span_queue_enqueue")
+            N.check(self._lib.wv_decode_stages_desc(g, a.mode, a.flags, N.WV_STAGE_FETCH, ws, css),
+                    "wv_decode_stages_desc")
+            self._results_host[slot].copy_(self._results[slot], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(cs)
+        p = _Pending()
+        p.slot, p.set_index, p.entry, p.existed, p.may_evict = slot, si, entry, existed, may_evict
+        p.event, p.ev, p.account_only, p.spanq = done, (None, None), True, pf.spanq
+        self._pending.append(p)
+        self._n_may_evict += bool(may_evict)
+        self._prefetch_ready[si] = done
 
     def join_prefetch(self):
         if self._prefetch_thread is not None:

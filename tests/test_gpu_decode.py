@@ -603,3 +603,39 @@ def test_eye_split_equals_whole_frame(wv, clip):
             assert torch.equal(oute[e][0], outw[e]), (i, e, "eye image")
     for s in [whole] + eyes:
         s.close()
+
+
+@pytest.mark.parametrize("name", ["smooth_hq.wvv", "golden_stereo.wvv"])
+def test_prefetch_spans_overlapped(wv, name):
+    """advance() under span residency (decoding.py:335-354): the next set's
+    selection, file reads and HBM copies run on the copy stream with the
+    selection-only workspace; the next set's decodes then equal a
+    whole-set-residency session's, call for call, including the cache
+    accounting of the prefetched blocks, and its file reads are spans."""
+    import torch
+    path = os.path.join(GOLDEN, name)
+    with wv.DecodeSession(path) as ref_s, wv.DecodeSession(path, residency="spans") as s:
+        h = s.header
+        pose = wv.CameraPose(yaw=20, pitch=5)
+        m = (wv.stereo_mask(pose, (h.mask_w, h.mask_h)) if h.stereo
+             else wv.viewport_to_mask(pose, (h.mask_w, h.mask_h)))
+        big = np.ones_like(m)
+        for sess in (ref_s, s):
+            sess.decode_viewport(0, m)
+            sess.advance(0, m)
+        # decodes of the current set run while the prefetch is in flight
+        out = torch.empty((2 if h.stereo else 1, 64, 64, h.channels), dtype=torch.uint8,
+                          device="cuda")
+        s.decode_render_device(1, "viewport", m, pose, (64, 64), out)
+        for sess in (ref_s, s):
+            sess.join_prefetch()
+        n = h.inter_size
+        for frame, mask in ((n, m), (n + 1, big), (n + 2, m)):
+            a = ref_s.decode_viewport(frame, mask)
+            b = s.decode_viewport(frame, mask)
+            np.testing.assert_array_equal(b[0], a[0])
+            np.testing.assert_array_equal(b[1], a[1])
+            assert (b[2].bytes_loaded, b[2].records_processed) == (
+                a[2].bytes_loaded, a[2].records_processed)
+        reads = [v for si, v in s.reader.io_trace if si == 1]
+        assert reads[0] == h.table_bytes and len(reads) >= 2
