@@ -605,7 +605,7 @@ def test_eye_split_equals_whole_frame(wv, clip):
         s.close()
 
 
-@pytest.mark.parametrize("name", ["smooth_hq.wvv", "golden_stereo.wvv"])
+@pytest.mark.parametrize("name", ["smooth_hq.wvv", "smooth_n8.wvv"])
 def test_prefetch_spans_overlapped(wv, name):
     """advance() under span residency (decoding.py:335-354): the next set's
     selection, file reads and HBM copies run on the copy stream with the
@@ -631,6 +631,8 @@ def test_prefetch_spans_overlapped(wv, name):
             sess.join_prefetch()
         n = h.inter_size
         for frame, mask in ((n, m), (n + 1, big), (n + 2, m)):
+            if frame >= h.frame_count:
+                continue
             a = ref_s.decode_viewport(frame, mask)
             b = s.decode_viewport(frame, mask)
             np.testing.assert_array_equal(b[0], a[0])
