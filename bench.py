@@ -444,7 +444,7 @@ def run_ours(args):
             gather(p_)
             with torch.cuda.stream(ss.stream):
                 host_outs[p_].copy_(results[p_], non_blocking=True)
-            bi += (pinned[s].numel() if args.residency == "set" else h.table_bytes)
+            bi += (pinned[s].numel() if args.residency == "set" else ss.table_upload_bytes)
             bi += h.mask_w * h.mask_h if mode != "full" else 0
             bo += host_outs[p_].numel()
         for ss in sessions[1:]:

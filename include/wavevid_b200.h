@@ -295,6 +295,12 @@ int wv_span_queue_push(wv_span_queue* q, const wv_span_job* job, uint32_t slot);
  * (cudaLaunchHostFunc; capturable into a CUDA graph, where every replay
  * consumes the next job). */
 int wv_span_queue_enqueue(wv_span_queue* q, void* stream);
+/* The BlockEnd table from per-(t, block) record counts (n_entries = n * NB,
+ * row major): d_table[i] = record_size * (counts[0] + ... + counts[i]), the
+ * cumulative ends of fileio.py:157-162.  Span residency uploads the 2-byte
+ * counts (a quarter of the table) and rebuilds the table in HBM. */
+int wv_table_expand(const uint16_t* d_counts, uint64_t n_entries, int record_size,
+                    uint64_t* d_table, void* stream);
 /* Device views of the fetch list of the last select (k_blocks output). */
 int wv_fetch_list_view(const wv_geometry* g, void* d_workspace, uint32_t** d_list,
                        uint32_t** d_count);

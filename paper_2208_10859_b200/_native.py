@@ -32,7 +32,7 @@ EXPORTS = ["wv_abi_version", "wv_status_string", "wv_workspace_bytes", "wv_works
            "wv_encode_payload_capacity", "wv_encode_set", "wv_enqueue_frame",
            "wv_desc_layout", "wv_synthesize_2d", "wv_spans_read", "wv_span_queue_push",
            "wv_span_queue_enqueue", "wv_fetch_list_view", "wv_synthesize_level_desc",
-           "wv_workspace_bytes_select"]
+           "wv_workspace_bytes_select", "wv_table_expand"]
 
 
 class Geometry(C.Structure):

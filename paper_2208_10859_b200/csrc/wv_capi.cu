@@ -240,6 +240,12 @@ int wv_synthesize_2d(const wv_geometry* g, const float* d_pyramid, float* d_out,
   return launch_synthesis_f32(lo, d_fa, w, d_out, s);
 }
 
+int wv_table_expand(const uint16_t* d_counts, uint64_t n_entries, int record_size,
+                    uint64_t* d_table, void* stream) {
+  if (!d_counts || !d_table || record_size < 1 || n_entries == 0) return WV_ERR_ARG;
+  return launch_table_expand(d_counts, n_entries, record_size, d_table, (cudaStream_t)stream);
+}
+
 int wv_desc_layout(const wv_geometry* g, uint64_t* mask_offset, uint64_t* slot_bytes) {
   Layout lo;
   int st = build_layout(g, &lo);

@@ -182,6 +182,8 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
                   const wv_frame_args* d_fa, uint8_t* ws, cudaStream_t s,
                   int stages = WV_STAGE_SELECT);
 int launch_fetch(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStream_t s);
+int launch_table_expand(const uint16_t* d_counts, uint64_t n, int rs, uint64_t* d_table,
+                        cudaStream_t s);
 int launch_temporal(const Layout& lo, const wv_geometry* g, int mode, const wv_frame_args* d_fa,
                     uint8_t* ws, cudaStream_t s);
 int launch_synthesis(const Layout& lo, const wv_geometry* g, const wv_frame_args* d_fa,

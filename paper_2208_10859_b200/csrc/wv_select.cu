@@ -1193,4 +1193,52 @@ int launch_fetch(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStr
   return WV_OK;
 }
 
+// ------------------------------------------------------ compact BlockEnd table
+// ends[i] = rs * (counts[0] + ... + counts[i]) (the BlockEnd table's
+// cumulative record ends, fileio.py:157-162), rebuilt on the device from
+// per-(t, block) record counts so span residency uploads 2 bytes per entry
+// instead of 8.  One CTA: each thread sums a contiguous run of entries, a
+// block-wide exclusive scan of the run sums, then each thread writes its run.
+__global__ void __launch_bounds__(1024) k_table_expand(const uint16_t* __restrict__ counts,
+                                                       uint64_t n, int rs,
+                                                       unsigned long long* __restrict__ ends) {
+  __shared__ unsigned long long wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const uint64_t b0 = min(n, (uint64_t)tid * per), b1 = min(n, b0 + per);
+  unsigned long long s = 0;
+  for (uint64_t i = b0; i < b1; ++i) s += counts[i];
+  unsigned long long inc = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, w, o);
+      if (lane >= o) w += u;
+    }
+    wsum[lane] = w;   // inclusive over warps
+  }
+  __syncthreads();
+  unsigned long long run = inc - s + (wid ? wsum[wid - 1] : 0ull);   // exclusive prefix
+  for (uint64_t i = b0; i < b1; ++i) {
+    run += counts[i];
+    ends[i] = run * (unsigned long long)rs;
+  }
+}
+
+int launch_table_expand(const uint16_t* d_counts, uint64_t n, int rs, uint64_t* d_table,
+                        cudaStream_t s) {
+  WV_CUDA(launch_k(k_table_expand, dim3(1), dim3(1024), 0, s, d_counts, n, rs,
+                   (unsigned long long*)d_table));
+  WV_CUDA(cudaGetLastError());
+  return WV_OK;
+}
+
 }  // namespace wv

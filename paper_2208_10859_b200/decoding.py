@@ -313,6 +313,7 @@ class DecodeSession:
         self._prefetch_thread: threading.Thread | None = None
         self._prefetch_job = None
         self._prefetcher = None          # spans residency: created by the first advance()
+        self._counts_cache: dict = {}    # spans residency: set -> (host payload, u16 counts)
         self._prefetch_ready: dict = {}  # set -> event of its prefetch on the copy stream
         self.time_stages = True
         self.kernel_timing = False
@@ -354,6 +355,33 @@ class DecodeSession:
             else:
                 self.reader.read_set_payload(set_index, memoryview(host.numpy()[:n]))
         return host
+
+    def _table_counts(self, set_index: int, host: torch.Tensor):
+        """Per-(t, block) record counts of a set's BlockEnd table as pinned
+        u16 (a quarter of the table's bytes), or None when the table is not
+        monotone / record-aligned / small enough (then it is uploaded as is,
+        so a corrupt table still reports the reference's errors)."""
+        hit = self._counts_cache.get(set_index)
+        if hit is not None and hit[0] is host:
+            return hit[1]
+        h = self.header
+        ends = np.frombuffer(host.numpy()[: h.table_bytes].tobytes(), dtype="<u8")
+        rs = h.record_size
+        out = None
+        if ends.size and np.all(ends[1:] >= ends[:-1]):
+            d = np.diff(ends, prepend=np.uint64(0))
+            if not np.any(d % rs) and int(d.max()) // rs < 65536:
+                out = torch.from_numpy((d // rs).astype(np.uint16).view(np.int16)).pin_memory()
+        self._counts_cache[set_index] = (host, out)
+        return out
+
+    @property
+    def table_upload_bytes(self) -> int:
+        """Host -> HBM bytes of one set's BlockEnd table under span residency
+        (the compact counts when the table allows it)."""
+        h = self.header
+        return h.table_bytes // 4 if self._counts_cache and all(
+            v[1] is not None for v in self._counts_cache.values()) else h.table_bytes
 
     def _push_span_job(self, set_index: int, host: torch.Tensor, slot: int,
                        q=None, flist=None, fcount=None) -> None:
@@ -418,7 +446,17 @@ class DecodeSession:
                 # them would report a corrupt stream).
                 tb = self.header.table_bytes
                 dev.fill_(0xFF)
-                dev[:tb].copy_(host[:tb], non_blocking=True)
+                counts = self._table_counts(set_index, host)
+                if counts is None:   # not a well-formed table: upload it as it is
+                    dev[:tb].copy_(host[:tb], non_blocking=True)
+                else:
+                    # 2-byte record counts, cumulative ends rebuilt in HBM
+                    dc = torch.empty(counts.numel(), dtype=torch.int16, device=self.device)
+                    dc.copy_(counts, non_blocking=True)
+                    N.check(self._lib.wv_table_expand(
+                        C.c_void_p(dc.data_ptr()), C.c_uint64(counts.numel()),
+                        self.header.record_size, C.c_void_p(dev.data_ptr()),
+                        C.c_void_p(torch.cuda.current_stream().cuda_stream)), "wv_table_expand")
                 fetched = torch.zeros(max(1, (self.header.num_blocks + 31) // 32),
                                       dtype=torch.int32, device=self.device)
             ext = torch.empty(ext_host.shape, dtype=torch.float32, device=self.device)

@@ -641,3 +641,25 @@ def test_prefetch_spans_overlapped(wv, name):
                 a[2].bytes_loaded, a[2].records_processed)
         reads = [v for si, v in s.reader.io_trace if si == 1]
         assert reads[0] == h.table_bytes and len(reads) >= 2
+
+
+@pytest.mark.parametrize("name", ["noise_bs16.wvv", "golden_float.wvv", "smooth_n8.wvv"])
+def test_table_expand_rebuilds_blockend_table(wv, name):
+    """wv_table_expand (span residency's compact table upload): the u16
+    record counts expand to the file's BlockEnd table bit for bit."""
+    import ctypes as C
+    import torch
+    from paper_2208_10859_b200 import _native as N
+    lib = N.load()
+    with wv.VideoReader(os.path.join(GOLDEN, name)) as r:
+        h = r.header
+        for si in range(h.num_sets):
+            raw = bytes(r.read_set_payload(si))[: h.table_bytes]
+            ends = np.frombuffer(raw, "<u8")
+            counts = (np.diff(ends, prepend=np.uint64(0)) // h.record_size).astype(np.uint16)
+            dc = torch.from_numpy(counts.view(np.int16)).cuda()
+            out = torch.zeros(ends.size, dtype=torch.int64, device="cuda")
+            assert lib.wv_table_expand(C.c_void_p(dc.data_ptr()), C.c_uint64(ends.size),
+                                       h.record_size, C.c_void_p(out.data_ptr()), None) == 0
+            torch.cuda.synchronize()
+            assert out.cpu().numpy().view(np.uint64).tobytes() == raw
