@@ -245,7 +245,13 @@ struct LevelArgs {
                        // alignment); else the boxes are filled with plain loads
   const float* ll_ptr; int ll_pitch, ll_rows;   // LDG fallback sources
   const float* plane; int plane_w, plane_h;
+  const uint8_t* bstate;   // K2's per-block state: 0 = the plane block is all +0.0
+  int bs_log2, nbx;        // plane block size (log2) and blocks per plane row
 };
+
+#ifndef WV_K3_SKIP0
+#define WV_K3_SKIP0 1   // detail boxes whose plane blocks are all zero are not loaded
+#endif
 
 // Items are (tile, channel).  Column pass: TY/SEGLEN_C segments x BOX_W
 // columns (each segment lifts SEGLEN_C output row pairs from its own 2-row
@@ -302,6 +308,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   float2* outb = reinterpret_cast<float2*>(smem);
   constexpr bool PF = FINAL;   // next item's boxes issued after the column pass
   __shared__ uint64_t bar;
+  __shared__ uint32_t s_skip;   // detail boxes of the loaded item that are all zero
 
   const int tid = threadIdx.x;
   if (tid == 0) mbar_init(&bar, 1);
@@ -321,12 +328,30 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     // B200, driver 580): x starts at ax-4 clamped to 0
     const int oy = max(ty * TY - HALO, 0), ox = max(tx * TX - XPAD, 0);
     const int c = (int)(it - itile * C);
+    // sparse detail bands: a box whose plane blocks K2 left all +0.0 (block
+    // state 0) is not loaded; the column pass reads it as 0.0 (the plane
+    // holds +0.0 there, so the result is bit-identical)
+    uint32_t skip = 0u;
+    if (WV_K3_SKIP0 && a.bstate) {
+      const int r0 = oy, r1 = min(oy + BOX_H, a.bh) - 1;
+      const int c0 = ox, c1 = min(ox + BOX_W, a.bw) - 1;
+#pragma unroll
+      for (int q = 1; q < 4; ++q) {
+        const int py = (q >= 2) ? a.bh : 0, px = (q & 1) ? a.bw : 0;
+        bool zero = true;
+        for (int br = (py + r0) >> a.bs_log2; br <= ((py + r1) >> a.bs_log2) && zero; ++br)
+          for (int bc = (px + c0) >> a.bs_log2; bc <= ((px + c1) >> a.bs_log2); ++bc)
+            if (a.bstate[(size_t)br * a.nbx + bc]) { zero = false; break; }
+        if (zero) skip |= 1u << (q - 1);
+      }
+    }
+    s_skip = skip;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&bar, 4u * BOX_FLOATS * 4u);
+    mbar_expect_tx(&bar, (4u - __popc(skip)) * BOX_FLOATS * 4u);
     tma_load_3d(box, &tm_ll, ox, oy, c, &bar);
-    tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar);
-    tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar);
-    tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar);
+    if (!(skip & 1u)) tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar);
+    if (!(skip & 2u)) tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar);
+    if (!(skip & 4u)) tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar);
   };
 
   bool issued = false;   // the current item's boxes are already in flight
@@ -374,10 +399,12 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
       }
     }
     if (PF && tid == 0 && a.use_tma && nxt < nitems) nxt_entry = a.list[nxt / a.divC];
+    uint32_t skip = 0u;
     if (a.use_tma) {
       if (!issued) issue(item);
       mbar_wait(&bar, phase);
       phase ^= 1u;
+      skip = s_skip;   // written before the arrive that completed this phase
     } else {
       // tiny levels whose subband width is not a multiple of 4 floats
       for (int i = tid; i < 4 * BOX_FLOATS; i += NTHREADS) {
@@ -411,8 +438,8 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
               [&](int j, float2& s, float2& d) {
                 const int o = (rb + j) * BOX_W + lc;
                 WV_ASSERT(o >= 0 && o < BOX_FLOATS);
-                s = make_float2(bLL[o], bHL[o]);
-                d = make_float2(bLH[o], bHH[o]);
+                s = make_float2(bLL[o], (skip & 1u) ? 0.0f : bHL[o]);
+                d = make_float2((skip & 2u) ? 0.0f : bLH[o], (skip & 4u) ? 0.0f : bHH[o]);
               },
               [&](int p, float2 s3, float2 d3) {
                 WV_ASSERT(qb + p >= 0 && qb + p < TY && lc < CB_PITCH);
@@ -425,8 +452,8 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
               [&](int j, float2& s, float2& d) {
                 const int o = (j - oy) * BOX_W + lc;
                 WV_ASSERT(o >= 0 && o < BOX_FLOATS);
-                s = make_float2(bLL[o], bHL[o]);
-                d = make_float2(bLH[o], bHH[o]);
+                s = make_float2(bLL[o], (skip & 1u) ? 0.0f : bHL[o]);
+                d = make_float2((skip & 2u) ? 0.0f : bLH[o], (skip & 4u) ? 0.0f : bHH[o]);
               },
               [&](int p, float2 s3, float2 d3) {
                 const int q = p - ay;
@@ -606,7 +633,7 @@ int make_map(CUtensorMap* m, const float* base, int cols, int rows, int pitch, i
 
 // one level with the per-tile TMA-box kernel (k_level)
 int launch_tiles(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStream_t s, int k,
-                 int sms, float* f32_out = nullptr) {
+                 int sms, float* f32_out = nullptr, bool use_bstate = true) {
   const int L = lo.L, C = lo.C;
   float* plane = (float*)(ws + lo.plane);
   const uint32_t* counters = (const uint32_t*)(ws + lo.counters);
@@ -641,6 +668,10 @@ int launch_tiles(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStr
   la.plane = plane; la.plane_w = lo.W; la.plane_h = lo.H;
   la.list = (const uint32_t*)(ws + lo.tlist[k]);
   la.count = counters + CNT_TILES + k;
+  // (wv_synthesize_2d fills the plane itself: K2's block state does not describe it)
+  la.bstate = use_bstate ? ws + lo.bstate : nullptr;
+  la.bs_log2 = 31 - __builtin_clz((unsigned)lo.bs);
+  la.nbx = lo.nbx;
   const int ntiles = lo.nty[k] * lo.ntx[k];
   if (k > 1 || f32_out) {
     // mid levels into the next level's LL buffer; with f32_out level 1 too
@@ -687,7 +718,7 @@ int launch_synthesis_f32(const Layout& lo, const wv_frame_args* fa, uint8_t* ws,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   for (int k = lo.L; k >= 1; --k) {
-    const int st = launch_tiles(lo, fa, ws, s, k, sms, k == 1 ? f32_out : nullptr);
+    const int st = launch_tiles(lo, fa, ws, s, k, sms, k == 1 ? f32_out : nullptr, false);
     if (st != WV_OK) return st;
   }
   return WV_OK;
