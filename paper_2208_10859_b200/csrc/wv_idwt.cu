@@ -78,16 +78,41 @@ __device__ __forceinline__ uint32_t u8_rint(float x) {
 // d * (1/K) feeds the packed add (d[i-1] + d[i]) of the next lifting step; a
 // packed multiply there would be contracted into FFMA2 by ptxas, so the
 // scale is two scalar round-to-nearest multiplies (never contracted).
+#ifndef WV_LIFT_FTZ
+#define WV_LIFT_FTZ 0   // 1: paired flush-to-zero multiplies (3 instead of 4 ops per step)
+#endif
+#if WV_LIFT_FTZ
+// mul.rn.ftz.f32x2: ptxas does not contract an FTZ multiply into the
+// following non-FTZ add, so the products stay rounded and every step is
+// FADD2 + FMUL2 + FADD2.  Identical to the reference unless an input or a
+// product is subnormal (below 1.2e-38), which dequantised coefficients and
+// their lifting never produce.
+__device__ __forceinline__ float2 fmul2_ftz(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.ftz.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 dscale(float2 d, float2 ik) { return fmul2_ftz(d, ik); }
+#define WV_KMUL(a, b) fmul2_ftz(a, b)
+#else
 __device__ __forceinline__ float2 dscale(float2 d, float2 ik) {
   return make_float2(__fmul_rn(d.x, ik.x), __fmul_rn(d.y, ik.y));
 }
+#define WV_KMUL(a, b) __fmul2_rn(a, b)
+#endif
 // x - k*(y1 + y2), written as x + (-k)*(y1+y2): identical rounding.  The
 // final add is issued as two scalar FADDs: ptxas contracts a paired
 // mul.rn.f32x2 feeding add.rn.f32x2 into FFMA2 (observed with CUDA 12.9),
 // which would change the rounding; scalar adds keep the product rounded.
 __device__ __forceinline__ float2 lstep(float2 x, float2 nk, float2 y1, float2 y2) {
+#if WV_LIFT_FTZ
+  return __fadd2_rn(x, fmul2_ftz(nk, __fadd2_rn(y1, y2)));
+#else
   const float2 t = __fmul2_rn(nk, __fadd2_rn(y1, y2));
   return make_float2(__fadd_rn(x.x, t.x), __fadd_rn(x.y, t.y));
+#endif
 }
 
 // Inverse CDF 9/7 lifting of one line (two packed lines) over global
@@ -107,13 +132,13 @@ __device__ __forceinline__ void lift_line(int g0, int g1, int N, int a, int b, L
   // j = g0 (at the left border d1[-1] = d1[0]; elsewhere the value is a halo)
   load(g0, sr, dr);
   float2 d1m = dscale(dr, IK);
-  float2 s2m = lstep(__fmul2_rn(sr, KS), ND, d1m, d1m);
+  float2 s2m = lstep(WV_KMUL(sr, KS), ND, d1m, d1m);
   float2 d2mm = d1m, s3mm = s2m;
   if (g1 - g0 >= 2) {
     // j = g0 + 1 (at the left border d2[-1] = d2[0])
     load(g0 + 1, sr, dr);
     float2 d1 = dscale(dr, IK);
-    float2 s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);
+    float2 s2 = lstep(WV_KMUL(sr, KS), ND, d1m, d1);
     float2 d2 = lstep(d1m, NG, s2m, s2);
     s3mm = lstep(s2m, NB, d2, d2);
     d2mm = d2;
@@ -123,7 +148,7 @@ __device__ __forceinline__ void lift_line(int g0, int g1, int N, int a, int b, L
     for (int j = g0 + 2; j < g1; ++j) {
       load(j, sr, dr);
       d1 = dscale(dr, IK);
-      s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);   // s2[j]
+      s2 = lstep(WV_KMUL(sr, KS), ND, d1m, d1);   // s2[j]
       d2 = lstep(d1m, NG, s2m, s2);                   // d2[j-1]
       float2 s3 = lstep(s2m, NB, d2mm, d2);           // s3[j-1]
       float2 d3 = lstep(d2mm, NA, s3mm, s3);          // d3[j-2]
@@ -158,10 +183,10 @@ __device__ __forceinline__ void lift_interior(Load load, Emit emit) {
   float2 sr, dr;
   load(0, sr, dr);
   float2 d1m = dscale(dr, IK);
-  float2 s2m = __fmul2_rn(sr, KS);         // s2[0] is a halo value: never emitted
+  float2 s2m = WV_KMUL(sr, KS);         // s2[0] is a halo value: never emitted
   load(1, sr, dr);
   float2 d1 = dscale(dr, IK);
-  float2 s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);
+  float2 s2 = lstep(WV_KMUL(sr, KS), ND, d1m, d1);
   float2 d2mm = lstep(d1m, NG, s2m, s2);   // d2[0] (halo)
   float2 s3mm = s2;                        // s3[0] (halo)
   d1m = d1;
@@ -170,7 +195,7 @@ __device__ __forceinline__ void lift_interior(Load load, Emit emit) {
   for (int j = 2; j < LEN + 4; ++j) {
     load(j, sr, dr);
     d1 = dscale(dr, IK);
-    s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);   // s2[j]
+    s2 = lstep(WV_KMUL(sr, KS), ND, d1m, d1);   // s2[j]
     const float2 d2 = lstep(d1m, NG, s2m, s2);      // d2[j-1]
     const float2 s3 = lstep(s2m, NB, d2mm, d2);     // s3[j-1]
     if (j >= 4) emit(j - 2, s3mm, lstep(d2mm, NA, s3mm, s3));   // d3[j-2]
