@@ -147,10 +147,14 @@ struct ViewConst {
 #define K4_TILE_Y 32
 #endif
 constexpr int K4_TX = 32, K4_TY = K4_TILE_Y, K4_PPT = K4_TY / 8;
-constexpr int WIN_WORDS = 9216;                 // window capacity, source pixels (32-bit words)
+#ifndef K4_WIN_WORDS
+#define K4_WIN_WORDS (9216 * K4_TILE_Y / 32)
+#endif
+constexpr int WIN_WORDS = K4_WIN_WORDS;         // window capacity, source pixels (32-bit words)
 constexpr int BOX_MAX_W = 128;                  // widest box the footprint test covers
 constexpr int OST_PITCH = K4_TX * 4;            // bytes per staged output row (C <= 4)
 constexpr int OST_VIEW = K4_TY * OST_PITCH;
+constexpr int K4_SMEM = WIN_WORDS * 4 + 2 * OST_VIEW;
 #ifndef K4_MIN_BLOCKS
 #define K4_MIN_BLOCKS 4
 #endif
@@ -563,8 +567,10 @@ __global__ void __launch_bounds__(256, K4_MIN_BLOCKS) k_perspective(const __grid
                                                      int shared_n) {
   pdl_sync();
   __shared__ ViewConst vc;
-  __shared__ __align__(16) uint32_t win[WIN_WORDS];
-  __shared__ __align__(16) uint8_t ost[2 * OST_VIEW];
+  // window + staged output tiles in dynamic shared memory (K4_SMEM bytes)
+  extern __shared__ __align__(16) uint32_t k4_dyn[];
+  uint32_t* win = k4_dyn;
+  uint8_t* ost = reinterpret_cast<uint8_t*>(k4_dyn + WIN_WORDS);
   __shared__ __align__(16) uint32_t s_ok[8];
   __shared__ int s_box[2][4];   // candidate-tap box: xmin, xmax, ymin, ymax
   const int vz = shared_n > 0 ? 0 : blockIdx.z;
@@ -674,7 +680,8 @@ int persistent_grid(K kernel, int ntiles) {
   int dev = 0, sms = 148, occ = K4_MIN_BLOCKS;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, 0);
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, K4_SMEM);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, K4_SMEM);
   return max(1, min(ntiles, sms * max(occ, 1)));
 }
 
@@ -704,7 +711,8 @@ int launch_perspective(const wv_view_args* views, int n, cudaStream_t s) {
   dim3 block(32, 8);
   dim3 grid(persistent_grid(k_perspective<false>, cdiv(mw, K4_TX) * cdiv(mh, K4_TY)), 1,
             shared ? 1 : n);
-  WV_CUDA(launch_k(k_perspective<false>, dim3(grid), dim3(block), 0, s, pv, nullptr, shared ? n : 0));
+  WV_CUDA(launch_k(k_perspective<false>, dim3(grid), dim3(block), (size_t)K4_SMEM, s, pv, nullptr,
+                   shared ? n : 0));
   WV_CUDA(cudaGetLastError());
   return WV_OK;
 }
@@ -717,7 +725,8 @@ int launch_perspective_dev(const wv_view_args* d_views, int n, int max_w, int ma
   dim3 block(32, 8);
   dim3 grid(persistent_grid(k_perspective<true>, cdiv(max_w, K4_TX) * cdiv(max_h, K4_TY)), 1,
             shared ? 1 : n);
-  WV_CUDA(launch_k(k_perspective<true>, dim3(grid), dim3(block), 0, s, none, d_views, shared ? n : 0));
+  WV_CUDA(launch_k(k_perspective<true>, dim3(grid), dim3(block), (size_t)K4_SMEM, s, none, d_views,
+                   shared ? n : 0));
   WV_CUDA(cudaGetLastError());
   return WV_OK;
 }
