@@ -78,41 +78,16 @@ __device__ __forceinline__ uint32_t u8_rint(float x) {
 // d * (1/K) feeds the packed add (d[i-1] + d[i]) of the next lifting step; a
 // packed multiply there would be contracted into FFMA2 by ptxas, so the
 // scale is two scalar round-to-nearest multiplies (never contracted).
-#ifndef WV_LIFT_FTZ
-#define WV_LIFT_FTZ 0   // 1: paired flush-to-zero multiplies (3 instead of 4 ops per step)
-#endif
-#if WV_LIFT_FTZ
-// mul.rn.ftz.f32x2: ptxas does not contract an FTZ multiply into the
-// following non-FTZ add, so the products stay rounded and every step is
-// FADD2 + FMUL2 + FADD2.  Identical to the reference unless an input or a
-// product is subnormal (below 1.2e-38), which dequantised coefficients and
-// their lifting never produce.
-__device__ __forceinline__ float2 fmul2_ftz(float2 a, float2 b) {
-  unsigned long long r;
-  asm("mul.rn.ftz.f32x2 %0, %1, %2;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
-  return *reinterpret_cast<float2*>(&r);
-}
-__device__ __forceinline__ float2 dscale(float2 d, float2 ik) { return fmul2_ftz(d, ik); }
-#define WV_KMUL(a, b) fmul2_ftz(a, b)
-#else
 __device__ __forceinline__ float2 dscale(float2 d, float2 ik) {
   return make_float2(__fmul_rn(d.x, ik.x), __fmul_rn(d.y, ik.y));
 }
-#define WV_KMUL(a, b) __fmul2_rn(a, b)
-#endif
 // x - k*(y1 + y2), written as x + (-k)*(y1+y2): identical rounding.  The
 // final add is issued as two scalar FADDs: ptxas contracts a paired
 // mul.rn.f32x2 feeding add.rn.f32x2 into FFMA2 (observed with CUDA 12.9),
 // which would change the rounding; scalar adds keep the product rounded.
 __device__ __forceinline__ float2 lstep(float2 x, float2 nk, float2 y1, float2 y2) {
-#if WV_LIFT_FTZ
-  return __fadd2_rn(x, fmul2_ftz(nk, __fadd2_rn(y1, y2)));
-#else
   const float2 t = __fmul2_rn(nk, __fadd2_rn(y1, y2));
   return make_float2(__fadd_rn(x.x, t.x), __fadd_rn(x.y, t.y));
-#endif
 }
 
 // Inverse CDF 9/7 lifting of one line (two packed lines) over global
@@ -132,13 +107,13 @@ __device__ __forceinline__ void lift_line(int g0, int g1, int N, int a, int b, L
   // j = g0 (at the left border d1[-1] = d1[0]; elsewhere the value is a halo)
   load(g0, sr, dr);
   float2 d1m = dscale(dr, IK);
-  float2 s2m = lstep(WV_KMUL(sr, KS), ND, d1m, d1m);
+  float2 s2m = lstep(__fmul2_rn(sr, KS), ND, d1m, d1m);
   float2 d2mm = d1m, s3mm = s2m;
   if (g1 - g0 >= 2) {
     // j = g0 + 1 (at the left border d2[-1] = d2[0])
     load(g0 + 1, sr, dr);
     float2 d1 = dscale(dr, IK);
-    float2 s2 = lstep(WV_KMUL(sr, KS), ND, d1m, d1);
+    float2 s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);
     float2 d2 = lstep(d1m, NG, s2m, s2);
     s3mm = lstep(s2m, NB, d2, d2);
     d2mm = d2;
@@ -148,7 +123,7 @@ __device__ __forceinline__ void lift_line(int g0, int g1, int N, int a, int b, L
     for (int j = g0 + 2; j < g1; ++j) {
       load(j, sr, dr);
       d1 = dscale(dr, IK);
-      s2 = lstep(WV_KMUL(sr, KS), ND, d1m, d1);   // s2[j]
+      s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);   // s2[j]
       d2 = lstep(d1m, NG, s2m, s2);                   // d2[j-1]
       float2 s3 = lstep(s2m, NB, d2mm, d2);           // s3[j-1]
       float2 d3 = lstep(d2mm, NA, s3mm, s3);          // d3[j-2]
@@ -183,10 +158,10 @@ __device__ __forceinline__ void lift_interior(Load load, Emit emit) {
   float2 sr, dr;
   load(0, sr, dr);
   float2 d1m = dscale(dr, IK);
-  float2 s2m = WV_KMUL(sr, KS);         // s2[0] is a halo value: never emitted
+  float2 s2m = __fmul2_rn(sr, KS);         // s2[0] is a halo value: never emitted
   load(1, sr, dr);
   float2 d1 = dscale(dr, IK);
-  float2 s2 = lstep(WV_KMUL(sr, KS), ND, d1m, d1);
+  float2 s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);
   float2 d2mm = lstep(d1m, NG, s2m, s2);   // d2[0] (halo)
   float2 s3mm = s2;                        // s3[0] (halo)
   d1m = d1;
@@ -195,7 +170,7 @@ __device__ __forceinline__ void lift_interior(Load load, Emit emit) {
   for (int j = 2; j < LEN + 4; ++j) {
     load(j, sr, dr);
     d1 = dscale(dr, IK);
-    s2 = lstep(WV_KMUL(sr, KS), ND, d1m, d1);   // s2[j]
+    s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);   // s2[j]
     const float2 d2 = lstep(d1m, NG, s2m, s2);      // d2[j-1]
     const float2 s3 = lstep(s2m, NB, d2mm, d2);     // s3[j-1]
     if (j >= 4) emit(j - 2, s3mm, lstep(d2mm, NA, s3mm, s3));   // d3[j-2]
@@ -270,13 +245,7 @@ struct LevelArgs {
                        // alignment); else the boxes are filled with plain loads
   const float* ll_ptr; int ll_pitch, ll_rows;   // LDG fallback sources
   const float* plane; int plane_w, plane_h;
-  const uint8_t* bstate;   // K2's per-block state: 0 = the plane block is all +0.0
-  int bs_log2, nbx;        // plane block size (log2) and blocks per plane row
 };
-
-#ifndef WV_K3_SKIP0
-#define WV_K3_SKIP0 1   // detail boxes whose plane blocks are all zero are not loaded
-#endif
 
 // Items are (tile, channel).  Column pass: TY/SEGLEN_C segments x BOX_W
 // columns (each segment lifts SEGLEN_C output row pairs from its own 2-row
@@ -311,7 +280,6 @@ __device__ __forceinline__ void row_map(int tid, int& i, int& sg) {
 #endif
 constexpr int OB4_PITCH = TX + 1;     // float4 units, odd
 static_assert(TY * OB4_PITCH * 16 <= 4 * BOX_SLOT, "float4 output tile must fit in the box region");
-constexpr int OUTB_BYTES = WV_K3_OUT4 ? TY * OB4_PITCH * 16 : TY * OB_PITCH * 8;
 constexpr int SMEM_MID = BOXSET + COL_BYTES;
 constexpr int SMEM_FIN = BOXSET + COL_BYTES;   // the u8 tile goes from registers to HBM
 
@@ -333,7 +301,6 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   float2* outb = reinterpret_cast<float2*>(smem);
   constexpr bool PF = FINAL;   // next item's boxes issued after the column pass
   __shared__ uint64_t bar;
-  __shared__ uint32_t s_skip;   // detail boxes of the loaded item that are all zero
 
   const int tid = threadIdx.x;
   if (tid == 0) mbar_init(&bar, 1);
@@ -343,10 +310,9 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   const uint32_t nitems = *a.count * (uint32_t)C;
   const int H = 2 * a.bh, W = 2 * a.bw;
 
-  // issue the four box loads of an item: warp 0 checks K2's block state of
-  // the detail boxes (one independent load per lane), lane 0 issues
+  // issue the four box loads of an item (elected thread)
   auto issue = [&](uint32_t it) {
-    if (tid >= 32) return;
+    if (tid != 0) return;
     const uint32_t itile = it / a.divC;
     const uint32_t tile = a.list[itile] & ~ZERO_FLAG;
     const int ty = (int)(tile / a.divN), tx = (int)tile - ty * a.ntx;
@@ -354,34 +320,12 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     // B200, driver 580): x starts at ax-4 clamped to 0
     const int oy = max(ty * TY - HALO, 0), ox = max(tx * TX - XPAD, 0);
     const int c = (int)(it - itile * C);
-    // sparse detail bands: a box whose plane blocks K2 left all +0.0 (block
-    // state 0) is not loaded; the column pass reads it as 0.0 (the plane
-    // holds +0.0 there, so the result is bit-identical).  Lane 9(q-1)+j
-    // checks block j (3 x 3 around the box) of subband q.
-    uint32_t skip = 0u;
-    if (WV_K3_SKIP0 && a.bstate) {
-      const int r0 = oy >> a.bs_log2, r1 = (min(oy + BOX_H, a.bh) - 1) >> a.bs_log2;
-      const int c0 = ox >> a.bs_log2, c1 = (min(ox + BOX_W, a.bw) - 1) >> a.bs_log2;
-      const int q = 1 + tid / 9, j = tid % 9;
-      const int br = r0 + j / 3, bc = c0 + j % 3;
-      bool nz = false;
-      if (tid < 27 && br <= r1 && bc <= c1) {
-        const int py = (q >= 2) ? (a.bh >> a.bs_log2) : 0, px = (q & 1) ? (a.bw >> a.bs_log2) : 0;
-        nz = __ldg(a.bstate + (size_t)(py + br) * a.nbx + px + bc) != 0;
-      }
-      const uint32_t m = __ballot_sync(0xFFFFFFFFu, nz);
-#pragma unroll
-      for (int qq = 0; qq < 3; ++qq)
-        if (!((m >> (9 * qq)) & 0x1FFu)) skip |= 1u << qq;
-    }
-    if (tid != 0) return;
-    s_skip = skip;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&bar, (4u - __popc(skip)) * BOX_FLOATS * 4u);
+    mbar_expect_tx(&bar, 4u * BOX_FLOATS * 4u);
     tma_load_3d(box, &tm_ll, ox, oy, c, &bar);
-    if (!(skip & 1u)) tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar);
-    if (!(skip & 2u)) tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar);
-    if (!(skip & 4u)) tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar);
+    tma_load_3d(box + BOX_SLOT / 4, &tm_det, a.bw + ox, oy, c, &bar);
+    tma_load_3d(box + 2 * BOX_SLOT / 4, &tm_det, ox, a.bh + oy, c, &bar);
+    tma_load_3d(box + 3 * BOX_SLOT / 4, &tm_det, a.bw + ox, a.bh + oy, c, &bar);
   };
 
   bool issued = false;   // the current item's boxes are already in flight
@@ -428,13 +372,11 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
         }
       }
     }
-    if (PF && tid < 32 && a.use_tma && nxt < nitems) nxt_entry = a.list[nxt / a.divC];
-    uint32_t skip = 0u;
+    if (PF && tid == 0 && a.use_tma && nxt < nitems) nxt_entry = a.list[nxt / a.divC];
     if (a.use_tma) {
       if (!issued) issue(item);
       mbar_wait(&bar, phase);
       phase ^= 1u;
-      skip = s_skip;   // written before the arrive that completed this phase
     } else {
       // tiny levels whose subband width is not a multiple of 4 floats
       for (int i = tid; i < 4 * BOX_FLOATS; i += NTHREADS) {
@@ -468,8 +410,8 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
               [&](int j, float2& s, float2& d) {
                 const int o = (rb + j) * BOX_W + lc;
                 WV_ASSERT(o >= 0 && o < BOX_FLOATS);
-                s = make_float2(bLL[o], (skip & 1u) ? 0.0f : bHL[o]);
-                d = make_float2((skip & 2u) ? 0.0f : bLH[o], (skip & 4u) ? 0.0f : bHH[o]);
+                s = make_float2(bLL[o], bHL[o]);
+                d = make_float2(bLH[o], bHH[o]);
               },
               [&](int p, float2 s3, float2 d3) {
                 WV_ASSERT(qb + p >= 0 && qb + p < TY && lc < CB_PITCH);
@@ -482,8 +424,8 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
               [&](int j, float2& s, float2& d) {
                 const int o = (j - oy) * BOX_W + lc;
                 WV_ASSERT(o >= 0 && o < BOX_FLOATS);
-                s = make_float2(bLL[o], (skip & 1u) ? 0.0f : bHL[o]);
-                d = make_float2((skip & 2u) ? 0.0f : bLH[o], (skip & 4u) ? 0.0f : bHH[o]);
+                s = make_float2(bLL[o], bHL[o]);
+                d = make_float2(bLH[o], bHH[o]);
               },
               [&](int p, float2 s3, float2 d3) {
                 const int q = p - ay;
@@ -497,8 +439,8 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     __syncthreads();
     if (PF && a.use_tma) {
       // the boxes are consumed: start the next item's loads now (only the
-      // issuing warp read nxt_entry and issues)
-      issued = !(nxt_entry & ZERO_FLAG);   // meaningful for warp 0 only
+      // elected thread read nxt_entry and issues)
+      issued = !(nxt_entry & ZERO_FLAG);   // meaningful for the elected thread only
       if (issued) issue(nxt);
     }
     // row pass: (segment, output row pair) per thread, two rows packed
@@ -663,7 +605,7 @@ int make_map(CUtensorMap* m, const float* base, int cols, int rows, int pitch, i
 
 // one level with the per-tile TMA-box kernel (k_level)
 int launch_tiles(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStream_t s, int k,
-                 int sms, float* f32_out = nullptr, bool use_bstate = true) {
+                 int sms, float* f32_out = nullptr) {
   const int L = lo.L, C = lo.C;
   float* plane = (float*)(ws + lo.plane);
   const uint32_t* counters = (const uint32_t*)(ws + lo.counters);
@@ -698,14 +640,6 @@ int launch_tiles(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStr
   la.plane = plane; la.plane_w = lo.W; la.plane_h = lo.H;
   la.list = (const uint32_t*)(ws + lo.tlist[k]);
   la.count = counters + CNT_TILES + k;
-  // zero-box skipping on the mid levels only: the finest level is issue- and
-  // latency-bound, and the check would delay its prefetched loads (measured:
-  // level 1 51.6 vs 51.3 us viewport, 303 vs 286 us full frame; levels 6..2
-  // 53.4 vs 57.9 and 139 vs 150 us).  wv_synthesize_2d fills the plane itself,
-  // so K2's block state does not describe it there.
-  la.bstate = (use_bstate && k > 1) ? ws + lo.bstate : nullptr;
-  la.bs_log2 = 31 - __builtin_clz((unsigned)lo.bs);
-  la.nbx = lo.nbx;
   const int ntiles = lo.nty[k] * lo.ntx[k];
   if (k > 1 || f32_out) {
     // mid levels into the next level's LL buffer; with f32_out level 1 too
@@ -752,7 +686,7 @@ int launch_synthesis_f32(const Layout& lo, const wv_frame_args* fa, uint8_t* ws,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   for (int k = lo.L; k >= 1; --k) {
-    const int st = launch_tiles(lo, fa, ws, s, k, sms, k == 1 ? f32_out : nullptr, false);
+    const int st = launch_tiles(lo, fa, ws, s, k, sms, k == 1 ? f32_out : nullptr);
     if (st != WV_OK) return st;
   }
   return WV_OK;
