@@ -214,6 +214,7 @@ def run_ours(args):
     from paper_2208_10859_b200.projection import CameraPose, stereo_mask, viewport_to_mask
     from paper_2208_10859_b200.sharding import assign, gather_views
     from paper_2208_10859_b200.replay import circle_trajectory
+    from paper_2208_10859_b200 import _native as N
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -397,20 +398,22 @@ def run_ours(args):
     tiles = mean([fo.result().n_tiles for fo in frames_out])
     sel_blocks = mean([fo.result().n_selected for fo in frames_out])
     C = h.channels
-    # K3 finest level, per launch: read 4 subband tiles (32x32 f32 each per
-    # channel) and write a 64x64 u8 tile per channel (SURVEY §8d K3+K4 terms)
-    alg = tiles * (4 * 32 * 32 * 4 * C + 64 * 64 * C)
+    # K3 finest level, per launch: read 4 subband tiles (ty x tx f32 each per
+    # channel, 32 x 28) and write a 2ty x 2tx u8 tile per channel (SURVEY §8d
+    # K3+K4 terms)
+    ty, tx = N.synthesis_tile()
+    alg = tiles * (4 * ty * tx * 4 * C + 4 * ty * tx * C)
     peak, peak_kind = peaks()
     achieved = alg / (k3f * 1e-3) / 1e9
     # whole display frame, SURVEY §8(d) byte model over the work actually done:
     # K2 = BlockEnd spans (8 B x n) + records (2 + C B, u8) + dense f32 block
-    # write; K3 level k >= 2 = 4 subband tiles read + 64x64 f32 written per
+    # write; K3 level k >= 2 = 4 subband tiles read + 2ty x 2tx f32 written per
     # tile-channel; K3 level 1 = `alg`; K4 = C B canvas read + C B written
     # per output pixel.  K1's bit masks (~3 MB) are left out.
     out_px_frame = views * OUT_W * OUT_H if mode != "full" else 0
     frame_bytes = (k2_items * (8 * h.inter_size + 4 * C * h.block_size ** 2)
                    + records * (2 + C)
-                   + sum(lvl_tiles[1:]) * (4 * 32 * 32 * 4 + 64 * 64 * 4) * C
+                   + sum(lvl_tiles[1:]) * (4 * ty * tx * 4 + 4 * ty * tx * 4) * C
                    + alg + 2 * C * out_px_frame)
     traffic, _ = ncu_traffic(mode)
 

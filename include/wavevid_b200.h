@@ -219,6 +219,10 @@ int wv_enqueue_frame(void* d_desc, const void* h_desc, uint64_t desc_bytes, void
 /* Bytes of the descriptor slot: wv_frame_args, 4 wv_view_args, then the
  * mask bytes (mask_h * mask_w) at wv_desc_mask_offset(). */
 int wv_desc_layout(const wv_geometry* g, uint64_t* mask_offset, uint64_t* slot_bytes);
+/* The synthesis tile of the inverse-DWT kernels: ty x tx coefficients of each
+ * subband per work item (2 ty x 2 tx output samples); tile counts reported
+ * by the decode (wv_block_list_view counters) are in these units. */
+int wv_synthesis_tile(int* ty, int* tx);
 
 /* shared_geometry != 0: all views share pose, FOV, region size and output
  * size (a stereo pair rendered with one head pose) -- the ray geometry is

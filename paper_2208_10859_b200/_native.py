@@ -32,7 +32,7 @@ EXPORTS = ["wv_abi_version", "wv_status_string", "wv_workspace_bytes", "wv_works
            "wv_encode_payload_capacity", "wv_encode_set", "wv_enqueue_frame",
            "wv_desc_layout", "wv_synthesize_2d", "wv_spans_read", "wv_span_queue_push",
            "wv_span_queue_enqueue", "wv_fetch_list_view", "wv_synthesize_level_desc",
-           "wv_workspace_bytes_select", "wv_table_expand"]
+           "wv_workspace_bytes_select", "wv_table_expand", "wv_synthesis_tile"]
 
 
 class Geometry(C.Structure):
@@ -144,6 +144,7 @@ def load(path: str | None = None):
     lib.wv_file_info_read.argtypes = [C.c_char_p, C.POINTER(FileInfo)]
     lib.wv_file_set_read.argtypes = [C.c_char_p, C.c_int, C.POINTER(SetInfo), C.c_void_p]
     lib.wv_file_payload_read.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_uint64]
+    lib.wv_synthesis_tile.argtypes = [C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     for fn in EXPORTS[2:]:
         getattr(lib, fn).restype = C.c_int
     if lib.wv_abi_version() != WV_ABI_VERSION:
@@ -156,6 +157,13 @@ def check(status: int, what: str) -> None:
     if status != WV_OK:
         msg = load().wv_status_string(status).decode()
         raise NativeError(f"{what} failed: {msg} (status {status})")
+
+
+def synthesis_tile() -> tuple:
+    """(ty, tx): coefficients per subband of one K3 work item (wv_synthesis_tile)."""
+    ty, tx = C.c_int32(), C.c_int32()
+    check(load().wv_synthesis_tile(C.byref(ty), C.byref(tx)), "wv_synthesis_tile")
+    return ty.value, tx.value
 
 
 def status_name(status: int) -> str:

@@ -256,6 +256,13 @@ int wv_desc_layout(const wv_geometry* g, uint64_t* mask_offset, uint64_t* slot_b
   return WV_OK;
 }
 
+int wv_synthesis_tile(int* ty, int* tx) {
+  if (!ty || !tx) return WV_ERR_ARG;
+  *ty = TY;
+  *tx = TX;
+  return WV_OK;
+}
+
 int wv_plane_view(const wv_geometry* g, void* ws, float** d_plane) {
   Layout lo;
   int st = build_layout(g, &lo);

@@ -12,11 +12,12 @@ namespace wv {
 #define WV_TILE_Y 32
 #endif
 constexpr int TY = WV_TILE_Y;
-constexpr int TX = 32;
+constexpr int TX = 28;                // + 2 halo columns each side = one warp's 32 lanes
 constexpr int HALO = 2;               // lifting support per side
 // TMA box: the innermost box coordinate must be 16-byte aligned (unaligned or
 // negative-unaligned starts raise an illegal-instruction fault on B200), so
-// the box starts at ax-4 (ax is a multiple of 32) and spans 40 floats.
+// the box starts at ax-4 (ax is a multiple of 28 floats = 112 bytes) and
+// spans 36 floats.
 constexpr int XPAD = 4;
 constexpr int BOX_W = TX + 2 * XPAD;
 constexpr int BOX_H = TY + 2 * HALO;

@@ -12,16 +12,21 @@
 // every lifting step at the true level borders only (index clamp, as numpy's
 // _shift_left/_shift_right do).
 //
-// Per (tile, channel) item: one elected thread issues four TMA box loads
-// (LL, HL, LH, HH; 40x36 f32 each, far-edge out-of-range zero-filled) completing on an
-// mbarrier.  The column pass streams each box column through registers with
-// the L-half (LL/LH) and H-half (HL/HH) lines packed as float2 and lifted with
-// Blackwell's paired FP32 ops (__fadd2_rn/__fmul2_rn, RN, no FMA); results land
-// row-pair-interleaved so the row pass again lifts two output rows per
-// thread as one float2 stream.  Mid levels stage the f32 output tile in shared
-// memory and write it with coalesced stores; the finest level converts to u8
-// in registers and stores each 16-pixel row segment, request-masked, straight
-// to the canvas.
+// Per (tile, channel) item (TY = 32 rows x TX = 28 columns of each subband ->
+// 64 x 56 outputs), 4 warps, one per 8-row-pair segment: one elected thread
+// issues four TMA box loads (LL, HL, LH, HH; 36 x 36 f32 each, far-edge
+// out-of-range zero-filled) completing on an mbarrier.  Lane l of a warp owns
+// coefficient column ax - 2 + l: the 28 output columns plus 2 halo columns on
+// each side, so a warp's 32 lanes hold everything its row lifting needs.  The
+// column pass streams the lane's column down the segment (the L-half LL/LH and
+// H-half HL/HH lines packed as float2, Blackwell's paired FP32 ops
+// __fadd2_rn/__fmul2_rn, RN, no FMA) and keeps the 8 emitted row pairs in
+// registers; the row pass then lifts each row pair (two rows packed) across
+// the lanes, neighbour values exchanged by warp shuffles -- no shared column
+// buffer and one barrier per item (the boxes are free once every warp's
+// column pass is done, and the next item's TMA loads go out then).  Mid
+// levels store f32 pairs per lane, the finest level converts to u8 in
+// registers and stores 2-pixel pairs request-masked straight to the canvas.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -35,33 +40,28 @@ namespace {
 
 constexpr int BOX_FLOATS = BOX_W * BOX_H;
 constexpr int BOX_SLOT = ((BOX_FLOATS * 4 + 127) / 128) * 128;  // bytes
-constexpr int CB_PITCH = BOX_W + 1;   // float2 units, odd -> conflict-free row pass
-constexpr int OB_PITCH = OUT_W + 1;   // float2 units (row pairs), odd
-// line segments: every column (row) lifting stream covers SEGLEN_C
-// (SEGLEN_R) output pairs plus its own 2-pair halo on each side
 #ifndef WV_K3_CVT_U8
 #define WV_K3_CVT_U8 1
 #endif
-#ifndef WV_SEGLEN_C
-#define WV_SEGLEN_C 8
+#ifndef WV_K3_UNMASKED
+#define WV_K3_UNMASKED 1   // fully requested tiles skip the per-pixel masking
 #endif
-#ifndef WV_SEGLEN_R
-#define WV_SEGLEN_R 8
+#ifndef WV_K3_MINB
+#define WV_K3_MINB 8   // 64 registers: 8 CTAs (32 warps) per SM, the shared-memory limit too
 #endif
-#ifndef WV_SEGLEN_RF
-#define WV_SEGLEN_RF 8    // finest level row segments (16 measured slower)
-#endif
-constexpr int SEGLEN_C = WV_SEGLEN_C, SEGLEN_R = WV_SEGLEN_R, SEGLEN_RF = WV_SEGLEN_RF;
-constexpr int COL_SEGS = TY / SEGLEN_C, ROW_SEGS = TX / SEGLEN_R;
-static_assert(SEGLEN_RF % 8 == 0 && SEGLEN_RF <= TX, "finest row segments store 16-pixel chunks");
-constexpr int NTHREADS_MIN = (COL_SEGS * BOX_W > ROW_SEGS * TY ? COL_SEGS * BOX_W : ROW_SEGS * TY);
-#ifdef WV_K3_THREADS
-constexpr int NTHREADS = WV_K3_THREADS;
+#if WV_K3_MINB > 0
+#define K3_BOUNDS __launch_bounds__(NTHREADS, WV_K3_MINB)
 #else
-constexpr int NTHREADS = NTHREADS_MIN <= 64 ? 64 : (NTHREADS_MIN <= 128 ? 128 : (NTHREADS_MIN + 31) / 32 * 32);
+#define K3_BOUNDS __launch_bounds__(NTHREADS)
 #endif
-static_assert(NTHREADS >= NTHREADS_MIN, "every segment needs a thread");
-static_assert(TY * OB_PITCH * 8 <= 4 * BOX_SLOT, "output tile must fit in the box region");
+#ifndef WV_K3_MID_PREFETCH
+#define WV_K3_MID_PREFETCH 1   // mid levels also load the next item during the row pass
+#endif
+constexpr int SEG = 8;                 // output row pairs per warp (column-pass segment)
+constexpr int NWARP = TY / SEG;        // 4
+constexpr int NTHREADS = 32 * NWARP;   // 128
+static_assert(TX + 2 * HALO == 32, "a warp's lanes are the tile's columns plus the halo");
+static_assert(BOX_W >= TX + 2 * XPAD, "the box covers the halo columns");
 
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 // clip(rint(x), 0, 255) (decoding.py:301; rint is round-half-even): one
@@ -88,59 +88,6 @@ __device__ __forceinline__ float2 dscale(float2 d, float2 ik) {
 __device__ __forceinline__ float2 lstep(float2 x, float2 nk, float2 y1, float2 y2) {
   const float2 t = __fmul2_rn(nk, __fadd2_rn(y1, y2));
   return make_float2(__fadd_rn(x.x, t.x), __fadd_rn(x.y, t.y));
-}
-
-// Inverse CDF 9/7 lifting of one line (two packed lines) over global
-// coefficient indices [g0, g1) of a level of length N; emits pairs p in
-// [a, b) as (s3[p], d3[p]).  Left/right symmetric extension applies only when
-// g0 == 0 / g1 == N (wavelets.py:82-91, :94-101).
-template <class Load, class Emit>
-__device__ __forceinline__ void lift_line(int g0, int g1, int N, int a, int b, Load load,
-                                          Emit emit) {
-  const float2 KS = f2(__uint_as_float(0x3f9d7658u));    // K
-  const float2 IK = f2(__uint_as_float(0x3f5019c3u));    // 1/K
-  const float2 ND = f2(-__uint_as_float(0x3ee31355u));   // -delta
-  const float2 NG = f2(-__uint_as_float(0x3f620676u));   // -gamma
-  const float2 NB = f2(-__uint_as_float(0xbd5901aeu));   // -beta
-  const float2 NA = f2(-__uint_as_float(0xbfcb0673u));   // -alpha
-  float2 sr, dr;
-  // j = g0 (at the left border d1[-1] = d1[0]; elsewhere the value is a halo)
-  load(g0, sr, dr);
-  float2 d1m = dscale(dr, IK);
-  float2 s2m = lstep(__fmul2_rn(sr, KS), ND, d1m, d1m);
-  float2 d2mm = d1m, s3mm = s2m;
-  if (g1 - g0 >= 2) {
-    // j = g0 + 1 (at the left border d2[-1] = d2[0])
-    load(g0 + 1, sr, dr);
-    float2 d1 = dscale(dr, IK);
-    float2 s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);
-    float2 d2 = lstep(d1m, NG, s2m, s2);
-    s3mm = lstep(s2m, NB, d2, d2);
-    d2mm = d2;
-    d1m = d1;
-    s2m = s2;
-#pragma unroll 4
-    for (int j = g0 + 2; j < g1; ++j) {
-      load(j, sr, dr);
-      d1 = dscale(dr, IK);
-      s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);   // s2[j]
-      d2 = lstep(d1m, NG, s2m, s2);                   // d2[j-1]
-      float2 s3 = lstep(s2m, NB, d2mm, d2);           // s3[j-1]
-      float2 d3 = lstep(d2mm, NA, s3mm, s3);          // d3[j-2]
-      const int p = j - 2;
-      if (p >= a && p < b) emit(p, s3mm, d3);
-      d2mm = d2;
-      s3mm = s3;
-      d1m = d1;
-      s2m = s2;
-    }
-  }
-  if (g1 == N) {
-    float2 d2 = lstep(d1m, NG, s2m, s2m);                     // d2[N-1]
-    float2 s3 = lstep(s2m, NB, N == 1 ? d2 : d2mm, d2);       // s3[N-1]
-    if (N >= 2 && N - 2 >= a && N - 2 < b) emit(N - 2, s3mm, lstep(d2mm, NA, s3mm, s3));
-    if (N - 1 >= a && N - 1 < b) emit(N - 1, s3, lstep(d2, NA, s3, s3));
-  }
 }
 
 // Interior segment (no level border inside [g0, g0 + LEN + 4)): the same
@@ -247,44 +194,21 @@ struct LevelArgs {
   const float* plane; int plane_w, plane_h;
 };
 
-// Items are (tile, channel).  Column pass: TY/SEGLEN_C segments x BOX_W
-// columns (each segment lifts SEGLEN_C output row pairs from its own 2-row
-// halo); row pass: TX/SEGLEN_R segments x TY row pairs.  Mid levels stage the
-// f32 output tile in the box region (dead after the column pass) and store it
-// coalesced.  The finest level needs no output tile: each row-pass thread
-// keeps its 2 x 16 output bytes in registers and writes them with the
-// request mask applied, so the box region is free as soon as the column pass
-// ends and the next item's four TMA boxes are issued there, loading while
-// this item's row pass runs (43 KB of shared memory: 5 CTAs per SM).
+// Items are (tile, channel), 4 warps per item, warp w = output row pairs
+// [8w, 8w+8) of the tile.  The finest level stages the tile's request-mask
+// words (two dependent loads per row) while the boxes load and ANDs them
+// over the tile: a fully requested tile stores unmasked.  Once every warp's
+// column pass is done (the one barrier per item) the boxes are dead and the
+// next item's four loads go out, overlapping this item's row pass.  21 KB
+// of boxes + 2 KB of request staging and 64 registers: 8 CTAs per SM.
 constexpr int BOXSET = 4 * BOX_SLOT;
-constexpr int COL_BYTES = 2 * TY * CB_PITCH * 8;
-#ifndef WV_K3_PAIRSEG
-#define WV_K3_PAIRSEG 1  // finest row pass: a warp = 16 row pairs x 2 adjacent segments, so
-                         // each 16-B store pair fills whole 32-B sectors
-#endif
-// row-pass thread -> (row pair i, segment sg)
-template <bool FINAL>
-__device__ __forceinline__ void row_map(int tid, int& i, int& sg) {
-  if (FINAL && WV_K3_PAIRSEG && TY == 32) {
-    const int w = tid >> 5, l = tid & 31;
-    i = 16 * (w & 1) + (l & 15);
-    sg = 2 * (w >> 1) + (l >> 4);
-  } else {
-    i = tid % TY;
-    sg = tid / TY;
-  }
-}
-#ifndef WV_K3_OUT4
-#define WV_K3_OUT4 1   // mid-level output tile as float4 (s3.x, d3.x, s3.y, d3.y) per pair:
-                       // one conflict-free 16-B shared store / load instead of two 8-B ones
-#endif
-constexpr int OB4_PITCH = TX + 1;     // float4 units, odd
-static_assert(TY * OB4_PITCH * 16 <= 4 * BOX_SLOT, "float4 output tile must fit in the box region");
-constexpr int SMEM_MID = BOXSET + COL_BYTES;
-constexpr int SMEM_FIN = BOXSET + COL_BYTES;   // the u8 tile goes from registers to HBM
+constexpr int RQ_WORDS = 4;                     // request-mask words per staged row
+constexpr int RQ_SLOT = OUT_H * RQ_WORDS;       // u32 per staging slot
+constexpr int SMEM_MID = BOXSET;
+constexpr int SMEM_FIN = BOXSET + 2 * RQ_SLOT * 4;
 
 template <bool FINAL>
-__global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUtensorMap tm_ll,
+__global__ void K3_BOUNDS k_level(const __grid_constant__ CUtensorMap tm_ll,
                                                     const __grid_constant__ CUtensorMap tm_det,
                                                     LevelArgs a) {
   pdl_sync();
@@ -295,20 +219,22 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   const float* bHL = box + BOX_SLOT / 4;
   const float* bLH = box + 2 * BOX_SLOT / 4;
   const float* bHH = box + 3 * BOX_SLOT / 4;
-  float2* colL = reinterpret_cast<float2*>(smem + BOXSET);  // [TY][CB_PITCH]
-  float2* colH = colL + TY * CB_PITCH;
-  // mid levels: the f32 output tile aliases the boxes
-  float2* outb = reinterpret_cast<float2*>(smem);
-  constexpr bool PF = FINAL;   // next item's boxes issued after the column pass
+  uint32_t* rq_stage = reinterpret_cast<uint32_t*>(smem + BOXSET);   // final: 2 slots
   __shared__ uint64_t bar;
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) mbar_init(&bar, 1);
   __syncthreads();
   uint32_t phase = 0u;
   const int C = a.C;
   const uint32_t nitems = *a.count * (uint32_t)C;
   const int H = 2 * a.bh, W = 2 * a.bw;
+  const float2 KS = f2(__uint_as_float(0x3f9d7658u));    // K
+  const float2 IK = f2(__uint_as_float(0x3f5019c3u));    // 1/K
+  const float2 ND = f2(-__uint_as_float(0x3ee31355u));   // -delta
+  const float2 NG = f2(-__uint_as_float(0x3f620676u));   // -gamma
+  const float2 NB = f2(-__uint_as_float(0xbd5901aeu));   // -beta
+  const float2 NA = f2(-__uint_as_float(0xbfcb0673u));   // -alpha
 
   // issue the four box loads of an item (elected thread)
   auto issue = [&](uint32_t it) {
@@ -317,7 +243,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     const uint32_t tile = a.list[itile] & ~ZERO_FLAG;
     const int ty = (int)(tile / a.divN), tx = (int)tile - ty * a.ntx;
     // TMA faults on unaligned/negative innermost box coordinates (observed on
-    // B200, driver 580): x starts at ax-4 clamped to 0
+    // B200, driver 580): x starts at ax-4 (ax = 28 tx: 16-byte aligned) clamped to 0
     const int oy = max(ty * TY - HALO, 0), ox = max(tx * TX - XPAD, 0);
     const int c = (int)(it - itile * C);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -329,6 +255,7 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
   };
 
   bool issued = false;   // the current item's boxes are already in flight
+  int slot = 0;          // final: request-staging slot of this item
   for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
     const uint32_t itile = item / a.divC;
     const uint32_t entry = a.list[itile];
@@ -340,39 +267,35 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     const int ny = 2 * (by - ay), nx = 2 * (bx - ax);
     if (FINAL && (entry & ZERO_FLAG)) {
       // tile left the request: clear what an earlier frame wrote there
-      const int qw = nx >> 2;
+      const int qw = nx >> 1;   // u16 pairs per row (56-px tiles start 8-byte aligned)
       for (int idx = tid; idx < ny * qw; idx += NTHREADS) {
-        const int r = idx / qw, q = idx % qw;
-        *reinterpret_cast<uint32_t*>(canvas + ((uint64_t)c * H + 2 * ay + r) * W + 2 * ax +
-                                     4 * q) = 0u;
+        const int r = idx / qw, q = idx - (idx / qw) * qw;
+        *reinterpret_cast<uint16_t*>(canvas + ((uint64_t)c * H + 2 * ay + r) * W + 2 * ax + 2 * q) = 0;
       }
       continue;
     }
     const int oy = max(ay - HALO, 0), ox = max(ax - XPAD, 0);
-    // finest level: fetch this thread's request-mask words (rowmap -> R, two
-    // dependent global loads) and the next item's list entry now, so their
-    // latency hides behind the box wait and the column pass
-    constexpr int SR = FINAL ? SEGLEN_RF : SEGLEN_R;
-    uint32_t rq[2][SR / 8];
-    uint32_t nxt_entry = ZERO_FLAG;
     const uint32_t nxt = item + gridDim.x;
+    uint32_t nxt_entry = ZERO_FLAG;
+    if ((FINAL || WV_K3_MID_PREFETCH) && tid == 0 && a.use_tma && nxt < nitems) nxt_entry = a.list[nxt / a.divC];
+    uint32_t* rq = rq_stage + slot * RQ_SLOT;
+    const int w0 = (2 * ax) >> 5;   // first request word of the tile's pixel columns
+    bool rq_all = true;             // final: the whole tile is requested (no masking)
     if (FINAL) {
-      int i, sg;
-      row_map<FINAL>(tid, i, sg);
-      const int pa = ax + sg * SR;
-      if (tid < (TX / SR) * TY && i < by - ay && pa < bx) {
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const uint32_t* req = a.R + (uint64_t)a.rowmap[2 * ay + 2 * i + rr] * a.wpr0;
-#pragma unroll
-          for (int k = 0; k < SR / 8; ++k) {
-            const int px = 2 * pa + 16 * k;
-            rq[rr][k] = px < W ? req[px >> 5] : 0u;
-          }
-        }
+      // the tile's request-mask words (row map -> mask row, two dependent
+      // loads per row) staged while the boxes load
+      for (int i = tid; i < ny * RQ_WORDS; i += NTHREADS) {
+        const int r = i / RQ_WORDS, k = i - r * RQ_WORDS;
+        const int w = w0 + k;
+        const uint32_t v = w < a.wpr0 ? a.R[(uint64_t)a.rowmap[2 * ay + r] * a.wpr0 + w] : 0u;
+        rq[i] = v;
+        // the tile's pixel columns [2ax, 2ax + nx) inside this word
+        const int lo = max(2 * ax - 32 * w, 0), hi = min(2 * ax + nx - 32 * w, 32);
+        const uint32_t need =
+            lo >= hi ? 0u : ((hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & (0xFFFFFFFFu << lo));
+        rq_all &= (v & need) == need;
       }
     }
-    if (PF && tid == 0 && a.use_tma && nxt < nitems) nxt_entry = a.list[nxt / a.divC];
     if (a.use_tma) {
       if (!issued) issue(item);
       mbar_wait(&bar, phase);
@@ -397,186 +320,136 @@ __global__ void __launch_bounds__(NTHREADS) k_level(const __grid_constant__ CUte
     }
     issued = false;
 
-    // column pass: (segment, box column) per thread, L and H halves packed
-    if (tid < COL_SEGS * BOX_W) {
-      const int lc = tid % BOX_W, sg = tid / BOX_W;
-      const int cg = ox + lc;
-      const int pa = ay + sg * SEGLEN_C, pb = min(pa + SEGLEN_C, by);
-      if (pa < pb && cg >= max(ax - HALO, 0) && cg < min(bx + HALO, a.bw)) {
-        if (pa >= HALO && pb + HALO <= a.bh && pb - pa == SEGLEN_C) {
-          const int rb = pa - HALO - oy;          // local box row of input 0
-          const int qb = pa - HALO - ay;          // output pair of input 0
-          lift_interior<SEGLEN_C>(
-              [&](int j, float2& s, float2& d) {
-                const int o = (rb + j) * BOX_W + lc;
-                WV_ASSERT(o >= 0 && o < BOX_FLOATS);
-                s = make_float2(bLL[o], bHL[o]);
-                d = make_float2(bLH[o], bHH[o]);
-              },
-              [&](int p, float2 s3, float2 d3) {
-                WV_ASSERT(qb + p >= 0 && qb + p < TY && lc < CB_PITCH);
-                colL[(qb + p) * CB_PITCH + lc] = make_float2(s3.x, d3.x);
-                colH[(qb + p) * CB_PITCH + lc] = make_float2(s3.y, d3.y);
-              });
-        } else {
-          lift_line(
-              max(pa - HALO, 0), min(pb + HALO, a.bh), a.bh, pa, pb,
-              [&](int j, float2& s, float2& d) {
-                const int o = (j - oy) * BOX_W + lc;
-                WV_ASSERT(o >= 0 && o < BOX_FLOATS);
-                s = make_float2(bLL[o], bHL[o]);
-                d = make_float2(bLH[o], bHH[o]);
-              },
-              [&](int p, float2 s3, float2 d3) {
-                const int q = p - ay;
-                WV_ASSERT(q >= 0 && q < TY && lc < CB_PITCH);
-                colL[q * CB_PITCH + lc] = make_float2(s3.x, d3.x);
-                colH[q * CB_PITCH + lc] = make_float2(s3.y, d3.y);
-              });
-        }
+    // column pass: lane = column x, warp = segment of SEG output row pairs;
+    // the 8 pairs (L and H halves packed) stay in registers
+    const int x = ax - HALO + lane;
+    const int pa = ay + SEG * warp, pb = min(pa + SEG, by);
+    float2 cs[SEG], cd[SEG];   // (s3, d3) of pair q: .x = L half, .y = H half
+    const bool col_live = x >= max(ax - HALO, 0) && x < min(bx + HALO, a.bw) && pa < pb;
+    if (col_live) {
+      const int lc = x - ox;
+      auto emit = [&](int p, float2 s3, float2 d3) {
+        cs[p - HALO] = s3;   // compile-time index after unrolling
+        cd[p - HALO] = d3;
+      };
+      if (pa >= HALO && pa + SEG + HALO <= a.bh) {
+        const int rb = pa - HALO - oy;
+        lift_interior<SEG>(
+            [&](int j, float2& s_, float2& d_) {
+              const int o = (rb + j) * BOX_W + lc;
+              WV_ASSERT(o >= 0 && o < BOX_FLOATS);
+              s_ = make_float2(bLL[o], bHL[o]);
+              d_ = make_float2(bLH[o], bHH[o]);
+            },
+            emit);
+      } else {
+        // a level border inside the segment: whole-sample symmetric extension
+        // of the interleaved line (x[-k] = x[k], x[2N-1+k] = x[2N-1-k]) is
+        // carried through every lifting step unchanged, so loading mirrored
+        // coefficients equals the reference's per-step extension
+        // (wavelets.py:82-101) bit for bit: s[-k] = s[k], d[-k] = d[k-1],
+        // s[N+m] = s[N-1-m], d[N+m] = d[N-2-m].  Pairs past the border are
+        // computed from rows clamped into the box and never emitted.
+        const int g0 = pa - HALO, N = a.bh;
+        const int glo = oy, ghi = min(N, oy + BOX_H) - 1;   // rows held by the box
+        lift_interior<SEG>(
+            [&](int j, float2& s_, float2& d_) {
+              const int g = g0 + j;
+              int gs = g, gd = g;
+              if (g < 0) {
+                gs = -g;
+                gd = -g - 1;
+              } else if (g >= N) {
+                gs = 2 * N - 1 - g;
+                gd = 2 * N - 2 - g;
+              }
+              gs = min(max(gs, glo), ghi);
+              gd = min(max(gd, glo), ghi);
+              const int os = (gs - oy) * BOX_W + lc, od = (gd - oy) * BOX_W + lc;
+              WV_ASSERT(os >= 0 && os < BOX_FLOATS && od >= 0 && od < BOX_FLOATS);
+              s_ = make_float2(bLL[os], bHL[os]);
+              d_ = make_float2(bLH[od], bHH[od]);
+            },
+            emit);
       }
     }
-    __syncthreads();
-    if (PF && a.use_tma) {
+    // every warp is done with the boxes (and the staged request words)
+    const bool unmasked = __syncthreads_and(rq_all) != 0 && WV_K3_UNMASKED;
+    if ((FINAL || WV_K3_MID_PREFETCH) && a.use_tma) {
       // the boxes are consumed: start the next item's loads now (only the
       // elected thread read nxt_entry and issues)
       issued = !(nxt_entry & ZERO_FLAG);   // meaningful for the elected thread only
       if (issued) issue(nxt);
     }
-    // row pass: (segment, output row pair) per thread, two rows packed
-    if (tid < (TX / SR) * TY) {
-      int i, sg;
-      row_map<FINAL>(tid, i, sg);
-      const int pa = ax + sg * SR, pb = min(pa + SR, bx);
-      if (i < by - ay && pa < pb) {
-        // finest level: clip(rint(x*255)) (decoding.py:301; rint is
-        // round-half-even like __float2uint_rn, which also saturates below 0)
-        // of the segment's 2 x 16 output pixels, kept in registers and
-        // written to the canvas with the request mask applied
-        auto cv = [](float v) { return u8_rint(__fmul_rn(v, 255.0f)); };
-        uint32_t w0[SR / 2] = {}, w1[SR / 2] = {};   // rows 2i, 2i+1
-        uint8_t* crow = FINAL ? canvas + ((uint64_t)c * H + 2 * ay + 2 * i) * W : nullptr;
-        // mid levels: f32 pairs into outb
-        auto emit_mid = [&](int q, float2 s3, float2 d3) {
-          WV_ASSERT(q >= 0 && q < TX && i < TY);
-          if (WV_K3_OUT4) {
-            reinterpret_cast<float4*>(outb)[i * OB4_PITCH + q] = make_float4(s3.x, d3.x, s3.y, d3.y);
-          } else {
-            outb[i * OB_PITCH + 2 * q] = s3;
-            outb[i * OB_PITCH + 2 * q + 1] = d3;
-          }
-        };
-        if (pa >= HALO && pb + HALO <= a.bw && pb - pa == SR) {
-          const int cb = pa - HALO - ox, qb = pa - HALO - ax;
-          lift_interior<SR>(
-              [&](int j, float2& s, float2& d) {
-                WV_ASSERT(cb + j >= 0 && cb + j < CB_PITCH);
-                s = colL[i * CB_PITCH + cb + j];
-                d = colH[i * CB_PITCH + cb + j];
-              },
-              [&](int p, float2 s3, float2 d3) {
-                if (!FINAL) {
-                  emit_mid(qb + p, s3, d3);
-                } else {
-                  // p - HALO is the segment-local pair: compile-time after unrolling
-                  const int lq = p - HALO;
-                  w0[lq >> 1] |= (cv(s3.x) | (cv(d3.x) << 8)) << (16 * (lq & 1));
-                  w1[lq >> 1] |= (cv(s3.y) | (cv(d3.y) << 8)) << (16 * (lq & 1));
-                }
-              });
-          if (FINAL) {
-            // 16-pixel chunks of each row: request bits -> byte masks, 16-byte stores
-            auto bm = [](uint32_t b4) { return ((b4 * 0x00204081u) & 0x01010101u) * 0xFFu; };
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-              const uint32_t* wr = rr ? w1 : w0;
-#pragma unroll
-              for (int k = 0; k < SR / 8; ++k) {
-                const int px = 2 * pa + 16 * k;
-                const uint32_t bits = (rq[rr][k] >> (px & 31)) & 0xFFFFu;
-                const uint4 v = make_uint4(wr[4 * k] & bm(bits & 0xFu),
-                                           wr[4 * k + 1] & bm((bits >> 4) & 0xFu),
-                                           wr[4 * k + 2] & bm((bits >> 8) & 0xFu),
-                                           wr[4 * k + 3] & bm(bits >> 12));
-                uint8_t* dst = crow + (uint64_t)rr * W + px;
-                if ((W & 15) == 0) {
-                  *reinterpret_cast<uint4*>(dst) = v;
-                } else {
-                  uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
-                  d4[0] = v.x;
-                  d4[1] = v.y;
-                  d4[2] = v.z;
-                  d4[3] = v.w;
-                }
-              }
-            }
-          }
-        } else {
-          lift_line(
-              max(pa - HALO, 0), min(pb + HALO, a.bw), a.bw, pa, pb,
-              [&](int j, float2& s, float2& d) {
-                WV_ASSERT(j - ox >= 0 && j - ox < CB_PITCH);
-                s = colL[i * CB_PITCH + (j - ox)];
-                d = colH[i * CB_PITCH + (j - ox)];
-              },
-              [&](int p, float2 s3, float2 d3) {
-                if (!FINAL) {
-                  emit_mid(p - ax, s3, d3);
-                } else {
-                  // level borders: two pixels per row straight to the canvas
-                  const int px = 2 * p;
-#pragma unroll
-                  for (int rr = 0; rr < 2; ++rr) {
-                    const int y = 2 * ay + 2 * i + rr;
-                    const uint32_t bits =
-                        (a.R[(uint64_t)a.rowmap[y] * a.wpr0 + (px >> 5)] >> (px & 31)) & 3u;
-                    const uint32_t lo = rr ? cv(s3.y) : cv(s3.x), hi = rr ? cv(d3.y) : cv(d3.x);
-                    *reinterpret_cast<uint16_t*>(crow + (uint64_t)rr * W + px) =
-                        (uint16_t)(((bits & 1u) ? lo : 0u) | (((bits >> 1) & 1u) ? hi << 8 : 0u));
-                  }
-                }
-              });
-        }
-      }
-    }
-    __syncthreads();   // mid: outb complete; final: colL / colH free for the next item
+    // row pass: each row pair (two output rows packed) lifted across the
+    // lanes; neighbours by shuffle, symmetric extension at the level borders
+    // (wavelets.py:94-101) by reading the lane's own value there.  Lanes
+    // 2..29 emit; 0, 1, 30, 31 are the halo.  All eight pairs are lifted
+    // unconditionally (the shuffles stay warp-converged); pairs past the
+    // segment's end are not stored.
+    const int up = x == 0 ? lane : lane - 1;          // source of d[x-1]
+    const int dn = x == a.bw - 1 ? lane : lane + 1;   // source of s[x+1]
+    const bool emit = lane >= HALO && lane < 32 - HALO && x < bx;
+    const int npairs = pb - pa;   // <= SEG, may be <= 0
+    auto sh2 = [](float2 v, int src) {
+      return make_float2(__shfl_sync(0xFFFFFFFFu, v.x, src), __shfl_sync(0xFFFFFFFFu, v.y, src));
+    };
+    auto cv = [](float v) { return u8_rint(__fmul_rn(v, 255.0f)); };
+    // final: this lane's request bits (pixels 2x, 2x+1) sit at bit px & 31 of
+    // staged word (px >> 5) - w0 of each output row
+    const int px = 2 * x;
+    const uint32_t* rql = rq + (2 * (pa - ay)) * RQ_WORDS + ((px >> 5) - w0);
+    const int rsh = px & 31;
+    uint8_t* crow = FINAL ? canvas + ((uint64_t)c * H + 2 * pa) * W + px : nullptr;
+    float* orow = FINAL ? nullptr : a.out + ((uint64_t)c * H + 2 * pa) * a.out_pitch + 2 * x;
+    // lift pair q across the lanes -> (s3, d3): .x = row 2p, .y = row 2p+1
+    auto lift_pair = [&](int q, float2& s3, float2& d3) {
+      const float2 s = make_float2(cs[q].x, cd[q].x);   // L half, rows 2p and 2p+1
+      const float2 d = make_float2(cs[q].y, cd[q].y);   // H half
+      const float2 s1 = __fmul2_rn(s, KS);
+      const float2 d1 = dscale(d, IK);
+      const float2 s2 = lstep(s1, ND, sh2(d1, up), d1);
+      const float2 d2 = lstep(d1, NG, s2, sh2(s2, dn));
+      s3 = lstep(s2, NB, sh2(d2, up), d2);
+      d3 = lstep(d2, NA, s3, sh2(s3, dn));
+    };
+    // one unrolled loop per store kind (a branch inside the loop would keep
+    // both epilogues' registers live)
     if (!FINAL) {
-      float* base = a.out + ((uint64_t)c * H + 2 * ay) * a.out_pitch + 2 * ax;
-      if (nx == OUT_W && ny == OUT_H) {
-        // full tile: 32 row pairs x 32 float2 columns, shifts only
-        for (int idx = tid; idx < TY * TX; idx += NTHREADS) {
-          const int i = idx / TX, x2 = idx % TX;
-          float* r0 = base + (uint64_t)(2 * i) * a.out_pitch + 2 * x2;
-          if (WV_K3_OUT4) {
-            const float4 t = reinterpret_cast<const float4*>(outb)[i * OB4_PITCH + x2];
-            *reinterpret_cast<float2*>(r0) = make_float2(t.x, t.y);
-            *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(t.z, t.w);
-          } else {
-            const float2 u = outb[i * OB_PITCH + 2 * x2];
-            const float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
-            *reinterpret_cast<float2*>(r0) = make_float2(u.x, v.x);
-            *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
-          }
-        }
-      } else {
-        const int half = nx >> 1;   // float2 columns per row
-        for (int idx = tid; idx < (ny >> 1) * half; idx += NTHREADS) {
-          const int i = idx / half, x2 = idx % half;
-          float* r0 = base + (uint64_t)(2 * i) * a.out_pitch + 2 * x2;
-          if (WV_K3_OUT4) {
-            const float4 t = reinterpret_cast<const float4*>(outb)[i * OB4_PITCH + x2];
-            *reinterpret_cast<float2*>(r0) = make_float2(t.x, t.y);
-            *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(t.z, t.w);
-          } else {
-            const float2 u = outb[i * OB_PITCH + 2 * x2];
-            const float2 v = outb[i * OB_PITCH + 2 * x2 + 1];
-            *reinterpret_cast<float2*>(r0) = make_float2(u.x, v.x);
-            *reinterpret_cast<float2*>(r0 + a.out_pitch) = make_float2(u.y, v.y);
-          }
+#pragma unroll
+      for (int q = 0; q < SEG; ++q) {
+        float2 s3, d3;
+        lift_pair(q, s3, d3);
+        if (emit && q < npairs) {
+          *reinterpret_cast<float2*>(orow + (2 * q) * (size_t)a.out_pitch) = make_float2(s3.x, d3.x);
+          *reinterpret_cast<float2*>(orow + (2 * q + 1) * (size_t)a.out_pitch) =
+              make_float2(s3.y, d3.y);
         }
       }
-      __syncthreads();
+    } else {
+      // clip(rint(x*255)) (decoding.py:301), request-masked unless the whole
+      // tile is requested; 2 pixels per row
+#pragma unroll
+      for (int q = 0; q < SEG; ++q) {
+        float2 s3, d3;
+        lift_pair(q, s3, d3);
+        if (emit && q < npairs) {
+          uint32_t m0 = 0xFFFFu, m1 = 0xFFFFu;
+          if (!unmasked) {
+            const uint32_t b0 = (rql[(2 * q) * RQ_WORDS] >> rsh) & 3u;
+            const uint32_t b1 = (rql[(2 * q + 1) * RQ_WORDS] >> rsh) & 3u;
+            // bits (0, 1) -> byte masks (0x00FF, 0xFF00)
+            m0 = ((b0 | (b0 << 7)) & 0x101u) * 0xFFu;
+            m1 = ((b1 | (b1 << 7)) & 0x101u) * 0xFFu;
+          }
+          const uint32_t v0 = (cv(s3.x) | (cv(d3.x) << 8)) & m0;
+          const uint32_t v1 = (cv(s3.y) | (cv(d3.y) << 8)) & m1;
+          *reinterpret_cast<uint16_t*>(crow + (2 * q) * (size_t)W) = (uint16_t)v0;
+          *reinterpret_cast<uint16_t*>(crow + (2 * q + 1) * (size_t)W) = (uint16_t)v1;
+        }
+      }
     }
+    slot ^= 1;
   }
 }
 

@@ -622,12 +622,18 @@ __global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
 // Finest footprint step restricted to the level-1 synthesis tiles: the
 // footprint is ANDed with the request, so it is zero outside the tiles that
 // touch the request; tiles that left the request (ZERO_FLAG) are cleared.
-// One CTA-iteration per 64x64-pixel tile (64 rows x 2 words, one word per
-// thread); source: 37 rows x 3 words of V_1 & D_1.
+// One CTA-iteration per OUT_H x OUT_W-pixel tile: 64 rows x FT_OW words, one
+// word per thread; source: 37 rows x 3 words of V_1 & D_1.  Tiles are not
+// word aligned (OUT_W = 56), so a word can straddle two listed tiles: each
+// tile updates only the bits of its own pixel columns (atomicAnd to clear,
+// atomicOr to set -- neighbouring tiles touch disjoint bits).
 constexpr int FT_SR = OUT_H / 2 + DIL + 1, FT_SW = 3;
+constexpr int FT_OW = (OUT_W + 31) / 32 + (OUT_W % 32 ? 1 : 0);   // output words a tile touches
+constexpr int FT_THREADS = OUT_H * FT_OW;
+static_assert(FT_SW * 2 >= FT_OW + 2, "source window covers the tile's words and neighbours");
 
-__global__ void __launch_bounds__(128) k_footprint_tiles(FootArgs a, const uint32_t* list,
-                                                         const uint32_t* count, int ntx1) {
+__global__ void __launch_bounds__(FT_THREADS) k_footprint_tiles(FootArgs a, const uint32_t* list,
+                                                                const uint32_t* count, int ntx1) {
   pdl_sync();
   __shared__ uint32_t sv[FT_SR][FT_SW];
   const uint32_t n = *count;
@@ -637,15 +643,16 @@ __global__ void __launch_bounds__(128) k_footprint_tiles(FootArgs a, const uint3
     const uint32_t e = list[it];
     const int tile = (int)(e & ~ZERO_FLAG);
     const int ty = tile / ntx1, tx = tile - (tile / ntx1) * ntx1;
-    const int r0 = ty * OUT_H, w0 = tx * (OUT_W / 32);
-    const int lr = tid >> 1, lw = tid & 1;
-    const int r = r0 + lr, w = w0 + lw;
-    const bool mine = r < a.rows && w < a.wpr;
+    const int r0 = ty * OUT_H, c0 = tx * OUT_W, c1 = min(c0 + OUT_W, a.cols);
+    const int wa = c0 >> 5;
+    const int lr = tid / FT_OW, lw = tid - (tid / FT_OW) * FT_OW;
+    const int r = r0 + lr, w = wa + lw;
+    const uint32_t own = (r < a.rows && w < a.wpr) ? range_mask(c0, c1, w) : 0u;
     if (e & ZERO_FLAG) {
-      if (mine) out[(uint64_t)r * a.wpr + w] = 0u;
+      if (own) atomicAnd(&out[(uint64_t)r * a.wpr + w], ~own);
       continue;   // no shared memory touched
     }
-    const int sr0 = (r0 - DIL) >> 1, sw0 = tx - 1;
+    const int sr0 = (r0 - DIL) >> 1, sw0 = (wa - 1) >> 1;
     for (int i = tid; i < FT_SR * FT_SW; i += blockDim.x) {
       const int ir = i / FT_SW, iw = i - (i / FT_SW) * FT_SW;
       const int sr = sr0 + ir, sw = sw0 + iw;
@@ -657,17 +664,16 @@ __global__ void __launch_bounds__(128) k_footprint_tiles(FootArgs a, const uint3
       sv[ir][iw] = v;
     }
     __syncthreads();
-    // AND over each output row's 4-5 source rows, once per source word: the
-    // thread of output word lw = 0 needs source words 0, 1; lw = 1 needs 1, 2
-    uint32_t va0 = 0xFFFFFFFFu, va1 = 0xFFFFFFFFu;
-    {
+    if (own) {
+      // AND over the output row's 4-5 source rows for each source word the
+      // thread's neighbourhood (words w-1 .. w+1) reads
       const int s_lo = ((r - DIL) >> 1) - sr0, s_hi = ((r + DIL) >> 1) - sr0;
+      const int q0 = ((w - 1) >> 1) - sw0;   // 0 or 1; the words are q0, q0 + 1
+      uint32_t va0 = 0xFFFFFFFFu, va1 = 0xFFFFFFFFu;
       for (int k = s_lo; k <= s_hi; ++k) {
-        va0 &= sv[k][lw];
-        va1 &= sv[k][lw + 1];
+        va0 &= sv[k][q0];
+        va1 &= sv[k][q0 + 1];
       }
-    }
-    if (mine) {
       uint32_t nb[3];
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
@@ -676,13 +682,18 @@ __global__ void __launch_bounds__(128) k_footprint_tiles(FootArgs a, const uint3
           nb[d] = 0xFFFFFFFFu;
           continue;
         }
-        // source word (ww >> 1) - sw0 is lw or lw + 1 for this thread
-        const uint32_t v = ((ww >> 1) - sw0) > lw ? va1 : va0;
+        const uint32_t v = ((ww >> 1) - sw0) > q0 ? va1 : va0;
         nb[d] = double_bits(v >> (16 * (ww & 1))) | ~last_word_mask(a.cols, ww);
       }
       uint32_t v = shrink(nb[0], nb[1], nb[2]) & last_word_mask(a.cols, w);
       v &= a.R[(uint64_t)a.rowmap[r] * a.wpr + w];
-      out[(uint64_t)r * a.wpr + w] = v;
+      uint32_t* o = &out[(uint64_t)r * a.wpr + w];
+      if (own == 0xFFFFFFFFu) {
+        *o = v;
+      } else {
+        atomicAnd(o, ~own);
+        if (v & own) atomicOr(o, v & own);
+      }
     }
     __syncthreads();
   }
@@ -1163,7 +1174,7 @@ int launch_select(const Layout& lo, const wv_geometry* g, int mode, int flags,
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      WV_CUDA(launch_k(k_footprint_tiles, dim3(min(nt1, 8 * sms)), dim3(128), 0, s, f,
+      WV_CUDA(launch_k(k_footprint_tiles, dim3(min(nt1, 8 * sms)), dim3(FT_THREADS), 0, s, f,
                        (const uint32_t*)t.list[1], (const uint32_t*)(counters + CNT_TILES + 1),
                        lo.ntx[1]));
     }

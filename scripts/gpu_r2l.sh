@@ -1,5 +1,8 @@
 #!/bin/bash
+# adopted 28-column K3: full GPU suite + smoke, bench lines, K3 ncu
 O=gpurun_out/r2l; mkdir -p $O
-WV_LIB=$PWD/paper_2208_10859_b200/variants/k4y64.so timeout 900 python -m pytest tests/test_gpu_decode.py -m gpu -q -rf -p no:cacheprovider -k "perspective or eye_split or hundred" > $O/k4y64_tests.log 2>&1; echo "k4y64 tests rc=$?"; tail -3 $O/k4y64_tests.log
-bash scripts/gpu_variants.sh $O default noskip k4y64
-bash scripts/gpu_variants.sh $O default noskip k4y64
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/gpu_tests.log 2>&1; echo "tests exit $?" >> $O/gpu_tests.log
+tail -3 $O/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?"
+timeout 600 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err; echo "bench exit $?"; cut -c1-300 $O/bench_c3.json
+bash scripts/prof_k3.sh ${1:-r02l} > /dev/null 2>&1

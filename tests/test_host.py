@@ -51,6 +51,9 @@ def test_abi_host_functions(lib):
     # decode entry points reject missing pointers before touching the GPU
     a = N.FrameArgs()
     assert lib.wv_decode_frame(C.byref(g), C.byref(a), None, None) == N.WV_ERR_ARG
+    # K3 work item: 32 rows x 28 columns per subband (a warp = 28 columns + 2 x 2 halo)
+    assert N.synthesis_tile() == (32, 28)
+    assert lib.wv_synthesis_tile(None, None) == N.WV_ERR_ARG
 
 
 def test_encode_abi_host_checks(lib):
