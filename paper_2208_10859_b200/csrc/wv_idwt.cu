@@ -202,7 +202,7 @@ struct LevelArgs {
 // next item's four loads go out, overlapping this item's row pass.  21 KB
 // of boxes + 2 KB of request staging and 64 registers: 8 CTAs per SM.
 constexpr int BOXSET = 4 * BOX_SLOT;
-constexpr int RQ_WORDS = 4;                     // request-mask words per staged row
+constexpr int RQ_WORDS = 4;                     // request-mask words per staged row (3 used)
 constexpr int RQ_SLOT = OUT_H * RQ_WORDS;       // u32 per staging slot
 constexpr int SMEM_MID = BOXSET;
 constexpr int SMEM_FIN = BOXSET + 2 * RQ_SLOT * 4;
@@ -282,18 +282,23 @@ __global__ void K3_BOUNDS k_level(const __grid_constant__ CUtensorMap tm_ll,
     const int w0 = (2 * ax) >> 5;   // first request word of the tile's pixel columns
     bool rq_all = true;             // final: the whole tile is requested (no masking)
     if (FINAL) {
-      // the tile's request-mask words (row map -> mask row, two dependent
-      // loads per row) staged while the boxes load
-      for (int i = tid; i < ny * RQ_WORDS; i += NTHREADS) {
-        const int r = i / RQ_WORDS, k = i - r * RQ_WORDS;
-        const int w = w0 + k;
-        const uint32_t v = w < a.wpr0 ? a.R[(uint64_t)a.rowmap[2 * ay + r] * a.wpr0 + w] : 0u;
-        rq[i] = v;
-        // the tile's pixel columns [2ax, 2ax + nx) inside this word
-        const int lo = max(2 * ax - 32 * w, 0), hi = min(2 * ax + nx - 32 * w, 32);
-        const uint32_t need =
-            lo >= hi ? 0u : ((hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & (0xFFFFFFFFu << lo));
-        rq_all &= (v & need) == need;
+      // the tile's request-mask words, one output row per thread (row map ->
+      // mask row, then the row's 3 words), staged while the boxes load; a
+      // 56-px tile starting at bit 2ax & 31 spans at most 3 words
+      if (tid < ny) {
+        const uint32_t* Rrow = a.R + (uint64_t)a.rowmap[2 * ay + tid] * a.wpr0;
+        uint32_t v[RQ_WORDS];
+#pragma unroll
+        for (int k = 0; k < RQ_WORDS; ++k) {
+          const int w = w0 + k;
+          v[k] = (k < 3 && w < a.wpr0) ? Rrow[w] : 0u;
+          // the tile's pixel columns [2ax, 2ax + nx) inside this word
+          const int lo = max(2 * ax - 32 * w, 0), hi = min(2 * ax + nx - 32 * w, 32);
+          const uint32_t need =
+              lo >= hi ? 0u : ((hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & (0xFFFFFFFFu << lo));
+          rq_all &= (v[k] & need) == need;
+        }
+        *reinterpret_cast<uint4*>(rq + tid * RQ_WORDS) = make_uint4(v[0], v[1], v[2], v[3]);
       }
     }
     if (a.use_tma) {
