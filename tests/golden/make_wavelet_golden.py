@@ -13,7 +13,11 @@ from wavevid.wavelets import CoefficientPyramid, WaveletKind, analyze_2d, synthe
 out = {}
 rng = np.random.default_rng(21)
 cases = {"rgb_cdf97": ((64, 128, 3), 3, "CDF97"), "mono_cdf97": ((96, 64), 4, "CDF97"),
-         "rgb_haar": ((32, 64, 3), 2, "HAAR")}
+         "rgb_haar": ((32, 64, 3), 2, "HAAR"),
+         # K3 edge shapes: subband widths that are not multiples of 4 floats
+         # (plain-load boxes), partial 32x28 tiles, a 1x1 coarsest level
+         "odd_cdf97": ((80, 40, 3), 3, "CDF97"), "tall_cdf97": ((144, 112), 4, "CDF97"),
+         "tiny_cdf97": ((16, 16), 4, "CDF97"), "wide_cdf97": ((64, 232), 3, "CDF97")}
 for name, (shape, levels, kind) in cases.items():
     x = rng.random(shape).astype(np.float32)
     p = analyze_2d(x, levels, WaveletKind[kind])

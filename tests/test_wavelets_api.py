@@ -9,7 +9,8 @@ import pytest
 
 from conftest import GOLDEN
 
-CASES = ["rgb_cdf97", "mono_cdf97", "rgb_haar"]
+CASES = ["rgb_cdf97", "mono_cdf97", "rgb_haar", "odd_cdf97", "tall_cdf97", "tiny_cdf97",
+         "wide_cdf97"]
 
 
 @pytest.fixture(scope="module")
