@@ -147,6 +147,7 @@ struct ViewConst {
 #define K4_TILE_Y 32
 #endif
 constexpr int K4_TX = 32, K4_TY = K4_TILE_Y, K4_PPT = K4_TY / 8;
+static_assert(K4_PPT % 2 == 0, "channel 2 is blended for pixel pairs");
 #ifndef K4_WIN_WORDS
 #define K4_WIN_WORDS (9216 * K4_TILE_Y / 32)
 #endif
@@ -172,23 +173,29 @@ __device__ __forceinline__ uint32_t blend(float b00, float b01, float b10, float
   return __float_as_uint(fmaf(ay, bot - top, top) + 8388608.0f) & 0xFFu;
 }
 
-// blend() of channels 0 and 1 at once with paired FP32 operations (each lane
-// rounds exactly like the scalar code); returns byte 0 | byte 1 << 8.
-__device__ __forceinline__ uint32_t blend2(uint32_t w00, uint32_t w01, uint32_t w10, uint32_t w11,
-                                           float ax, float ay) {
-  const uint32_t K = 0x4B000000u;
-  auto biased = [&](uint32_t w) {   // 2^23 + byte 0, 2^23 + byte 1
-    return make_float2(__uint_as_float(__byte_perm(K, w, 0x3004u)),
-                       __uint_as_float(__byte_perm(K, w, 0x3005u)));
-  };
-  const float2 b00 = biased(w00), b01 = biased(w01), b10 = biased(w10), b11 = biased(w11);
+// blend() of two lanes at once with paired FP32 operations (each lane
+// rounds exactly like the scalar code), per-lane weights; the taps are
+// 2^23-biased channel values.  Returns byte x | byte y << 8.
+__device__ __forceinline__ uint32_t blend_v2(float2 b00, float2 b01, float2 b10, float2 b11,
+                                             float2 A, float2 B) {
   const float2 nk = make_float2(-8388608.0f, -8388608.0f);
-  const float2 A = make_float2(ax, ax), B = make_float2(ay, ay);
   auto neg = [](float2 v) { return make_float2(-v.x, -v.y); };
   const float2 top = __ffma2_rn(A, __fadd2_rn(b01, neg(b00)), __fadd2_rn(b00, nk));
   const float2 bot = __ffma2_rn(A, __fadd2_rn(b11, neg(b10)), __fadd2_rn(b10, nk));
   const float2 v = __fadd2_rn(__ffma2_rn(B, __fadd2_rn(bot, neg(top)), top), neg(nk));
   return __byte_perm(__float_as_uint(v.x), __float_as_uint(v.y), 0x0040u);
+}
+
+// 2^23 + byte s of tap word w (selector: byte s, zeros, 0x4B)
+__device__ __forceinline__ float biased(uint32_t w, uint32_t s) {
+  return __uint_as_float(__byte_perm(0x4B000000u, w, 0x3004u + s));
+}
+
+// blend() of channels 0 and 1 of one pixel; returns byte 0 | byte 1 << 8.
+__device__ __forceinline__ uint32_t blend2(uint32_t w00, uint32_t w01, uint32_t w10, uint32_t w11,
+                                           float ax, float ay) {
+  auto b = [](uint32_t w) { return make_float2(biased(w, 0), biased(w, 1)); };
+  return blend_v2(b(w00), b(w01), b(w10), b(w11), make_float2(ax, ax), make_float2(ay, ay));
 }
 
 // t / d and t % d for 0 <= t <= 256 and 1 <= d <= 64 without an integer
@@ -480,6 +487,7 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
     // (4a) common case, uniform over the CTA: whole tile inside the output,
     // box covered by the footprint and staged -- taps straight from the window
     if (covered && use_win && full_tile) {
+      uint32_t pw[4];   // CT == 3: taps of the previous (even) pixel
 #pragma unroll
       for (int k = 0; k < K4_PPT; ++k) {
         WV_ASSERT(off[k] >= 0 && off[k] + P + 1 < rows * P);
@@ -488,14 +496,25 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
         uint8_t* o = oj + (threadIdx.y + 8 * k) * OST_PITCH + threadIdx.x * C;
         if (CT == 3) {
           // channels 0 and 1 as one paired-FP32 stream (same per-lane rounding
-          // as blend()), channel 2 scalar
+          // as blend()); channel 2 paired with channel 2 of the thread's next
+          // pixel (k odd: done with pixel k-1)
           const uint32_t rg = blend2(w00, w01, w10, w11, ax[k], ay[k]);
           o[0] = (uint8_t)rg;
           o[1] = (uint8_t)(rg >> 8);
-          o[2] = (uint8_t)blend(__uint_as_float(__byte_perm(K, w00, 0x3006u)),
-                                __uint_as_float(__byte_perm(K, w01, 0x3006u)),
-                                __uint_as_float(__byte_perm(K, w10, 0x3006u)),
-                                __uint_as_float(__byte_perm(K, w11, 0x3006u)), ax[k], ay[k]);
+          if (k & 1) {
+            const uint32_t bb = blend_v2(
+                make_float2(biased(pw[0], 2), biased(w00, 2)), make_float2(biased(pw[1], 2), biased(w01, 2)),
+                make_float2(biased(pw[2], 2), biased(w10, 2)),
+                make_float2(biased(pw[3], 2), biased(w11, 2)), make_float2(ax[k - 1], ax[k]),
+                make_float2(ay[k - 1], ay[k]));
+            o[2 - 8 * OST_PITCH] = (uint8_t)bb;
+            o[2] = (uint8_t)(bb >> 8);
+          } else {
+            pw[0] = w00;
+            pw[1] = w01;
+            pw[2] = w10;
+            pw[3] = w11;
+          }
         } else {
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
