@@ -278,6 +278,9 @@ __global__ void K3_BOUNDS k_level(const __grid_constant__ CUtensorMap tm_ll,
     const uint32_t nxt = item + gridDim.x;
     uint32_t nxt_entry = ZERO_FLAG;
     if ((FINAL || WV_K3_MID_PREFETCH) && tid == 0 && a.use_tma && nxt < nitems) nxt_entry = a.list[nxt / a.divC];
+    // the boxes go out before the request words are staged (the elected
+    // thread would otherwise wait for its staging loads first)
+    if (FINAL && a.use_tma && !issued) issue(item);
     uint32_t* rq = rq_stage + slot * RQ_SLOT;
     const int w0 = (2 * ax) >> 5;   // first request word of the tile's pixel columns
     bool rq_all = true;             // final: the whole tile is requested (no masking)
@@ -302,7 +305,7 @@ __global__ void K3_BOUNDS k_level(const __grid_constant__ CUtensorMap tm_ll,
       }
     }
     if (a.use_tma) {
-      if (!issued) issue(item);
+      if (!FINAL && !issued) issue(item);
       mbar_wait(&bar, phase);
       phase ^= 1u;
     } else {
