@@ -710,7 +710,6 @@ extern "C" int wv_encode_set(const wv_encode_params* p, const uint8_t* d_frames,
   uint32_t* nzbits = (uint32_t*)(ws + lo.nzbits);
   const int H = p->height, W = p->width, C = p->channels, n = p->inter_size;
   const int planes_n = n * C;
-  const size_t plane = (size_t)H * W;
   constexpr int T = 256;
 
   int h = H, w = W;

@@ -70,6 +70,7 @@ __device__ __forceinline__ float sqrt_approx(float x) {   // MUFU.SQRT; sqrt(0) 
   return r;
 }
 
+#if !WV_K4_GEO2
 __device__ __forceinline__ float fast_atan2(float y, float x) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
@@ -88,6 +89,7 @@ __device__ __forceinline__ float fast_atan2(float y, float x) {
   r = x < 0.0f ? 3.141592653589793f - r : r;
   return copysignf(r, y);
 }
+#endif
 
 // bits of columns [c0, c1) that fall in word w
 __device__ __forceinline__ uint32_t range_bits(int c0, int c1, int w) {
@@ -418,7 +420,7 @@ __device__ __forceinline__ void finish(const ViewConst& vc, const wv_view_args& 
                                        int xh, int yl, int yh, int wx0, int ww, bool box_ok,
                                        bool use_win, int tid) {
   const int C = CT ? CT : vc.C;
-  const int m = vc.m, n = vc.n, out_w = vc.out_w, out_h = vc.out_h;
+  const int n = vc.n, out_w = vc.out_w, out_h = vc.out_h;
   const int rows = yh - yl + 1;
   const int P = 4 * ww;           // window pitch (words)
   const int VW = rows * P;        // words per view in the window
