@@ -20,7 +20,7 @@
 // each side, so a warp's 32 lanes hold everything its row lifting needs.  The
 // column pass streams the lane's column down the segment (the L-half LL/LH and
 // H-half HL/HH lines packed as float2, Blackwell's paired FP32 ops
-// __fadd2_rn/__fmul2_rn, RN, no FMA) and keeps the 8 emitted row pairs in
+// __fadd2_rn and products as __ffma2_rn(a, b, -0.0), each rounded like numpy) and keeps the 8 emitted row pairs in
 // registers; the row pass then lifts each row pair (two rows packed) across
 // the lanes, neighbour values exchanged by warp shuffles -- no shared column
 // buffer and one barrier per item (the boxes are free once every warp's
@@ -75,19 +75,17 @@ __device__ __forceinline__ uint32_t u8_rint(float x) {
   return min(__float2uint_rn(x), 255u);
 #endif
 }
-// d * (1/K) feeds the packed add (d[i-1] + d[i]) of the next lifting step; a
-// packed multiply there would be contracted into FFMA2 by ptxas, so the
-// scale is two scalar round-to-nearest multiplies (never contracted).
-__device__ __forceinline__ float2 dscale(float2 d, float2 ik) {
-  return make_float2(__fmul_rn(d.x, ik.x), __fmul_rn(d.y, ik.y));
-}
-// x - k*(y1 + y2), written as x + (-k)*(y1+y2): identical rounding.  The
-// final add is issued as two scalar FADDs: ptxas contracts a paired
-// mul.rn.f32x2 feeding add.rn.f32x2 into FFMA2 (observed with CUDA 12.9),
-// which would change the rounding; scalar adds keep the product rounded.
-__device__ __forceinline__ float2 lstep(float2 x, float2 nk, float2 y1, float2 y2) {
-  const float2 t = __fmul2_rn(nk, __fadd2_rn(y1, y2));
-  return make_float2(__fadd_rn(x.x, t.x), __fadd_rn(x.y, t.y));
+// RN products as fma.rn.f32x2(a, b, z) with z = -0.0 supplied at run time
+// (a kernel argument): a*b + (-0) rounds exactly like mul.rn (a -0 addend
+// changes no product, +0 included), and an FMA result is never contracted
+// into a following add -- ptxas (CUDA 12.9) contracts a paired mul.rn.f32x2
+// feeding add.rn.f32x2 into FFMA2 despite the .rn, and it folds a literal
+// -0 addend back into a multiply.  So every lifting step is three paired
+// instructions: add, "multiply", add, each rounded once like numpy's.
+__device__ __forceinline__ float2 pmul(float2 a, float2 b, float2 z) { return __ffma2_rn(a, b, z); }
+// x - k*(y1 + y2), written as x + (-k)*(y1+y2): identical rounding.
+__device__ __forceinline__ float2 lstep(float2 x, float2 nk, float2 y1, float2 y2, float2 z) {
+  return __fadd2_rn(x, pmul(nk, __fadd2_rn(y1, y2), z));
 }
 
 // Interior segment (no level border inside [g0, g0 + LEN + 4)): the same
@@ -95,7 +93,7 @@ __device__ __forceinline__ float2 lstep(float2 x, float2 nk, float2 y1, float2 y
 // no emission tests, constant shared-memory offsets.  Local indices: inputs
 // 0 .. LEN+3, emitted pairs 2 .. LEN+1.
 template <int LEN, class Load, class Emit>
-__device__ __forceinline__ void lift_interior(Load load, Emit emit) {
+__device__ __forceinline__ void lift_interior(float2 z, Load load, Emit emit) {
   const float2 KS = f2(__uint_as_float(0x3f9d7658u));
   const float2 IK = f2(__uint_as_float(0x3f5019c3u));
   const float2 ND = f2(-__uint_as_float(0x3ee31355u));
@@ -104,23 +102,23 @@ __device__ __forceinline__ void lift_interior(Load load, Emit emit) {
   const float2 NA = f2(-__uint_as_float(0xbfcb0673u));
   float2 sr, dr;
   load(0, sr, dr);
-  float2 d1m = dscale(dr, IK);
-  float2 s2m = __fmul2_rn(sr, KS);         // s2[0] is a halo value: never emitted
+  float2 d1m = pmul(dr, IK, z);
+  float2 s2m = pmul(sr, KS, z);         // s2[0] is a halo value: never emitted
   load(1, sr, dr);
-  float2 d1 = dscale(dr, IK);
-  float2 s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);
-  float2 d2mm = lstep(d1m, NG, s2m, s2);   // d2[0] (halo)
+  float2 d1 = pmul(dr, IK, z);
+  float2 s2 = lstep(pmul(sr, KS, z), ND, d1m, d1, z);
+  float2 d2mm = lstep(d1m, NG, s2m, s2, z);   // d2[0] (halo)
   float2 s3mm = s2;                        // s3[0] (halo)
   d1m = d1;
   s2m = s2;
 #pragma unroll
   for (int j = 2; j < LEN + 4; ++j) {
     load(j, sr, dr);
-    d1 = dscale(dr, IK);
-    s2 = lstep(__fmul2_rn(sr, KS), ND, d1m, d1);   // s2[j]
-    const float2 d2 = lstep(d1m, NG, s2m, s2);      // d2[j-1]
-    const float2 s3 = lstep(s2m, NB, d2mm, d2);     // s3[j-1]
-    if (j >= 4) emit(j - 2, s3mm, lstep(d2mm, NA, s3mm, s3));   // d3[j-2]
+    d1 = pmul(dr, IK, z);
+    s2 = lstep(pmul(sr, KS, z), ND, d1m, d1, z);   // s2[j]
+    const float2 d2 = lstep(d1m, NG, s2m, s2, z);     // d2[j-1]
+    const float2 s3 = lstep(s2m, NB, d2mm, d2, z);    // s3[j-1]
+    if (j >= 4) emit(j - 2, s3mm, lstep(d2mm, NA, s3mm, s3, z));   // d3[j-2]
     d2mm = d2;
     s3mm = s3;
     d1m = d1;
@@ -192,6 +190,7 @@ struct LevelArgs {
                        // alignment); else the boxes are filled with plain loads
   const float* ll_ptr; int ll_pitch, ll_rows;   // LDG fallback sources
   const float* plane; int plane_w, plane_h;
+  float neg_zero;      // -0.0f (see pmul)
 };
 
 // Items are (tile, channel), 4 warps per item, warp w = output row pairs
@@ -235,6 +234,7 @@ __global__ void K3_BOUNDS k_level(const __grid_constant__ CUtensorMap tm_ll,
   const float2 NG = f2(-__uint_as_float(0x3f620676u));   // -gamma
   const float2 NB = f2(-__uint_as_float(0xbd5901aeu));   // -beta
   const float2 NA = f2(-__uint_as_float(0xbfcb0673u));   // -alpha
+  const float2 z = f2(a.neg_zero);                       // -0.0, opaque to ptxas
 
   // issue the four box loads of an item (elected thread)
   auto issue = [&](uint32_t it) {
@@ -343,6 +343,7 @@ __global__ void K3_BOUNDS k_level(const __grid_constant__ CUtensorMap tm_ll,
       if (pa >= HALO && pa + SEG + HALO <= a.bh) {
         const int rb = pa - HALO - oy;
         lift_interior<SEG>(
+            z,
             [&](int j, float2& s_, float2& d_) {
               const int o = (rb + j) * BOX_W + lc;
               WV_ASSERT(o >= 0 && o < BOX_FLOATS);
@@ -361,6 +362,7 @@ __global__ void K3_BOUNDS k_level(const __grid_constant__ CUtensorMap tm_ll,
         const int g0 = pa - HALO, N = a.bh;
         const int glo = oy, ghi = min(N, oy + BOX_H) - 1;   // rows held by the box
         lift_interior<SEG>(
+            z,
             [&](int j, float2& s_, float2& d_) {
               const int g = g0 + j;
               int gs = g, gd = g;
@@ -414,12 +416,12 @@ __global__ void K3_BOUNDS k_level(const __grid_constant__ CUtensorMap tm_ll,
     auto lift_pair = [&](int q, float2& s3, float2& d3) {
       const float2 s = make_float2(cs[q].x, cd[q].x);   // L half, rows 2p and 2p+1
       const float2 d = make_float2(cs[q].y, cd[q].y);   // H half
-      const float2 s1 = __fmul2_rn(s, KS);
-      const float2 d1 = dscale(d, IK);
-      const float2 s2 = lstep(s1, ND, sh2(d1, up), d1);
-      const float2 d2 = lstep(d1, NG, s2, sh2(s2, dn));
-      s3 = lstep(s2, NB, sh2(d2, up), d2);
-      d3 = lstep(d2, NA, s3, sh2(s3, dn));
+      const float2 s1 = pmul(s, KS, z);
+      const float2 d1 = pmul(d, IK, z);
+      const float2 s2 = lstep(s1, ND, sh2(d1, up), d1, z);
+      const float2 d2 = lstep(d1, NG, s2, sh2(s2, dn), z);
+      s3 = lstep(s2, NB, sh2(d2, up), d2, z);
+      d3 = lstep(d2, NA, s3, sh2(s3, dn), z);
     };
     // one unrolled loop per store kind (a branch inside the loop would keep
     // both epilogues' registers live)
@@ -511,6 +513,7 @@ int launch_tiles(const Layout& lo, const wv_frame_args* fa, uint8_t* ws, cudaStr
       return WV_ERR_CUDA;
   }
   LevelArgs la{};
+  la.neg_zero = -0.0f;
   la.k = k; la.bh = lo.H >> k; la.bw = lo.W >> k; la.C = C; la.ntx = lo.ntx[k];
   la.divC = fast_div((uint32_t)C);
   la.divN = fast_div((uint32_t)lo.ntx[k]);
