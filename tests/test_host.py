@@ -240,20 +240,30 @@ def test_decode_session_requires_gpu():
 
 
 def test_lifting_kernels_have_no_fused_multiply_add(lib):
-    """Bit-exact synthesis needs every product rounded before its add: the
-    K3 kernels' SASS must contain no FFMA/FFMA2 (ptxas contracts paired f32x2
-    mul/add otherwise)."""
+    """Bit-exact synthesis needs every product rounded before its add: in the
+    K3 kernels' SASS every FFMA2 is a product with the run-time -0.0 addend,
+    a scalar broadcast to both lanes (a*b + -0 rounds like mul.rn), and there
+    is no scalar FFMA.  A contracted paired multiply-add would show a packed
+    (F32x2) addend."""
+    import re
     import subprocess
     from paper_2208_10859_b200 import _native
     sass = subprocess.run(["cuobjdump", "-sass", _native.LIB_PATH], capture_output=True,
                           text=True).stdout
-    fn, bad = None, []
+    fn, bad, n_ffma2 = None, [], 0
     for line in sass.splitlines():
         if "Function :" in line:
             fn = line.split(":")[1].strip()
-        elif fn and "k_level" in fn and ("FFMA" in line):
-            bad.append((fn, line.strip()[:60]))
+        elif fn and "k_level" in fn:
+            if re.search(r"\bFFMA\b", line):
+                bad.append((fn, line.strip()[:60]))
+            m = re.search(r"FFMA2 [^;]*,\s*(\S+)\s*;", line)
+            if m:
+                n_ffma2 += 1
+                if not m.group(1).endswith(".F32"):   # broadcast scalar addend
+                    bad.append((fn, line.strip()[:80]))
     assert "k_level" in sass and not bad, bad[:3]
+    assert n_ffma2 > 0
     assert "UTMALDG" in sass      # the synthesis tiles are TMA-fed
 
 
