@@ -58,6 +58,11 @@ constexpr int BOX_SLOT = ((BOX_FLOATS * 4 + 127) / 128) * 128;  // bytes
 #define WV_K3_MID_PREFETCH 1   // mid levels also load the next item during the row pass
 #endif
 constexpr int SEG = 8;                 // output row pairs per warp (column-pass segment)
+#ifndef WV_K3_RP
+#define WV_K3_RP 2   // row pairs lifted together in the row pass (shuffle latency overlap)
+#endif
+constexpr int RP = WV_K3_RP;
+static_assert(SEG % RP == 0, "row-pass groups tile the segment");
 constexpr int NWARP = TY / SEG;        // 4
 constexpr int NTHREADS = 32 * NWARP;   // 128
 static_assert(TX + 2 * HALO == 32, "a warp's lanes are the tile's columns plus the halo");
@@ -413,49 +418,67 @@ __global__ void K3_BOUNDS k_level(const __grid_constant__ CUtensorMap tm_ll,
     uint8_t* crow = FINAL ? canvas + ((uint64_t)c * H + 2 * pa) * W + px : nullptr;
     float* orow = FINAL ? nullptr : a.out + ((uint64_t)c * H + 2 * pa) * a.out_pitch + 2 * x;
     // lift pair q across the lanes -> (s3, d3): .x = row 2p, .y = row 2p+1
-    auto lift_pair = [&](int q, float2& s3, float2& d3) {
-      const float2 s = make_float2(cs[q].x, cd[q].x);   // L half, rows 2p and 2p+1
-      const float2 d = make_float2(cs[q].y, cd[q].y);   // H half
-      const float2 s1 = pmul(s, KS, z);
-      const float2 d1 = pmul(d, IK, z);
-      const float2 s2 = lstep(s1, ND, sh2(d1, up), d1, z);
-      const float2 d2 = lstep(d1, NG, s2, sh2(s2, dn), z);
-      s3 = lstep(s2, NB, sh2(d2, up), d2, z);
-      d3 = lstep(d2, NA, s3, sh2(s3, dn), z);
+    // lift RP row pairs q .. q+RP-1 across the lanes, stage by stage, so
+    // their shuffle round trips overlap -> (s3, d3): .x = row 2p, .y = 2p+1
+    auto lift_pairs = [&](int q, float2 (&s3)[RP], float2 (&d3)[RP]) {
+      float2 s2[RP], d1[RP], d2[RP];
+#pragma unroll
+      for (int r = 0; r < RP; ++r) {
+        d1[r] = pmul(make_float2(cs[q + r].y, cd[q + r].y), IK, z);   // H half
+        s2[r] = pmul(make_float2(cs[q + r].x, cd[q + r].x), KS, z);   // L half (s1)
+      }
+#pragma unroll
+      for (int r = 0; r < RP; ++r) s2[r] = lstep(s2[r], ND, sh2(d1[r], up), d1[r], z);
+#pragma unroll
+      for (int r = 0; r < RP; ++r) d2[r] = lstep(d1[r], NG, s2[r], sh2(s2[r], dn), z);
+#pragma unroll
+      for (int r = 0; r < RP; ++r) s3[r] = lstep(s2[r], NB, sh2(d2[r], up), d2[r], z);
+#pragma unroll
+      for (int r = 0; r < RP; ++r) d3[r] = lstep(d2[r], NA, s3[r], sh2(s3[r], dn), z);
     };
     // one unrolled loop per store kind (a branch inside the loop would keep
     // both epilogues' registers live)
     if (!FINAL) {
 #pragma unroll
-      for (int q = 0; q < SEG; ++q) {
-        float2 s3, d3;
-        lift_pair(q, s3, d3);
-        if (emit && q < npairs) {
-          *reinterpret_cast<float2*>(orow + (2 * q) * (size_t)a.out_pitch) = make_float2(s3.x, d3.x);
-          *reinterpret_cast<float2*>(orow + (2 * q + 1) * (size_t)a.out_pitch) =
-              make_float2(s3.y, d3.y);
+      for (int q0 = 0; q0 < SEG; q0 += RP) {
+        float2 s3v[RP], d3v[RP];
+        lift_pairs(q0, s3v, d3v);
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          const int q = q0 + r;
+          const float2 s3 = s3v[r], d3 = d3v[r];
+          if (emit && q < npairs) {
+            *reinterpret_cast<float2*>(orow + (2 * q) * (size_t)a.out_pitch) = make_float2(s3.x, d3.x);
+            *reinterpret_cast<float2*>(orow + (2 * q + 1) * (size_t)a.out_pitch) =
+                make_float2(s3.y, d3.y);
+          }
         }
       }
     } else {
       // clip(rint(x*255)) (decoding.py:301), request-masked unless the whole
       // tile is requested; 2 pixels per row
 #pragma unroll
-      for (int q = 0; q < SEG; ++q) {
-        float2 s3, d3;
-        lift_pair(q, s3, d3);
-        if (emit && q < npairs) {
-          uint32_t m0 = 0xFFFFu, m1 = 0xFFFFu;
-          if (!unmasked) {
-            const uint32_t b0 = (rql[(2 * q) * RQ_WORDS] >> rsh) & 3u;
-            const uint32_t b1 = (rql[(2 * q + 1) * RQ_WORDS] >> rsh) & 3u;
-            // bits (0, 1) -> byte masks (0x00FF, 0xFF00)
-            m0 = ((b0 | (b0 << 7)) & 0x101u) * 0xFFu;
-            m1 = ((b1 | (b1 << 7)) & 0x101u) * 0xFFu;
+      for (int q0 = 0; q0 < SEG; q0 += RP) {
+        float2 s3v[RP], d3v[RP];
+        lift_pairs(q0, s3v, d3v);
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          const int q = q0 + r;
+          const float2 s3 = s3v[r], d3 = d3v[r];
+          if (emit && q < npairs) {
+            uint32_t m0 = 0xFFFFu, m1 = 0xFFFFu;
+            if (!unmasked) {
+              const uint32_t b0 = (rql[(2 * q) * RQ_WORDS] >> rsh) & 3u;
+              const uint32_t b1 = (rql[(2 * q + 1) * RQ_WORDS] >> rsh) & 3u;
+              // bits (0, 1) -> byte masks (0x00FF, 0xFF00)
+              m0 = ((b0 | (b0 << 7)) & 0x101u) * 0xFFu;
+              m1 = ((b1 | (b1 << 7)) & 0x101u) * 0xFFu;
+            }
+            const uint32_t v0 = (cv(s3.x) | (cv(d3.x) << 8)) & m0;
+            const uint32_t v1 = (cv(s3.y) | (cv(d3.y) << 8)) & m1;
+            *reinterpret_cast<uint16_t*>(crow + (2 * q) * (size_t)W) = (uint16_t)v0;
+            *reinterpret_cast<uint16_t*>(crow + (2 * q + 1) * (size_t)W) = (uint16_t)v1;
           }
-          const uint32_t v0 = (cv(s3.x) | (cv(d3.x) << 8)) & m0;
-          const uint32_t v1 = (cv(s3.y) | (cv(d3.y) << 8)) & m1;
-          *reinterpret_cast<uint16_t*>(crow + (2 * q) * (size_t)W) = (uint16_t)v0;
-          *reinterpret_cast<uint16_t*>(crow + (2 * q + 1) * (size_t)W) = (uint16_t)v1;
         }
       }
     }
