@@ -325,11 +325,15 @@ def run_ours(args):
     unc = sum(ss.uncovered() for ss in sessions)
     # host cost of one frame's enqueue (the public call), measured where the
     # GPU cannot push back: an idle GPU, fewer frames than the session ring
+    # (one step's frame repeated: a frame of another set would make the call
+    # settle the pending decodes first -- the reference's two-set cache can
+    # evict, decoding.py:236-241 -- and time the GPU instead of the host)
     torch.cuda.synchronize()
+    sess._settle_until(None)
     nh = min(args.steps, 8)   # few enough that no launch queue fills up
     th = time.perf_counter()
     for i in range(nh):
-        step(args.warmup + i, 0)
+        step(args.warmup, 0)
     host_enqueue_us = (time.perf_counter() - th) * 1e6 / nh
     torch.cuda.synchronize()
     sess._settle_until(None)

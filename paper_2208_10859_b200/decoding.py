@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import contextlib
 import ctypes as C
+import functools
 import math
 import os
 import threading
@@ -95,18 +96,35 @@ class SessionStats:
     total_ms: float = 0.0
 
 
+@functools.lru_cache(maxsize=16)
+def _upscale_ranges(n: int, m: int):
+    """For the nearest upscale of m cells to n pixels (index map
+    ``arange(n) * m // n``, fileio.py:430-436): per cell the pixel range
+    [start, end) that maps to it (empty when n < m skips the cell)."""
+    idx = np.arange(n, dtype=np.int64) * m // n
+    cells = np.arange(m)
+    return np.searchsorted(idx, cells, "left"), np.searchsorted(idx, cells, "right")
+
+
+def _axis_extent(any_cells: np.ndarray, n: int):
+    start, end = _upscale_ranges(n, any_cells.size)
+    hit = np.flatnonzero(any_cells & (end > start))
+    if hit.size == 0:
+        return None
+    return int(start[hit[0]]), int(end[hit[-1]])
+
+
 def mask_bbox(mask: np.ndarray, width: int, height: int):
     """Bounding box (y0, y1, x0, x1) of the upscaled pixel mask, computed
     from the low-resolution mask through the nearest-neighbour index maps
-    (fileio.py:430-436) without materialising the full-resolution mask."""
+    (fileio.py:430-436) without materialising the full-resolution mask: the
+    first and last set cells per axis whose pixel range is not empty."""
     m = np.asarray(mask, bool)
-    mh, mw = m.shape
-    rows = m.any(axis=1)[np.arange(height, dtype=np.int64) * mh // height]
-    cols = m.any(axis=0)[np.arange(width, dtype=np.int64) * mw // width]
-    ry, cx = np.flatnonzero(rows), np.flatnonzero(cols)
-    if ry.size == 0 or cx.size == 0:
+    ys = _axis_extent(m.any(axis=1), height)
+    xs = _axis_extent(m.any(axis=0), width) if ys is not None else None
+    if ys is None or xs is None:
         return None
-    return int(ry[0]), int(ry[-1]) + 1, int(cx[0]), int(cx[-1]) + 1
+    return ys[0], ys[1], xs[0], xs[1]
 
 
 def fovea_rects(bbox, height: int, width: int, schedule: FoveationSchedule, levels: int):

@@ -2,7 +2,7 @@
 path), isolated from GPU time: a small stereo file (tests/golden/
 golden_stereo.wvv, so the kernels are short), cProfile over N frames after
 warm-up, plus the unprofiled wall time per frame.  Run on the GPU box:
-    python scripts/host_profile.py [N]"""
+    python scripts/host_profile.py [N] [viewport|foveated]"""
 import cProfile
 import os
 import pstats
@@ -18,17 +18,19 @@ import paper_2208_10859_b200 as wv  # noqa: E402
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 400
+    mode = sys.argv[2] if len(sys.argv) > 2 else "viewport"
     s = wv.DecodeSession(os.path.join(ROOT, "tests", "golden", "golden_stereo.wvv"))
     s.time_stages = False
     h = s.header
     poses = [wv.CameraPose(yaw=-60 + 0.5 * i, pitch=10) for i in range(64)]
     masks = [wv.stereo_mask(p, (h.mask_w, h.mask_h)) for p in poses]
     out = torch.empty((2, 256, 256, 3), dtype=torch.uint8, device="cuda")
+    sc = wv.FoveationSchedule.default(h.levels, 0.5, 0.5) if mode == "foveated" else None
 
     def run(k):
         for i in range(k):
-            s.decode_render_device(i % h.frame_count, "viewport", masks[i % 64], poses[i % 64],
-                                   (256, 256), out)
+            s.decode_render_device(i % h.frame_count, mode, masks[i % 64], poses[i % 64],
+                                   (256, 256), out, schedule=sc)
 
     run(80)
     torch.cuda.synchronize()
