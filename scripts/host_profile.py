@@ -2,7 +2,7 @@
 path), isolated from GPU time: a small stereo file (tests/golden/
 golden_stereo.wvv, so the kernels are short), cProfile over N frames after
 warm-up, plus the unprofiled wall time per frame.  Run on the GPU box:
-    python scripts/host_profile.py [N] [viewport|foveated]"""
+    python scripts/host_profile.py [N] [viewport|foveated|full]"""
 import cProfile
 import os
 import pstats
@@ -29,8 +29,11 @@ def main():
 
     def run(k):
         for i in range(k):
-            s.decode_render_device(i % h.frame_count, mode, masks[i % 64], poses[i % 64],
-                                   (256, 256), out, schedule=sc)
+            if mode == "full":
+                s.decode_full_device(i % h.frame_count)
+            else:
+                s.decode_render_device(i % h.frame_count, mode, masks[i % 64], poses[i % 64],
+                                       (256, 256), out, schedule=sc)
 
     run(80)
     torch.cuda.synchronize()
