@@ -1,5 +1,6 @@
 """Host cost per decode_render_device call on the 8K bench clip, per mode
-(idle GPU, fewer calls than the result ring), with a per-function split."""
+(idle GPU, one frame repeated so the set cache never evicts), with a
+per-function split."""
 import cProfile, os, pstats, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "scripts"))
@@ -14,13 +15,18 @@ h = s.header
 poses = [wv.CameraPose(yaw=-60 + 2 * i, pitch=10) for i in range(8)]
 masks = [wv.stereo_mask(p, (h.mask_w, h.mask_h)) for p in poses]
 out = torch.empty((2, 2000, 2000, 3), dtype=torch.uint8, device="cuda")
-for mode in ("viewport", "foveated"):
+for mode in ("viewport", "foveated", "viewport"):
     sc = wv.FoveationSchedule.default(h.levels, 0.5, 0.5) if mode == "foveated" else None
-    run = lambda k: [s.decode_render_device(i % h.frame_count, mode, masks[i % 8], poses[i % 8], (2000, 2000), out, schedule=sc) for i in range(k)]
-    run(16); torch.cuda.synchronize(); s._settle_until(None)
-    t = time.perf_counter(); run(6); dt = (time.perf_counter() - t) / 6 * 1e6
+    call = lambda i: s.decode_render_device(0, mode, masks[i % 8], poses[i % 8], (2000, 2000), out, schedule=sc)
+    for i in range(16): call(i)
     torch.cuda.synchronize(); s._settle_until(None)
-    pr = cProfile.Profile(); pr.enable(); run(6); pr.disable()
+    ts = []
+    for i in range(8):
+        t = time.perf_counter(); call(i); ts.append((time.perf_counter() - t) * 1e6)
     torch.cuda.synchronize(); s._settle_until(None)
-    print(f"== {mode}: {dt:.1f} us/call")
-    pstats.Stats(pr).sort_stats("tottime").print_stats(12)
+    print(mode, " ".join(f"{x:.0f}" for x in ts))
+    pr = cProfile.Profile(); pr.enable()
+    for i in range(8): call(i)
+    pr.disable()
+    torch.cuda.synchronize(); s._settle_until(None)
+    pstats.Stats(pr).sort_stats("tottime").print_stats(8)
