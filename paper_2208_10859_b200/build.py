@@ -46,7 +46,7 @@ def _stale(lib: str = LIB) -> bool:
 
 def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
     """Build the library (``out``/``defines``: an experimental variant, e.g.
-    ``defines=["WV_SEGLEN_R=8"]``, loaded with ``WV_LIB=<out>``)."""
+    ``defines=["WV_K3_RP=4"]``, loaded with ``WV_LIB=<out>``)."""
     lib = out or LIB
     if not out and not defines and not force and not _stale():
         return LIB
