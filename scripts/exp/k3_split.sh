@@ -1,7 +1,7 @@
 #!/bin/bash
 # timing-only variants (results wrong by design): K3 finest without loads / without compute
 O=gpurun_out/k3split; mkdir -p $O
-for v in default noload nocompute; do
+for v in ${VARIANTS:-default noload nocompute}; do
   if [ $v = default ]; then lib=$PWD/paper_2208_10859_b200/_wvb200.so; else lib=$PWD/paper_2208_10859_b200/variants/$v.so; fi
   for m in viewport full; do
     WV_LIB=$lib timeout 300 python bench.py --steps 40 --warmup 5 --mode $m --no-cpu-baseline --no-e2e > $O/$v.$m.json 2>$O/$v.$m.err
