@@ -12,7 +12,11 @@ namespace wv {
 #define WV_TILE_Y 32
 #endif
 constexpr int TY = WV_TILE_Y;
-constexpr int TX = 28;                // + 2 halo columns each side = one warp's 32 lanes
+#ifndef WV_K3_STRIPS
+#define WV_K3_STRIPS 1
+#endif
+constexpr int TXS = 28;               // columns of one warp strip (+ 2 halo each side = 32 lanes)
+constexpr int TX = TXS * WV_K3_STRIPS;   // tile width: WV_K3_STRIPS strips side by side
 constexpr int HALO = 2;               // lifting support per side
 // TMA box: the innermost box coordinate must be 16-byte aligned (unaligned or
 // negative-unaligned starts raise an illegal-instruction fault on B200), so

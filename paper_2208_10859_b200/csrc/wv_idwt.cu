@@ -49,7 +49,9 @@ constexpr int BOX_SLOT = ((BOX_FLOATS * 4 + 127) / 128) * 128;  // bytes
 #ifndef WV_K3_MINB
 #define WV_K3_MINB 8   // 64 registers: 8 CTAs (32 warps) per SM, the shared-memory limit too
 #endif
-#if WV_K3_MINB > 0
+#if WV_K3_MINB > 0 && WV_K3_STRIPS > 1
+#define K3_BOUNDS __launch_bounds__(NTHREADS, WV_K3_MINB / WV_K3_STRIPS)
+#elif WV_K3_MINB > 0
 #define K3_BOUNDS __launch_bounds__(NTHREADS, WV_K3_MINB)
 #else
 #define K3_BOUNDS __launch_bounds__(NTHREADS)
@@ -63,9 +65,10 @@ constexpr int SEG = 8;                 // output row pairs per warp (column-pass
 #endif
 constexpr int RP = WV_K3_RP;
 static_assert(SEG % RP == 0, "row-pass groups tile the segment");
-constexpr int NWARP = TY / SEG;        // 4
-constexpr int NTHREADS = 32 * NWARP;   // 128
-static_assert(TX + 2 * HALO == 32, "a warp's lanes are the tile's columns plus the halo");
+constexpr int NSTRIP = WV_K3_STRIPS;
+constexpr int NWARP = TY / SEG * NSTRIP;   // 4 per strip
+constexpr int NTHREADS = 32 * NWARP;       // 128 per strip
+static_assert(TXS + 2 * HALO == 32, "a warp's lanes are its strip's columns plus the halo");
 static_assert(BOX_W >= TX + 2 * XPAD, "the box covers the halo columns");
 
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
@@ -206,7 +209,8 @@ struct LevelArgs {
 // next item's four loads go out, overlapping this item's row pass.  21 KB
 // of boxes + 2 KB of request staging and 64 registers: 8 CTAs per SM.
 constexpr int BOXSET = 4 * BOX_SLOT;
-constexpr int RQ_WORDS = 4;                     // request-mask words per staged row (3 used)
+constexpr int RQ_USED = (30 + 2 * TX + 31) / 32;   // request words a tile row can touch
+constexpr int RQ_WORDS = RQ_USED <= 4 ? 4 : 8;      // staged per row (16-B stores)
 constexpr int RQ_SLOT = OUT_H * RQ_WORDS;       // u32 per staging slot
 constexpr int SMEM_MID = BOXSET;
 constexpr int SMEM_FIN = BOXSET + 2 * RQ_SLOT * 4;
@@ -299,14 +303,17 @@ __global__ void K3_BOUNDS k_level(const __grid_constant__ CUtensorMap tm_ll,
 #pragma unroll
         for (int k = 0; k < RQ_WORDS; ++k) {
           const int w = w0 + k;
-          v[k] = (k < 3 && w < a.wpr0) ? Rrow[w] : 0u;
+          v[k] = (k < RQ_USED && w < a.wpr0) ? Rrow[w] : 0u;
           // the tile's pixel columns [2ax, 2ax + nx) inside this word
           const int lo = max(2 * ax - 32 * w, 0), hi = min(2 * ax + nx - 32 * w, 32);
           const uint32_t need =
               lo >= hi ? 0u : ((hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & (0xFFFFFFFFu << lo));
           rq_all &= (v[k] & need) == need;
         }
-        *reinterpret_cast<uint4*>(rq + tid * RQ_WORDS) = make_uint4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+        for (int k = 0; k < RQ_WORDS; k += 4)
+          *reinterpret_cast<uint4*>(rq + tid * RQ_WORDS + k) =
+              make_uint4(v[k], v[k + 1], v[k + 2], v[k + 3]);
       }
     }
     if (a.use_tma) {
@@ -335,10 +342,11 @@ __global__ void K3_BOUNDS k_level(const __grid_constant__ CUtensorMap tm_ll,
 
     // column pass: lane = column x, warp = segment of SEG output row pairs;
     // the 8 pairs (L and H halves packed) stay in registers
-    const int x = ax - HALO + lane;
-    const int pa = ay + SEG * warp, pb = min(pa + SEG, by);
+    const int strip = warp % NSTRIP, seg = warp / NSTRIP;
+    const int x = ax + TXS * strip - HALO + lane;
+    const int pa = ay + SEG * seg, pb = min(pa + SEG, by);
     float2 cs[SEG], cd[SEG];   // (s3, d3) of pair q: .x = L half, .y = H half
-    const bool col_live = x >= max(ax - HALO, 0) && x < min(bx + HALO, a.bw) && pa < pb;
+    const bool col_live = x >= 0 && x < min(bx + HALO, a.bw) && pa < pb;
     if (col_live) {
       const int lc = x - ox;
       auto emit = [&](int p, float2 s3, float2 d3) {

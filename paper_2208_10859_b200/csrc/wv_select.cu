@@ -623,12 +623,12 @@ __global__ void __launch_bounds__(256) k_footprint(FootArgs a) {
 // footprint is ANDed with the request, so it is zero outside the tiles that
 // touch the request; tiles that left the request (ZERO_FLAG) are cleared.
 // One CTA-iteration per OUT_H x OUT_W-pixel tile: 64 rows x FT_OW words, one
-// word per thread; source: 37 rows x 3 words of V_1 & D_1.  Tiles are not
+// word per thread; source: 37 rows x FT_SW words of V_1 & D_1.  Tiles are not
 // word aligned (OUT_W = 56), so a word can straddle two listed tiles: each
 // tile updates only the bits of its own pixel columns (atomicAnd to clear,
 // atomicOr to set -- neighbouring tiles touch disjoint bits).
-constexpr int FT_SR = OUT_H / 2 + DIL + 1, FT_SW = 3;
 constexpr int FT_OW = (OUT_W + 31) / 32 + (OUT_W % 32 ? 1 : 0);   // output words a tile touches
+constexpr int FT_SR = OUT_H / 2 + DIL + 1, FT_SW = FT_OW / 2 + 2;   // source rows / words
 constexpr int FT_THREADS = OUT_H * FT_OW;
 static_assert(FT_SW * 2 >= FT_OW + 2, "source window covers the tile's words and neighbours");
 
@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(FT_THREADS) k_footprint_tiles(FootArgs a, cons
       // AND over the output row's 4-5 source rows for each source word the
       // thread's neighbourhood (words w-1 .. w+1) reads
       const int s_lo = ((r - DIL) >> 1) - sr0, s_hi = ((r + DIL) >> 1) - sr0;
-      const int q0 = ((w - 1) >> 1) - sw0;   // 0 or 1; the words are q0, q0 + 1
+      const int q0 = ((w - 1) >> 1) - sw0;   // the words are q0, q0 + 1 (< FT_SW)
       uint32_t va0 = 0xFFFFFFFFu, va1 = 0xFFFFFFFFu;
       for (int k = s_lo; k <= s_hi; ++k) {
         va0 &= sv[k][q0];
