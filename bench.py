@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--mode", choices=["viewport", "foveated", "full"], default=None,
                     help="default: viewport for c3, full for c2")
     ap.add_argument("--clip", default=None, help="decode this .wvv instead of the config's clip")
+    ap.add_argument("--tile-strips", type=int, choices=[1, 2], default=None,
+                    help="K3 tile width in 28-column strips (default: 2 for full mode, else 1)")
     ap.add_argument("--cache-dir", default="/tmp/wvb200_bench")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -233,8 +235,12 @@ def run_ours(args):
     mode = args.mode
 
     P = max(1, args.pipeline)
+    # whole-frame decodes use the 56-column synthesis tiles (faster there;
+    # the viewport headline keeps 28-column tiles)
+    strips = args.tile_strips or (2 if mode == "full" else 1)
     sessions = [wv.DecodeSession(path, device=dev, max_resident_sets=8,
-                                 residency=args.residency) for _ in range(P)]
+                                 residency=args.residency, tile_strips=strips)
+                for _ in range(P)]
     for s_ in sessions:
         s_.time_stages = False
     sess = sessions[0]
@@ -405,7 +411,7 @@ def run_ours(args):
     # K3 finest level, per launch: read 4 subband tiles (ty x tx f32 each per
     # channel, 32 x 28) and write a 2ty x 2tx u8 tile per channel (SURVEY §8d
     # K3+K4 terms)
-    ty, tx = N.synthesis_tile()
+    ty, tx = N.synthesis_tile(sess._lib)
     alg = tiles * (4 * ty * tx * 4 * C + 4 * ty * tx * C)
     peak, peak_kind = peaks()
     achieved = alg / (k3f * 1e-3) / 1e9
@@ -541,6 +547,7 @@ def run_ours(args):
                        "before every step"),
                 "pipeline": f"{P} decode sessions (CUDA streams) per GPU, steps round-robin",
                 "residency": args.residency,
+                "synthesis_tile": f"{ty}x{tx} coefficients ({strips} warp strip(s))",
                 "parallelism": ((f"sets round-robin over {world} GPU(s), "
                                  if eye is None else
                                  f"stereo eyes split over rank pairs, sets round-robin over "

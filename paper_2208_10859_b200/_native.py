@@ -10,6 +10,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_wvb200.so")
+LIB_WIDE_PATH = os.path.join(HERE, "_wvb200_wide.so")   # 56-column synthesis tiles
 
 WV_OK, WV_ERR_ARG, WV_ERR_CUDA, WV_ERR_UNSUPPORTED, WV_ERR_FORMAT, WV_ERR_IO = 0, 1, 2, 3, 4, 5
 WV_MODE_FULL, WV_MODE_VIEWPORT, WV_MODE_FOVEATED = 0, 1, 2
@@ -107,16 +108,16 @@ class NativeError(RuntimeError):
     pass
 
 
-_lib = None
+_libs: dict = {}
 
 
 def load(path: str | None = None):
     """Load the decode library (raises if it is absent: no fallback).
     ``WV_LIB`` selects an experimental build variant (build.build(out=...))."""
-    global _lib
-    if _lib is not None:
-        return _lib
     path = path or os.environ.get("WV_LIB") or LIB_PATH
+    lib = _libs.get(path)
+    if lib is not None:
+        return lib
     if not os.path.exists(path):
         raise NativeError(
             f"B200 decode library not built: {path} (run python -m paper_2208_10859_b200.build)")
@@ -149,8 +150,19 @@ def load(path: str | None = None):
         getattr(lib, fn).restype = C.c_int
     if lib.wv_abi_version() != WV_ABI_VERSION:
         raise NativeError("decode library ABI mismatch")
-    _lib = lib
+    _libs[path] = lib
     return lib
+
+
+def load_tiles(strips: int = 1):
+    """The library whose synthesis tiles are ``strips`` warp strips wide:
+    1 -> 28 columns (the default build), 2 -> 56 columns (``_wvb200_wide.so``,
+    faster for full-frame decodes, slower for viewports)."""
+    if strips == 1:
+        return load()
+    if strips == 2:
+        return load(LIB_WIDE_PATH)
+    raise ValueError(f"tile_strips must be 1 or 2, not {strips}")
 
 
 def check(status: int, what: str) -> None:
@@ -159,10 +171,10 @@ def check(status: int, what: str) -> None:
         raise NativeError(f"{what} failed: {msg} (status {status})")
 
 
-def synthesis_tile() -> tuple:
+def synthesis_tile(lib=None) -> tuple:
     """(ty, tx): coefficients per subband of one K3 work item (wv_synthesis_tile)."""
     ty, tx = C.c_int32(), C.c_int32()
-    check(load().wv_synthesis_tile(C.byref(ty), C.byref(tx)), "wv_synthesis_tile")
+    check((lib or load()).wv_synthesis_tile(C.byref(ty), C.byref(tx)), "wv_synthesis_tile")
     return ty.value, tx.value
 
 

@@ -4,10 +4,14 @@
 
 Produces ``paper_2208_10859_b200/_wvb200.so`` (static cudart, so the library
 does not depend on which CUDA runtime torch loaded; device pointers and
-streams are shared through the primary context).
+streams are shared through the primary context) and ``_wvb200_wide.so``, the
+same sources with 56-column synthesis tiles (two warp strips per K3 work
+item, ``WV_K3_STRIPS=2``) for full-frame sessions
+(``DecodeSession(..., tile_strips=2)``).
 """
 from __future__ import annotations
 
+import concurrent.futures
 import os
 import shutil
 import subprocess
@@ -20,6 +24,8 @@ SOURCES = ["wv_select.cu", "wv_temporal.cu", "wv_idwt.cu", "wv_perspective.cu", 
            "wv_file.cpp", "wv_encode.cu", "wv_spans.cpp"]
 HEADERS = ["wv_common.cuh"]
 LIB = os.path.join(HERE, "_wvb200.so")
+LIB_WIDE = os.path.join(HERE, "_wvb200_wide.so")
+LIBS = {LIB: (), LIB_WIDE: ("WV_K3_STRIPS=2",)}   # the shipped builds
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-diag-suppress", "177"]
 # Bit-exact arithmetic (dequantisation, temporal sums, lifting) forbids FMA
@@ -45,23 +51,35 @@ def _stale(lib: str = LIB) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
-    """Build the library (``out``/``defines``: an experimental variant, e.g.
-    ``defines=["WV_K3_RP=4"]``, loaded with ``WV_LIB=<out>``)."""
-    lib = out or LIB
-    if not out and not defines and not force and not _stale():
-        return LIB
+    """Build the shipped libraries (``LIBS``), or with ``out``/``defines`` an
+    experimental variant, e.g. ``defines=["WV_K3_RP=4"]``, loaded with
+    ``WV_LIB=<out>``."""
+    if out or defines:
+        return _build_one(out or LIB, tuple(defines), verbose)
+    for lib, d in LIBS.items():
+        if force or _stale(lib):
+            _build_one(lib, d, verbose)
+    return LIB
+
+
+def _build_one(lib: str, defines, verbose: bool) -> str:
     objdir = os.path.join(HERE, "build_obj", os.path.basename(lib).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    cmds, objs = [], []
     for f in SOURCES:
         obj = os.path.join(objdir, f.rsplit(".", 1)[0] + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, f"--fmad={FMAD.get(f, 'false')}", "-I",
-               os.path.join(ROOT, "include"), *[f"-D{d}" for d in defines], "-c", "-o", obj,
-               os.path.join(CSRC, f)]
-        if verbose:
-            print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
+        cmds.append([nvcc(), *ARCH, *FLAGS, f"--fmad={FMAD.get(f, 'false')}", "-I",
+                     os.path.join(ROOT, "include"), *[f"-D{d}" for d in defines], "-c", "-o",
+                     obj, os.path.join(CSRC, f)])
         objs.append(obj)
+    if verbose:
+        for cmd in cmds:
+            print(" ".join(cmd))
+    # one nvcc per source, in parallel
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
+        for r in ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds):
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed: {' '.join(r.args)}\n{r.stderr}")
     tmp = lib + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     if verbose:

@@ -224,21 +224,26 @@ _MODES = {"full": N.WV_MODE_FULL, "viewport": N.WV_MODE_VIEWPORT, "foveated": N.
 class DecodeSession:
     """Single-owner decode session on one GPU stream with one-slot prefetch."""
 
-    def __init__(self, path, device=None, max_resident_sets: int = 4, residency: str = "set"):
+    def __init__(self, path, device=None, max_resident_sets: int = 4, residency: str = "set",
+                 tile_strips: int = 1):
         """``residency``: "set" reads a set's whole payload and uploads it to
         HBM when it is first decoded; "spans" reads and uploads only its
         BlockEnd table, and each decode streams the record spans of newly
         selected blocks from the file (VideoReader.load_blocks,
         fileio.py:346-390, 4 KiB coalescing) inside the frame's stream order:
         the GPU lists the blocks, a stream-ordered host function reads their
-        spans into pinned memory, and the fetch kernel copies them to HBM."""
+        spans into pinned memory, and the fetch kernel copies them to HBM.
+        ``tile_strips``: synthesis tile width in 28-column warp strips -- 2
+        (56 columns, the ``_wvb200_wide.so`` build) is faster for sessions
+        that decode whole frames, 1 for viewport decodes; results are
+        identical."""
         if residency not in ("set", "spans"):
             raise ValueError(f"residency {residency!r} not in ('set', 'spans')")
         self.residency = residency
         self.bytes_fetched = 0         # spans residency: record bytes copied host -> HBM
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 decode path needs a CUDA device (no CPU fallback)")
-        self._lib = N.load()
+        self._lib = N.load_tiles(tile_strips)
         self.reader = VideoReader(path)
         h = self.reader.header
         self.header = h

@@ -66,13 +66,18 @@ CASES = ["c3_viewport_step0", "c3_viewport_step37", "c3_viewport_fixed_f3",
          "c2_full_f1", "c2_full_f13", "c2_viewport_step50"]
 
 
-@pytest.mark.parametrize("name", CASES)
-def test_bench_clip_decode_equals_reference(wv, fixture, name):
+# the 56-column synthesis tiles (tile_strips=2, the full-frame bench's
+# sessions) on every kind of case
+WIDE = ["c3_viewport_step37", "c4_foveated_gaze_f9", "c5_full_f6", "c2_full_f13"]
+
+
+@pytest.mark.parametrize("name,strips", [(n, 1) for n in CASES] + [(n, 2) for n in WIDE])
+def test_bench_clip_decode_equals_reference(wv, fixture, name, strips):
     """GPU decode of the benchmarked clip == the reference decoder, bit for
     bit (pixels, footprint, stats); fresh session as in the fixture."""
     rec = fixture["cases"][name]
     path = mbi.ensure_clip(rec["clip"], CACHE)
-    with wv.DecodeSession(path, device="cuda:0") as sess:
+    with wv.DecodeSession(path, device="cuda:0", tile_strips=strips) as sess:
         h = sess.header
         pose, mask = _inputs(wv, rec, h)
         pix, fp, st = _decode(wv, sess, rec, mask)

@@ -24,9 +24,9 @@ def pkg():
     return p
 
 
-def _replay(pkg, name, decode_cases, device_api=False):
+def _replay(pkg, name, decode_cases, device_api=False, tile_strips=1):
     from paper_2208_10859_b200.decoding import FoveationSchedule
-    sess = pkg.DecodeSession(os.path.join(GOLDEN, name))
+    sess = pkg.DecodeSession(os.path.join(GOLDEN, name), tile_strips=tile_strips)
     h = sess.header
     for i, c in enumerate(case_calls(decode_cases, name)):
         mask = None
@@ -50,6 +50,14 @@ def _replay(pkg, name, decode_cases, device_api=False):
 @pytest.mark.parametrize("name", FILES)
 def test_replay_reference_decodes(pkg, decode_cases, name):
     _replay(pkg, name, decode_cases)
+
+
+@pytest.mark.parametrize("name", ["golden_quantized.wvv", "golden_stereo.wvv", "smooth_n8.wvv",
+                                  "noise_bs16.wvv", "wide_equirect.wvv"])
+def test_replay_reference_decodes_wide_tiles(pkg, decode_cases, name):
+    """The same reference call sequences through the 56-column synthesis
+    tiles (the _wvb200_wide.so build): identical pixels, footprints, stats."""
+    _replay(pkg, name, decode_cases, tile_strips=2)
 
 
 @pytest.mark.parametrize("name", ["golden_quantized.wvv", "golden_float.wvv",

@@ -51,8 +51,13 @@ def test_abi_host_functions(lib):
     # decode entry points reject missing pointers before touching the GPU
     a = N.FrameArgs()
     assert lib.wv_decode_frame(C.byref(g), C.byref(a), None, None) == N.WV_ERR_ARG
-    # K3 work item: 32 rows x 28 columns per subband (a warp = 28 columns + 2 x 2 halo)
+    # K3 work item: 32 rows x 28 columns per subband (a warp = 28 columns + 2 x 2 halo);
+    # the wide build (full-frame sessions) puts two warp strips side by side
     assert N.synthesis_tile() == (32, 28)
+    wide = N.load_tiles(2)
+    assert wide is not lib and N.synthesis_tile(wide) == (32, 56)
+    assert wide.wv_abi_version() == N.WV_ABI_VERSION
+    assert all(hasattr(wide, n) for n in _declared_functions())
     assert lib.wv_synthesis_tile(None, None) == N.WV_ERR_ARG
 
 
